@@ -1,0 +1,282 @@
+"""Parameter selection for the spectral SOG solver (oracle side).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  The CUDA library has its
+own, independent implementation of the same rules (paper_2412_04595_b200/csrc/
+plan.cpp); tests/test_plan_parity.py compares the two.
+
+The paper gives the ingredients (section 4.3) with
+unit-prefactor O(.) estimates; the concrete rules are the readings R1-R9 of
+DESIGN.md ("Readings of the paper").  Every constant below is named there.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+from scipy.special import erfcinv
+
+# Table 1: b, r0, omega, energy error, M_E, force error, M_F.
+TABLE1 = (
+    (2.0, 1.9892536839080267, 0.9944464927622323, 3.12e-2, 16, 9.93e-3, 11),
+    (1.62976708826776469, 2.7520026668023417, 1.0078069793438068, 2.33e-3, 31, 6.21e-4, 16),
+    (1.48783512395703226, 3.7554672283554990, 0.9919117057598183, 2.29e-4, 46, 7.98e-5, 26),
+    (1.32070036405934420, 4.3914554711638349, 1.0018891411481198, 1.18e-6, 76, 5.76e-7, 41),
+    (1.21812525709410644, 5.6355288151271085, 1.0009014615603334, 7.14e-10, 166, 5.14e-10, 71),
+    (1.14878150173321925, 7.2956245490719404, 1.0000368348358225, 1.30e-15, 271, 1.98e-14, 116),
+)
+
+# ---- plan constants (R2, R4-R9); tuned on B200 / calibrated vs Ewald2D ----
+RC_FACTOR = 3.5      # R2: r_c = RC_FACTOR * rho^(-1/3)
+ETA = 0.3            # R4: range-splitting factor
+KAPPA = 1.15         # R5/R8: Nyquist safety, h <= pi s /(2 KAPPA sqrt(ln 1/tol))
+WIN_C = 0.3          # R6: window error target eps_w = WIN_C * tol
+PAD_C = 10.0         # R7: z padding  s_m * sqrt(ln(PAD_C/tol))
+CHEB_C = 0.1         # R9: Chebyshev two-variable interpolation target CHEB_C * tol
+FFT_COST = 43.0      # R6: cost of one FFT grid point in units of one stencil point (B200 model)
+LONG_FFT_COST = 43.0
+TOL_MIN = 2e-14      # Table 1 force floor 1.98e-14
+TOL_MAX = 1e-1
+
+
+def select_row(tol: float):
+    """R1: the coarsest Table-1 row whose force error is <= tol."""
+    if not (TOL_MIN <= tol <= TOL_MAX):
+        raise ValueError(f"tol {tol} outside [{TOL_MIN}, {TOL_MAX}]")
+    for row in TABLE1:
+        if row[5] <= tol:
+            return row
+    raise ValueError("infeasible tolerance")
+
+
+def sog_nodes_weights(b: float, sigma: float, omega: float, M: int):
+    """w_l = (pi/2)^(-1/2) b^(-l) sigma^(-1) log b, s_l = sqrt(2) b^l sigma;
+    w_0 carries the extra factor omega."""
+    ell = np.arange(M + 1, dtype=np.float64)
+    w = (math.pi / 2.0) ** -0.5 * b ** (-ell) / sigma * math.log(b)
+    w[0] *= omega
+    s = math.sqrt(2.0) * b ** ell * sigma
+    return w, s
+
+
+def is_friendly(n: int) -> bool:
+    for p in (2, 3, 5, 7):
+        while n % p == 0:
+            n //= p
+    return n == 1
+
+
+def friendly_even(n: int) -> int:
+    """Smallest even integer >= n whose prime factors are in {2,3,5,7} (FFT sizes)."""
+    n = max(int(n), 2)
+    if n % 2:
+        n += 1
+    while not is_friendly(n):
+        n += 2
+    return n
+
+
+def window_h_alias(P: int, S: float, eps_w: float, s: float) -> float:
+    """Largest mesh size h for which the aliasing term of Thm 4.2,
+    exp(-pi^2 mu (P-1)^2 / (4 s^2 S)) with mu = s^2 - H^2/S, H=(P-1)h/2,
+    stays <= eps_w.  Returns 0 if no h > 0 works (P too small for S)."""
+    a = P - 1.0
+    rhs = 1.0 - 4.0 * S * math.log(1.0 / eps_w) / (math.pi ** 2 * a * a)
+    if rhs <= 0.0:
+        return 0.0
+    return 2.0 * s * math.sqrt(S) / a * math.sqrt(rhs)
+
+
+def choose_window(s: float, eps_w: float, tol: float, cost_fn):
+    """R6: Gaussian window W=exp(-S (x/H)^2).  S = erfcinv(eps_w)^2 so the
+    erfc(sqrt S) term of Thms 4.2/4.3 is eps_w; the support P (odd) and mesh size
+    h minimise cost_fn(P, h) subject to the aliasing bound and the Nyquist
+    truncation h <= pi s / (2 KAPPA sqrt(ln 1/tol)) (Thm 4.1 with R5's exponent)."""
+    S = float(erfcinv(eps_w)) ** 2
+    h_nyq = math.pi * s / (2.0 * KAPPA * math.sqrt(math.log(1.0 / tol)))
+    best = None
+    for P in range(3, 61, 2):
+        ha = window_h_alias(P, S, eps_w, s)
+        if ha <= 0.0:
+            continue
+        h = min(h_nyq, ha)
+        c = cost_fn(P, h)
+        if best is None or c < best[0]:
+            best = (c, P, h)
+    if best is None:
+        raise ValueError("no feasible window")
+    return best[1], S, best[2]
+
+
+def cheb_nodes(P: int) -> np.ndarray:
+    """First-kind Chebyshev nodes x_i = cos((i-1/2) pi / P), i=1..P."""
+    i = np.arange(1, P + 1, dtype=np.float64)
+    return np.cos((i - 0.5) * np.pi / P)
+
+
+def cheb_T(x: np.ndarray, P: int) -> np.ndarray:
+    """T_n(x), n=0..P-1, by the three-term recurrence; shape x.shape+(P,)."""
+    x = np.asarray(x, dtype=np.float64)
+    T = np.empty(x.shape + (P,), dtype=np.float64)
+    T[..., 0] = 1.0
+    if P > 1:
+        T[..., 1] = x
+    for n in range(1, P - 1):
+        T[..., n + 1] = 2.0 * x * T[..., n] - T[..., n - 1]
+    return T
+
+
+def lagrange_matrix(x: np.ndarray, P: int) -> np.ndarray:
+    """Values L_a(x) of the interpolation basis: Chebyshev interpolation a = V^{-1} f
+     followed by evaluation E a, i.e. L(x) = T(x) V^{-1}."""
+    V = cheb_T(cheb_nodes(P), P)            # V(i,j) = T_j(x_i)
+    return cheb_T(x, P) @ np.linalg.inv(V)
+
+
+def cheb_two_sided_error(P: int, Lz: float, s: float, ntest: int = 65) -> float:
+    """Max error of the two-variable interpolant sum_ab L_a(z) g(z_a-z_b) L_b(z')
+    of g(d)=exp(-d^2/s^2) on a test grid of [-Lz/2, Lz/2]^2 (R9; Thm 3.1)."""
+    xt = np.linspace(-1.0, 1.0, ntest)
+    za = 0.5 * Lz * cheb_nodes(P)
+    G = np.exp(-((za[:, None] - za[None, :]) / s) ** 2)
+    Lt = lagrange_matrix(xt, P)
+    approx = Lt @ G @ Lt.T
+    zt = 0.5 * Lz * xt
+    exact = np.exp(-((zt[:, None] - zt[None, :]) / s) ** 2)
+    return float(np.max(np.abs(approx - exact)))
+
+
+def choose_cheb(Lz: float, s: float, eps: float) -> int:
+    """R9: smallest P (>=2) with two-sided interpolation error <= eps."""
+    for P in range(2, 65):
+        if cheb_two_sided_error(P, Lz, s) <= eps:
+            return P
+    raise ValueError("Chebyshev order > 64 needed")
+
+
+@dataclasses.dataclass
+class Plan:
+    N: int
+    Lx: float
+    Ly: float
+    Lz: float
+    tol: float
+    b: float
+    r0: float
+    omega: float
+    rc: float
+    sigma: float
+    M: int
+    m: int
+    # mid-range grid (R5-R7); unused when m < 0
+    Ix: int = 0
+    Iy: int = 0
+    Iz: int = 0           # interior z count, h_z = Lz / Iz
+    Izs: int = 0          # extended z grid count I_z^*
+    P: int = 0            # window support (odd)
+    S: float = 0.0        # window shape
+    # long-range (R8-R9)
+    Ilx: int = 0
+    Ily: int = 0
+    Pl: int = 0
+    Sl: float = 0.0
+    Pc: int = 0           # Chebyshev proxy layers
+
+    # derived quantities (recomputed, never stored separately)
+    @property
+    def hx(self) -> float:
+        return self.Lx / self.Ix
+
+    @property
+    def hy(self) -> float:
+        return self.Ly / self.Iy
+
+    @property
+    def hz(self) -> float:
+        return self.Lz / self.Iz
+
+    @property
+    def Lzs(self) -> float:
+        return self.hz * self.Izs
+
+    @property
+    def hlx(self) -> float:
+        return self.Lx / self.Ilx
+
+    @property
+    def hly(self) -> float:
+        return self.Ly / self.Ily
+
+    def weights(self):
+        return sog_nodes_weights(self.b, self.sigma, self.omega, self.M)
+
+    def describe(self) -> dict:
+        d = dataclasses.asdict(self)
+        return d
+
+
+def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Plan:
+    """Rules R1-R9.  Keyword overrides replace any chosen value
+    (rc_factor, eta, b-row via `row`, or any Plan field)."""
+    if N < 1 or not all(math.isfinite(v) and v > 0 for v in (Lx, Ly, Lz)):
+        raise ValueError("invalid N or box")
+    row = over.pop("row", None) or select_row(tol)
+    b, r0, omega = row[0], row[1], row[2]
+    rc_factor = over.pop("rc_factor", RC_FACTOR)
+    eta = over.pop("eta", ETA)
+    rho = N / (Lx * Ly * Lz)
+    rc = over.pop("rc", None)
+    if rc is None:
+        rc = min(rc_factor * rho ** (-1.0 / 3.0), 0.5 * min(Lx, Ly))
+    if rc > 0.5 * min(Lx, Ly) * (1 + 1e-15):
+        raise ValueError("r_c > min(Lx,Ly)/2")
+    sigma = rc / r0
+    s0 = math.sqrt(2.0) * sigma
+    Lmax = max(Lx, Ly, Lz)
+    M = over.pop("M", None)
+    if M is None:                                            # R3
+        M = max(0, math.ceil(math.log(Lmax / tol / s0) / math.log(b)))
+        while s0 * b ** M < Lmax / tol:
+            M += 1
+        while M > 0 and s0 * b ** (M - 1) >= Lmax / tol:
+            M -= 1
+    m = over.pop("m", None)
+    if m is None:                                            # R4
+        m = -1
+        for ell in range(M + 1):
+            if s0 * b ** ell <= eta * Lz:
+                m = ell
+    m = min(m, M - 1)                                        # keep >= 1 long-range Gaussian
+    p = Plan(N=N, Lx=Lx, Ly=Ly, Lz=Lz, tol=tol, b=b, r0=r0, omega=omega, rc=rc,
+             sigma=sigma, M=M, m=m)
+    eps_w = WIN_C * tol
+    if m >= 0:
+        sm = s0 * b ** m
+
+        def cost_mid(P, h):
+            pad = max(2.0 * ((P - 1) * h / 2.0 + h), sm * math.sqrt(math.log(PAD_C / tol)))
+            return P ** 3 + FFT_COST * (Lx * Ly * (Lz + pad)) / (N * h ** 3)
+
+        P, S, h = choose_window(s0, eps_w, tol, cost_mid)
+        p.P, p.S = P, S
+        p.Ix = friendly_even(math.ceil(Lx / h))
+        p.Iy = friendly_even(math.ceil(Ly / h))
+        p.Iz = max(1, math.ceil(Lz / h))
+        Hz = (P - 1) * p.hz / 2.0
+        pad = max(2.0 * (Hz + p.hz), sm * math.sqrt(math.log(PAD_C / tol)))   # R7
+        p.Izs = friendly_even(math.ceil((Lz + pad) / p.hz))
+    sl = s0 * b ** (m + 1)
+
+    def cost_long(P, h):
+        return P ** 2 + LONG_FFT_COST * (Lx * Ly) / (N * h ** 2)
+
+    Pl, Sl, hl = choose_window(sl, eps_w, tol, cost_long)          # R8
+    p.Pl, p.Sl = Pl, Sl
+    p.Ilx = max(friendly_even(math.ceil(Lx / hl)), friendly_even(Pl))
+    p.Ily = max(friendly_even(math.ceil(Ly / hl)), friendly_even(Pl))
+    p.Pc = choose_cheb(Lz, sl, CHEB_C * tol)                         # R9
+    for k, v in over.items():
+        if not hasattr(p, k):
+            raise KeyError(k)
+        setattr(p, k, v)
+    return p

@@ -1,0 +1,355 @@
+"""Step-by-step spectral SOG evaluation (the oracle).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain NumPy/SciPy, fp64,
+no blocking or fusion: each function follows one passage of PAPER.md in the
+paper's order and notation, on the plan's scalar parameters (oracle/plan.py).
+
+    phi_i = Phi^N_i + Phi^mid_i + Phi^long_i - Phi^self_i
+    F_i   = -q_i grad phi(r_i)
+    U     = 1/2 sum_i q_i phi_i
+
+Readings used: R6 stencil, R7 padding, R9 two-sided proxies,
+R10 expm1 at kdot=0, R11 analytic gather gradient, R12 normalisations,
+R14 coordinates.  Every function here is pinned by tests/test_oracle_*.py.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import scipy.fft
+from scipy.spatial import cKDTree
+
+from .plan import Plan, cheb_T, cheb_nodes
+
+_WORKERS = -1  # scipy.fft: all host cores
+
+
+# ----------------------------------------------------------------------------- geometry
+def canonicalize(xyz: np.ndarray, plan: Plan) -> np.ndarray:
+    """R14: wrap x,y into [-L/2, L/2) (P:106-117 periodic in x,y); z must lie in the
+    closed interval [-Lz/2, Lz/2] (free direction), else ValueError."""
+    xyz = np.array(xyz, dtype=np.float64, copy=True)
+    if not np.all(np.isfinite(xyz)):
+        raise ValueError("non-finite position")
+    for d, L in ((0, plan.Lx), (1, plan.Ly)):
+        xyz[:, d] = xyz[:, d] - L * np.floor((xyz[:, d] + 0.5 * L) / L)
+        xyz[:, d] = np.where(xyz[:, d] >= 0.5 * L, xyz[:, d] - L, xyz[:, d])
+    if np.any(np.abs(xyz[:, 2]) > 0.5 * plan.Lz):
+        raise ValueError("z outside [-Lz/2, Lz/2]")
+    return xyz
+
+
+def min_image(d: np.ndarray, L: float) -> np.ndarray:
+    """Minimum-image displacement in a periodic direction (Assumption 1)."""
+    return d - L * np.round(d / L)
+
+
+# ----------------------------------------------------------------------------- near field
+def near_kernel(plan: Plan, r: np.ndarray):
+    """N(r) = 1/r - F(r), F(r) = sum_{l=0}^{M} w_l exp(-r^2/s_l^2), for r < r_c, else 0
+    (Eqs. eq::SOGDEcomp, eq::SOGField); returns (N, dN/dr).  Exact sum."""
+    w, s = plan.weights()
+    r = np.asarray(r, dtype=np.float64)
+    e = np.exp(-(r[..., None] / s) ** 2) * w
+    F = e.sum(-1)
+    dF = (e * (-2.0 * r[..., None] / s ** 2)).sum(-1)
+    inside = r < plan.rc
+    N = np.where(inside, 1.0 / r - F, 0.0)
+    dN = np.where(inside, -1.0 / r ** 2 - dF, 0.0)
+    return N, dN
+
+
+def _near_pairs_accumulate(plan, xyz, q, ti, sj, out_phi, out_grad, out_rows):
+    dx = min_image(xyz[ti, 0] - xyz[sj, 0], plan.Lx)
+    dy = min_image(xyz[ti, 1] - xyz[sj, 1], plan.Ly)
+    dz = xyz[ti, 2] - xyz[sj, 2]                       # z never wrapped (free)
+    r = np.sqrt(dx * dx + dy * dy + dz * dz)
+    keep = (r < plan.rc) & (r > 0.0)
+    ti, sj, dx, dy, dz, r = ti[keep], sj[keep], dx[keep], dy[keep], dz[keep], r[keep]
+    N, dN = near_kernel(plan, r)
+    rows = out_rows[ti]
+    np.add.at(out_phi, rows, q[sj] * N)
+    g = q[sj] * dN / r
+    np.add.at(out_grad, (rows, 0), g * dx)
+    np.add.at(out_grad, (rows, 1), g * dy)
+    np.add.at(out_grad, (rows, 2), g * dz)
+
+
+def near_field(plan: Plan, xyz, q, targets=None, brute_force=None):
+    """Phi^N_i = sum'_n sum_j q_j N(|r_ij + n L|) (Eq. eq::phiNDR) and its
+    gradient; only r < r_c <= min(Lx,Ly)/2 contributes, i.e. the minimum image
+    (P:264 cell list).  Candidate pairs come from a periodic k-d tree (library
+    neighbour search) or, for brute_force=True, the O(N^2) double loop."""
+    N = len(q)
+    tgt = np.arange(N) if targets is None else np.asarray(targets)
+    rows = np.full(N, -1, dtype=np.int64)
+    rows[tgt] = np.arange(len(tgt))
+    phi = np.zeros(len(tgt))
+    grad = np.zeros((len(tgt), 3))
+    if brute_force is None:
+        brute_force = N * len(tgt) <= 4_000_000
+    if brute_force:
+        chunk = max(1, 2_000_000 // N)
+        for c0 in range(0, len(tgt), chunk):
+            t = tgt[c0:c0 + chunk]
+            ti = np.repeat(t, N)
+            sj = np.tile(np.arange(N), len(t))
+            _near_pairs_accumulate(plan, xyz, q, ti, sj, phi, grad, rows)
+        return phi, grad
+    pos = np.empty_like(xyz)
+    pos[:, 0] = np.mod(xyz[:, 0] + 0.5 * plan.Lx, plan.Lx)
+    pos[:, 1] = np.mod(xyz[:, 1] + 0.5 * plan.Ly, plan.Ly)
+    pos[:, 0] = np.where(pos[:, 0] >= plan.Lx, 0.0, pos[:, 0])
+    pos[:, 1] = np.where(pos[:, 1] >= plan.Ly, 0.0, pos[:, 1])
+    pos[:, 2] = xyz[:, 2] + 0.5 * plan.Lz
+    box = [plan.Lx, plan.Ly, plan.Lz + 4.0 * plan.rc + 1.0]   # z box large: never wraps
+    tree = cKDTree(pos, boxsize=box)
+    rq = plan.rc * (1.0 + 1e-9)
+    for c0 in range(0, len(tgt), 65536):
+        t = tgt[c0:c0 + 65536]
+        lists = tree.query_ball_point(pos[t], rq)
+        cnt = np.fromiter((len(l) for l in lists), dtype=np.int64, count=len(t))
+        sj = np.fromiter((j for l in lists for j in l), dtype=np.int64, count=int(cnt.sum()))
+        ti = np.repeat(t, cnt)
+        _near_pairs_accumulate(plan, xyz, q, ti, sj, phi, grad, rows)
+    return phi, grad
+
+
+def self_coefficient(plan: Plan) -> float:
+    """Phi^self_i / q_i = sum_{l=0}^{M} w_l (Eq. eq::phiNDR)."""
+    w, _ = plan.weights()
+    return float(w.sum())
+
+
+# ----------------------------------------------------------------------------- windows
+def gaussian_window_hat(k, H: float, S: float):
+    """W_hat_GS(k) = sqrt(pi/S) H exp(-k^2 H^2 / (4S)) (Eq. eq::GS), the
+    untruncated closed form used for deconvolution (R6)."""
+    return math.sqrt(math.pi / S) * H * np.exp(-(np.asarray(k) ** 2) * H * H / (4.0 * S))
+
+
+def stencil(x: np.ndarray, I: int, h: float, P: int, S: float, periodic: bool):
+    """R6: the P (odd) consecutive grid points centred at the nearest grid point
+    g0 = floor(x/h + I/2 + 1/2) of the grid x_g = (g - I/2) h; window
+    W(x_g - x) = exp(-S ((x_g - x)/H)^2), H = (P-1)h/2 (Eq. eq::GS),
+    evaluated at all P points.  Returns (flat index, W, dW/dx_particle)."""
+    p = (P - 1) // 2
+    H = (P - 1) * h / 2.0
+    g0 = np.floor(x / h + (I / 2.0 + 0.5)).astype(np.int64)
+    g = g0[:, None] + np.arange(-p, p + 1)[None, :]
+    d = (g - I / 2.0) * h - x[:, None]
+    W = np.exp(-S * (d / H) ** 2)
+    dW = 2.0 * S * d / (H * H) * W          # d/dx_i W(x_i - x_g)  (R11)
+    if periodic:
+        g = np.mod(g, I)
+    elif np.any(g < 0) or np.any(g >= I):
+        raise ValueError("stencil leaves the extended z grid (R7 violated)")
+    return g, W, dW
+
+
+# ----------------------------------------------------------------------------- mid range
+def mid_multiplier(plan: Plan) -> np.ndarray:
+    """Scaling factor of Eq. eq::widehat-tilde on the rfftn half spectrum:
+    tau_hat^mid(k)/k^2 * 4 pi |W_hat|^-2 = pi^{3/2} sum_{l<=m} w_l s_l^3
+    exp(-s_l^2 |k|^2 / 4) / (W_hat_x W_hat_y W_hat_z)^2   (R12),
+    k_d = 2 pi n_d / L_d with L_z -> L_z^* (P:580)."""
+    w, s = plan.weights()
+    kx = 2.0 * np.pi * np.fft.fftfreq(plan.Ix, d=plan.hx)
+    ky = 2.0 * np.pi * np.fft.fftfreq(plan.Iy, d=plan.hy)
+    kz = 2.0 * np.pi * np.fft.rfftfreq(plan.Izs, d=plan.hz)
+    k2 = kx[:, None, None] ** 2 + ky[None, :, None] ** 2 + kz[None, None, :] ** 2
+    tau = np.zeros_like(k2)
+    for ell in range(plan.m + 1):
+        tau += w[ell] * s[ell] ** 3 * np.exp(-s[ell] ** 2 * k2 / 4.0)
+    Hx, Hy, Hz = ((plan.P - 1) * h / 2.0 for h in (plan.hx, plan.hy, plan.hz))
+    What = (gaussian_window_hat(kx, Hx, plan.S)[:, None, None]
+            * gaussian_window_hat(ky, Hy, plan.S)[None, :, None]
+            * gaussian_window_hat(kz, Hz, plan.S)[None, None, :])
+    return math.pi ** 1.5 * tau / What ** 2
+
+
+def mid_stencils(plan: Plan, xyz):
+    sx = stencil(xyz[:, 0], plan.Ix, plan.hx, plan.P, plan.S, True)
+    sy = stencil(xyz[:, 1], plan.Iy, plan.hy, plan.P, plan.S, True)
+    sz = stencil(xyz[:, 2], plan.Izs, plan.hz, plan.P, plan.S, False)
+    return sx, sy, sz
+
+
+def mid_spread(plan: Plan, xyz, q) -> np.ndarray:
+    """Algorithm 1 step 1 (gridding, Eq. eq::gridding):
+    S[g] = sum_j q_j W(x_g-x_j)_* W(y_g-y_j)_* W(z_g-z_j) on the I_x x I_y x I_z^* grid."""
+    (gx, Wx, _), (gy, Wy, _), (gz, Wz, _) = mid_stencils(plan, xyz)
+    G = np.zeros(plan.Ix * plan.Iy * plan.Izs)
+    for a in range(plan.P):
+        for b in range(plan.P):
+            base = (gx[:, a] * plan.Iy + gy[:, b]) * plan.Izs
+            idx = base[:, None] + gz
+            val = (q * Wx[:, a] * Wy[:, b])[:, None] * Wz
+            np.add.at(G, idx.ravel(), val.ravel())
+    return G.reshape(plan.Ix, plan.Iy, plan.Izs)
+
+
+def mid_solve(plan: Plan, S: np.ndarray) -> np.ndarray:
+    """Algorithm 1 steps 2-4: forward 3D FFT, scaling, backward 3D FFT."""
+    Shat = scipy.fft.rfftn(S, workers=_WORKERS)
+    Shat *= mid_multiplier(plan)
+    return scipy.fft.irfftn(Shat, s=S.shape, workers=_WORKERS)
+
+
+def mid_gather(plan: Plan, xyz, Psi: np.ndarray):
+    """Algorithm 1 step 5 (gathering, Eq. eq::Phiconv discretised by the trapezoidal
+    rule): phi_i = V_h sum_g W W W Psi[g]; gradient with W' (R11)."""
+    (gx, Wx, dWx), (gy, Wy, dWy), (gz, Wz, dWz) = mid_stencils(plan, xyz)
+    flat = Psi.ravel()
+    n = len(xyz)
+    phi = np.zeros(n)
+    grad = np.zeros((n, 3))
+    for a in range(plan.P):
+        for b in range(plan.P):
+            base = (gx[:, a] * plan.Iy + gy[:, b]) * plan.Izs
+            vals = flat[base[:, None] + gz]
+            t0 = (Wz * vals).sum(1)
+            t1 = (dWz * vals).sum(1)
+            phi += Wx[:, a] * Wy[:, b] * t0
+            grad[:, 0] += dWx[:, a] * Wy[:, b] * t0
+            grad[:, 1] += Wx[:, a] * dWy[:, b] * t0
+            grad[:, 2] += Wx[:, a] * Wy[:, b] * t1
+    Vh = plan.hx * plan.hy * plan.hz
+    return Vh * phi, Vh * grad
+
+
+def mid_range(plan: Plan, xyz, q, targets=None):
+    """Phi^mid (Algorithm 1) at the targets, with gradient."""
+    tgt = slice(None) if targets is None else np.asarray(targets)
+    n = len(q) if targets is None else len(tgt)
+    if plan.m < 0:
+        return np.zeros(n), np.zeros((n, 3))
+    Psi = mid_solve(plan, mid_spread(plan, xyz, q))
+    return mid_gather(plan, xyz[tgt], Psi)
+
+
+# ----------------------------------------------------------------------------- long range
+def long_kernel(plan: Plan) -> np.ndarray:
+    """K_ab(kdot) on the rfft2 half plane, shape (Pc, Pc, Ilx, Ily//2+1):
+    pi sum_{l=m+1}^{M} w_l s_l^2 exp(-s_l^2 |kdot|^2 / 4) E_l(z_a - z_b) / (W_hat_x W_hat_y)^2
+    with E_l(d) = exp(-d^2/s_l^2), and expm1(-d^2/s_l^2) at kdot = 0 (R10).
+    Derivation: Eq. eq::trun2 + two-sided Chebyshev proxies (R9) + the
+    window sandwich of Eq. eq::phi2M / eq::overlineSscal."""
+    w, s = plan.weights()
+    za = 0.5 * plan.Lz * cheb_nodes(plan.Pc)
+    d2 = (za[:, None] - za[None, :]) ** 2
+    kx = 2.0 * np.pi * np.fft.fftfreq(plan.Ilx, d=plan.hlx)
+    ky = 2.0 * np.pi * np.fft.rfftfreq(plan.Ily, d=plan.hly)
+    k2 = kx[:, None] ** 2 + ky[None, :] ** 2
+    K = np.zeros((plan.Pc, plan.Pc) + k2.shape)
+    K0 = np.zeros((plan.Pc, plan.Pc))
+    nonzero = k2 > 0.0
+    for ell in range(plan.m + 1, plan.M + 1):
+        E = np.exp(-d2 / s[ell] ** 2)
+        spec = np.where(nonzero, w[ell] * s[ell] ** 2 * np.exp(-s[ell] ** 2 * k2 / 4.0), 0.0)
+        K += E[:, :, None, None] * spec[None, None]
+        K0 += w[ell] * s[ell] ** 2 * np.expm1(-d2 / s[ell] ** 2)
+    K[:, :, 0, 0] = K0
+    Hx = (plan.Pl - 1) * plan.hlx / 2.0
+    Hy = (plan.Pl - 1) * plan.hly / 2.0
+    What = gaussian_window_hat(kx, Hx, plan.Sl)[:, None] * gaussian_window_hat(ky, Hy, plan.Sl)[None, :]
+    return math.pi * K / What[None, None] ** 2
+
+
+def long_basis(plan: Plan, z: np.ndarray):
+    """Lagrange basis L_a(z) at the Pc Chebyshev proxies and dL_a/dz (App. A.2)."""
+    x = 2.0 * np.asarray(z) / plan.Lz
+    V = cheb_T(cheb_nodes(plan.Pc), plan.Pc)
+    Vinv = np.linalg.inv(V)
+    T = cheb_T(x, plan.Pc)
+    # T_n'(x) via T'_{n+1} = 2 T_n + 2 x T'_n - T'_{n-1}
+    dT = np.zeros_like(T)
+    if plan.Pc > 1:
+        dT[..., 1] = 1.0
+    for n in range(1, plan.Pc - 1):
+        dT[..., n + 1] = 2.0 * T[..., n] + 2.0 * x * dT[..., n] - dT[..., n - 1]
+    return T @ Vinv, (dT @ Vinv) * (2.0 / plan.Lz)
+
+
+def long_stencils(plan: Plan, xyz):
+    sx = stencil(xyz[:, 0], plan.Ilx, plan.hlx, plan.Pl, plan.Sl, True)
+    sy = stencil(xyz[:, 1], plan.Ily, plan.hly, plan.Pl, plan.Sl, True)
+    return sx, sy
+
+
+def long_spread(plan: Plan, xyz, q) -> np.ndarray:
+    """Anterpolation to the proxy layers (Alg. 2 step 1, two-sided form R9):
+    S_b[g] = sum_j q_j L_b(z_j) W(x_g-x_j)_* W(y_g-y_j)_*  (P:529)."""
+    (gx, Wx, _), (gy, Wy, _) = long_stencils(plan, xyz)
+    Lb, _ = long_basis(plan, xyz[:, 2])
+    G = np.zeros(plan.Pc * plan.Ilx * plan.Ily)
+    layer = np.arange(plan.Pc) * (plan.Ilx * plan.Ily)
+    for a in range(plan.Pl):
+        for b in range(plan.Pl):
+            idx = (gx[:, a] * plan.Ily + gy[:, b])[:, None] + layer[None, :]
+            val = (q * Wx[:, a] * Wy[:, b])[:, None] * Lb
+            np.add.at(G, idx.ravel(), val.ravel())
+    return G.reshape(plan.Pc, plan.Ilx, plan.Ily)
+
+
+def long_solve(plan: Plan, S: np.ndarray) -> np.ndarray:
+    """Alg. 2 steps 2-4: 2D FFT per layer, scaling by the wide
+    Gaussians' spectra coupled across layers (K_ab), backward 2D FFT per layer."""
+    Shat = scipy.fft.rfft2(S, axes=(1, 2), workers=_WORKERS)
+    K = long_kernel(plan)
+    Shat2 = np.einsum("abxy,bxy->axy", K, Shat)
+    return scipy.fft.irfft2(Shat2, s=S.shape[1:], axes=(1, 2), workers=_WORKERS)
+
+
+def long_gather(plan: Plan, xyz, Psi: np.ndarray):
+    """Alg. 2 step 5 (Eq. eq::SOGLong): phi_i = h_x h_y sum_g W W sum_a L_a(z_i) Psi_a[g]."""
+    (gx, Wx, dWx), (gy, Wy, dWy) = long_stencils(plan, xyz)
+    La, dLa = long_basis(plan, xyz[:, 2])
+    n = len(xyz)
+    phi = np.zeros(n)
+    grad = np.zeros((n, 3))
+    flat = Psi.reshape(plan.Pc, -1)
+    for a in range(plan.Pl):
+        for b in range(plan.Pl):
+            vals = flat[:, gx[:, a] * plan.Ily + gy[:, b]].T          # (n, Pc)
+            t0 = (La * vals).sum(1)
+            t1 = (dLa * vals).sum(1)
+            phi += Wx[:, a] * Wy[:, b] * t0
+            grad[:, 0] += dWx[:, a] * Wy[:, b] * t0
+            grad[:, 1] += Wx[:, a] * dWy[:, b] * t0
+            grad[:, 2] += Wx[:, a] * Wy[:, b] * t1
+    A = plan.hlx * plan.hly
+    return A * phi, A * grad
+
+
+def long_range(plan: Plan, xyz, q, targets=None):
+    """Phi^long (Algorithm 2 with two-sided Chebyshev proxies, R9) at the targets."""
+    tgt = slice(None) if targets is None else np.asarray(targets)
+    Psi = long_solve(plan, long_spread(plan, xyz, q))
+    return long_gather(plan, xyz[tgt], Psi)
+
+
+# ----------------------------------------------------------------------------- total
+def evaluate(plan: Plan, xyz, q, targets=None, parts: bool = False):
+    """phi_i = Phi^N + Phi^mid + Phi^long - q_i sum w_l and
+    F_i = -q_i grad phi, at all particles or the given targets."""
+    xyz = canonicalize(xyz, plan)
+    q = np.asarray(q, dtype=np.float64)
+    if abs(q.sum()) > 1e-12 * np.abs(q).sum():
+        raise ValueError("system not charge neutral (P:119-121)")
+    tq = q if targets is None else q[np.asarray(targets)]
+    pn, gn = near_field(plan, xyz, q, targets)
+    pm, gm = mid_range(plan, xyz, q, targets)
+    pl, gl = long_range(plan, xyz, q, targets)
+    phi = pn + pm + pl - tq * self_coefficient(plan)
+    grad = gn + gm + gl
+    force = -tq[:, None] * grad
+    if parts:
+        return phi, force, {"near": (pn, gn), "mid": (pm, gm), "long": (pl, gl)}
+    return phi, force
+
+
+def energy(q, phi) -> float:
+    """U = 1/2 sum_i q_i phi_i."""
+    return 0.5 * float(np.dot(q, phi))

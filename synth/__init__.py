@@ -1,0 +1,75 @@
+"""Seeded synthetic inputs shared by the oracle tests and the CUDA path.
+
+This module holds NO arithmetic of the SOG method: it only draws positions and
+charges.  It is the one module both `oracle/` and the product tests/bench may
+use (the oracle and the CUDA path share nothing else).
+
+Workload recipe (PAPER.md P:997, P:1044, P:1066 -- "randomly distributed
+monovalent particles satisfying the charge neutrality condition"):
+  * positions uniform in the centred box [-Lx/2,Lx/2) x [-Ly/2,Ly/2) x [-Lz/2,Lz/2]
+    (box centred at the origin);
+  * charges: exactly N/2 of +1 and N/2 of -1 (N even), randomly permuted, so
+    sum(q) == 0 exactly.  For odd N one extra +1/-1 pair is not
+    possible; odd N gets a final charge 0.
+Seeds: numpy.random.default_rng(2412_04595 + config_index).
+
+The BASELINE.json configurations are listed in CONFIGS (c1..c5).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+SEED_BASE = 2412_04595
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    N: int
+    L: tuple[float, float, float]
+    tol: float
+    index: int           # seed offset (BASELINE.json configs[index-1])
+    note: str = ""
+
+
+# BASELINE.json "configs" (index 1..5); c2 is swept over tolerances.
+CONFIGS = {
+    "c1": Config("c1", 1000, (10.0, 10.0, 10.0), 1e-6, 1, "N=1e3 cube 10^3, Ewald2D-checked"),
+    "c2": Config("c2", 100_000, (46.4, 46.4, 46.4), 1e-6, 2, "N=1e5 cube density ~1; tol in {1e-4,1e-8,1e-12}"),
+    "c3": Config("c3", 1_000_000, (200.0, 200.0, 25.0), 1e-6, 3, "N=1e6 slab 200x200x25"),
+    "c4": Config("c4", 1_000_000, (50.0, 50.0, 400.0), 1e-6, 4, "N=1e6 tall box 50x50x400"),
+    "c5": Config("c5", 10_000_000, (215.0, 215.0, 215.0), 1e-6, 5, "N=1e7 cube 215^3"),
+}
+
+
+def neutral_charges(N: int, rng: np.random.Generator) -> np.ndarray:
+    """Exactly N//2 charges +1 and N//2 charges -1 (one 0 if N is odd), permuted."""
+    q = np.zeros(N, dtype=np.float64)
+    h = N // 2
+    q[:h] = 1.0
+    q[h:2 * h] = -1.0
+    rng.shuffle(q)
+    return q
+
+
+def uniform_system(N: int, L, seed: int):
+    """Return (xyz [N,3] float64 C-contiguous, q [N] float64) for a seeded uniform system."""
+    rng = np.random.default_rng(seed)
+    L = np.asarray(L, dtype=np.float64)
+    xyz = (rng.random((N, 3)) - 0.5) * L[None, :]
+    q = neutral_charges(N, rng)
+    return np.ascontiguousarray(xyz), q
+
+
+def config_system(name: str, N: int | None = None, seed_offset: int = 0):
+    """Inputs for BASELINE config `name` (optionally with a different N at the same density/shape)."""
+    c = CONFIGS[name]
+    n = c.N if N is None else N
+    L = c.L
+    if N is not None and N != c.N:
+        # keep the density and aspect ratio: scale every side by (n/N)^(1/3)
+        f = (n / c.N) ** (1.0 / 3.0)
+        L = tuple(float(v * f) for v in c.L)
+    return uniform_system(n, L, SEED_BASE + c.index + seed_offset) + (L,)
