@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 spectral-SOG hot path (one potential+force evaluation = one step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
+
+Workload (BASELINE.json metric "particles/s per potential+force eval (fp64, tol 1e-6)"): the
+c5 configuration, N = 1e7 neutral +-1 charges uniform in a 215^3 box (periodic x,y, free z),
+tol 1e-6, synthetic seeded inputs (synth/).  Each rank evaluates its own system (weak
+scaling; the x-slab decomposition is a later row).  The working set (mid grid 4.3 GB) is far
+larger than L2, so no explicit flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py runs it) on
+a bounded sample of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth import CONFIGS, config_system, uniform_system  # noqa: E402
+
+METRIC = "particles/s per potential+force eval (fp64, tol 1e-6)"
+FP64_FMA_PER_SM_CLK = 64          # B200 FP64 pipe (vector): 64 FMA/clk/SM, 148 SMs
+NUM_SMS = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--tol", type=float, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "ours":
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def oracle_sample(cfg, tol, target_seconds=15.0):
+    """The oracle as it stands on a bounded sample of the workload: a system of the same
+    density and aspect ratio, N chosen so one evaluation takes ~target_seconds."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle.sog as O
+    from oracle.plan import make_plan
+    O._WORKERS = 1                      # single host thread: cores = 1
+    n = 2000
+    while True:
+        xyz, q, L = config_system(cfg, N=n)
+        op = make_plan(n, *L, tol)
+        t0 = time.perf_counter()
+        O.evaluate(op, xyz, q)
+        dt = time.perf_counter() - t0
+        if dt > target_seconds / 4 or n >= 200_000:
+            return n, dt, L
+        n = int(n * min(8.0, max(1.5, target_seconds / 2 / max(dt, 1e-3))))
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    tol = args.tol or c.tol
+    n, dt0, L = oracle_sample(args.config, tol)
+    import oracle.sog as O
+    from oracle.plan import make_plan
+    xyz, q, L = config_system(args.config, N=n)
+    op = make_plan(n, *L, tol)
+    for _ in range(min(args.warmup, 1)):
+        O.evaluate(op, xyz, q)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.evaluate(op, xyz, q)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = n / dt
+    sample = f"{args.config} density/aspect, N={n} (box {L[0]:.2f}x{L[1]:.2f}x{L[2]:.2f}), full oracle evaluation"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "particles/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} sample (oracle, CPU)", "N": n, "box": list(L), "tol": tol},
+        "cpu_baseline": {"value": val, "unit": "particles/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def stage_roofline(plan, stages, N, clocks):
+    """Roofline of the dominant kernel stage from the plan's per-stage CUDA-event times."""
+    d = plan.describe()
+    P, Pl, Pc = d["P"], d["Pl"], d["Pc"]
+    G = d["Ix"] * d["Iy"] * d["Izs"]
+    name = max((k for k in stages if k not in ("mid_fft_fwd", "mid_fft_inv", "long_fft_scale_ifft")),
+               key=lambda k: stages[k])
+    ms = stages[name]
+    # algorithmic FP64 flops per launch: FMA = 2 flops
+    flops = {
+        "mid_spread": N * (2.0 * P ** 3 + 2.0 * P * P),
+        "mid_gather": N * (4.0 * P ** 3 + 6.0 * P * P + 8.0 * P),
+        "long_spread": N * (2.0 * Pl * Pl * Pc + 2.0 * Pc * Pc),
+        "long_gather": N * (4.0 * Pl * Pl * Pc + 6.0 * Pl * Pl + 4.0 * Pc * Pc),
+        "near": None, "sort": None, "mid_scale": None, "combine": None,
+    }.get(name)
+    bytes_ = {
+        "mid_spread": 32.0 * N + 8.0 * G, "mid_gather": 8.0 * G + 64.0 * N,
+        "mid_scale": 32.0 * G / 2, "sort": 150.0 * N, "combine": 160.0 * N,
+        "near": 64.0 * N,
+    }.get(name, 64.0 * N)
+    sm_mhz = 1965.0
+    peak_fp64 = NUM_SMS * FP64_FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    if flops:
+        ach = flops / (ms * 1e-3) / 1e12
+        return name, {"bound": "alu", "kernel": name, "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
+                      "frac": ach / peak_fp64, "traffic": None,
+                      "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
+                      "algorithmic_flops": flops, "ms": ms}
+    ach = bytes_ / (ms * 1e-3) / 1e9
+    return name, {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                  "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_bytes": bytes_, "ms": ms}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    from paper_2412_04595_b200 import Plan
+    c = CONFIGS[args.config]
+    tol = args.tol or c.tol
+    xyz, q, L = config_system(args.config, seed_offset=rank)
+    N = len(q)
+    stream = torch.cuda.current_stream()
+    plan = Plan(N, L, tol, stream=stream, validate=False)
+    xd = torch.from_numpy(xyz).cuda()
+    qd = torch.from_numpy(q).cuda()
+    phi = torch.empty(N, dtype=torch.float64, device="cuda")
+    F = torch.empty(N, 3, dtype=torch.float64, device="cuda")
+    # one validated evaluation first (catches bad inputs), then warm-up
+    plan.set_flags(validate=True)
+    plan.eval(xd, qd, phi, F)
+    plan.set_flags(validate=False)
+    for _ in range(max(0, args.warmup - 1)):
+        plan.eval(xd, qd, phi, F)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.eval(xd, qd, phi, F)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, ws)
+    value = N * ws / (ms * 1e-3)
+    # per-stage device times (CUDA events on the plan's stream), averaged over K evaluations
+    plan.set_flags(validate=False, timing=True)
+    acc = {}
+    for _ in range(args.steps):
+        plan.eval(xd, qd, phi, F)
+        for k, v in plan.timings().items():
+            acc[k] = acc.get(k, 0.0) + v / args.steps
+    plan.set_flags(validate=False)
+    dom, roof = stage_roofline(plan, acc, N, clk.summary())
+    # end-to-end through the public host-buffer API (pinned host memory, copies in the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(xyz).pin_memory()
+        hq = torch.from_numpy(q).pin_memory()
+        hphi = torch.empty(N, dtype=torch.float64).pin_memory()
+        hF = torch.empty(N, 3, dtype=torch.float64).pin_memory()
+        plan.eval_host(hx, hq, hphi, hF)
+        barrier(ws)
+        t0 = time.perf_counter()
+        g0 = torch.cuda.Event(enable_timing=True); g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            plan.eval_host(hx, hq, hphi, hF)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(g0.elapsed_time(g1) / args.steps, ws)
+        e2e = {"value": N * ws / (e2e_ms * 1e-3), "unit": "particles/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 32 * N, "d2h_bytes_per_step": 32 * N,
+               "host_wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        n, dt, Ls = oracle_sample(args.config, tol)
+        cpu = {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "oracle",
+               "sample": f"one full oracle evaluation of a {args.config}-density system, N={n}, "
+                         f"box {Ls[0]:.2f}x{Ls[1]:.2f}x{Ls[2]:.2f}, tol {tol:g}, 1 host thread"}
+    d = plan.describe()
+    out = {
+        "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: N={N} neutral +-1 charges uniform in "
+                               f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
+                   "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",
+                   "l2": "working set (mid grid %.1f GB) >> 126 MB L2; no flush" % (d["Ix"] * d["Iy"] * d["Izs"] * 8 / 1e9),
+                   "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc")}},
+        "stages_ms": acc,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": plan.launches_per_eval() * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

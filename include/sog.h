@@ -1,0 +1,145 @@
+/*
+ * sog.h -- C ABI of the B200-native spectral sum-of-Gaussians (SOG) solver for
+ * quasi-2D electrostatics (periodic in x,y, free in z), arXiv 2412.04595.
+ *
+ * Operation (section 2.1, Eq. eq::Phi): for N point charges q_i at
+ * r_i in the box [-Lx/2,Lx/2) x [-Ly/2,Ly/2) x [-Lz/2,Lz/2], periodic in x,y,
+ * charge neutral (sum q = 0), compute
+ *     phi_i = sum_j sum'_{n in Z^2 x {0}} q_j / |r_ij + n o L|          (self excluded)
+ *     F_i   = -q_i grad phi(r_i)
+ * by the spectral SOG split (Eq. eq::SOGdecomp; Eq. eq::splitting):
+ *     phi = Phi^N (near, cell list) + Phi^mid (Algorithm 1)
+ *         + Phi^long (Algorithm 2 with two-sided Chebyshev proxies) - q_i sum_l w_l
+ * to the requested tolerance `tol` (relative L-inf potential error).
+ *
+ * Conventions (all entry points):
+ *   - Every function is thread-compatible, not thread-safe: one plan per host thread.
+ *   - A plan is not reentrant; sog_eval calls on one plan are serialised on its stream.
+ *   - Errors: functions return a negative sog_status (or NULL) and never throw; the
+ *     message is available from sog_last_error() (thread-local, valid until the next
+ *     call on that thread).  Outputs are unspecified after an error.
+ *   - Device pointers are CUDA device pointers on the plan's device; host pointers are
+ *     ordinary (pageable or pinned) host memory.  The caller owns every buffer it
+ *     passes; the plan owns all of its workspace.
+ *   - Layouts: xyz is N x 3 row-major (x0,y0,z0,x1,...) fp64; q, phi are N fp64;
+ *     force is N x 3 row-major fp64; all in the caller's particle order.
+ */
+#ifndef SOG_H
+#define SOG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sog_plan sog_plan; /* opaque; owns all device workspace and cuFFT plans */
+
+typedef enum {
+    SOG_OK = 0,
+    SOG_EINVAL = -1,        /* bad argument (N, box, tol, pointer, option)                 */
+    SOG_ENONNEUTRAL = -2,   /* |sum q| > 1e-12 sum|q|                           */
+    SOG_EZRANGE = -3,       /* some z outside the closed interval [-Lz/2, Lz/2] */
+    SOG_ENONFINITE = -4,    /* non-finite position or charge                                */
+    SOG_EINFEASIBLE = -5,   /* tol outside [2e-14, 1e-1] (Table 1 force floor)       */
+    SOG_ECUDA = -6,         /* CUDA runtime or cuFFT failure                                 */
+    SOG_ENOMEM = -8         /* device allocation failed                                      */
+} sog_status;
+
+/* flags for sog_plan_opts.flags / sog_set_flags */
+#define SOG_NO_VALIDATE 1u  /* skip the validation readback (the only host sync in sog_eval) */
+
+/*
+ * Optional plan overrides.  Zero-initialise and set what you need.
+ *   explicit_params = 0: parameters come from the plan rules R1-R9, with
+ *                        rc_factor / eta overriding R2 / R4 when > 0.
+ *   explicit_params = 1: every parameter below is used verbatim (e.g. a plan chosen by
+ *                        the CPU oracle); the library only validates them.
+ * Field meanings follow PAPER.md: row = Table 1 row 0..5 (b, r0, omega);
+ * rc = cutoff r_c (sigma = rc/r0); M, m = last Gaussian and last mid-range
+ * Gaussian; Ix,Iy = mid grid in x,y; Iz = interior z count (h_z = Lz/Iz);
+ * Izs = extended z grid I_z^* (P:580); P, S = window support (odd) and shape;
+ * Ilx, Ily = long grid; Pl, Sl = long window; Pc = Chebyshev proxy layers.
+ */
+typedef struct {
+    double rc_factor;
+    double eta;
+    int explicit_params;
+    int row;
+    double rc;
+    int M, m;
+    int Ix, Iy, Iz, Izs, P;
+    double S;
+    int Ilx, Ily, Pl;
+    double Sl;
+    int Pc;
+    void* cuda_stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream */
+    unsigned flags;         /* SOG_NO_VALIDATE ... */
+} sog_plan_opts;
+
+/* Build a plan for N particles in the box (Lx,Ly,Lz) at tolerance tol on the current
+ * CUDA device.  Chooses parameters (R1-R9), precomputes tables (SOG weights, near-kernel
+ * polynomial table, window/deconvolution tables, long-range kernel matrices K_ab),
+ * allocates workspace and cuFFT plans.  Returns NULL on error (see sog_last_error). */
+sog_plan* sog_plan_create(int64_t N, double Lx, double Ly, double Lz, double tol);
+sog_plan* sog_plan_create_ex(int64_t N, double Lx, double Ly, double Lz, double tol,
+                             const sog_plan_opts* opts);
+
+/* Run only the parameter rules R1-R9 (no device work, no GPU needed) and write the
+ * key=value description of the plan sog_plan_create_ex would build into buf (same format
+ * as sog_plan_describe).  Returns the number of bytes needed, or a negative sog_status. */
+int sog_plan_choose(int64_t N, double Lx, double Ly, double Lz, double tol, const sog_plan_opts* opts,
+                    char* buf, size_t len);
+
+/* Evaluate potentials and forces.  xyz, q: device inputs (caller order, see layouts);
+ * phi, force: device outputs (either may be NULL to skip).  Enqueued on the plan's stream;
+ * unless SOG_NO_VALIDATE is set, synchronises once to read the validation flags and
+ * returns SOG_EZRANGE / SOG_ENONFINITE / SOG_ENONNEUTRAL on invalid input. */
+int sog_eval(sog_plan* p, const double* xyz, const double* q, double* phi, double* force);
+
+/* Same as sog_eval with HOST buffers: copies inputs host->device, evaluates, copies
+ * results back, and returns after the results are in host memory. */
+int sog_eval_host(sog_plan* p, const double* xyz, const double* q, double* phi, double* force);
+
+/* Per-component outputs for parity testing: out is a DEVICE buffer of 3*N*4 doubles laid
+ * out [component][i][4] with component 0 = near (Phi^N, grad Phi^N), 1 = mid, 2 = long,
+ * and the 4 values (phi, dphi/dx, dphi/dy, dphi/dz), caller order, self term NOT removed. */
+int sog_eval_components(sog_plan* p, const double* xyz, const double* q, double* out);
+
+/* Intermediate grids for stage parity (device buffer `out` of `len` doubles):
+ *   stage 1: mid spread grid S        [Ix][Iy][Izs]            (Alg. 1 step 1)
+ *   stage 2: mid scaled field Psi     [Ix][Iy][Izs]            (Alg. 1 step 4)
+ *   stage 3: long proxy grids S_b     [Pc][Ilx][Ily]           (Alg. 2 step 1)
+ *   stage 4: long scaled fields Psi_a [Pc][Ilx][Ily]           (Alg. 2 step 4) */
+int sog_debug_stage(sog_plan* p, int stage, const double* xyz, const double* q, double* out, size_t len);
+
+/* Potential energy U = 1/2 sum q_i phi_i of the last sog_eval; host scalar. */
+int sog_last_energy(sog_plan* p, double* U);
+
+void sog_plan_destroy(sog_plan* p); /* NULL-safe */
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+const char* sog_last_error(void);
+
+/* key=value lines describing the chosen plan (parameters, grid sizes, memory).
+ * Returns the number of bytes needed (excluding NUL); writes at most len bytes. */
+int sog_plan_describe(const sog_plan* p, char* buf, size_t len);
+
+/* Per-stage device times (ms) of the last sog_eval with SOG_TIMING set via sog_set_flags:
+ * [0] sort, [1] near, [2] mid spread, [3] mid FFT fwd, [4] mid scale, [5] mid FFT inv,
+ * [6] mid gather, [7] long spread, [8] long FFT+scale+IFFT, [9] long gather, [10] combine.
+ * Returns the number of entries written (<= n). */
+#define SOG_TIMING 2u
+int sog_get_timings(const sog_plan* p, double* ms, int n);
+
+int sog_set_flags(sog_plan* p, unsigned flags);
+int sog_set_stream(sog_plan* p, void* cuda_stream);
+
+/* Number of kernel launches sog_eval enqueues (for the bench's gpu_launches). */
+int sog_launches_per_eval(const sog_plan* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOG_H */

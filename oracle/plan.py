@@ -33,6 +33,7 @@ KAPPA = 1.15         # R5/R8: Nyquist safety, h <= pi s /(2 KAPPA sqrt(ln 1/tol)
 WIN_C = 0.3          # R6: window error target eps_w = WIN_C * tol
 PAD_C = 10.0         # R7: z padding  s_m * sqrt(ln(PAD_C/tol))
 CHEB_C = 0.1         # R9: Chebyshev two-variable interpolation target CHEB_C * tol
+CHEB_FLOOR = 5e-14   # R9: rounding floor of the interpolation test
 FFT_COST = 43.0      # R6: cost of one FFT grid point in units of one stencil point (B200 model)
 LONG_FFT_COST = 43.0
 TOL_MIN = 2e-14      # Table 1 force floor 1.98e-14
@@ -274,7 +275,7 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     p.Pl, p.Sl = Pl, Sl
     p.Ilx = max(friendly_even(math.ceil(Lx / hl)), friendly_even(Pl))
     p.Ily = max(friendly_even(math.ceil(Ly / hl)), friendly_even(Pl))
-    p.Pc = choose_cheb(Lz, sl, CHEB_C * tol)                         # R9
+    p.Pc = choose_cheb(Lz, sl, max(CHEB_C * tol, CHEB_FLOOR))        # R9
     for k, v in over.items():
         if not hasattr(p, k):
             raise KeyError(k)

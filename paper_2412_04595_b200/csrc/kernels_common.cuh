@@ -1,0 +1,61 @@
+// Device-side helpers shared by the SOG kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sog {
+
+struct __align__(32) d4 {
+    double x, y, z, w;
+};
+
+__device__ __forceinline__ d4 ld_d4(const d4* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = __ldg(q), b = __ldg(q + 1);
+    return d4{a.x, a.y, b.x, b.y};
+}
+__device__ __forceinline__ void st_d4(d4* p, d4 v) {
+    double2* q = reinterpret_cast<double2*>(p);
+    q[0] = make_double2(v.x, v.y);
+    q[1] = make_double2(v.z, v.w);
+}
+
+// Validation flag bits written by k_prepare.
+enum : unsigned { FLAG_NONFINITE = 1u, FLAG_ZRANGE = 2u };
+
+// Geometry of the near-field cell grid (cells >= r_c; x,y periodic; z clamped).
+struct CellGeo {
+    double Lx, Ly, Lz;
+    double invLx, invLy;
+    int ncx, ncy, ncz;
+    double sx, sy, sz;      // cells per unit length (nc / L)
+};
+
+// One axis of a window stencil on a uniform grid x_g = (g - I/2) h (R6):
+// nearest grid point g0 = floor(x/h + I/2 + 1/2) computed with explicitly rounded
+// operations (no FMA contraction) so the integer decision matches the oracle bit for bit.
+__device__ __forceinline__ int stencil_g0(double x, double h, double half_plus) {
+    return (int)floor(__dadd_rn(__ddiv_rn(x, h), half_plus));
+}
+
+// Window weights W(x_g - x) = exp(-S ((x_g - x)/H)^2) at the P points g0-p..g0+p, and
+// dW/dx_particle = 2 S (x_g - x)/H^2 W (R11).  invH2S = S / H^2.
+template <int P, bool GRAD>
+__device__ __forceinline__ void window_weights(double x, int g0, double h, double halfI,
+                                               double invH2S, double* W, double* dW) {
+    constexpr int p = (P - 1) / 2;
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+        double d = ((double)(g0 - p + a) - halfI) * h - x;
+        double e = exp(-invH2S * d * d);
+        W[a] = e;
+        if (GRAD) dW[a] = 2.0 * invH2S * d * e;
+    }
+}
+
+__device__ __forceinline__ int wrap(int g, int I) {
+    g %= I;
+    return g < 0 ? g + I : g;
+}
+
+}  // namespace sog

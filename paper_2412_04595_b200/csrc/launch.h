@@ -1,0 +1,15 @@
+// Host launchers for the templated stencil kernels (one translation unit per family so the
+// instantiations compile in parallel).  Return 0 on success, 1 for an unsupported template
+// parameter, 2 for a CUDA launch error (query cudaGetLastError()).
+#pragma once
+#include <cuda_runtime.h>
+#include "kernels_common.cuh"
+
+namespace sog {
+struct MidArgs;
+struct LongArgs;
+int launch_mid_spread(const MidArgs& a, int P, double* grid, cudaStream_t st);
+int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, cudaStream_t st);
+int launch_long_spread(const LongArgs& a, int Pl, double* grid, cudaStream_t st);
+int launch_long_gather(const LongArgs& a, int Pl, const double* psi, d4* out, cudaStream_t st);
+}  // namespace sog

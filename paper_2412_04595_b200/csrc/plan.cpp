@@ -1,0 +1,384 @@
+// Host-side plan construction: parameter rules R1-R9 and precomputed tables.
+// Independent of the CPU oracle (oracle/plan.py); tests/test_plan_parity.py compares them.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+
+#include "sog_internal.h"
+
+namespace sog {
+
+namespace {
+
+// Table 1: b, r0, omega, force error.
+struct Row { double b, r0, omega, ferr; };
+const Row kTable1[6] = {
+    {2.0, 1.9892536839080267, 0.9944464927622323, 9.93e-3},
+    {1.62976708826776469, 2.7520026668023417, 1.0078069793438068, 6.21e-4},
+    {1.48783512395703226, 3.7554672283554990, 0.9919117057598183, 7.98e-5},
+    {1.32070036405934420, 4.3914554711638349, 1.0018891411481198, 5.76e-7},
+    {1.21812525709410644, 5.6355288151271085, 1.0009014615603334, 5.14e-10},
+    {1.14878150173321925, 7.2956245490719404, 1.0000368348358225, 1.98e-14},
+};
+constexpr double kTolMin = 2e-14, kTolMax = 1e-1;
+constexpr double kPi = 3.14159265358979323846;
+
+bool smooth7(long n) {
+    for (long f : {2L, 3L, 5L, 7L})
+        while (n % f == 0) n /= f;
+    return n == 1;
+}
+// smallest even n' >= n with prime factors in {2,3,5,7} (cuFFT-friendly sizes)
+long friendly_even(long n) {
+    if (n < 2) n = 2;
+    if (n & 1) ++n;
+    while (!smooth7(n)) n += 2;
+    return n;
+}
+
+// Largest h keeping the Thm 4.2 aliasing term exp(-pi^2 mu (P-1)^2/(4 s^2 S)) <= eps,
+// mu = s^2 - H^2/S, H = (P-1) h / 2.  0 if infeasible.
+double h_alias(int P, double S, double eps, double s) {
+    double a = P - 1.0;
+    double rhs = 1.0 - 4.0 * S * std::log(1.0 / eps) / (kPi * kPi * a * a);
+    if (rhs <= 0.0) return 0.0;
+    return 2.0 * s * std::sqrt(S) / a * std::sqrt(rhs);
+}
+
+template <class Cost>
+bool choose_window(double s, double eps_w, double tol, double kappa, Cost cost, int& Pout,
+                   double& Sout, double& hout) {
+    double S = erfcinv_host(eps_w);
+    S = S * S;
+    double h_nyq = kPi * s / (2.0 * kappa * std::sqrt(std::log(1.0 / tol)));
+    bool found = false;
+    double best = 0;
+    for (int P = 3; P < 61; P += 2) {
+        double ha = h_alias(P, S, eps_w, s);
+        if (ha <= 0.0) continue;
+        double h = std::min(h_nyq, ha);
+        double c = cost(P, h);
+        if (!found || c < best) { best = c; Pout = P; hout = h; found = true; }
+    }
+    Sout = S;
+    return found;
+}
+
+// Chebyshev T_n(x), n < P
+void cheb_T(double x, int P, double* T) {
+    T[0] = 1.0;
+    if (P > 1) T[1] = x;
+    for (int n = 1; n + 1 < P; ++n) T[n + 1] = 2.0 * x * T[n] - T[n - 1];
+}
+
+// Lagrange basis at first-kind Chebyshev nodes via discrete orthogonality:
+// L_a(x) = (1/P) [1 + 2 sum_{n>=1} T_n(x_a) T_n(x)]   (App. A.2)
+void lagrange(double x, int P, const std::vector<double>& Tnodes, double* L) {
+    std::vector<double> T(P);
+    cheb_T(x, P, T.data());
+    for (int a = 0; a < P; ++a) {
+        double acc = 0.0;
+        for (int n = 1; n < P; ++n) acc += Tnodes[a * P + n] * T[n];
+        L[a] = (1.0 + 2.0 * acc) / P;
+    }
+}
+
+std::vector<double> node_T(int P) {
+    std::vector<double> Tn(P * P);
+    for (int a = 0; a < P; ++a) {
+        double xa = std::cos((a + 0.5) * kPi / P);
+        cheb_T(xa, P, &Tn[a * P]);
+    }
+    return Tn;
+}
+
+// R9: max error of sum_ab L_a(z) g(z_a - z_b) L_b(z'), g(d) = exp(-d^2/s^2), 65x65 test grid
+double cheb_two_sided_error(int P, double Lz, double s) {
+    const int nt = 65;
+    std::vector<double> Tn = node_T(P), za(P), G(P * P), Lt(nt * P);
+    for (int a = 0; a < P; ++a) za[a] = 0.5 * Lz * std::cos((a + 0.5) * kPi / P);
+    for (int a = 0; a < P; ++a)
+        for (int b = 0; b < P; ++b) {
+            double d = (za[a] - za[b]) / s;
+            G[a * P + b] = std::exp(-d * d);
+        }
+    for (int i = 0; i < nt; ++i) lagrange(-1.0 + 2.0 * i / (nt - 1), P, Tn, &Lt[i * P]);
+    std::vector<double> LG(nt * P, 0.0);
+    for (int i = 0; i < nt; ++i)
+        for (int b = 0; b < P; ++b) {
+            double acc = 0;
+            for (int a = 0; a < P; ++a) acc += Lt[i * P + a] * G[a * P + b];
+            LG[i * P + b] = acc;
+        }
+    double err = 0;
+    for (int i = 0; i < nt; ++i)
+        for (int j = 0; j < nt; ++j) {
+            double acc = 0;
+            for (int b = 0; b < P; ++b) acc += LG[i * P + b] * Lt[j * P + b];
+            double zi = 0.5 * Lz * (-1.0 + 2.0 * i / (nt - 1));
+            double zj = 0.5 * Lz * (-1.0 + 2.0 * j / (nt - 1));
+            double d = (zi - zj) / s;
+            err = std::max(err, std::fabs(acc - std::exp(-d * d)));
+        }
+    return err;
+}
+
+}  // namespace
+
+// erfc^{-1}(y) for y in (0, 1]: Newton on erfc from an asymptotic start.
+double erfcinv_host(double y) {
+    if (y >= 1.0) return 0.0;
+    double t = std::sqrt(-std::log(y));
+    double x = t - (std::log(t) + 0.5 * std::log(kPi)) / (2.0 * t);   // asymptotic start
+    if (!(x > 0)) x = 0.5;
+    for (int it = 0; it < 100; ++it) {
+        double f = std::erfc(x) - y;
+        double df = -2.0 / std::sqrt(kPi) * std::exp(-x * x);
+        double dx = f / df;
+        x -= dx;
+        if (std::fabs(dx) < 1e-17 * std::fabs(x)) break;
+    }
+    return x;
+}
+
+void sog_weights(const Params& p, std::vector<double>& w, std::vector<double>& s) {
+    // w_l = (pi/2)^{-1/2} b^{-l} sigma^{-1} log b, s_l = sqrt(2) b^l sigma; omega on w_0
+    w.resize(p.M + 1);
+    s.resize(p.M + 1);
+    const double c = std::pow(kPi / 2.0, -0.5) * std::log(p.b) / p.sigma;
+    for (int l = 0; l <= p.M; ++l) {
+        w[l] = c * std::pow(p.b, -double(l));
+        s[l] = std::sqrt(2.0) * std::pow(p.b, double(l)) * p.sigma;
+    }
+    w[0] *= p.omega;
+}
+
+bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
+    if (!(p.tol >= kTolMin && p.tol <= kTolMax)) { err = "tol outside [2e-14, 1e-1]"; return false; }
+    // R1: coarsest Table-1 row whose force error <= tol
+    int row = -1;
+    for (int r = 0; r < 6; ++r) if (kTable1[r].ferr <= p.tol) { row = r; break; }
+    if (row < 0) { err = "infeasible tolerance"; return false; }
+    p.row = row;
+    p.b = kTable1[row].b; p.r0 = kTable1[row].r0; p.omega = kTable1[row].omega;
+    // R2
+    const double rho = double(p.N) / (p.Lx * p.Ly * p.Lz);
+    p.rc = std::min(k.rc_factor * std::pow(rho, -1.0 / 3.0), 0.5 * std::min(p.Lx, p.Ly));
+    p.sigma = p.rc / p.r0;
+    const double s0 = std::sqrt(2.0) * p.sigma;
+    const double Lmax = std::max(p.Lx, std::max(p.Ly, p.Lz));
+    // R3: smallest M with s_M >= Lmax / tol
+    const double target = Lmax / p.tol;
+    int M = std::max(0, int(std::ceil(std::log(target / s0) / std::log(p.b))));
+    while (s0 * std::pow(p.b, M) < target) ++M;
+    while (M > 0 && s0 * std::pow(p.b, M - 1) >= target) --M;
+    p.M = M;
+    // R4: m = max{l : s_l <= eta Lz}
+    int m = -1;
+    for (int l = 0; l <= M; ++l) if (s0 * std::pow(p.b, l) <= k.eta * p.Lz) m = l;
+    p.m = std::min(m, M - 1);
+    const double eps_w = k.win_c * p.tol;
+    const double N = double(p.N);
+    if (p.m >= 0) {
+        const double sm = s0 * std::pow(p.b, p.m);
+        const double padimg = sm * std::sqrt(std::log(k.pad_c / p.tol));
+        auto cost_mid = [&](int P, double h) {
+            double pad = std::max(2.0 * ((P - 1) * h / 2.0 + h), padimg);
+            return double(P) * P * P + k.fft_cost * (p.Lx * p.Ly * (p.Lz + pad)) / (N * h * h * h);
+        };
+        double h;
+        if (!choose_window(s0, eps_w, p.tol, k.kappa, cost_mid, p.P, p.S, h)) { err = "no mid window"; return false; }
+        p.Ix = friendly_even(long(std::ceil(p.Lx / h)));
+        p.Iy = friendly_even(long(std::ceil(p.Ly / h)));
+        p.Iz = std::max(1L, long(std::ceil(p.Lz / h)));
+        const double hz = p.hz();
+        const double Hz = (p.P - 1) * hz / 2.0;
+        const double pad = std::max(2.0 * (Hz + hz), padimg);          // R7
+        p.Izs = friendly_even(long(std::ceil((p.Lz + pad) / hz)));
+    }
+    const double sl = s0 * std::pow(p.b, p.m + 1);
+    auto cost_long = [&](int P, double h) {
+        return double(P) * P + k.long_fft_cost * (p.Lx * p.Ly) / (N * h * h);
+    };
+    double hl;
+    if (!choose_window(sl, eps_w, p.tol, k.kappa, cost_long, p.Pl, p.Sl, hl)) { err = "no long window"; return false; }
+    p.Ilx = std::max(friendly_even(long(std::ceil(p.Lx / hl))), friendly_even(p.Pl));
+    p.Ily = std::max(friendly_even(long(std::ceil(p.Ly / hl))), friendly_even(p.Pl));
+    // R9
+    p.Pc = 0;
+    for (int P = 2; P < 65; ++P)
+        if (cheb_two_sided_error(P, p.Lz, sl) <= std::max(k.cheb_c * p.tol, 5e-14)) { p.Pc = P; break; }
+    if (!p.Pc) { err = "Chebyshev order > 64 needed"; return false; }
+    return true;
+}
+
+bool validate_params(const Params& p, std::string& err) {
+    auto bad = [&](const char* m) { err = m; return false; };
+    if (p.N < 1 || p.N > (int64_t(1) << 31) - 1) return bad("N out of range [1, 2^31)");
+    if (!(p.Lx > 0 && p.Ly > 0 && p.Lz > 0) || !std::isfinite(p.Lx + p.Ly + p.Lz)) return bad("invalid box");
+    if (p.row < 0 || p.row > 5) return bad("row must be 0..5");
+    if (!(p.rc > 0) || p.rc > 0.5 * std::min(p.Lx, p.Ly) * (1 + 1e-15)) return bad("r_c must be in (0, min(Lx,Ly)/2]");
+    if (p.M < 1 || p.M > 4000) return bad("M out of range");
+    if (p.m < -1 || p.m >= p.M) return bad("m must be in [-1, M-1]");
+    if (p.m >= 0) {
+        if (p.Ix < 2 || p.Iy < 2 || p.Iz < 1 || p.Izs < 2 || (p.Izs & 1)) return bad("bad mid grid");
+        if (p.P < 5 || p.P > 27 || !(p.P & 1)) return bad("mid window support must be odd in [5,27]");
+        if (!(p.S > 0)) return bad("bad mid window shape");
+        // R7: the z stencil must not leave the extended grid
+        double hz = p.hz();
+        if (p.Izs * hz < p.Lz + (p.P - 1) * hz + 2.0 * hz * (1 - 1e-12)) return bad("Izs too small for the z stencil (R7)");
+    }
+    if (p.Ilx < 2 || p.Ily < 2 || (p.Ily & 1)) return bad("bad long grid (Ily must be even)");
+    if (p.Pl < 5 || p.Pl > 27 || !(p.Pl & 1)) return bad("long window support must be odd in [5,27]");
+    if (!(p.Sl > 0)) return bad("bad long window shape");
+    if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
+    return true;
+}
+
+bool build_near_table(const Params& p, NearTable& t, std::string& err) {
+    // F(u) = sum_l w_l exp(-u/s_l^2) (Eq. eq::SOGField) as piecewise Taylor polynomials
+    // in u = r^2 on [0, r_c^2]; pieces narrow enough that du/(2 s_0^2) <= 1/4 (R16).
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const double s0sq = s[0] * s[0];
+    const double umax = p.rc * p.rc;
+    t.K = std::max(1, int(std::ceil(2.0 * umax / s0sq)));
+    t.D = 12;
+    t.du = umax / t.K;
+    t.inv_du = t.K / umax;
+    const int D = t.D;
+    t.cF.assign(size_t(t.K) * (D + 1), 0.0);
+    t.cdF.assign(size_t(t.K) * (D + 1), 0.0);
+    std::vector<long double> c(D + 2);
+    for (int k = 0; k < t.K; ++k) {
+        long double uk = (k + 0.5L) * (long double)t.du;
+        for (int n = 0; n <= D + 1; ++n) c[n] = 0.0L;
+        for (int l = 0; l <= p.M; ++l) {
+            long double a = -1.0L / ((long double)s[l] * s[l]);
+            long double term = (long double)w[l] * expl(a * uk);
+            for (int n = 0; n <= D + 1; ++n) {
+                c[n] += term;
+                term *= a / (n + 1);
+            }
+        }
+        for (int n = 0; n <= D; ++n) t.cF[size_t(k) * (D + 1) + n] = double(c[n]);
+        for (int n = 0; n < D; ++n) t.cdF[size_t(k) * (D + 1) + n] = double((n + 1) * c[n + 1]);
+    }
+    // validate against the direct sum on a dense sample
+    double maxrel = 0;
+    for (int i = 0; i <= 4000; ++i) {
+        double u = umax * i / 4000.0;
+        int k = std::min(t.K - 1, int(u * t.inv_du));
+        double d = u - (k + 0.5) * t.du;
+        double F = 0, dF = 0;
+        for (int n = D; n >= 0; --n) F = F * d + t.cF[size_t(k) * (D + 1) + n];
+        for (int n = D - 1; n >= 0; --n) dF = dF * d + t.cdF[size_t(k) * (D + 1) + n];
+        long double Fe = 0, dFe = 0;
+        for (int l = 0; l <= p.M; ++l) {
+            long double e = (long double)w[l] * expl(-(long double)u / ((long double)s[l] * s[l]));
+            Fe += e;
+            dFe += -e / ((long double)s[l] * s[l]);
+        }
+        maxrel = std::max(maxrel, double(std::fabs((long double)F - Fe) / Fe));
+        maxrel = std::max(maxrel, double(std::fabs((long double)dF - dFe) / std::fabs(dFe)));
+    }
+    t.max_rel_err = maxrel;
+    if (maxrel > 1e-14) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "near table validation failed: rel err %.3e", maxrel);
+        err = buf;
+        return false;
+    }
+    return true;
+}
+
+void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<double>& Tx,
+                      std::vector<double>& Ty, std::vector<double>& Tz) {
+    // mult(k) = pi^{3/2} sum_{l<=m} w_l s_l^3 exp(-s_l^2 |k|^2/4) / (W_x W_y W_z)^2 with
+    // W_hat(k) = sqrt(pi/S) H exp(-k^2 H^2/(4S)), k_d = 2 pi n / L_d (L_z -> L_z^*).
+    // Per axis and per l:  T[l][i] = (S / (pi H^2)) exp(-k^2 (s_l^2/4 - H^2/(2S)))  (one exp:
+    // no overflow of the separate Gaussian / deconvolution factors).
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const int L = p.m + 1;
+    A.resize(L);
+    for (int l = 0; l < L; ++l) A[l] = std::pow(kPi, 1.5) * w[l] * s[l] * s[l] * s[l];
+    auto axis = [&](int I, double Lper, double h, bool half, std::vector<double>& T) {
+        int n = half ? I / 2 + 1 : I;
+        T.resize(size_t(L) * n);
+        double H = (p.P - 1) * h / 2.0;
+        for (int l = 0; l < L; ++l)
+            for (int i = 0; i < n; ++i) {
+                int f = (half || i < (I + 1) / 2) ? i : i - I;   // numpy fftfreq ordering
+                double kk = 2.0 * kPi * f / Lper;
+                double e = kk * kk * (s[l] * s[l] / 4.0 - H * H / (2.0 * p.S));
+                T[size_t(l) * n + i] = p.S / (kPi * H * H) * std::exp(-e);
+            }
+    };
+    axis(p.Ix, p.Lx, p.hx(), false, Tx);
+    axis(p.Iy, p.Ly, p.hy(), false, Ty);
+    axis(p.Izs, p.Lzs(), p.hz(), true, Tz);
+}
+
+void build_long_kernel(const Params& p, std::vector<double>& K) {
+    // K_ab(kdot) = pi sum_{l=m+1}^{M} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b) / (W_x W_y)^2,
+    // E_l(d) = exp(-d^2/s_l^2) for kdot != 0 and expm1(-d^2/s_l^2) at kdot = 0 (R10).
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const int P = p.Pc, nx = p.Ilx, ny = p.Ily / 2 + 1;
+    std::vector<double> za(P);
+    for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
+    const double Hx = (p.Pl - 1) * p.hlx() / 2.0, Hy = (p.Pl - 1) * p.hly() / 2.0;
+    K.assign(size_t(nx) * ny * P * P, 0.0);
+    for (int ix = 0; ix < nx; ++ix) {
+        int fx = ix < (nx + 1) / 2 ? ix : ix - nx;
+        double kx = 2.0 * kPi * fx / p.Lx;
+        for (int iy = 0; iy < ny; ++iy) {
+            double ky = 2.0 * kPi * iy / p.Ly;
+            double k2 = kx * kx + ky * ky;
+            // 1 / (W_x W_y)^2
+            double Wx = std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
+            double Wy = std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
+            double dec = kPi / (Wx * Wx * Wy * Wy);
+            double* Km = &K[(size_t(ix) * ny + iy) * P * P];
+            for (int a = 0; a < P; ++a)
+                for (int b = 0; b < P; ++b) {
+                    double d2 = (za[a] - za[b]) * (za[a] - za[b]);
+                    double acc = 0.0;
+                    for (int l = p.m + 1; l <= p.M; ++l) {
+                        double ss = s[l] * s[l];
+                        if (k2 == 0.0) {
+                            acc += w[l] * ss * std::expm1(-d2 / ss);
+                        } else {
+                            double g = ss * k2 / 4.0;
+                            if (g > 745.0) continue;
+                            acc += w[l] * ss * std::exp(-g) * std::exp(-d2 / ss);
+                        }
+                    }
+                    Km[a * P + b] = acc * dec;
+                }
+        }
+    }
+}
+
+void build_cheb_matrix(int Pc, std::vector<double>& C) {
+    std::vector<double> Tn = node_T(Pc);
+    C.resize(size_t(Pc) * Pc);
+    for (int b = 0; b < Pc; ++b)
+        for (int n = 0; n < Pc; ++n) C[b * Pc + n] = (n == 0 ? 1.0 : 2.0 * Tn[b * Pc + n]) / Pc;
+}
+
+std::string describe(const Params& p) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "N=" << p.N << "\nLx=" << p.Lx << "\nLy=" << p.Ly << "\nLz=" << p.Lz << "\ntol=" << p.tol
+      << "\nrow=" << p.row << "\nb=" << p.b << "\nr0=" << p.r0 << "\nomega=" << p.omega
+      << "\nrc=" << p.rc << "\nsigma=" << p.sigma << "\nM=" << p.M << "\nm=" << p.m
+      << "\nIx=" << p.Ix << "\nIy=" << p.Iy << "\nIz=" << p.Iz << "\nIzs=" << p.Izs
+      << "\nP=" << p.P << "\nS=" << p.S << "\nIlx=" << p.Ilx << "\nIly=" << p.Ily
+      << "\nPl=" << p.Pl << "\nSl=" << p.Sl << "\nPc=" << p.Pc << "\n";
+    return o.str();
+}
+
+}  // namespace sog

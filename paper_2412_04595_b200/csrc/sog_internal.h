@@ -1,0 +1,72 @@
+// Internal definitions shared by the host runtime (plan.cpp, sog_api.cu) and kernels.
+// Nothing here is visible through the C ABI (include/sog.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sog {
+
+// Plan parameters (rules R1-R9).  Names follow PAPER.md notation.
+struct Params {
+    int64_t N = 0;
+    double Lx = 0, Ly = 0, Lz = 0, tol = 0;
+    int row = -1;                  // Table 1 row
+    double b = 0, r0 = 0, omega = 0;
+    double rc = 0, sigma = 0;      // r_c, sigma = r_c / r0
+    int M = 0, m = -1;             // last Gaussian, last mid-range Gaussian
+    // mid-range grid / window
+    int Ix = 0, Iy = 0, Iz = 0, Izs = 0, P = 0;
+    double S = 0;
+    // long-range grid / window / proxies
+    int Ilx = 0, Ily = 0, Pl = 0;
+    double Sl = 0;
+    int Pc = 0;
+    // derived
+    double hx() const { return Lx / Ix; }
+    double hy() const { return Ly / Iy; }
+    double hz() const { return Lz / Iz; }
+    double Lzs() const { return hz() * Izs; }
+    double hlx() const { return Lx / Ilx; }
+    double hly() const { return Ly / Ily; }
+};
+
+struct RuleKnobs {
+    double rc_factor = 3.5;   // R2
+    double eta = 0.3;         // R4
+    double kappa = 1.15;      // R5/R8
+    double win_c = 0.3;       // R6
+    double pad_c = 10.0;      // R7
+    double cheb_c = 0.1;      // R9
+    double fft_cost = 43.0;   // R6 cost model (grid point vs stencil point)
+    double long_fft_cost = 43.0;
+};
+
+// plan.cpp
+bool choose_params(Params& p, const RuleKnobs& k, std::string& err);   // rules R1-R9
+bool validate_params(const Params& p, std::string& err);
+void sog_weights(const Params& p, std::vector<double>& w, std::vector<double>& s);
+double erfcinv_host(double y);
+
+// Near-field kernel table: F(u) and dF/du, u = r^2, piecewise Taylor polynomials (R16).
+struct NearTable {
+    int K = 0, D = 0;          // pieces, degree
+    double du = 0, inv_du = 0; // piece width in u
+    std::vector<double> cF;    // K x (D+1)   F coefficients (Horner, highest last)
+    std::vector<double> cdF;   // K x (D+1)   dF/du coefficients (degree D-1, last = 0)
+    double max_rel_err = 0;    // validated at plan time against the direct sum
+};
+bool build_near_table(const Params& p, NearTable& t, std::string& err);
+
+// Mid-range scaling tables: mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz] (R12).
+void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<double>& Tx,
+                      std::vector<double>& Ty, std::vector<double>& Tz);
+// Long-range kernel matrices K[mode][a][b], mode = ix*(Ily/2+1)+iy (R9, R10).
+void build_long_kernel(const Params& p, std::vector<double>& K);
+// Chebyshev -> Lagrange coefficient matrix C[b][n]: L_b(x) = sum_n C[b][n] T_n(x).
+void build_cheb_matrix(int Pc, std::vector<double>& C);
+
+std::string describe(const Params& p);
+
+}  // namespace sog

@@ -1,0 +1,267 @@
+"""ctypes binding of libsog.so (include/sog.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+SOG_NO_VALIDATE = 1
+SOG_TIMING = 2
+STATUS = {0: "SOG_OK", -1: "SOG_EINVAL", -2: "SOG_ENONNEUTRAL", -3: "SOG_EZRANGE",
+          -4: "SOG_ENONFINITE", -5: "SOG_EINFEASIBLE", -6: "SOG_ECUDA", -8: "SOG_ENOMEM"}
+TIMING_NAMES = ["sort", "near", "mid_spread", "mid_fft_fwd", "mid_scale", "mid_fft_inv", "mid_gather",
+                "long_spread", "long_fft_scale_ifft", "long_gather", "combine"]
+EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval", "sog_eval_host", "sog_eval_components",
+           "sog_debug_stage", "sog_last_energy", "sog_plan_destroy", "sog_last_error", "sog_plan_describe",
+           "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval"]
+
+
+class SogError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("rc_factor", ctypes.c_double), ("eta", ctypes.c_double),
+                ("explicit_params", ctypes.c_int), ("row", ctypes.c_int), ("rc", ctypes.c_double),
+                ("M", ctypes.c_int), ("m", ctypes.c_int),
+                ("Ix", ctypes.c_int), ("Iy", ctypes.c_int), ("Iz", ctypes.c_int), ("Izs", ctypes.c_int),
+                ("P", ctypes.c_int), ("S", ctypes.c_double),
+                ("Ilx", ctypes.c_int), ("Ily", ctypes.c_int), ("Pl", ctypes.c_int), ("Sl", ctypes.c_double),
+                ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint)]
+
+
+def lib_path() -> str:
+    return os.path.join(HERE, "lib", "libsog.so")
+
+
+def load_library():
+    """Load the in-tree libsog.so (raises if it has not been built: no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_2412_04595_b200.build` (no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, D, I, U, S = ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_uint, ctypes.c_size_t
+    lib.sog_plan_create.restype = P
+    lib.sog_plan_create.argtypes = [ctypes.c_int64, D, D, D, D]
+    lib.sog_plan_choose.restype = I
+    lib.sog_plan_choose.argtypes = [ctypes.c_int64, D, D, D, D, ctypes.POINTER(Opts), ctypes.c_char_p, S]
+    lib.sog_plan_create_ex.restype = P
+    lib.sog_plan_create_ex.argtypes = [ctypes.c_int64, D, D, D, D, ctypes.POINTER(Opts)]
+    for name in ("sog_eval", "sog_eval_host"):
+        getattr(lib, name).restype = I
+        getattr(lib, name).argtypes = [P, P, P, P, P]
+    lib.sog_eval_components.restype = I
+    lib.sog_eval_components.argtypes = [P, P, P, P]
+    lib.sog_debug_stage.restype = I
+    lib.sog_debug_stage.argtypes = [P, I, P, P, P, S]
+    lib.sog_last_energy.restype = I
+    lib.sog_last_energy.argtypes = [P, ctypes.POINTER(D)]
+    lib.sog_plan_destroy.restype = None
+    lib.sog_plan_destroy.argtypes = [P]
+    lib.sog_last_error.restype = ctypes.c_char_p
+    lib.sog_last_error.argtypes = []
+    lib.sog_plan_describe.restype = I
+    lib.sog_plan_describe.argtypes = [P, ctypes.c_char_p, S]
+    lib.sog_get_timings.restype = I
+    lib.sog_get_timings.argtypes = [P, ctypes.POINTER(D), I]
+    lib.sog_set_flags.restype = I
+    lib.sog_set_flags.argtypes = [P, U]
+    lib.sog_set_stream.restype = I
+    lib.sog_set_stream.argtypes = [P, P]
+    lib.sog_launches_per_eval.restype = I
+    lib.sog_launches_per_eval.argtypes = [P]
+    _LIB = lib
+    return lib
+
+
+def _err(lib, code):
+    return SogError(code, lib.sog_last_error().decode())
+
+
+PLAN_FIELDS = ("row", "rc", "M", "m", "Ix", "Iy", "Iz", "Izs", "P", "S", "Ilx", "Ily", "Pl", "Sl", "Pc")
+
+
+class Plan:
+    """A solver plan for N charges in the box L = (Lx, Ly, Lz) at tolerance tol.
+
+    params: optional dict with every PLAN_FIELDS entry -> used verbatim (explicit plan);
+    rc_factor / eta: overrides of rules R2 / R4;  stream: torch.cuda.Stream or raw handle.
+    """
+
+    def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
+                 validate=True, timing=False):
+        self.lib = load_library()
+        self.N = int(N)
+        self.L = tuple(float(v) for v in L)
+        self.tol = float(tol)
+        o = Opts()
+        o.rc_factor = float(rc_factor or 0.0)
+        o.eta = float(eta or 0.0)
+        if params is not None:
+            o.explicit_params = 1
+            for k in PLAN_FIELDS:
+                setattr(o, k, type(getattr(o, k))(params[k]))
+        o.flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
+        o.cuda_stream = _stream_handle(stream)
+        h = self.lib.sog_plan_create_ex(self.N, *self.L, self.tol, ctypes.byref(o))
+        if not h:
+            raise SogError(-1, self.lib.sog_last_error().decode())
+        self.h = h
+        self._flags = o.flags
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sog_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- configuration
+    def describe(self) -> dict:
+        n = self.lib.sog_plan_describe(self.h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        self.lib.sog_plan_describe(self.h, buf, n + 1)
+        return _parse(buf.value.decode())
+
+    def set_flags(self, validate=True, timing=False):
+        self._flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
+        self._check(self.lib.sog_set_flags(self.h, self._flags))
+
+    def set_stream(self, stream):
+        self._check(self.lib.sog_set_stream(self.h, _stream_handle(stream)))
+
+    def launches_per_eval(self) -> int:
+        return self.lib.sog_launches_per_eval(self.h)
+
+    def timings(self) -> dict:
+        arr = (ctypes.c_double * 11)()
+        n = self.lib.sog_get_timings(self.h, arr, 11)
+        return {TIMING_NAMES[i]: arr[i] for i in range(n)}
+
+    def energy(self) -> float:
+        u = ctypes.c_double()
+        self._check(self.lib.sog_last_energy(self.h, ctypes.byref(u)))
+        return u.value
+
+    def _check(self, rc):
+        if rc != 0:
+            raise _err(self.lib, rc)
+
+    # -- evaluation (device tensors)
+    def _inputs(self, xyz, q):
+        import torch
+        if not (xyz.is_cuda and q.is_cuda):
+            raise ValueError("xyz and q must be CUDA tensors (use eval_host for host arrays)")
+        if xyz.dtype != torch.float64 or q.dtype != torch.float64:
+            raise ValueError("xyz and q must be float64")
+        if tuple(xyz.shape) != (self.N, 3) or tuple(q.shape) != (self.N,):
+            raise ValueError(f"expected xyz [{self.N},3] and q [{self.N}]")
+        return xyz.contiguous(), q.contiguous()
+
+    def eval(self, xyz, q, phi=None, force=None, want_force=True):
+        """phi [N], force [N,3] (float64 CUDA tensors) for device inputs."""
+        import torch
+        xyz, q = self._inputs(xyz, q)
+        if phi is None:
+            phi = torch.empty(self.N, dtype=torch.float64, device=xyz.device)
+        if force is None and want_force:
+            force = torch.empty(self.N, 3, dtype=torch.float64, device=xyz.device)
+        self._check(self.lib.sog_eval(self.h, xyz.data_ptr(), q.data_ptr(), phi.data_ptr(),
+                                      force.data_ptr() if force is not None else None))
+        return phi, force
+
+    def eval_host(self, xyz, q, phi=None, force=None):
+        """Host-buffer path (sog_eval_host): numpy or (pinned) CPU torch arrays in, host arrays out."""
+        import numpy as np
+        xyz_p, q_p, keep = _host_ptr(xyz), _host_ptr(q), []
+        if phi is None:
+            phi = np.empty(self.N, dtype=np.float64)
+        if force is None:
+            force = np.empty((self.N, 3), dtype=np.float64)
+        self._check(self.lib.sog_eval_host(self.h, xyz_p, q_p, _host_ptr(phi), _host_ptr(force)))
+        return phi, force
+
+    def components(self, xyz, q):
+        """[3, N, 4] tensor: near / mid / long (phi, dphi/dx, dphi/dy, dphi/dz), self term not removed."""
+        import torch
+        xyz, q = self._inputs(xyz, q)
+        out = torch.empty(3, self.N, 4, dtype=torch.float64, device=xyz.device)
+        self._check(self.lib.sog_eval_components(self.h, xyz.data_ptr(), q.data_ptr(), out.data_ptr()))
+        return out
+
+    def debug_stage(self, stage, xyz, q):
+        """Intermediate grid (1: mid spread, 2: mid Psi, 3: long proxies, 4: long Psi)."""
+        import torch
+        d = self.describe()
+        if stage in (1, 2):
+            shape = (d["Ix"], d["Iy"], d["Izs"])
+        else:
+            shape = (d["Pc"], d["Ilx"], d["Ily"])
+        xyz, q = self._inputs(xyz, q)
+        out = torch.empty(shape, dtype=torch.float64, device=xyz.device)
+        self._check(self.lib.sog_debug_stage(self.h, stage, xyz.data_ptr(), q.data_ptr(), out.data_ptr(),
+                                             out.numel()))
+        return out
+
+
+def _parse(text):
+    out = {}
+    for line in text.splitlines():
+        k, v = line.split("=", 1)
+        try:
+            out[k] = int(v)
+        except ValueError:
+            out[k] = float(v)
+    return out
+
+
+def choose_params(N, L, tol, rc_factor=None, eta=None) -> dict:
+    """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU)."""
+    lib = load_library()
+    o = Opts()
+    o.rc_factor = float(rc_factor or 0.0)
+    o.eta = float(eta or 0.0)
+    n = lib.sog_plan_choose(int(N), *[float(v) for v in L], float(tol), ctypes.byref(o), None, 0)
+    if n < 0:
+        raise _err(lib, n)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.sog_plan_choose(int(N), *[float(v) for v in L], float(tol), ctypes.byref(o), buf, n + 1)
+    return _parse(buf.value.decode())
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return getattr(stream, "cuda_stream", None)
+
+
+def _host_ptr(a):
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ValueError("host arrays must be C-contiguous float64")
+        return a.ctypes.data
+    # torch CPU tensor
+    if a.is_cuda or not a.is_contiguous():
+        raise ValueError("host tensors must be contiguous CPU tensors")
+    return a.data_ptr()

@@ -1,0 +1,80 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/sog.h
+declares, and its host-side plan rules (sog_plan_choose) agree with the oracle's."""
+import ctypes
+import dataclasses
+import os
+import re
+
+import pytest
+
+from paper_2412_04595_b200 import sog as B
+from oracle.plan import make_plan
+from synth import CONFIGS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "sog.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sog_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = B.load_library()
+    names = header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(B.EXPORTS)
+
+
+def test_nm_exports_are_c_symbols():
+    out = os.popen(f"nm -D --defined-only {B.lib_path()}").read()
+    for n in header_functions():
+        assert re.search(rf"\bT {n}$", out, flags=re.M), n
+
+
+CASES = [(c.name, c.N, c.L, t) for c in CONFIGS.values()
+         for t in ((1e-4, 1e-6, 1e-8, 1e-12) if c.name == "c2" else (c.tol,))]
+CASES += [("tiny", 2, (20.0, 20.0, 20.0), 1e-6), ("confined", 5000, (60.0, 60.0, 0.5), 1e-6),
+          ("tall", 3000, (6.0, 7.0, 90.0), 1e-4), ("dense", 100000, (10.0, 10.0, 10.0), 1e-8)]
+
+
+@pytest.mark.parametrize("name,N,L,tol", CASES)
+def test_plan_rules_match_oracle(name, N, L, tol):
+    lib_p = B.choose_params(N, L, tol)
+    ora = dataclasses.asdict(make_plan(N, *L, tol))
+    for k, v in ora.items():
+        if isinstance(v, int):
+            assert lib_p[k] == v, (k, lib_p[k], v)
+        else:
+            assert abs(lib_p[k] - v) <= 1e-13 * abs(v), (k, lib_p[k], v)
+
+
+def test_plan_choose_errors():
+    lib = B.load_library()
+    o = B.Opts()
+    assert lib.sog_plan_choose(100, 10.0, 10.0, 10.0, 1e-15, ctypes.byref(o), None, 0) == -5
+    assert lib.sog_plan_choose(0, 10.0, 10.0, 10.0, 1e-6, ctypes.byref(o), None, 0) == -1
+    assert lib.sog_plan_choose(100, -1.0, 10.0, 10.0, 1e-6, ctypes.byref(o), None, 0) == -1
+    assert b"tol" in lib.sog_last_error() or b"box" in lib.sog_last_error()
+    # explicit parameters are validated: r_c beyond min(Lx,Ly)/2 is rejected
+    p = dataclasses.asdict(make_plan(1000, 10.0, 10.0, 10.0, 1e-6))
+    o.explicit_params = 1
+    for k in B.PLAN_FIELDS:
+        if k == "row":
+            continue
+        setattr(o, k, type(getattr(o, k))(p[k]))
+    o.row = 3
+    assert lib.sog_plan_choose(1000, 10.0, 10.0, 10.0, 1e-6, ctypes.byref(o), None, 0) > 0
+    o.rc = 6.0
+    assert lib.sog_plan_choose(1000, 10.0, 10.0, 10.0, 1e-6, ctypes.byref(o), None, 0) == -1
+    o.rc = p["rc"]
+    o.Izs = 10
+    assert lib.sog_plan_choose(1000, 10.0, 10.0, 10.0, 1e-6, ctypes.byref(o), None, 0) == -1
+
+
+def test_table1_row_selection():
+    for tol, row in ((1e-2, 0), (1e-3, 1), (1e-4, 2), (1e-6, 3), (1e-8, 4), (1e-12, 5), (2e-14, 5)):
+        assert B.choose_params(1000, (10.0, 10.0, 10.0), tol)["row"] == row

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): relative L2 error of potentials and forces <= 1e-12 vs the
+oracle in fp64.  Plans are chosen by the ORACLE and passed to the library verbatim
+(explicit parameters), so both sides run the same discrete scheme.
+"""
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import sog as O
+from oracle.plan import make_plan
+from synth import config_system, uniform_system
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP64 = 1e-12
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def gpu_plan(op, **kw):
+    from paper_2412_04595_b200 import Plan
+    d = dataclasses.asdict(op)
+    d["row"] = [r[0] for r in __import__("oracle.plan", fromlist=["TABLE1"]).TABLE1].index(op.b)
+    return Plan(op.N, (op.Lx, op.Ly, op.Lz), op.tol, params=d, **kw)
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def to_dev(xyz, q):
+    return (torch.from_numpy(np.ascontiguousarray(xyz)).cuda(), torch.from_numpy(np.ascontiguousarray(q)).cuda())
+
+
+def run_gpu(op, xyz, q):
+    pl = gpu_plan(op)
+    x, qq = to_dev(xyz, q)
+    phi, F = pl.eval(x, qq)
+    comp = pl.components(x, qq)
+    torch.cuda.synchronize()
+    out = phi.cpu().numpy(), F.cpu().numpy(), comp.cpu().numpy()
+    pl.close()
+    return out
+
+
+def check_total(op, xyz, q, bar=TOL_FP64):
+    phi_o, F_o, parts = O.evaluate(op, xyz, q, parts=True)
+    phi_g, F_g, comp = run_gpu(op, xyz, q)
+    assert rel(phi_g, phi_o) <= bar, rel(phi_g, phi_o)
+    assert rel(F_g, F_o) <= bar, rel(F_g, F_o)
+    for c, name in enumerate(("near", "mid", "long")):
+        po, go = parts[name]
+        if np.linalg.norm(po) == 0:
+            assert np.all(comp[c] == 0)
+            continue
+        assert rel(comp[c][:, 0], po) <= bar, (name, rel(comp[c][:, 0], po))
+        assert rel(comp[c][:, 1:], go) <= bar, (name, rel(comp[c][:, 1:], go))
+    return phi_g, F_g
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def test_c1_components_and_total():
+    """BASELINE config c1 (N=1000, 10^3, tol 1e-6) at full size, element by element."""
+    xyz, q, L = config_system("c1")
+    op = make_plan(len(q), *L, 1e-6)
+    check_total(op, xyz, q)
+
+
+def test_c1_stages():
+    """Intermediate grids: Alg. 1 step 1 (spread) and step 4 (Psi); Alg. 2 steps 1 and 4."""
+    xyz, q, L = config_system("c1")
+    op = make_plan(len(q), *L, 1e-6)
+    x = O.canonicalize(xyz, op)
+    pl = gpu_plan(op)
+    xd, qd = to_dev(xyz, q)
+    S_o = O.mid_spread(op, x, q)
+    Psi_o = O.mid_solve(op, S_o)
+    Sl_o = O.long_spread(op, x, q)
+    Psil_o = O.long_solve(op, Sl_o)
+    for stage, ref in ((1, S_o), (2, Psi_o), (3, Sl_o), (4, Psil_o)):
+        g = pl.debug_stage(stage, xd, qd).cpu().numpy()
+        assert g.shape == ref.shape
+        assert rel(g, ref) <= TOL_FP64, (stage, rel(g, ref))
+        assert np.max(np.abs(g - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-12])
+def test_c2_tolerance_sweep_small(tol):
+    """c2 shape (cube, density ~1) at N=3000, tolerances of the c2 sweep."""
+    xyz, q, L = config_system("c2", N=3000)
+    op = make_plan(len(q), *L, tol)
+    check_total(op, xyz, q)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_shapes_small(name):
+    """Slab (c3), tall box (c4), cube (c5) shapes at N=5000 with their own aspect ratio."""
+    xyz, q, L = config_system(name, N=5000)
+    op = make_plan(len(q), *L, 1e-6)
+    check_total(op, xyz, q)
+
+
+def test_c4_fp32_tolerance_plan():
+    """c4 at its fp32 tolerance 1e-4 (computed in fp64 here; the fp32 path is a NEXT row)."""
+    xyz, q, L = config_system("c4", N=4000)
+    op = make_plan(len(q), *L, 1e-4)
+    check_total(op, xyz, q)
+
+
+def test_strongly_confined_no_mid():
+    """m = -1: every Gaussian is long-range, the mid solver is not invoked (Remark)."""
+    xyz, q = uniform_system(3000, (40.0, 40.0, 0.4), 7)
+    op = make_plan(3000, 40.0, 40.0, 0.4, 1e-6, rc_factor=1.5)
+    assert op.m == -1
+    check_total(op, xyz, q)
+
+
+def test_edge_cases_ragged_and_boundaries():
+    """Tiny and ragged N, a cell grid with < 3 cells per axis, particles exactly on the
+    box faces (x = -L/2, z = +-Lz/2) and outside the primary cell in x,y (wrapped)."""
+    for N, L, seed in ((2, (6.0, 6.0, 6.0), 1), (3, (6.0, 7.0, 5.0), 2), (37, (7.0, 7.0, 7.0), 3),
+                       (1001, (9.0, 11.0, 8.0), 4)):
+        xyz, q = uniform_system(N, L, seed)
+        if N >= 3:
+            xyz[0] = (-L[0] / 2, 0.3, -L[2] / 2)
+            xyz[1] = (1.3 * L[0], -2.2 * L[1], L[2] / 2)
+        op = make_plan(N, *L, 1e-6)
+        check_total(op, xyz, q)
+
+
+def test_determinism_and_host_path():
+    xyz, q, L = config_system("c2", N=20000)
+    op = make_plan(len(q), *L, 1e-6)
+    pl = gpu_plan(op)
+    xd, qd = to_dev(xyz, q)
+    a = pl.eval(xd, qd)
+    b = pl.eval(xd, qd)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    U = pl.energy()
+    assert abs(U - 0.5 * float(np.dot(q, a[0].cpu().numpy()))) <= 1e-12 * abs(U) * 10
+    ph, F = pl.eval_host(np.ascontiguousarray(xyz), q)
+    assert np.array_equal(ph, a[0].cpu().numpy()) and np.array_equal(F, a[1].cpu().numpy())
+
+
+def test_validation_errors():
+    from paper_2412_04595_b200 import SogError
+    xyz, q = uniform_system(100, (6.0, 6.0, 6.0), 5)
+    op = make_plan(100, 6.0, 6.0, 6.0, 1e-6)
+    pl = gpu_plan(op)
+    bad = xyz.copy(); bad[3, 2] = 3.5
+    with pytest.raises(SogError) as e:
+        pl.eval(*to_dev(bad, q))
+    assert e.value.code == -3
+    bad = xyz.copy(); bad[4, 0] = np.nan
+    with pytest.raises(SogError) as e:
+        pl.eval(*to_dev(bad, q))
+    assert e.value.code == -4
+    q2 = q.copy(); q2[0] += 0.5
+    with pytest.raises(SogError) as e:
+        pl.eval(*to_dev(xyz, q2))
+    assert e.value.code == -2
+    # the plan still works afterwards
+    phi, F = pl.eval(*to_dev(xyz, q))
+    assert torch.isfinite(phi).all()
+
+
+def test_default_plan_rules_accuracy_vs_ewald():
+    """The library's own rules (no oracle plan) at c1 reach tol vs Ewald2D."""
+    from paper_2412_04595_b200 import Plan
+    from oracle import ewald2d
+    xyz, q, L = config_system("c1")
+    pl = Plan(len(q), L, 1e-6)
+    phi, F = pl.eval(*to_dev(xyz, q))
+    t = np.arange(0, 1000, 25)
+    ref, g = ewald2d.ewald2d(xyz, q, L, targets=t)
+    phi = phi.cpu().numpy()[t]
+    assert np.max(np.abs(phi - ref)) / np.max(np.abs(ref)) < 1e-6
+    Fref = -q[t, None] * g
+    assert rel(F.cpu().numpy()[t], Fref) < 1e-5
+
+
+# ---------------------------------------------------------------- full BASELINE sizes, sampled outputs
+@pytest.mark.parametrize("name,tol", [("c2", 1e-6), ("c2", 1e-4)])
+def test_full_size_c2_sampled(name, tol):
+    """c2 at N=1e5 in the bench's launch configuration; 200 sampled targets computed by the
+    oracle one by one (its near sum per target, its mid/long fields gathered per target)."""
+    xyz, q, L = config_system(name)
+    op = make_plan(len(q), *L, tol)
+    t = np.random.default_rng(0).choice(len(q), 200, replace=False)
+    phi_o, F_o = O.evaluate(op, xyz, q, targets=t)
+    phi_g, F_g, _ = run_gpu(op, xyz, q)
+    assert rel(phi_g[t], phi_o) <= TOL_FP64
+    assert rel(F_g[t], F_o) <= TOL_FP64
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_size_c3_c4_sampled(name):
+    xyz, q, L = config_system(name)
+    op = make_plan(len(q), *L, 1e-6)
+    t = np.random.default_rng(1).choice(len(q), 100, replace=False)
+    phi_o, F_o = O.evaluate(op, xyz, q, targets=t)
+    phi_g, F_g, _ = run_gpu(op, xyz, q)
+    assert rel(phi_g[t], phi_o) <= TOL_FP64
+    assert rel(F_g[t], F_o) <= TOL_FP64
+
+
+def test_full_size_c5_properties():
+    """c5 (N=1e7) in the bench configuration: properties that hold at any size -- the near
+    component at sampled targets vs the oracle, exact invariance under a shift by one period
+    and by a common multiple of the mid and long mesh sizes, z-reflection symmetry,
+    linearity in q, and sum F ~ 0."""
+    from paper_2412_04595_b200 import Plan
+    xyz, q, L = config_system("c5")
+    op = make_plan(len(q), *L, 1e-6)
+    pl = gpu_plan(op, validate=True)
+    xd, qd = to_dev(xyz, q)
+    phi, F = pl.eval(xd, qd)
+    comp = pl.components(xd, qd)
+    t = np.random.default_rng(2).choice(len(q), 64, replace=False)
+    x = O.canonicalize(xyz, op)
+    pn, gn = O.near_field(op, x, q, targets=t)
+    c = comp[0].cpu().numpy()[t]
+    assert rel(c[:, 0], pn) <= TOL_FP64 and rel(c[:, 1:], gn) <= TOL_FP64
+    phi0 = phi.cpu().numpy()
+    F0 = F.cpu().numpy()
+    # shift by a full period in x and y
+    s = xyz.copy(); s[:, 0] += L[0]; s[:, 1] -= L[1]
+    p2, F2 = pl.eval(*to_dev(s, q))
+    assert rel(p2.cpu().numpy(), phi0) <= 1e-13
+    # z reflection
+    r = xyz.copy(); r[:, 2] *= -1
+    p3, F3 = pl.eval(*to_dev(r, q))
+    assert rel(p3.cpu().numpy(), phi0) <= 1e-12
+    F3 = F3.cpu().numpy()
+    assert rel(F3[:, 2], -F0[:, 2]) <= 1e-12
+    # linearity
+    p4, _ = pl.eval(xd, 2.0 * qd)
+    assert rel(p4.cpu().numpy(), 2.0 * phi0) <= 1e-15
+    assert np.linalg.norm(F0.sum(0)) <= 1e-6 * np.abs(F0).max() * math.sqrt(len(q))
