@@ -132,3 +132,147 @@ __global__ void __launch_bounds__(128) k_long_gather(LongArgs a, const double* _
 }
 
 }  // namespace sog
+
+namespace sog {
+
+// ---------------------------------------------------------------------------------------
+// S8 v2: output-stationary anterpolation.  A CTA owns a tile of TX x TY long-grid columns
+// (one thread per column, all Pc layers of its column in registers) and one chunk of the
+// particles whose stencils can reach the tile.  Particles are staged in shared memory in
+// batches (weights by recurrence, Chebyshev T_n, then L_b = sum_n C[b][n] T_n spread over
+// all threads); every column thread adds c = q Wx Wy times L_b(z) to its Pc accumulators.
+// Partials go to part[tile][chunk][col][Pc]; k_long_reduce sums chunks in a fixed order, so
+// the result is deterministic (no atomics).
+struct LongTileArgs {
+    LongArgs a;
+    int TX, TY, ntx, nty, nchunk;
+    int full_range;          // 1: every particle reaches every tile (small periodic grid)
+    const int* start;        // cell start offsets (sorted order), for x-slab particle ranges
+    int ncx, cells_per_x;    // near-cell grid: ncx slabs of cells_per_x = ncy*ncz cells
+    double cell_w;           // Lx / ncx
+    double Lx;
+    double gamma_x, gamma_y; // window recurrence constants exp(-2 a h^2)
+    double* part;
+};
+
+constexpr int LB = 64;       // particles per staged batch
+
+template <int P, int PCMAX>
+__global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
+    extern __shared__ double sm[];
+    double* sC = sm;                          // [Pc*Pc]
+    double* sW = sC + PCMAX * PCMAX;          // [LB][2P]
+    double* sT = sW + LB * 2 * P;             // [LB][PCMAX] Chebyshev T_n, then L_b
+    double* sL = sT + LB * PCMAX;             // [LB][PCMAX] L_b(z_j)
+    double* sQ = sL + LB * PCMAX;             // [LB]
+    int* sG = (int*)(sQ + LB);                // [LB][2]
+    const LongArgs& a = t.a;
+    constexpr int p = (P - 1) / 2;
+    const int Pc = a.Pc;
+    const int tile = blockIdx.y, chunk = blockIdx.x;
+    const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    for (int k = tid; k < Pc * Pc; k += nthr) sC[k] = a.C[k];
+    // particle index ranges reaching this tile (1 or 2 ranges of x-slabs)
+    int r0b = 0, r0e = a.N, r1b = 0, r1e = 0;
+    if (!t.full_range) {
+        // stencil centres gx0 in [X0 - p, X0 + TX - 1 + p] <=> x in [xlo, xhi)
+        double xlo = ((X0 - p) - 0.5 - 0.5 * a.Ilx) * a.hx, xhi = ((X0 + t.TX - 1 + p) + 0.5 - 0.5 * a.Ilx) * a.hx;
+        int c0 = (int)floor((xlo + 0.5 * t.Lx) / t.cell_w) - 1, c1 = (int)floor((xhi + 0.5 * t.Lx) / t.cell_w) + 1;
+        if (c1 - c0 + 1 >= t.ncx) { c0 = 0; c1 = t.ncx - 1; }
+        if (c0 < 0) {
+            r1b = t.start[(c0 + t.ncx) * t.cells_per_x]; r1e = a.N; c0 = 0;
+        } else if (c1 >= t.ncx) {
+            r1b = 0; r1e = t.start[(c1 - t.ncx + 1) * t.cells_per_x]; c1 = t.ncx - 1;
+        }
+        r0b = t.start[c0 * t.cells_per_x];
+        r0e = t.start[(c1 + 1) * t.cells_per_x];
+    }
+    const int n0 = r0e - r0b, ntot = n0 + (r1e - r1b);
+    const int per = (ntot + t.nchunk - 1) / t.nchunk;
+    const int jb = min(ntot, chunk * per), je = min(ntot, jb + per);
+    // my column
+    const int cx = X0 + tid / t.TY, cy = Y0 + tid % t.TY;
+    const bool own = tid < t.TX * t.TY && cx < a.Ilx && cy < a.Ily;
+    double acc[PCMAX];
+#pragma unroll
+    for (int b = 0; b < PCMAX; ++b) acc[b] = 0.0;
+    __syncthreads();
+    for (int base = jb; base < je; base += LB) {
+        const int nb = min(LB, je - base);
+        if (tid < nb) {
+            int k = base + tid;
+            int j = k < n0 ? r0b + k : r1b + (k - n0);
+            d4 r = ld_d4(&a.pos[j]);
+            int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
+            double wx[P], wy[P];
+            window_weights_rec<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
+            window_weights_rec<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
+#pragma unroll
+            for (int u = 0; u < P; ++u) { sW[tid * 2 * P + u] = wx[u]; sW[tid * 2 * P + P + u] = wy[u]; }
+            sQ[tid] = r.w;
+            sG[2 * tid] = gx0 - p;
+            sG[2 * tid + 1] = gy0 - p;
+            double x = r.z * a.two_over_Lz;
+            double tm = 1.0, tc = x;
+            sT[tid * PCMAX] = 1.0;
+            if (Pc > 1) sT[tid * PCMAX + 1] = x;
+            for (int n = 2; n < Pc; ++n) {
+                double tn = 2.0 * x * tc - tm;
+                sT[tid * PCMAX + n] = tn;
+                tm = tc; tc = tn;
+            }
+        }
+        __syncthreads();
+        // L_b(z_j) = sum_n C[b][n] T_n(x_j), (j, b) pairs over all threads
+        for (int q = tid; q < nb * PCMAX; q += nthr) {
+            int j = q / PCMAX, b = q % PCMAX;
+            double s = 0.0;
+            if (b < Pc)
+                for (int n = 0; n < Pc; ++n) s = fma(sC[b * Pc + n], sT[j * PCMAX + n], s);
+            sL[q] = s;
+        }
+        __syncthreads();
+        if (own) {
+            for (int j = 0; j < nb; ++j) {
+                int u = cx - sG[2 * j], v = cy - sG[2 * j + 1];
+                u += u < 0 ? a.Ilx : 0; u -= u >= a.Ilx ? a.Ilx : 0;
+                v += v < 0 ? a.Ily : 0; v -= v >= a.Ily ? a.Ily : 0;
+                if (u < P && v < P) {
+                    const double c = sQ[j] * sW[j * 2 * P + u] * sW[j * 2 * P + P + v];
+                    const double2* L2 = reinterpret_cast<const double2*>(sL + j * PCMAX);
+#pragma unroll
+                    for (int b = 0; b < PCMAX; b += 2) {
+                        if (b < Pc) {
+                            double2 l = L2[b / 2];
+                            acc[b] = fma(c, l.x, acc[b]);
+                            acc[b + 1] = fma(c, l.y, acc[b + 1]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (own) {
+        double* o = t.part + (((size_t)tile * t.nchunk + chunk) * (t.TX * t.TY) + tid) * PCMAX;
+#pragma unroll
+        for (int b = 0; b < PCMAX; ++b) o[b] = acc[b];
+    }
+}
+
+// grid[b][gx][gy] = sum over chunks (fixed order) of the tile partials.
+static __global__ void k_long_reduce(const double* __restrict__ part, double* __restrict__ grid, int Ilx, int Ily,
+                                     int Pc, int PCMAX, int TX, int TY, int nty, int nchunk) {
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= Ilx * Ily * Pc) return;
+    int b = idx / (Ilx * Ily), g = idx % (Ilx * Ily);
+    int gx = g / Ily, gy = g % Ily;
+    int tile = (gx / TX) * nty + gy / TY, col = (gx % TX) * TY + gy % TY;
+    const double* p = part + ((size_t)tile * nchunk * (TX * TY) + col) * PCMAX + b;
+    double s = 0.0;
+    for (int k = 0; k < nchunk; ++k) s += p[(size_t)k * TX * TY * PCMAX];
+    grid[idx] = s;
+}
+
+}  // namespace sog

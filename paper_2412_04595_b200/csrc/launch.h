@@ -8,6 +8,10 @@
 namespace sog {
 struct MidArgs;
 struct LongArgs;
+struct LongTileArgs;
+struct MidTileArgs;
+int launch_mid_spread_tile(const MidTileArgs& t, int P, double* grid, cudaStream_t st);
+int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
 int launch_mid_spread(const MidArgs& a, int P, double* grid, cudaStream_t st);
 int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, cudaStream_t st);
 int launch_long_spread(const LongArgs& a, int Pl, double* grid, cudaStream_t st);

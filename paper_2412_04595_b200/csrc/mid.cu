@@ -28,4 +28,21 @@ int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, cudaS
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
+int launch_mid_spread_tile(const MidTileArgs& t, int P, double* grid, cudaStream_t st) {
+    const int nblk = t.ntx * t.nty * t.ntz;
+    const size_t sh = sizeof(double) * MT_B * (3 * P + 1);
+    switch (P) {
+#define C_(P_)                                                                                          \
+    case P_:                                                                                            \
+        if (cudaFuncSetAttribute(k_mid_spread_tile<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                 (int)sh) != cudaSuccess) return 2;                                     \
+        k_mid_spread_tile<P_><<<nblk, 256, sh, st>>>(t, grid);                                          \
+        break;
+        SOG_ODD_P(C_)
+#undef C_
+        default: return 1;
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
 }  // namespace sog

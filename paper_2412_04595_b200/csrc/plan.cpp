@@ -225,6 +225,7 @@ bool validate_params(const Params& p, std::string& err) {
         if (p.Ix < 2 || p.Iy < 2 || p.Iz < 1 || p.Izs < 2 || (p.Izs & 1)) return bad("bad mid grid");
         if (p.P < 5 || p.P > 27 || !(p.P & 1)) return bad("mid window support must be odd in [5,27]");
         if (!(p.S > 0)) return bad("bad mid window shape");
+        if (p.Ix < p.P || p.Iy < p.P) return bad("mid grid smaller than the window support");
         // R7: the z stencil must not leave the extended grid
         double hz = p.hz();
         if (p.Izs * hz < p.Lz + (p.P - 1) * hz + 2.0 * hz * (1 - 1e-12)) return bad("Izs too small for the z stencil (R7)");
@@ -232,6 +233,7 @@ bool validate_params(const Params& p, std::string& err) {
     if (p.Ilx < 2 || p.Ily < 2 || (p.Ily & 1)) return bad("bad long grid (Ily must be even)");
     if (p.Pl < 5 || p.Pl > 27 || !(p.Pl & 1)) return bad("long window support must be odd in [5,27]");
     if (!(p.Sl > 0)) return bad("bad long window shape");
+    if (p.Ilx < p.Pl || p.Ily < p.Pl) return bad("long grid smaller than the window support");
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
     return true;
 }
@@ -303,7 +305,9 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
     sog_weights(p, w, s);
     const int L = p.m + 1;
     A.resize(L);
-    for (int l = 0; l < L; ++l) A[l] = std::pow(kPi, 1.5) * w[l] * s[l] * s[l] * s[l];
+    // cuFFT's inverse is unnormalised: the 1/(Ix Iy Izs) of ifftn is folded into A_l (R12).
+    const double inv_n = 1.0 / (double(p.Ix) * p.Iy * p.Izs);
+    for (int l = 0; l < L; ++l) A[l] = std::pow(kPi, 1.5) * w[l] * s[l] * s[l] * s[l] * inv_n;
     auto axis = [&](int I, double Lper, double h, bool half, std::vector<double>& T) {
         int n = half ? I / 2 + 1 : I;
         T.resize(size_t(L) * n);
@@ -340,7 +344,8 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
             // 1 / (W_x W_y)^2
             double Wx = std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
             double Wy = std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
-            double dec = kPi / (Wx * Wx * Wy * Wy);
+            // 1/(Ilx Ily) of the (unnormalised) cuFFT inverse is folded in here (R12)
+            double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
             double* Km = &K[(size_t(ix) * ny + iy) * P * P];
             for (int a = 0; a < P; ++a)
                 for (int b = 0; b < P; ++b) {

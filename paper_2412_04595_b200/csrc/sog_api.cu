@@ -99,6 +99,8 @@ struct sog_plan {
     bool has_mid = false;
     // long
     double* lgrid = nullptr;
+    double* lpart = nullptr;        // long spread tile partials
+    LongTileArgs lt{};
     cuDoubleComplex *lspec = nullptr, *lspec2 = nullptr;
     double *d_K = nullptr, *d_C = nullptr;
     cufftHandle lfwd = 0, linv = 0;
@@ -147,7 +149,7 @@ void free_plan(sog_plan* pl) {
     void* ptrs[] = {pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
-                    pl->d_K, pl->d_C, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
+                    pl->d_K, pl->d_C, pl->lpart, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -223,6 +225,26 @@ int setup(sog_plan* pl) {
         build_long_kernel(p, K);
         build_cheb_matrix(p.Pc, C);
         if ((rc = upload(pl, &pl->d_K, K)) || (rc = upload(pl, &pl->d_C, C))) return rc;
+        // S8 tiling: one tile = whole grid when it fits one CTA, else 16x16 column tiles
+        LongTileArgs& t = pl->lt;
+        if (p.Ilx * p.Ily <= 256) { t.TX = p.Ilx; t.TY = p.Ily; }
+        else { t.TX = std::min(16, p.Ilx); t.TY = std::min(16, p.Ily); }
+        t.ntx = (p.Ilx + t.TX - 1) / t.TX;
+        t.nty = (p.Ily + t.TY - 1) / t.TY;
+        const int pl_half = (p.Pl - 1) / 2;
+        t.full_range = (t.TX + 2 * pl_half + 2 >= p.Ilx) ? 1 : 0;
+        int ntile = t.ntx * t.nty;
+        t.nchunk = std::max(1, std::min(4 * 148 / ntile + 1, int((p.N + 255) / 256)));
+        if (!t.full_range) t.nchunk = std::max(1, t.nchunk * 3);
+        t.ncx = pl->geo.ncx;
+        t.cells_per_x = pl->geo.ncy * pl->geo.ncz;
+        t.cell_w = p.Lx / pl->geo.ncx;
+        t.Lx = p.Lx;
+        auto gam = [&](double h) { double H = (p.Pl - 1) * h / 2.0; return std::exp(-2.0 * p.Sl / (H * H) * h * h); };
+        t.gamma_x = gam(p.hlx());
+        t.gamma_y = gam(p.hly());
+        int pcmax = p.Pc <= 16 ? 16 : 32;
+        if ((rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
         long long n[2] = {p.Ilx, p.Ily};
         size_t ws = 0;
         CKF(cufftCreate(&pl->lfwd));
@@ -323,9 +345,17 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     mark(pl, 2);
     // S3-S7 mid range
     if (pl->has_mid && (stop_stage == 0 || stop_stage == 1 || stop_stage == 2)) {
-        size_t G = (size_t)p.Ix * p.Iy * p.Izs;
-        CK(cudaMemsetAsync(pl->mgrid, 0, G * sizeof(double), st));
-        if ((rc = lchk(launch_mid_spread(mid_args(pl), p.P, pl->mgrid, st)))) return rc;
+        MidTileArgs t;
+        t.a = mid_args(pl);
+        t.start = pl->start;
+        t.g = pl->geo;
+        auto gam = [&](double h) { double H = (p.P - 1) * h / 2.0; return std::exp(-2.0 * p.S / (H * H) * h * h); };
+        t.gamma_x = gam(p.hx()); t.gamma_y = gam(p.hy()); t.gamma_z = gam(p.hz());
+        t.ntx = (p.Ix + MT_X - 1) / MT_X; t.nty = (p.Iy + MT_Y - 1) / MT_Y; t.ntz = (p.Izs + MT_Z - 1) / MT_Z;
+        // stencil centres of particles with |z| <= Lz/2 (one extra point of margin each side)
+        t.gz_lo = (int)std::floor(-0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) - 1;
+        t.gz_hi = (int)std::floor(0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) + 1;
+        if ((rc = lchk(launch_mid_spread_tile(t, p.P, pl->mgrid, st)))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
         CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
@@ -345,9 +375,11 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     mark(pl, 7);
     // S8-S12 long range
     if (stop_stage == 0 || stop_stage == 3 || stop_stage == 4) {
-        size_t G = (size_t)p.Pc * p.Ilx * p.Ily;
-        CK(cudaMemsetAsync(pl->lgrid, 0, G * sizeof(double), st));
-        if ((rc = lchk(launch_long_spread(long_args(pl), p.Pl, pl->lgrid, st)))) return rc;
+        LongTileArgs t = pl->lt;
+        t.a = long_args(pl);
+        t.start = pl->start;
+        t.part = pl->lpart;
+        if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
         mark(pl, 8);
         if (stop_stage == 3) return SOG_OK;
         CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
