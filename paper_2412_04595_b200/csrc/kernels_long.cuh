@@ -50,32 +50,6 @@ __device__ __forceinline__ void cheb_lagrange(double x, int Pc, const double* __
     }
 }
 
-template <int P, int PCMAX>
-__global__ void __launch_bounds__(128) k_long_spread_atomic(LongArgs a, double* __restrict__ grid) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.N) return;
-    constexpr int p = (P - 1) / 2;
-    d4 r = ld_d4(&a.pos[i]);
-    int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
-    double wx[P], wy[P], L[PCMAX];
-    window_weights<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, wx, nullptr);
-    window_weights<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, wy, nullptr);
-    cheb_lagrange<PCMAX>(r.z * a.two_over_Lz, a.Pc, a.C, L, nullptr);
-    const size_t layer = (size_t)a.Ilx * a.Ily;
-    for (int u = 0; u < P; ++u) {
-        int gx = wrap(gx0 - p + u, a.Ilx);
-        double qx = r.w * wx[u];
-        for (int v = 0; v < P; ++v) {
-            int gy = wrap(gy0 - p + v, a.Ily);
-            double* col = grid + (size_t)gx * a.Ily + gy;
-            double qxy = qx * wy[v];
-#pragma unroll
-            for (int b = 0; b < PCMAX; ++b)
-                if (b < a.Pc) atomicAdd(col + b * layer, qxy * L[b]);
-        }
-    }
-}
-
 // S10: one thread per (half mode, a).
 static __global__ void k_long_scale(const cuDoubleComplex* __restrict__ in, cuDoubleComplex* __restrict__ out,
                              const double* __restrict__ K, int nmode, int Pc) {
@@ -90,45 +64,6 @@ static __global__ void k_long_scale(const cuDoubleComplex* __restrict__ in, cuDo
         im = fma(Km[b], v.y, im);
     }
     out[(size_t)aa * nmode + mode] = make_cuDoubleComplex(re, im);
-}
-
-template <int P, int PCMAX>
-__global__ void __launch_bounds__(128) k_long_gather(LongArgs a, const double* __restrict__ psi, d4* __restrict__ out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.N) return;
-    constexpr int p = (P - 1) / 2;
-    d4 r = ld_d4(&a.pos[i]);
-    int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
-    double wx[P], wy[P], dwx[P], dwy[P], L[PCMAX], dL[PCMAX];
-    window_weights<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, wx, dwx);
-    window_weights<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, wy, dwy);
-    cheb_lagrange<PCMAX>(r.z * a.two_over_Lz, a.Pc, a.C, L, dL);
-    const size_t layer = (size_t)a.Ilx * a.Ily;
-    double phi = 0, gx = 0, gy = 0, gz = 0;
-    for (int u = 0; u < P; ++u) {
-        int ix = wrap(gx0 - p + u, a.Ilx);
-        double px = 0, pdy = 0, pdz = 0;
-        for (int v = 0; v < P; ++v) {
-            int iy = wrap(gy0 - p + v, a.Ily);
-            const double* col = psi + (size_t)ix * a.Ily + iy;
-            double t0 = 0, t1 = 0;
-#pragma unroll
-            for (int b = 0; b < PCMAX; ++b)
-                if (b < a.Pc) {
-                    double g = __ldg(col + b * layer);
-                    t0 = fma(L[b], g, t0);
-                    t1 = fma(dL[b], g, t1);
-                }
-            px = fma(wy[v], t0, px);
-            pdy = fma(dwy[v], t0, pdy);
-            pdz = fma(wy[v], t1, pdz);
-        }
-        phi = fma(wx[u], px, phi);
-        gx = fma(dwx[u], px, gx);
-        gy = fma(wx[u], pdy, gy);
-        gz = fma(wx[u], pdz, gz);
-    }
-    st_d4(&out[i], d4{a.A * phi, a.A * gx, a.A * gy, a.A * gz * a.two_over_Lz});
 }
 
 }  // namespace sog
@@ -273,6 +208,99 @@ static __global__ void k_long_reduce(const double* __restrict__ part, double* __
     double s = 0.0;
     for (int k = 0; k < nchunk; ++k) s += p[(size_t)k * TX * TY * PCMAX];
     grid[idx] = s;
+}
+
+}  // namespace sog
+
+namespace sog {
+
+// Psi [Pc][Ilx][Ily] -> PsiT [Ilx][Ily][PCMAX] (layer fastest, zero padded) for the gather.
+static __global__ void k_long_transpose(const double* __restrict__ psi, double* __restrict__ psiT, int Ilx, int Ily,
+                                        int Pc, int PCMAX) {
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= Ilx * Ily * PCMAX) return;
+    int a = idx % PCMAX, g = idx / PCMAX;
+    psiT[idx] = a < Pc ? psi[(size_t)a * Ilx * Ily + g] : 0.0;
+}
+
+// S12 v2: interpolation back to the particles.  One thread per particle; the (small) proxy
+// field is read from shared memory (or L1/L2 for big grids) with all PCMAX layers of a grid
+// column contiguous, so a column costs PCMAX/2 128-bit loads for 2*PCMAX FMAs.
+template <int P, int PCMAX>
+__global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* __restrict__ psiT, d4* __restrict__ out,
+                                                      double gamma_x, double gamma_y, int SMEM) {
+    extern __shared__ double sm[];
+    const int Pc = a.Pc;
+    double* sC = sm;                                   // [Pc*Pc]
+    double* sP = sm + PCMAX * PCMAX;                   // [Ilx*Ily*PCMAX]
+    for (int k = threadIdx.x; k < Pc * Pc; k += blockDim.x) sC[k] = a.C[k];
+    if (SMEM) {
+        const int n = a.Ilx * a.Ily * PCMAX;
+        const double2* s2 = reinterpret_cast<const double2*>(psiT);
+        double2* d2 = reinterpret_cast<double2*>(sP);
+        for (int k = threadIdx.x; k < n / 2; k += blockDim.x) d2[k] = s2[k];
+    }
+    __syncthreads();
+    const double* P_ = SMEM ? sP : psiT;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.N) return;
+    constexpr int p = (P - 1) / 2;
+    d4 r = ld_d4(&a.pos[i]);
+    const int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
+    double wx[P], wy[P], dwx[P], dwy[P];
+    window_weights_rec<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
+    window_weights_rec<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
+    // Chebyshev T_n, T_n' at x = 2z/Lz, then L_b, L_b' (zero beyond Pc)
+    const double x = r.z * a.two_over_Lz;
+    double L[PCMAX], dL[PCMAX];
+    {
+        double T[PCMAX], dT[PCMAX];
+        T[0] = 1.0; dT[0] = 0.0; T[1] = x; dT[1] = 1.0;
+#pragma unroll
+        for (int n = 1; n + 1 < PCMAX; ++n) {
+            T[n + 1] = 2.0 * x * T[n] - T[n - 1];
+            dT[n + 1] = 2.0 * T[n] + 2.0 * x * dT[n] - dT[n - 1];
+        }
+#pragma unroll
+        for (int b = 0; b < PCMAX; ++b) {
+            double l = 0.0, dl = 0.0;
+            if (b < Pc) {
+                const double* c = sC + b * Pc;
+#pragma unroll
+                for (int n = 0; n < PCMAX; ++n)
+                    if (n < Pc) { l = fma(c[n], T[n], l); dl = fma(c[n], dT[n], dl); }
+            }
+            L[b] = l; dL[b] = dl;
+        }
+    }
+    double phi = 0, gx = 0, gy = 0, gz = 0;
+#pragma unroll 1
+    for (int u = 0; u < P; ++u) {
+        int ix = gx0 - p + u;
+        ix += ix < 0 ? a.Ilx : 0; ix -= ix >= a.Ilx ? a.Ilx : 0;
+        double px = 0, pdy = 0, pdz = 0;
+#pragma unroll
+        for (int v = 0; v < P; ++v) {
+            int iy = gy0 - p + v;
+            iy += iy < 0 ? a.Ily : 0; iy -= iy >= a.Ily ? a.Ily : 0;
+            const double2* col = reinterpret_cast<const double2*>(P_ + ((size_t)ix * a.Ily + iy) * PCMAX);
+            double t0 = 0, t1 = 0;
+#pragma unroll
+            for (int b = 0; b < PCMAX; b += 2) {
+                double2 g = col[b / 2];
+                t0 = fma(L[b], g.x, t0); t0 = fma(L[b + 1], g.y, t0);
+                t1 = fma(dL[b], g.x, t1); t1 = fma(dL[b + 1], g.y, t1);
+            }
+            px = fma(wy[v], t0, px);
+            pdy = fma(dwy[v], t0, pdy);
+            pdz = fma(wy[v], t1, pdz);
+        }
+        phi = fma(wx[u], px, phi);
+        gx = fma(dwx[u], px, gx);
+        gy = fma(wx[u], pdy, gy);
+        gz = fma(wx[u], pdz, gz);
+    }
+    st_d4(&out[i], d4{a.A * phi, a.A * gx, a.A * gy, a.A * gz * a.two_over_Lz});
 }
 
 }  // namespace sog

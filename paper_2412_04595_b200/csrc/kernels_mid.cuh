@@ -20,31 +20,6 @@ struct MidArgs {
     double Vh;                           // h_x h_y h_z
 };
 
-// v1 spread: one thread per particle, separable weights in registers, fp64 RED to global.
-template <int P>
-__global__ void __launch_bounds__(128) k_mid_spread_atomic(MidArgs a, double* __restrict__ grid) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.N) return;
-    constexpr int p = (P - 1) / 2;
-    d4 r = ld_d4(&a.pos[i]);
-    int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy), gz0 = stencil_g0(r.z, a.hz, a.hpz);
-    double wx[P], wy[P], wz[P];
-    window_weights<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, wx, nullptr);
-    window_weights<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, wy, nullptr);
-    window_weights<P, false>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, wz, nullptr);
-    const size_t zb = (size_t)(gz0 - p);
-    for (int u = 0; u < P; ++u) {
-        size_t bx = (size_t)wrap(gx0 - p + u, a.Ix) * a.Iy;
-        double qx = r.w * wx[u];
-        for (int v = 0; v < P; ++v) {
-            double* col = grid + ((bx + wrap(gy0 - p + v, a.Iy)) * a.Izs + zb);
-            double qxy = qx * wy[v];
-#pragma unroll
-            for (int c = 0; c < P; ++c) atomicAdd(col + c, qxy * wz[c]);
-        }
-    }
-}
-
 // S5: multiply the half spectrum by mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz].
 static __global__ void k_mid_scale(cuDoubleComplex* __restrict__ spec, int Ix, int Iy, int nz, int L,
                             const double* __restrict__ A, const double* __restrict__ Tx,
@@ -60,25 +35,34 @@ static __global__ void k_mid_scale(cuDoubleComplex* __restrict__ spec, int Ix, i
     spec[idx] = make_cuDoubleComplex(v.x * mult, v.y * mult);
 }
 
-// v1 gather: one thread per particle, reads the P^3 stencil of Psi (L1/L2 cached).
+// S7 gather: one thread per particle, separable weights (recurrence) in registers, reads
+// the P^3 stencil of Psi through L1 (particles are cell-sorted, so neighbours share lines).
 template <int P>
-__global__ void __launch_bounds__(128) k_mid_gather(MidArgs a, const double* __restrict__ psi, d4* __restrict__ out) {
+__global__ void __launch_bounds__(128, 4) k_mid_gather(MidArgs a, const double* __restrict__ psi, d4* __restrict__ out,
+                                                       double gamma_x, double gamma_y, double gamma_z) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.N) return;
     constexpr int p = (P - 1) / 2;
     d4 r = ld_d4(&a.pos[i]);
     int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy), gz0 = stencil_g0(r.z, a.hz, a.hpz);
     double wx[P], wy[P], wz[P], dwx[P], dwy[P], dwz[P];
-    window_weights<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, wx, dwx);
-    window_weights<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, wy, dwy);
-    window_weights<P, true>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, wz, dwz);
+    window_weights_rec<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
+    window_weights_rec<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
+    window_weights_rec<P, true>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, gamma_z, wz, dwz);
     const size_t zb = (size_t)(gz0 - p);
     double phi = 0, gx = 0, gy = 0, gz = 0;
+    int ix = gx0 - p;
+    ix += ix < 0 ? a.Ix : 0; ix -= ix >= a.Ix ? a.Ix : 0;
+    int iy0 = gy0 - p;
+    iy0 += iy0 < 0 ? a.Iy : 0; iy0 -= iy0 >= a.Iy ? a.Iy : 0;
+#pragma unroll 1
     for (int u = 0; u < P; ++u) {
-        size_t bx = (size_t)wrap(gx0 - p + u, a.Ix) * a.Iy;
+        const double* plane = psi + (size_t)ix * a.Iy * a.Izs + zb;
         double px = 0, pdz = 0, pdy = 0;
+        int iy = iy0;
+#pragma unroll
         for (int v = 0; v < P; ++v) {
-            const double* col = psi + ((bx + wrap(gy0 - p + v, a.Iy)) * a.Izs + zb);
+            const double* col = plane + (size_t)iy * a.Izs;
             double t0 = 0, t1 = 0;
 #pragma unroll
             for (int c = 0; c < P; ++c) {
@@ -89,11 +73,13 @@ __global__ void __launch_bounds__(128) k_mid_gather(MidArgs a, const double* __r
             px = fma(wy[v], t0, px);
             pdy = fma(dwy[v], t0, pdy);
             pdz = fma(wy[v], t1, pdz);
+            iy = (iy + 1 == a.Iy) ? 0 : iy + 1;
         }
         phi = fma(wx[u], px, phi);
         gx = fma(dwx[u], px, gx);
         gy = fma(wx[u], pdy, gy);
         gz = fma(wx[u], pdz, gz);
+        ix = (ix + 1 == a.Ix) ? 0 : ix + 1;
     }
     st_d4(&out[i], d4{a.Vh * phi, a.Vh * gx, a.Vh * gy, a.Vh * gz});
 }

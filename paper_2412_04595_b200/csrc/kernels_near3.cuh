@@ -1,0 +1,163 @@
+// S2 v3: near-field pair sum (Eq. eq::phiNDR), one CTA per near-field cell.
+// The 27 neighbouring cells' particles are staged once per CTA in shared memory (fp64, with
+// their periodic image shift applied: cells >= r_c and >= 3 per periodic axis, so each
+// neighbour cell has exactly one relevant image).  Each warp owns one target at a time; its
+// lanes sweep the staged sources 32 at a time, passing pairs (r < r_c) are compacted by
+// ballot into a per-warp list and evaluated 32 at a time with all lanes busy, and the lane
+// partials are reduced with shuffles.  F(u), u = r^2, and F'(u) come from one piecewise
+// polynomial per piece (joint Horner).
+#pragma once
+#include "kernels_common.cuh"
+
+namespace sog {
+
+struct Near3Args {
+    const d4* pos;          // sorted (x,y,z,q)
+    const int* start;       // cell start offsets [ncell+1]
+    const double* cF;       // K x (D+1) polynomial coefficients of F on each piece
+    d4* out;
+    int K;
+    double du, inv_du, rc2;
+    CellGeo g;
+    int cap;                // staged-source capacity (shared memory)
+    float rc2f;             // conservative fp32 pre-test threshold
+};
+
+constexpr int NEAR3_WARPS = 4;
+
+template <int D>
+__device__ __forceinline__ void near_pair(const double* tab, const Near3Args& a, const d4& pi, int code,
+                                          const double2* shift, double& phi, double& gx, double& gy, double& gz) {
+    const d4 s = ld_d4(&a.pos[code >> 4]);
+    const double2 sh = shift[code & 15];
+    const double dx = pi.x - (s.x + sh.x), dy = pi.y - (s.y + sh.y), dz = pi.z - s.z;
+    const double u = fma(dx, dx, fma(dy, dy, dz * dz));
+    if (!(u < a.rc2 && u > 0.0)) return;        // exact fp64 decision (the fp32 test is a superset)
+    const int kk = min(a.K - 1, (int)(u * a.inv_du));
+    const double d = u - (kk + 0.5) * a.du;
+    const double* cf = tab + kk * (D + 1);
+    double F = cf[D], dF = 0.0;
+#pragma unroll
+    for (int n = D - 1; n >= 0; --n) {
+        dF = fma(dF, d, F);
+        F = fma(F, d, cf[n]);
+    }
+    const double rinv = rsqrt(u);
+    phi = fma(s.w, rinv - F, phi);
+    const double cc = s.w * (-rinv * rinv * rinv - 2.0 * dF);
+    gx = fma(cc, dx, gx);
+    gy = fma(cc, dy, gy);
+    gz = fma(cc, dz, gz);
+}
+
+template <int D>
+__global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
+    extern __shared__ double sm[];
+    double* tab = sm;                                                   // [K*(D+1)]
+    double2* shift = reinterpret_cast<double2*>(sm + ((a.K * (D + 1) + 1) & ~1));   // [9]
+    int* lists = reinterpret_cast<int*>(shift + 10);                    // [warps][160]
+    float4* src = reinterpret_cast<float4*>(lists + NEAR3_WARPS * 160); // [cap]: rel. xyz + code
+    const CellGeo& g = a.g;
+    const int c = blockIdx.x;
+    const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+    const int t0 = a.start[c], t1 = a.start[c + 1];
+    if (t0 == t1) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = a.cF[t];
+    if (threadIdx.x < 9) {
+        const int k = threadIdx.x, ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
+        shift[k] = make_double2(ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0), uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0));
+    }
+    const double ox = cx / g.sx - 0.5 * g.Lx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
+    const int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
+    int* wl = lists + warp * 160;
+    int ns_total = 0;
+    for (int k = 0; k < 9; ++k) {
+        int nx = cx + k / 3 - 1, ny = cy + k % 3 - 1;
+        nx += nx < 0 ? g.ncx : 0; nx -= nx >= g.ncx ? g.ncx : 0;
+        ny += ny < 0 ? g.ncy : 0; ny -= ny >= g.ncy ? g.ncy : 0;
+        const int cb = (nx * g.ncy + ny) * g.ncz;
+        ns_total += a.start[cb + z1 + 1] - a.start[cb + z0];
+    }
+    // process the neighbourhood in capacity-sized pieces (usually one)
+    for (int sbeg = 0; sbeg < ns_total; sbeg += a.cap) {
+        const int send = min(ns_total, sbeg + a.cap);
+        __syncthreads();
+        // stage sources [sbeg, send) of the concatenated 9-column list with image shifts
+        {
+            int base = 0;
+            for (int k = 0; k < 9; ++k) {
+                const int ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
+                const int nx = ux < 0 ? ux + g.ncx : (ux >= g.ncx ? ux - g.ncx : ux);
+                const int ny = uy < 0 ? uy + g.ncy : (uy >= g.ncy ? uy - g.ncy : uy);
+                const double sx = ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0);
+                const double sy = uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0);
+                const int cb = (nx * g.ncy + ny) * g.ncz;
+                const int jb = a.start[cb + z0], n = a.start[cb + z1 + 1] - jb;
+                const int lo = max(sbeg, base), hi = min(send, base + n);
+                for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+                    const int j = jb + (q - base);
+                    const d4 s = ld_d4(&a.pos[j]);
+                    src[q - sbeg] = make_float4((float)(s.x + sx - ox), (float)(s.y + sy - oy), (float)(s.z - oz),
+                                                __int_as_float((j << 4) | k));
+                }
+                base += n;
+            }
+        }
+        __syncthreads();
+        const int nsrc = send - sbeg;
+        for (int it = t0 + warp; it < t1; it += NEAR3_WARPS) {
+            const d4 pi = ld_d4(&a.pos[it]);
+            const float xi = (float)(pi.x - ox), yi = (float)(pi.y - oy), zi = (float)(pi.z - oz);
+            double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+            int npend = 0;
+            for (int q0 = 0; q0 < nsrc; q0 += 128) {
+                // fp32 pre-test of 4 x 32 sources (independent chains)
+                bool pass[4];
+                int code[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int q = q0 + 32 * r + lane;
+                    pass[r] = false;
+                    code[r] = 0;
+                    if (q < nsrc) {
+                        const float4 s = src[q];
+                        const float dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
+                        pass[r] = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < a.rc2f;
+                        code[r] = __float_as_int(s.w);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned m = __ballot_sync(0xffffffffu, pass[r]);
+                    if (pass[r]) wl[npend + __popc(m & ((1u << lane) - 1))] = code[r];
+                    npend += __popc(m);
+                }
+                __syncwarp();
+                while (npend >= 32) {                    // evaluate 32 pending pairs, all lanes busy
+                    npend -= 32;
+                    near_pair<D>(tab, a, pi, wl[npend + lane], shift, phi, gx, gy, gz);
+                }
+                __syncwarp();
+            }
+            if (lane < npend) near_pair<D>(tab, a, pi, wl[lane], shift, phi, gx, gy, gz);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                phi += __shfl_xor_sync(0xffffffffu, phi, o);
+                gx += __shfl_xor_sync(0xffffffffu, gx, o);
+                gy += __shfl_xor_sync(0xffffffffu, gy, o);
+                gz += __shfl_xor_sync(0xffffffffu, gz, o);
+            }
+            if (lane == 0) {
+                if (sbeg == 0) st_d4(&a.out[it], d4{phi, gx, gy, gz});
+                else {
+                    d4 o = a.out[it];
+                    st_d4(&a.out[it], d4{o.x + phi, o.y + gx, o.z + gy, o.w + gz});
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace sog

@@ -11,9 +11,10 @@ struct LongArgs;
 struct LongTileArgs;
 struct MidTileArgs;
 int launch_mid_spread_tile(const MidTileArgs& t, int P, double* grid, cudaStream_t st);
+int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* psiT, d4* out, double gx, double gy,
+                        cudaStream_t st);
+int long_pcmax(int Pc);
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
-int launch_mid_spread(const MidArgs& a, int P, double* grid, cudaStream_t st);
-int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, cudaStream_t st);
-int launch_long_spread(const LongArgs& a, int Pl, double* grid, cudaStream_t st);
-int launch_long_gather(const LongArgs& a, int Pl, const double* psi, d4* out, cudaStream_t st);
+int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, double gx, double gy, double gz,
+                      cudaStream_t st);
 }  // namespace sog

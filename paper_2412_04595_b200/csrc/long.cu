@@ -4,35 +4,7 @@
 
 namespace sog {
 
-#define SOG_ODD_P(M) M(5) M(7) M(9) M(11) M(13) M(15) M(17) M(19) M(21) M(23) M(25) M(27)
-
-template <int PCMAX>
-int long_dispatch(const LongArgs& a, int Pl, bool spread, double* grid, const double* psi, d4* out, cudaStream_t st) {
-    int nb = (a.N + 127) / 128;
-    switch (Pl) {
-#define C_(P_)                                                                        \
-    case P_:                                                                          \
-        if (spread) k_long_spread_atomic<P_, PCMAX><<<nb, 128, 0, st>>>(a, grid);     \
-        else k_long_gather<P_, PCMAX><<<nb, 128, 0, st>>>(a, psi, out);               \
-        break;
-        SOG_ODD_P(C_)
-#undef C_
-        default: return 1;
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
-}
-
-int launch_long_spread(const LongArgs& a, int Pl, double* grid, cudaStream_t st) {
-    if (a.Pc <= 16) return long_dispatch<16>(a, Pl, true, grid, nullptr, nullptr, st);
-    if (a.Pc <= 32) return long_dispatch<32>(a, Pl, true, grid, nullptr, nullptr, st);
-    return 1;
-}
-
-int launch_long_gather(const LongArgs& a, int Pl, const double* psi, d4* out, cudaStream_t st) {
-    if (a.Pc <= 16) return long_dispatch<16>(a, Pl, false, nullptr, psi, out, st);
-    if (a.Pc <= 32) return long_dispatch<32>(a, Pl, false, nullptr, psi, out, st);
-    return 1;
-}
+#define SOG_ODD_P(M) M(5) M(7) M(9) M(11) M(13) M(15) M(17) M(19) M(21) M(23) M(25)
 
 template <int PCMAX>
 int long_tile_dispatch(const LongTileArgs& t, int Pl, cudaStream_t st) {
@@ -61,6 +33,49 @@ int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStr
     k_long_reduce<<<(n + 255) / 256, 256, 0, st>>>(t.part, grid, t.a.Ilx, t.a.Ily, t.a.Pc, pcmax, t.TX, t.TY, t.nty,
                                                    t.nchunk);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+#define SOG_PCMAX(M) M(8) M(12) M(16) M(20) M(24) M(28) M(32)
+
+int long_pcmax(int Pc) {
+    for (int m : {8, 12, 16, 20, 24, 28, 32})
+        if (Pc <= m) return m;
+    return 0;
+}
+
+template <int P, int PCMAX>
+int long_gather2_go(const LongArgs& a, const double* psiT, d4* out, double gx, double gy, cudaStream_t st) {
+    const size_t grid_bytes = sizeof(double) * (size_t)a.Ilx * a.Ily * PCMAX;
+    const bool smem = grid_bytes <= 96 * 1024;
+    const size_t sh = sizeof(double) * PCMAX * PCMAX + (smem ? grid_bytes : 0);
+    auto k = k_long_gather2<P, PCMAX>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess) return 2;
+    k<<<(a.N + 127) / 128, 128, sh, st>>>(a, psiT, out, gx, gy, smem ? 1 : 0);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int PCMAX>
+int long_gather2_p(const LongArgs& a, int Pl, const double* psiT, d4* out, double gx, double gy, cudaStream_t st) {
+    switch (Pl) {
+#define C_(P_) case P_: return long_gather2_go<P_, PCMAX>(a, psiT, out, gx, gy, st);
+        SOG_ODD_P(C_)
+#undef C_
+        default: return 1;
+    }
+}
+
+int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* psiT, d4* out, double gx, double gy,
+                        cudaStream_t st) {
+    const int pm = long_pcmax(a.Pc);
+    if (!pm) return 1;
+    const int n = a.Ilx * a.Ily * pm;
+    k_long_transpose<<<(n + 255) / 256, 256, 0, st>>>(psi, psiT, a.Ilx, a.Ily, a.Pc, pm);
+    switch (pm) {
+#define C_(M_) case M_: return long_gather2_p<M_>(a, Pl, psiT, out, gx, gy, st);
+        SOG_PCMAX(C_)
+#undef C_
+    }
+    return 1;
 }
 
 }  // namespace sog

@@ -4,23 +4,13 @@
 
 namespace sog {
 
-#define SOG_ODD_P(M) M(5) M(7) M(9) M(11) M(13) M(15) M(17) M(19) M(21) M(23) M(25) M(27)
+#define SOG_ODD_P(M) M(5) M(7) M(9) M(11) M(13) M(15) M(17) M(19) M(21) M(23) M(25)
 
-int launch_mid_spread(const MidArgs& a, int P, double* grid, cudaStream_t st) {
+int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, double gx, double gy, double gz,
+                      cudaStream_t st) {
     int nb = (a.N + 127) / 128;
     switch (P) {
-#define C_(P_) case P_: k_mid_spread_atomic<P_><<<nb, 128, 0, st>>>(a, grid); break;
-        SOG_ODD_P(C_)
-#undef C_
-        default: return 1;
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
-}
-
-int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, cudaStream_t st) {
-    int nb = (a.N + 127) / 128;
-    switch (P) {
-#define C_(P_) case P_: k_mid_gather<P_><<<nb, 128, 0, st>>>(a, psi, out); break;
+#define C_(P_) case P_: k_mid_gather<P_><<<nb, 128, 0, st>>>(a, psi, out, gx, gy, gz); break;
         SOG_ODD_P(C_)
 #undef C_
         default: return 1;

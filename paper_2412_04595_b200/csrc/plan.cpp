@@ -223,7 +223,7 @@ bool validate_params(const Params& p, std::string& err) {
     if (p.m < -1 || p.m >= p.M) return bad("m must be in [-1, M-1]");
     if (p.m >= 0) {
         if (p.Ix < 2 || p.Iy < 2 || p.Iz < 1 || p.Izs < 2 || (p.Izs & 1)) return bad("bad mid grid");
-        if (p.P < 5 || p.P > 27 || !(p.P & 1)) return bad("mid window support must be odd in [5,27]");
+        if (p.P < 5 || p.P > 25 || !(p.P & 1)) return bad("mid window support must be odd in [5,25]");
         if (!(p.S > 0)) return bad("bad mid window shape");
         if (p.Ix < p.P || p.Iy < p.P) return bad("mid grid smaller than the window support");
         // R7: the z stencil must not leave the extended grid
@@ -231,7 +231,7 @@ bool validate_params(const Params& p, std::string& err) {
         if (p.Izs * hz < p.Lz + (p.P - 1) * hz + 2.0 * hz * (1 - 1e-12)) return bad("Izs too small for the z stencil (R7)");
     }
     if (p.Ilx < 2 || p.Ily < 2 || (p.Ily & 1)) return bad("bad long grid (Ily must be even)");
-    if (p.Pl < 5 || p.Pl > 27 || !(p.Pl & 1)) return bad("long window support must be odd in [5,27]");
+    if (p.Pl < 5 || p.Pl > 25 || !(p.Pl & 1)) return bad("long window support must be odd in [5,25]");
     if (!(p.Sl > 0)) return bad("bad long window shape");
     if (p.Ilx < p.Pl || p.Ily < p.Pl) return bad("long grid smaller than the window support");
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
@@ -245,8 +245,9 @@ bool build_near_table(const Params& p, NearTable& t, std::string& err) {
     sog_weights(p, w, s);
     const double s0sq = s[0] * s[0];
     const double umax = p.rc * p.rc;
-    t.K = std::max(1, int(std::ceil(2.0 * umax / s0sq)));
-    t.D = 12;
+    // pieces with du / (2 s_0^2) <= 1/8 and degree 10: Taylor remainders ~1e-17 (F), ~3e-16 (F')
+    t.K = std::max(1, int(std::ceil(4.0 * umax / s0sq)));
+    t.D = 10;
     t.du = umax / t.K;
     t.inv_du = t.K / umax;
     const int D = t.D;
@@ -273,9 +274,11 @@ bool build_near_table(const Params& p, NearTable& t, std::string& err) {
         double u = umax * i / 4000.0;
         int k = std::min(t.K - 1, int(u * t.inv_du));
         double d = u - (k + 0.5) * t.du;
-        double F = 0, dF = 0;
-        for (int n = D; n >= 0; --n) F = F * d + t.cF[size_t(k) * (D + 1) + n];
-        for (int n = D - 1; n >= 0; --n) dF = dF * d + t.cdF[size_t(k) * (D + 1) + n];
+        double F = t.cF[size_t(k) * (D + 1) + D], dF = 0;
+        for (int n = D - 1; n >= 0; --n) {
+            dF = dF * d + F;
+            F = F * d + t.cF[size_t(k) * (D + 1) + n];
+        }
         long double Fe = 0, dFe = 0;
         for (int l = 0; l <= p.M; ++l) {
             long double e = (long double)w[l] * expl(-(long double)u / ((long double)s[l] * s[l]));

@@ -21,6 +21,7 @@
 #include "kernels_mid.cuh"
 #include "launch.h"
 #include "kernels_near.cuh"
+#include "kernels_near3.cuh"
 #include "kernels_sort.cuh"
 #include "sog_internal.h"
 
@@ -100,6 +101,7 @@ struct sog_plan {
     // long
     double* lgrid = nullptr;
     double* lpart = nullptr;        // long spread tile partials
+    double* lpsiT = nullptr;        // long field, layer-fastest [Ilx][Ily][PCMAX]
     LongTileArgs lt{};
     cuDoubleComplex *lspec = nullptr, *lspec2 = nullptr;
     double *d_K = nullptr, *d_C = nullptr;
@@ -149,7 +151,7 @@ void free_plan(sog_plan* pl) {
     void* ptrs[] = {pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
-                    pl->d_K, pl->d_C, pl->lpart, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
+                    pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -245,6 +247,7 @@ int setup(sog_plan* pl) {
         t.gamma_y = gam(p.hly());
         int pcmax = p.Pc <= 16 ? 16 : 32;
         if ((rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
+        if ((rc = dalloc(pl, &pl->lpsiT, (size_t)p.Ilx * p.Ily * 32))) return rc;
         long long n[2] = {p.Ilx, p.Ily};
         size_t ws = 0;
         CKF(cufftCreate(&pl->lfwd));
@@ -330,16 +333,30 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     int rc;
     // S2 near field
     if (!stop_stage) {
-        NearArgs a;
-        a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.cdF = pl->d_cdF; a.out = pl->o_near;
-        a.N = N; a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
-        a.g = pl->geo;
-        for (int i = 0; i < 3; ++i) { a.ox[i] = pl->offx[i]; a.oy[i] = pl->offy[i]; }
-        a.noffx = pl->noffx; a.noffy = pl->noffy;
-        size_t sh = 2 * sizeof(double) * pl->near.K * (pl->near.D + 1);
-        if (pl->near.D != 12) return fail(SOG_EINVAL, "near table degree");
-        if (sh > 48 * 1024) CK(cudaFuncSetAttribute(k_near<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-        k_near<12><<<(N + 255) / 256, 256, sh, st>>>(a);
+        const int D = pl->near.D;
+        if (D != 10) return fail(SOG_EINVAL, "near table degree");
+        if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && p.N < (1 << 27)) {   // k_near3: warp per target
+            Near3Args a;
+            a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
+            a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+            a.g = pl->geo;
+            a.cap = 1536;
+            a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+            size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
+                        NEAR3_WARPS * 160 * sizeof(int) + sizeof(float4) * a.cap;
+            CK(cudaFuncSetAttribute(k_near3<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_near3<10><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+        } else {
+            NearArgs a;
+            a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.cdF = pl->d_cdF; a.out = pl->o_near;
+            a.N = N; a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+            a.g = pl->geo;
+            for (int i = 0; i < 3; ++i) { a.ox[i] = pl->offx[i]; a.oy[i] = pl->offy[i]; }
+            a.noffx = pl->noffx; a.noffy = pl->noffy;
+            size_t sh = 2 * sizeof(double) * pl->near.K * (D + 1);
+            CK(cudaFuncSetAttribute(k_near<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_near<10><<<(N + 255) / 256, 256, sh, st>>>(a);
+        }
         CK(cudaGetLastError());
     }
     mark(pl, 2);
@@ -368,7 +385,12 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mgrid));
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
-        if ((rc = lchk(launch_mid_gather(mid_args(pl), p.P, pl->mgrid, pl->o_mid, st)))) return rc;
+        {
+            auto gam = [&](double h) { double H = (p.P - 1) * h / 2.0; return std::exp(-2.0 * p.S / (H * H) * h * h); };
+            if ((rc = lchk(launch_mid_gather(mid_args(pl), p.P, pl->mgrid, pl->o_mid, gam(p.hx()), gam(p.hy()),
+                                             gam(p.hz()), st))))
+                return rc;
+        }
     } else if (!pl->has_mid && !stop_stage) {
         CK(cudaMemsetAsync(pl->o_mid, 0, sizeof(d4) * N, st));
     }
@@ -389,7 +411,9 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
         mark(pl, 9);
         if (stop_stage == 4) return SOG_OK;
-        if ((rc = lchk(launch_long_gather(long_args(pl), p.Pl, pl->lgrid, pl->o_long, st)))) return rc;
+        if ((rc = lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long, pl->lt.gamma_x,
+                                           pl->lt.gamma_y, st))))
+            return rc;
     }
     mark(pl, 10);
     return SOG_OK;

@@ -1,4 +1,4 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build=$?
+python -c "import paper_2412_04595_b200 as p; p.load_library()" > gpurun_out/build.log 2>&1; echo load=$?
 timeout 300 python scripts/diag_parity.py c1 1000 > gpurun_out/diag.log 2>&1; echo diag=$?; tail -8 gpurun_out/diag.log
 timeout 300 python scripts/diag_parity.py c5 20000 > gpurun_out/diag5.log 2>&1; echo diag5=$?; tail -8 gpurun_out/diag5.log
 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1; echo bench=$?
