@@ -109,92 +109,6 @@ struct MidTileArgs {
     int Y0;                     // tile origin in y (set per CTA)
 };
 
-template <int P, int K>
-__device__ __forceinline__ void zcase(double (&acc)[MT_Z], double c, const double* wz) {
-    constexpr int s = K - (P - 1);     // grid z = Z0 + s + k, k = 0..P-1
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        if (s + k >= 0 && s + k < MT_Z) acc[s + k] = fma(c, wz[k], acc[s + k]);
-    }
-}
-
-// jump table over the particle's z offset (one case per relative stencil position)
-template <int P>
-__device__ __forceinline__ void zdispatch(int key, double (&acc)[MT_Z], double c, const double* wz) {
-#define ZC_(K) \
-    case K:    \
-        if constexpr (K < MT_Z + P - 1) zcase<P, K>(acc, c, wz); \
-        break;
-    switch (key) {
-        ZC_(0)
-        ZC_(1)
-        ZC_(2)
-        ZC_(3)
-        ZC_(4)
-        ZC_(5)
-        ZC_(6)
-        ZC_(7)
-        ZC_(8)
-        ZC_(9)
-        ZC_(10)
-        ZC_(11)
-        ZC_(12)
-        ZC_(13)
-        ZC_(14)
-        ZC_(15)
-        ZC_(16)
-        ZC_(17)
-        ZC_(18)
-        ZC_(19)
-        ZC_(20)
-        ZC_(21)
-        ZC_(22)
-        ZC_(23)
-        ZC_(24)
-        ZC_(25)
-        ZC_(26)
-        ZC_(27)
-        ZC_(28)
-        ZC_(29)
-        ZC_(30)
-        ZC_(31)
-        ZC_(32)
-        ZC_(33)
-        ZC_(34)
-        ZC_(35)
-        ZC_(36)
-        ZC_(37)
-        ZC_(38)
-        ZC_(39)
-        ZC_(40)
-        ZC_(41)
-        ZC_(42)
-        ZC_(43)
-        ZC_(44)
-        ZC_(45)
-        ZC_(46)
-        ZC_(47)
-        ZC_(48)
-        ZC_(49)
-        ZC_(50)
-        ZC_(51)
-        ZC_(52)
-        ZC_(53)
-        ZC_(54)
-        ZC_(55)
-        ZC_(56)
-        ZC_(57)
-        ZC_(58)
-        ZC_(59)
-        ZC_(60)
-        ZC_(61)
-        ZC_(62)
-        ZC_(63)
-        default: break;
-    }
-#undef ZC_
-}
-
 // v mod n for v in (-2n, 2n) without integer division
 __device__ __forceinline__ int wrapc(int v, int n) {
     v += v < 0 ? n : 0;
@@ -204,32 +118,42 @@ __device__ __forceinline__ int wrapc(int v, int n) {
     return v;
 }
 
-// Stage weights of sIdx[0..nst) (offsets dxo = (ox - X0) mod Ix etc. precomputed at
-// compaction), build each warp's list of particles touching its 4 x 8 column patch, and
-// add them into the lanes' z registers.
+// Stage weights of sIdx[0..nst): Wx[P], Wy[P], q and Wz scattered into the tile's MT_Z
+// z slots (zeros elsewhere) with a 2-bit mask of the non-empty 12-slot halves; build each
+// warp's list of particles touching its 4 x 8 column patch; then every lane adds
+// c = q Wx Wy times the padded Wz into its registers, 12 dense FMAs per touched half
+// (no per-particle branching on the z offset).
+constexpr int MT_NW(int P) { return (2 * P + 1 + MT_Z + 1) & ~1; }   // [Wz padded | Wx | Wy | q], even
+
 template <int P>
-__device__ __forceinline__ void mid_tile_batch(const MidTileArgs& t, int nst, const int* sIdx, int* sO,
-                                               double* sW, unsigned char* sMask, int* sList,
-                                               double (&acc)[MT_Z], int X0, int Z0, bool colok) {
+__device__ __forceinline__ void mid_tile_batch(const MidTileArgs& t, const int4* __restrict__ g0, int nst,
+                                               const int* sIdx, int* sO, double* sW, unsigned char* sMask,
+                                               unsigned short* sList, double (&acc)[MT_Z], bool colok) {
     constexpr int p = (P - 1) / 2;
-    constexpr int NW = 3 * P + 1;
+    constexpr int NW = MT_NW(P);
     const MidArgs& a = t.a;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int s = tid; s < nst; s += blockDim.x) {
         d4 r = ld_d4(&a.pos[sIdx[s]]);
-        const int dxo = sO[3 * s], dyo = sO[3 * s + 1];
+        const int dxo = sO[3 * s], dyo = sO[3 * s + 1], key = sO[3 * s + 2];
         // unwrapped stencil centres (the weights need the particle's own periodic image)
-        const int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
-        const int gz0 = stencil_g0(r.z, a.hz, a.hpz);
+        const int4 o = g0[sIdx[s]];
+        const int gx0 = o.x, gy0 = o.y, gz0 = o.z;
         double wx[P], wy[P], wz[P];
         window_weights_rec<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
         window_weights_rec<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
         window_weights_rec<P, false>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, t.gamma_z, wz, nullptr);
-        double* w = sW + s * NW;
+        double* wzp = sW + s * NW;                     // 16-byte aligned (NW even)
+        double* w = wzp + MT_Z;
 #pragma unroll
-        for (int k = 0; k < P; ++k) { w[k] = wx[k]; w[P + k] = wy[k]; w[2 * P + k] = wz[k]; }
-        w[3 * P] = r.w;
-        // which of the 8 warp patches (4 in x by 2 in y) this stencil touches
+        for (int k = 0; k < P; ++k) { w[k] = wx[k]; w[P + k] = wy[k]; }
+        w[2 * P] = r.w;
+        const int zs = key - (P - 1);                  // tile slot of stencil point 0
+#pragma unroll
+        for (int z = 0; z < MT_Z; ++z) wzp[z] = 0.0;
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (zs + k >= 0 && zs + k < MT_Z) wzp[zs + k] = wz[k];
         unsigned m = 0;
 #pragma unroll
         for (int wq = 0; wq < 8; ++wq) {
@@ -237,10 +161,12 @@ __device__ __forceinline__ void mid_tile_batch(const MidTileArgs& t, int nst, co
             if ((u0 < P || u0 > a.Ix - 4) && (v0 < P || v0 > a.Iy - 8)) m |= 1u << wq;
         }
         sMask[s] = (unsigned char)m;
+        // halves of the z tile that hold stencil points: [zs, zs+P) intersect [0,12) / [12,24)
+        sO[3 * s + 2] = (zs < MT_Z / 2 ? 1 : 0) | (zs + P - 1 >= MT_Z / 2 ? 2 : 0);
     }
     __syncthreads();
     // per-warp compaction of the particles touching this warp's patch (order preserved)
-    int* myl = sList + warp * MT_B;
+    unsigned short* myl = sList + warp * MT_B;
     int nmy = 0;
     for (int s0 = 0; s0 < nst; s0 += 32) {
         const int s = s0 + lane;
@@ -253,31 +179,72 @@ __device__ __forceinline__ void mid_tile_batch(const MidTileArgs& t, int nst, co
     const int wofx = 4 * (warp & 3) + (lane & 3), wofy = 8 * (warp >> 2) + (lane >> 2);
     for (int i = 0; i < nmy; ++i) {
         const int s = myl[i];
-        const double* w = sW + s * NW;
+        const double* wzp = sW + s * NW;
+        const double* w = wzp + MT_Z;
         const int u = wrapc(wofx - sO[3 * s], a.Ix), v = wrapc(wofy - sO[3 * s + 1], a.Iy);
-        const double c = (colok && u < P && v < P) ? w[3 * P] * w[u] * w[P + v] : 0.0;
-        zdispatch<P>(sO[3 * s + 2], acc, c, w + 2 * P);
+        const double c = (colok && u < P && v < P) ? w[2 * P] * w[u] * w[P + v] : 0.0;
+        const int halves = sO[3 * s + 2];
+        const double2* wz2 = reinterpret_cast<const double2*>(wzp);
+        if (halves & 1) {
+#pragma unroll
+            for (int z = 0; z < MT_Z / 2; z += 2) {
+                const double2 q = wz2[z / 2];
+                acc[z] = fma(c, q.x, acc[z]);
+                acc[z + 1] = fma(c, q.y, acc[z + 1]);
+            }
+        }
+        if (halves & 2) {
+#pragma unroll
+            for (int z = MT_Z / 2; z < MT_Z; z += 2) {
+                const double2 q = wz2[z / 2];
+                acc[z] = fma(c, q.x, acc[z]);
+                acc[z + 1] = fma(c, q.y, acc[z + 1]);
+            }
+        }
     }
     __syncthreads();
 }
 
+// Stencil origins (nearest grid points, R6) of every sorted particle, computed once per
+// evaluation with the exact-rounding decision of stencil_g0 (shared by spread and gather).
+static __global__ void k_stencil_origins(const d4* __restrict__ pos, int N, MidArgs a, int has_mid, double lhx,
+                                         double lhy, double lhpx, double lhpy, int4* __restrict__ g0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const d4 r = ld_d4(&pos[i]);
+    int4 o;
+    if (has_mid) {
+        o.x = stencil_g0(r.x, a.hx, a.hpx);
+        o.y = stencil_g0(r.y, a.hy, a.hpy);
+        o.z = stencil_g0(r.z, a.hz, a.hpz);
+    } else {
+        o.x = o.y = o.z = 0;
+    }
+    const int lx = stencil_g0(r.x, lhx, lhpx), ly = stencil_g0(r.y, lhy, lhpy);
+    o.w = (lx + 32768) | ((ly + 32768) << 16);       // long-grid origins, biased 16-bit fields
+    g0[i] = o;
+}
+
+constexpr int MT_HCAP = 1024;    // hit entries kept per CTA pass
+
 template <int P>
-__global__ void __launch_bounds__(256, 2) k_mid_spread_tile(MidTileArgs t, double* __restrict__ grid) {
+__global__ void __launch_bounds__(256, 2) k_mid_spread_tile(MidTileArgs t, const int4* __restrict__ g0,
+                                                            double* __restrict__ grid) {
     constexpr int p = (P - 1) / 2;
-    extern __shared__ double sW[];                // [MT_B][3P+1] staged weights (dynamic)
-    __shared__ int sO[MT_B * 3];                  // (ox - X0) mod Ix, (oy - Y0) mod Iy, z switch key
+    extern __shared__ double sW[];                // [MT_B][MT_NW(P)] staged weights (dynamic)
+    __shared__ int sO[MT_B * 3];                  // (ox - X0) mod Ix, (oy - Y0) mod Iy, z key
     __shared__ int sIdx[MT_B];
-    __shared__ int sList[8 * MT_B];               // per-warp particle lists
+    __shared__ unsigned short sList[8 * MT_B];    // per-warp particle lists
     __shared__ unsigned char sMask[MT_B];
-    __shared__ int sWarpCnt[8];
+    __shared__ int sHit[MT_HCAP];                 // hit particle indices (deterministic order)
+    __shared__ int sCnt[256];
     const MidArgs& a = t.a;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bz = blockIdx.x % t.ntz, rest = blockIdx.x / t.ntz;
     const int by = rest % t.nty, bx = rest / t.nty;
     const int X0 = bx * MT_X, Y0 = by * MT_Y, Z0 = bz * MT_Z;
     t.Y0 = Y0;
-    const int wx0 = X0 + 4 * (warp & 3), wy0 = Y0 + 8 * (warp >> 2);
-    const int cx = wx0 + (lane & 3), cy = wy0 + (lane >> 2);
+    const int cx = X0 + 4 * (warp & 3) + (lane & 3), cy = Y0 + 8 * (warp >> 2) + (lane >> 2);
     const bool colok = cx < a.Ix && cy < a.Iy;
     double acc[MT_Z];
 #pragma unroll
@@ -285,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) k_mid_spread_tile(MidTileArgs t, doubl
 
     if ((Z0 + MT_Z - 1 + p >= t.gz_lo) && (Z0 - p <= t.gz_hi)) {
         const CellGeo& g = t.g;
-        // candidate cells: stencil centre g0 in [T0 - p, T0 + T - 1 + p]  <=>  x in [lo, hi)
+        // candidate cells: stencil origin in [T0 - P + 1, T0 + T - 1]  <=>  coordinate in [lo, hi)
         auto crange = [&](int T0, int T, double h, double half, double L, double sc, int& c0, int& c1) {
             double lo = ((T0 - p) - 0.5 - half) * h, hi = ((T0 + T - 1 + p) + 0.5 - half) * h;
             c0 = (int)floor((lo + 0.5 * L) * sc) - 1;
@@ -300,46 +267,69 @@ __global__ void __launch_bounds__(256, 2) k_mid_spread_tile(MidTileArgs t, doubl
         cz0 = max(cz0, 0);
         cz1 = min(cz1, g.ncz - 1);
         const int nyc = cy1 - cy0 + 1, ncol = (cx1 - cx0 + 1) * nyc;
-        int nst = 0;                                  // staged count (block-uniform)
-        for (int cc = 0; cc < ncol && cz0 <= cz1; ++cc) {
-            const int ccx = wrapc(cx0 + cc / nyc, g.ncx), ccy = wrapc(cy0 + cc % nyc, g.ncy);
-            const int cbase = (ccx * g.ncy + ccy) * g.ncz;
-            const int j0 = t.start[cbase + cz0], j1 = t.start[cbase + cz1 + 1];
-            for (int jb = j0; jb < j1; jb += 256) {
-                const int j = jb + tid;
-                bool hit = false;
-                int ox = 0, oy = 0, oz = 0;
-                if (j < j1) {
-                    d4 r = ld_d4(&a.pos[j]);
-                    ox = stencil_g0(r.x, a.hx, a.hpx) - p;
-                    oy = stencil_g0(r.y, a.hy, a.hpy) - p;
-                    oz = stencil_g0(r.z, a.hz, a.hpz) - p;
-                    ox = wrapc(ox - X0, a.Ix);
-                    oy = wrapc(oy - Y0, a.Iy);
-                    oz = oz - Z0 + (P - 1);                  // z switch key
-                    hit = (ox < MT_X || ox > a.Ix - P) && (oy < MT_Y || oy > a.Iy - P) && oz >= 0 && oz < MT_Z + P - 1;
+        auto is_hit = [&](int j, int& ox, int& oy, int& key) {
+            const int4 o = g0[j];
+            ox = wrapc(o.x - p - X0, a.Ix);
+            oy = wrapc(o.y - p - Y0, a.Iy);
+            key = o.z - p - Z0 + (P - 1);
+            return (ox < MT_X || ox > a.Ix - P) && (oy < MT_Y || oy > a.Iy - P) && key >= 0 && key < MT_Z + P - 1;
+        };
+        // Phase A: each thread counts the hits among its candidates (column-major cell order)
+        int mycnt = 0;
+        if (cz0 <= cz1)
+            for (int cc = 0; cc < ncol; ++cc) {
+                const int ccx = wrapc(cx0 + cc / nyc, g.ncx), ccy = wrapc(cy0 + cc % nyc, g.ncy);
+                const int cbase = (ccx * g.ncy + ccy) * g.ncz;
+                const int j0 = t.start[cbase + cz0], j1 = t.start[cbase + cz1 + 1];
+                for (int j = j0 + tid; j < j1; j += 256) {
+                    int ox, oy, key;
+                    mycnt += is_hit(j, ox, oy, key) ? 1 : 0;
                 }
-                // deterministic compaction: ballot + prefix over warps in order
-                const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (lane == 0) sWarpCnt[warp] = __popc(m);
+            }
+        sCnt[tid] = mycnt;
+        __syncthreads();
+        // exclusive prefix over threads (deterministic order: thread, then candidate)
+        for (int o = 1; o < 256; o <<= 1) {
+            const int v = tid >= o ? sCnt[tid - o] : 0;
+            __syncthreads();
+            sCnt[tid] += v;
+            __syncthreads();
+        }
+        const int total = sCnt[255];
+        const int myoff = sCnt[tid] - mycnt;
+        __syncthreads();
+        for (int w0 = 0; w0 < total; w0 += MT_HCAP) {          // usually one window
+            // Phase B: write the hits falling in this window
+            if (myoff + mycnt > w0 && myoff < w0 + MT_HCAP && cz0 <= cz1) {
+                int k = myoff;
+                for (int cc = 0; cc < ncol; ++cc) {
+                    const int ccx = wrapc(cx0 + cc / nyc, g.ncx), ccy = wrapc(cy0 + cc % nyc, g.ncy);
+                    const int cbase = (ccx * g.ncy + ccy) * g.ncz;
+                    const int j0 = t.start[cbase + cz0], j1 = t.start[cbase + cz1 + 1];
+                    for (int j = j0 + tid; j < j1; j += 256) {
+                        int ox, oy, key;
+                        if (is_hit(j, ox, oy, key)) {
+                            if (k >= w0 && k < w0 + MT_HCAP) sHit[k - w0] = j;
+                            ++k;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            const int nw = min(MT_HCAP, total - w0);
+            // Phase C: stage and apply in batches of MT_B
+            for (int b0 = 0; b0 < nw; b0 += MT_B) {
+                const int nst = min(MT_B, nw - b0);
+                for (int s = tid; s < nst; s += 256) {
+                    const int j = sHit[b0 + s];
+                    int ox, oy, key;
+                    is_hit(j, ox, oy, key);
+                    sIdx[s] = j; sO[3 * s] = ox; sO[3 * s + 1] = oy; sO[3 * s + 2] = key;
+                }
                 __syncthreads();
-                int off = 0, tot = 0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) { off += w < warp ? sWarpCnt[w] : 0; tot += sWarpCnt[w]; }
-                off += __popc(m & ((1u << lane) - 1));
-                if (nst + tot > MT_B) {                      // flush before it overflows
-                    mid_tile_batch<P>(t, nst, sIdx, sO, sW, sMask, sList, acc, X0, Z0, colok);
-                    nst = 0;
-                }
-                if (hit) {
-                    const int q = nst + off;
-                    sIdx[q] = j; sO[3 * q] = ox; sO[3 * q + 1] = oy; sO[3 * q + 2] = oz;
-                }
-                nst += tot;
-                __syncthreads();
+                mid_tile_batch<P>(t, g0, nst, sIdx, sO, sW, sMask, sList, acc, colok);
             }
         }
-        if (nst > 0) mid_tile_batch<P>(t, nst, sIdx, sO, sW, sMask, sList, acc, X0, Z0, colok);
     }
     // write my column's MT_Z values: every grid point is written exactly once
     if (colok) {

@@ -10,7 +10,9 @@ struct MidArgs;
 struct LongArgs;
 struct LongTileArgs;
 struct MidTileArgs;
-int launch_mid_spread_tile(const MidTileArgs& t, int P, double* grid, cudaStream_t st);
+int launch_mid_spread_tile(const MidTileArgs& t, int P, const int4* g0, double* grid, cudaStream_t st);
+int launch_stencil_origins(const d4* pos, int N, const MidArgs& a, int has_mid, double lhx, double lhy, double lhpx,
+                           double lhpy, int4* g0, cudaStream_t st);
 int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* psiT, d4* out, double gx, double gy,
                         cudaStream_t st);
 int long_pcmax(int Pc);

@@ -89,6 +89,7 @@ struct sog_plan {
     // workspace
     d4 *pos = nullptr, *pos_s = nullptr, *o_near = nullptr, *o_mid = nullptr, *o_long = nullptr;
     int *cell = nullptr, *tmp = nullptr, *perm = nullptr, *count = nullptr, *start = nullptr, *cursor = nullptr;
+    int4* g0 = nullptr;             // stencil origins per sorted particle (mid x,y,z; long packed)
     unsigned* dflags = nullptr;
     double* qsums = nullptr;   // [0] sum q, [1] sum |q|, [2] energy
     double *d_cF = nullptr, *d_cdF = nullptr;
@@ -148,7 +149,7 @@ int upload(sog_plan* pl, T** ptr, const std::vector<T>& v) {
 
 void free_plan(sog_plan* pl) {
     if (!pl) return;
-    void* ptrs[] = {pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
+    void* ptrs[] = {pl->g0, pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
@@ -192,7 +193,7 @@ int setup(sog_plan* pl) {
     int rc;
     if ((rc = dalloc(pl, &pl->pos, N)) || (rc = dalloc(pl, &pl->pos_s, N)) || (rc = dalloc(pl, &pl->o_near, N)) ||
         (rc = dalloc(pl, &pl->o_mid, N)) || (rc = dalloc(pl, &pl->o_long, N)) || (rc = dalloc(pl, &pl->cell, N)) ||
-        (rc = dalloc(pl, &pl->tmp, N)) || (rc = dalloc(pl, &pl->perm, N)) ||
+        (rc = dalloc(pl, &pl->tmp, N)) || (rc = dalloc(pl, &pl->perm, N)) || (rc = dalloc(pl, &pl->g0, N)) ||
         (rc = dalloc(pl, &pl->count, pl->ncell + 1)) || (rc = dalloc(pl, &pl->start, pl->ncell + 1)) ||
         (rc = dalloc(pl, &pl->cursor, pl->ncell + 1)) || (rc = dalloc(pl, &pl->dflags, 1)) ||
         (rc = dalloc(pl, &pl->qsums, 4)) || (rc = upload(pl, &pl->d_cF, pl->near.cF)) ||
@@ -319,6 +320,7 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     const int N = int(p.N);
     cudaStream_t st = pl->stream;
     mark(pl, 0);
+    int rc;
     // S1
     CK(cudaMemsetAsync(pl->count, 0, sizeof(int) * (pl->ncell + 1), st));
     CK(cudaMemsetAsync(pl->dflags, 0, sizeof(unsigned), st));
@@ -328,9 +330,17 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     k_scan<<<1, 1024, 0, st>>>(pl->count, pl->ncell, pl->start, pl->cursor);
     k_scatter<<<nb, 256, 0, st>>>(pl->cell, N, pl->cursor, pl->tmp);
     k_cellsort<<<(pl->ncell * 32 + 255) / 256, 256, 0, st>>>(pl->start, pl->ncell, pl->tmp, pl->pos, pl->pos_s, pl->perm);
+    {
+        const Params& pp = pl->p;
+        MidArgs ma{};
+        if (pl->has_mid) ma = mid_args(pl);
+        const double lhx = pp.hlx(), lhy = pp.hly();
+        if ((rc = lchk(launch_stencil_origins(pl->pos_s, N, ma, pl->has_mid ? 1 : 0, lhx, lhy, 0.5 * pp.Ilx + 0.5,
+                                              0.5 * pp.Ily + 0.5, pl->g0, st))))
+            return rc;
+    }
     CK(cudaGetLastError());
     mark(pl, 1);
-    int rc;
     // S2 near field
     if (!stop_stage) {
         const int D = pl->near.D;
@@ -372,7 +382,7 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         // stencil centres of particles with |z| <= Lz/2 (one extra point of margin each side)
         t.gz_lo = (int)std::floor(-0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) - 1;
         t.gz_hi = (int)std::floor(0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) + 1;
-        if ((rc = lchk(launch_mid_spread_tile(t, p.P, pl->mgrid, st)))) return rc;
+        if ((rc = lchk(launch_mid_spread_tile(t, p.P, pl->g0, pl->mgrid, st)))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
         CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
