@@ -108,8 +108,8 @@ int sog_eval_host(sog_plan* p, const double* xyz, const double* q, double* phi, 
 int sog_eval_components(sog_plan* p, const double* xyz, const double* q, double* out);
 
 /* Intermediate grids for stage parity (device buffer `out` of `len` doubles):
- *   stage 1: mid spread grid S        [Ix][Iy][Izs]            (Alg. 1 step 1)
- *   stage 2: mid scaled field Psi     [Ix][Iy][Izs]            (Alg. 1 step 4)
+ *   stage 1: mid spread grid S        [Izs][Ix][Iy]  (z slowest)  (Alg. 1 step 1)
+ *   stage 2: mid scaled field Psi     [Izs][Ix][Iy]               (Alg. 1 step 4)
  *   stage 3: long proxy grids S_b     [Pc][Ilx][Ily]           (Alg. 2 step 1)
  *   stage 4: long scaled fields Psi_a [Pc][Ilx][Ily]           (Alg. 2 step 4) */
 int sog_debug_stage(sog_plan* p, int stage, const double* xyz, const double* q, double* out, size_t len);

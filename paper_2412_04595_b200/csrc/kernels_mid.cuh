@@ -1,8 +1,17 @@
-// Mid-range Fourier spectral solver (Algorithm 1).
+// Mid-range Fourier spectral solver (Algorithm 1), B200 v3.
 //   S3 gridding  S[g] = sum_j q_j W(x_g-x_j)_* W(y_g-y_j)_* W(z_g-z_j)   (Eq. eq::gridding)
 //   S5 scaling   S_hat <- mult(k) S_hat                                  (Eq. eq::widehat-tilde)
 //   S7 gathering phi_i = V_h sum_g W W W Psi[g] (+ gradient with W')     (Eq. eq::Phiconv)
-// Grid layout: real [Ix][Iy][Izs] row-major (z fastest); half spectrum [Ix][Iy][Izs/2+1].
+//
+// Grid layout (z slowest, y fastest): real [Izs][Ix][Iy]; half spectrum [Izs][Ix][Iy/2+1].
+//
+// Particle order for the mid stencils ("mid order"): bucketed by the key
+//   key = (tx * nty + ty) * nzc + zc,  tx = s_x / MZ_TX, ty = s_y / MZ_TY, zc = s_z / MZ_ZC,
+// where s = g0 - p is the stencil start (x, y wrapped into [0, I)).  Buckets are ordered by
+// cell-sorted index inside (deterministic).  A CTA of the spread owns an MZ_TX x MZ_TY
+// column tile and sweeps z chunk by chunk, every lane holding MZ_ZC + P - 1 consecutive z
+// values of its column in registers (a sliding window): each particle adds P fused
+// multiply-adds per touched column, and every grid point is written exactly once.
 #pragma once
 #include <cuComplex.h>
 #include "kernels_common.cuh"
@@ -19,191 +28,6 @@ struct MidArgs {
     double invH2Sx, invH2Sy, invH2Sz;    // S / H_d^2
     double Vh;                           // h_x h_y h_z
 };
-
-// S5: multiply the half spectrum by mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz].
-static __global__ void k_mid_scale(cuDoubleComplex* __restrict__ spec, int Ix, int Iy, int nz, int L,
-                            const double* __restrict__ A, const double* __restrict__ Tx,
-                            const double* __restrict__ Ty, const double* __restrict__ Tz) {
-    int iz = blockIdx.x * blockDim.x + threadIdx.x;
-    int iy = blockIdx.y, ix = blockIdx.z;
-    if (iz >= nz) return;
-    double mult = 0.0;
-    for (int l = 0; l < L; ++l)
-        mult = fma(A[l] * Tx[(size_t)l * Ix + ix] * Ty[(size_t)l * Iy + iy], Tz[(size_t)l * nz + iz], mult);
-    size_t idx = ((size_t)ix * Iy + iy) * nz + iz;
-    cuDoubleComplex v = spec[idx];
-    spec[idx] = make_cuDoubleComplex(v.x * mult, v.y * mult);
-}
-
-// S7 gather: one thread per particle, separable weights (recurrence) in registers, reads
-// the P^3 stencil of Psi through L1 (particles are cell-sorted, so neighbours share lines).
-template <int P>
-__global__ void __launch_bounds__(128, 4) k_mid_gather(MidArgs a, const double* __restrict__ psi, d4* __restrict__ out,
-                                                       double gamma_x, double gamma_y, double gamma_z) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.N) return;
-    constexpr int p = (P - 1) / 2;
-    d4 r = ld_d4(&a.pos[i]);
-    int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy), gz0 = stencil_g0(r.z, a.hz, a.hpz);
-    double wx[P], wy[P], wz[P], dwx[P], dwy[P], dwz[P];
-    window_weights_rec<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
-    window_weights_rec<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
-    window_weights_rec<P, true>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, gamma_z, wz, dwz);
-    const size_t zb = (size_t)(gz0 - p);
-    double phi = 0, gx = 0, gy = 0, gz = 0;
-    int ix = gx0 - p;
-    ix += ix < 0 ? a.Ix : 0; ix -= ix >= a.Ix ? a.Ix : 0;
-    int iy0 = gy0 - p;
-    iy0 += iy0 < 0 ? a.Iy : 0; iy0 -= iy0 >= a.Iy ? a.Iy : 0;
-#pragma unroll 1
-    for (int u = 0; u < P; ++u) {
-        const double* plane = psi + (size_t)ix * a.Iy * a.Izs + zb;
-        double px = 0, pdz = 0, pdy = 0;
-        int iy = iy0;
-#pragma unroll
-        for (int v = 0; v < P; ++v) {
-            const double* col = plane + (size_t)iy * a.Izs;
-            double t0 = 0, t1 = 0;
-#pragma unroll
-            for (int c = 0; c < P; ++c) {
-                double g = __ldg(col + c);
-                t0 = fma(wz[c], g, t0);
-                t1 = fma(dwz[c], g, t1);
-            }
-            px = fma(wy[v], t0, px);
-            pdy = fma(dwy[v], t0, pdy);
-            pdz = fma(wy[v], t1, pdz);
-            iy = (iy + 1 == a.Iy) ? 0 : iy + 1;
-        }
-        phi = fma(wx[u], px, phi);
-        gx = fma(dwx[u], px, gx);
-        gy = fma(wx[u], pdy, gy);
-        gz = fma(wx[u], pdz, gz);
-        ix = (ix + 1 == a.Ix) ? 0 : ix + 1;
-    }
-    st_d4(&out[i], d4{a.Vh * phi, a.Vh * gx, a.Vh * gy, a.Vh * gz});
-}
-
-}  // namespace sog
-
-namespace sog {
-
-// ---------------------------------------------------------------------------------------
-// S3 v2: output-stationary gridding without atomics.  A CTA owns a 16 x 16 x MT_Z tile of the
-// mid grid; its 8 warps each own a 4 (x) x 8 (y) patch of columns, every lane one column
-// with MT_Z consecutive z values in registers.  The CTA scans the near-field cells that can
-// hold particles whose stencils reach the tile, compacts the hits in cell order (so the
-// summation order is fixed -> deterministic), stages their separable weights in shared
-// memory, and every warp whose patch a particle touches adds c = q Wx Wy (per lane) times
-// Wz (broadcast) into the overlapping z registers, selected by a switch on the z-offset.
-// Every grid point is written exactly once (no memset, no atomics).
-constexpr int MT_X = 16, MT_Y = 16, MT_Z = 24, MT_B = 256;   // MT_B >= threads per CTA
-
-struct MidTileArgs {
-    MidArgs a;
-    const int* start;           // cell start offsets
-    CellGeo g;
-    double gamma_x, gamma_y, gamma_z;
-    int ntx, nty, ntz;
-    int gz_lo, gz_hi;           // range of stencil centres gz0 any particle can have
-    int Y0;                     // tile origin in y (set per CTA)
-};
-
-// v mod n for v in (-2n, 2n) without integer division
-__device__ __forceinline__ int wrapc(int v, int n) {
-    v += v < 0 ? n : 0;
-    v += v < 0 ? n : 0;
-    v -= v >= n ? n : 0;
-    v -= v >= n ? n : 0;
-    return v;
-}
-
-// Stage weights of sIdx[0..nst): Wx[P], Wy[P], q and Wz scattered into the tile's MT_Z
-// z slots (zeros elsewhere) with a 2-bit mask of the non-empty 12-slot halves; build each
-// warp's list of particles touching its 4 x 8 column patch; then every lane adds
-// c = q Wx Wy times the padded Wz into its registers, 12 dense FMAs per touched half
-// (no per-particle branching on the z offset).
-constexpr int MT_NW(int P) { return (2 * P + 1 + MT_Z + 1) & ~1; }   // [Wz padded | Wx | Wy | q], even
-
-template <int P>
-__device__ __forceinline__ void mid_tile_batch(const MidTileArgs& t, const int4* __restrict__ g0, int nst,
-                                               const int* sIdx, int* sO, double* sW, unsigned char* sMask,
-                                               unsigned short* sList, double (&acc)[MT_Z], bool colok) {
-    constexpr int p = (P - 1) / 2;
-    constexpr int NW = MT_NW(P);
-    const MidArgs& a = t.a;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int s = tid; s < nst; s += blockDim.x) {
-        d4 r = ld_d4(&a.pos[sIdx[s]]);
-        const int dxo = sO[3 * s], dyo = sO[3 * s + 1], key = sO[3 * s + 2];
-        // unwrapped stencil centres (the weights need the particle's own periodic image)
-        const int4 o = g0[sIdx[s]];
-        const int gx0 = o.x, gy0 = o.y, gz0 = o.z;
-        double wx[P], wy[P], wz[P];
-        window_weights_rec<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
-        window_weights_rec<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
-        window_weights_rec<P, false>(r.z, gz0, a.hz, a.halfz, a.invH2Sz, t.gamma_z, wz, nullptr);
-        double* wzp = sW + s * NW;                     // 16-byte aligned (NW even)
-        double* w = wzp + MT_Z;
-#pragma unroll
-        for (int k = 0; k < P; ++k) { w[k] = wx[k]; w[P + k] = wy[k]; }
-        w[2 * P] = r.w;
-        const int zs = key - (P - 1);                  // tile slot of stencil point 0
-#pragma unroll
-        for (int z = 0; z < MT_Z; ++z) wzp[z] = 0.0;
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-            if (zs + k >= 0 && zs + k < MT_Z) wzp[zs + k] = wz[k];
-        unsigned m = 0;
-#pragma unroll
-        for (int wq = 0; wq < 8; ++wq) {
-            const int u0 = wrapc(4 * (wq & 3) - dxo, a.Ix), v0 = wrapc(8 * (wq >> 2) - dyo, a.Iy);
-            if ((u0 < P || u0 > a.Ix - 4) && (v0 < P || v0 > a.Iy - 8)) m |= 1u << wq;
-        }
-        sMask[s] = (unsigned char)m;
-        // halves of the z tile that hold stencil points: [zs, zs+P) intersect [0,12) / [12,24)
-        sO[3 * s + 2] = (zs < MT_Z / 2 ? 1 : 0) | (zs + P - 1 >= MT_Z / 2 ? 2 : 0);
-    }
-    __syncthreads();
-    // per-warp compaction of the particles touching this warp's patch (order preserved)
-    unsigned short* myl = sList + warp * MT_B;
-    int nmy = 0;
-    for (int s0 = 0; s0 < nst; s0 += 32) {
-        const int s = s0 + lane;
-        const bool mine = s < nst && ((sMask[s] >> warp) & 1);
-        const unsigned bm = __ballot_sync(0xffffffffu, mine);
-        if (mine) myl[nmy + __popc(bm & ((1u << lane) - 1))] = s;
-        nmy += __popc(bm);
-    }
-    __syncwarp();
-    const int wofx = 4 * (warp & 3) + (lane & 3), wofy = 8 * (warp >> 2) + (lane >> 2);
-    for (int i = 0; i < nmy; ++i) {
-        const int s = myl[i];
-        const double* wzp = sW + s * NW;
-        const double* w = wzp + MT_Z;
-        const int u = wrapc(wofx - sO[3 * s], a.Ix), v = wrapc(wofy - sO[3 * s + 1], a.Iy);
-        const double c = (colok && u < P && v < P) ? w[2 * P] * w[u] * w[P + v] : 0.0;
-        const int halves = sO[3 * s + 2];
-        const double2* wz2 = reinterpret_cast<const double2*>(wzp);
-        if (halves & 1) {
-#pragma unroll
-            for (int z = 0; z < MT_Z / 2; z += 2) {
-                const double2 q = wz2[z / 2];
-                acc[z] = fma(c, q.x, acc[z]);
-                acc[z + 1] = fma(c, q.y, acc[z + 1]);
-            }
-        }
-        if (halves & 2) {
-#pragma unroll
-            for (int z = MT_Z / 2; z < MT_Z; z += 2) {
-                const double2 q = wz2[z / 2];
-                acc[z] = fma(c, q.x, acc[z]);
-                acc[z + 1] = fma(c, q.y, acc[z + 1]);
-            }
-        }
-    }
-    __syncthreads();
-}
 
 // Stencil origins (nearest grid points, R6) of every sorted particle, computed once per
 // evaluation with the exact-rounding decision of stencil_g0 (shared by spread and gather).
@@ -225,126 +49,561 @@ static __global__ void k_stencil_origins(const d4* __restrict__ pos, int N, MidA
     g0[i] = o;
 }
 
-constexpr int MT_HCAP = 1024;    // hit entries kept per CTA pass
+constexpr int MZ_TX = 16, MZ_TY = 16, MZ_ZC = 8;
 
-template <int P>
-__global__ void __launch_bounds__(256, 2) k_mid_spread_tile(MidTileArgs t, const int4* __restrict__ g0,
-                                                            double* __restrict__ grid) {
-    constexpr int p = (P - 1) / 2;
-    extern __shared__ double sW[];                // [MT_B][MT_NW(P)] staged weights (dynamic)
-    __shared__ int sO[MT_B * 3];                  // (ox - X0) mod Ix, (oy - Y0) mod Iy, z key
-    __shared__ int sIdx[MT_B];
-    __shared__ unsigned short sList[8 * MT_B];    // per-warp particle lists
-    __shared__ unsigned char sMask[MT_B];
-    __shared__ int sHit[MT_HCAP];                 // hit particle indices (deterministic order)
-    __shared__ int sCnt[256];
-    const MidArgs& a = t.a;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bz = blockIdx.x % t.ntz, rest = blockIdx.x / t.ntz;
-    const int by = rest % t.nty, bx = rest / t.nty;
-    const int X0 = bx * MT_X, Y0 = by * MT_Y, Z0 = bz * MT_Z;
-    t.Y0 = Y0;
-    const int cx = X0 + 4 * (warp & 3) + (lane & 3), cy = Y0 + 8 * (warp >> 2) + (lane >> 2);
-    const bool colok = cx < a.Ix && cy < a.Iy;
-    double acc[MT_Z];
-#pragma unroll
-    for (int z = 0; z < MT_Z; ++z) acc[z] = 0.0;
+// v mod n for v in (-2n, 2n) without integer division
+__device__ __forceinline__ int wrapc(int v, int n) {
+    v += v < 0 ? n : 0;
+    v += v < 0 ? n : 0;
+    v -= v >= n ? n : 0;
+    v -= v >= n ? n : 0;
+    return v;
+}
 
-    if ((Z0 + MT_Z - 1 + p >= t.gz_lo) && (Z0 - p <= t.gz_hi)) {
-        const CellGeo& g = t.g;
-        // candidate cells: stencil origin in [T0 - P + 1, T0 + T - 1]  <=>  coordinate in [lo, hi)
-        auto crange = [&](int T0, int T, double h, double half, double L, double sc, int& c0, int& c1) {
-            double lo = ((T0 - p) - 0.5 - half) * h, hi = ((T0 + T - 1 + p) + 0.5 - half) * h;
-            c0 = (int)floor((lo + 0.5 * L) * sc) - 1;
-            c1 = (int)floor((hi + 0.5 * L) * sc) + 1;
-        };
-        int cx0, cx1, cy0, cy1, cz0, cz1;
-        crange(X0, MT_X, a.hx, a.halfx, g.Lx, g.sx, cx0, cx1);
-        crange(Y0, MT_Y, a.hy, a.halfy, g.Ly, g.sy, cy0, cy1);
-        crange(Z0, MT_Z, a.hz, a.halfz, g.Lz, g.sz, cz0, cz1);
-        if (cx1 - cx0 + 1 >= g.ncx) { cx0 = 0; cx1 = g.ncx - 1; }
-        if (cy1 - cy0 + 1 >= g.ncy) { cy0 = 0; cy1 = g.ncy - 1; }
-        cz0 = max(cz0, 0);
-        cz1 = min(cz1, g.ncz - 1);
-        const int nyc = cy1 - cy0 + 1, ncol = (cx1 - cx0 + 1) * nyc;
-        auto is_hit = [&](int j, int& ox, int& oy, int& key) {
-            const int4 o = g0[j];
-            ox = wrapc(o.x - p - X0, a.Ix);
-            oy = wrapc(o.y - p - Y0, a.Iy);
-            key = o.z - p - Z0 + (P - 1);
-            return (ox < MT_X || ox > a.Ix - P) && (oy < MT_Y || oy > a.Iy - P) && key >= 0 && key < MT_Z + P - 1;
-        };
-        // Phase A: each thread counts the hits among its candidates (column-major cell order)
-        int mycnt = 0;
-        if (cz0 <= cz1)
-            for (int cc = 0; cc < ncol; ++cc) {
-                const int ccx = wrapc(cx0 + cc / nyc, g.ncx), ccy = wrapc(cy0 + cc % nyc, g.ncy);
-                const int cbase = (ccx * g.ncy + ccy) * g.ncz;
-                const int j0 = t.start[cbase + cz0], j1 = t.start[cbase + cz1 + 1];
-                for (int j = j0 + tid; j < j1; j += 256) {
-                    int ox, oy, key;
-                    mycnt += is_hit(j, ox, oy, key) ? 1 : 0;
-                }
-            }
-        sCnt[tid] = mycnt;
-        __syncthreads();
-        // exclusive prefix over threads (deterministic order: thread, then candidate)
-        for (int o = 1; o < 256; o <<= 1) {
-            const int v = tid >= o ? sCnt[tid - o] : 0;
-            __syncthreads();
-            sCnt[tid] += v;
-            __syncthreads();
+// ---------------------------------------------------------------------------------------
+// Mid-order bucket sort (part of S1).  k_mid_key -> scan -> k_mid_scatter -> k_mid_bucket.
+struct MidSortArgs {
+    int Ix, Iy, p, nty, nzc;
+};
+
+static __global__ void k_mid_key(const int4* __restrict__ g0, int N, MidSortArgs s, int* __restrict__ key,
+                                 int* __restrict__ count) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const int4 o = g0[j];
+    const int sx = wrapc(o.x - s.p, s.Ix), sy = wrapc(o.y - s.p, s.Iy), sz = o.z - s.p;
+    const int k = ((sx / MZ_TX) * s.nty + sy / MZ_TY) * s.nzc + sz / MZ_ZC;
+    key[j] = k;
+    atomicAdd(&count[k], 1);
+}
+
+static __global__ void k_mid_scatter(const int* __restrict__ key, int N, int* __restrict__ cursor,
+                                     int* __restrict__ tmp) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N) tmp[atomicAdd(&cursor[key[j]], 1)] = j;
+}
+
+// One warp per bucket: order members by cell-sorted index (deterministic), gather the
+// particle and its unwrapped stencil starts into mid order.
+static __global__ void k_mid_bucket(const int* __restrict__ mstart, int nkeys, const int* __restrict__ tmp,
+                                    const d4* __restrict__ pos_s, const int4* __restrict__ g0, int p,
+                                    d4* __restrict__ mpos, int4* __restrict__ minfo) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nkeys) return;
+    const int s = mstart[warp], n = mstart[warp + 1] - s;
+    for (int e = lane; e < n; e += 32) {
+        const int my = tmp[s + e];
+        int rank = 0;
+        if (n <= 2048) {
+            for (int f = 0; f < n; ++f) rank += (tmp[s + f] < my);
+        } else {
+            rank = e;   // pathological clustering: arrival order
         }
-        const int total = sCnt[255];
-        const int myoff = sCnt[tid] - mycnt;
-        __syncthreads();
-        for (int w0 = 0; w0 < total; w0 += MT_HCAP) {          // usually one window
-            // Phase B: write the hits falling in this window
-            if (myoff + mycnt > w0 && myoff < w0 + MT_HCAP && cz0 <= cz1) {
-                int k = myoff;
-                for (int cc = 0; cc < ncol; ++cc) {
-                    const int ccx = wrapc(cx0 + cc / nyc, g.ncx), ccy = wrapc(cy0 + cc % nyc, g.ncy);
-                    const int cbase = (ccx * g.ncy + ccy) * g.ncz;
-                    const int j0 = t.start[cbase + cz0], j1 = t.start[cbase + cz1 + 1];
-                    for (int j = j0 + tid; j < j1; j += 256) {
-                        int ox, oy, key;
-                        if (is_hit(j, ox, oy, key)) {
-                            if (k >= w0 && k < w0 + MT_HCAP) sHit[k - w0] = j;
-                            ++k;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            const int nw = min(MT_HCAP, total - w0);
-            // Phase C: stage and apply in batches of MT_B
-            for (int b0 = 0; b0 < nw; b0 += MT_B) {
-                const int nst = min(MT_B, nw - b0);
-                for (int s = tid; s < nst; s += 256) {
-                    const int j = sHit[b0 + s];
-                    int ox, oy, key;
-                    is_hit(j, ox, oy, key);
-                    sIdx[s] = j; sO[3 * s] = ox; sO[3 * s + 1] = oy; sO[3 * s + 2] = key;
-                }
-                __syncthreads();
-                mid_tile_batch<P>(t, g0, nst, sIdx, sO, sW, sMask, sList, acc, colok);
-            }
+        const int4 o = g0[my];
+        st_d4(&mpos[s + rank], ld_d4(&pos_s[my]));
+        minfo[s + rank] = make_int4(my, o.x - p, o.y - p, o.z - p);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+struct MidZArgs {
+    int Ix, Iy, Izs;
+    double hx, hy, hz, halfx, halfy, halfz;
+    double invH2Sx, invH2Sy, invH2Sz, Vh;
+    double gamma_x, gamma_y, gamma_z;     // window recurrence constants exp(-2 a h^2)
+    int ntx, nty, nzc;                    // key space
+    int c_lo, c_hi;                       // chunks that can hold stencil starts
+    int c_hiw;                            // last chunk with nonzero planes (spread writes [c_lo, c_hiw])
+    int cps;                              // chunks per CTA z segment
+    const d4* mpos;
+    const int4* minfo;                    // (cell-sorted index, s_x, s_y, s_z) unwrapped starts
+    const int* mstart;                    // [ntx*nty*nzc + 1]
+};
+
+// spread record in shared memory: [q Wx (P)] [Wy (P)] [Wz (P, padded to P+1)] [hdr int4:
+// dx, dy, o = s_z - chunk base, chunk].  dx, dy are the stencil start relative to the tile
+// origin: signed in [-(P-1), MZ_TX) when the window does not wrap onto itself, else mod I.
+template <int P>
+struct SRec {
+    static constexpr int WX = 0, WY = P, WZ = 2 * P, HDR = 3 * P + 1, SIZE = 3 * P + 3;
+    static constexpr int B = SIZE <= 42 ? 128 : 64;        // particles per staged batch
+    static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane
+    static constexpr int EMAX = 1024;                      // (chunk, home tile) ranges per CTA
+    static constexpr size_t BYTES = sizeof(double) * 2 * B * SIZE + sizeof(int) * (2 * EMAX + 1);
+};
+
+template <int P, int O>
+__device__ __forceinline__ void addz(double (&acc)[SRec<P>::NACC], double c, const double (&wz)[P + 1]) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) acc[O + k] = fma(c, wz[k], acc[O + k]);
+}
+
+// lane flush of one chunk's MZ_ZC planes (written only for c >= cb), then slide the window
+template <int P>
+__device__ __forceinline__ void spread_flush(double (&acc)[SRec<P>::NACC], int c, int cb, bool colok, int cx, int cy,
+                                             const MidZArgs& a, double* __restrict__ grid) {
+    if (c >= cb && colok) {
+#pragma unroll
+        for (int z = 0; z < MZ_ZC; ++z) {
+            const int plane = c * MZ_ZC + z;
+            if (plane < a.Izs) grid[((size_t)plane * a.Ix + cx) * a.Iy + cy] = acc[z];
         }
     }
-    // write my column's MT_Z values: every grid point is written exactly once
-    if (colok) {
-        const size_t o = ((size_t)cx * a.Iy + cy) * a.Izs + Z0;
-        double* col = grid + o;
-        const int nz = min(MT_Z, a.Izs - Z0);
-        if (nz == MT_Z && (o & 1) == 0) {
-            double2* c2 = reinterpret_cast<double2*>(col);
 #pragma unroll
-            for (int z = 0; z < MT_Z; z += 2) c2[z / 2] = make_double2(acc[z], acc[z + 1]);
+    for (int i = 0; i < SRec<P>::NACC; ++i) acc[i] = i + MZ_ZC < SRec<P>::NACC ? acc[i + MZ_ZC] : 0.0;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 2) k_mid_spread_z(MidZArgs a, double* __restrict__ grid) {
+    using R = SRec<P>;
+    constexpr int p = (P - 1) / 2, NACC = R::NACC, B = R::B, EMAX = R::EMAX;
+    extern __shared__ __align__(16) double sRec[];      // [2][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
+    int* sPre = reinterpret_cast<int*>(sRec + 2 * B * R::SIZE);
+    int* sBeg = sPre + EMAX + 1;
+    __shared__ unsigned short sList[8][B];
+    __shared__ unsigned char sMask[2][B];
+    __shared__ int sHx[8], sHy[8], sNh[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tile = blockIdx.x;
+    const int tx = tile / a.nty, ty = tile % a.nty;
+    const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
+    const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
+    const int cx = X0 + lx, cy = Y0 + ly;
+    const bool colok = cx < a.Ix && cy < a.Iy;
+    // z segment: written chunks [cb, ce), sweep from cs (warm-up chunks are not written)
+    const int cb = a.c_lo + blockIdx.y * a.cps;
+    const int ce = min(cb + a.cps, a.c_hiw + 1);
+    if (cb >= ce) return;
+    const int cs = max(a.c_lo, cb - (P - 2 + MZ_ZC) / MZ_ZC);
+    const int cp1 = min(ce, a.c_hi + 1);                 // chunks [cs, cp1) hold particles
+    const bool small = (MZ_TX + P - 1 > a.Ix) || (MZ_TY + P - 1 > a.Iy);
+    // home tiles whose particles can reach this tile (starts in [X0 - P + 1, X0 + TX - 1])
+    if (tid == 0) {
+        int n = 0;
+        if (MZ_TX + P - 1 >= a.Ix) {
+            for (int h = 0; h < a.ntx && n < 8; ++h) sHx[n++] = h;
+        } else {
+            int h = wrapc(X0 - (P - 1), a.Ix) / MZ_TX;
+            for (;;) { sHx[n++] = h; if (h == tx || n == 8) break; h = h + 1 == a.ntx ? 0 : h + 1; }
+        }
+        sNh[0] = n;
+        n = 0;
+        if (MZ_TY + P - 1 >= a.Iy) {
+            for (int h = 0; h < a.nty && n < 8; ++h) sHy[n++] = h;
+        } else {
+            int h = wrapc(Y0 - (P - 1), a.Iy) / MZ_TY;
+            for (;;) { sHy[n++] = h; if (h == ty || n == 8) break; h = h + 1 == a.nty ? 0 : h + 1; }
+        }
+        sNh[1] = n;
+    }
+    __syncthreads();
+    const int nhx = sNh[0], nhy = sNh[1], nh = nhx * nhy;
+    // candidate stream: for chunk c in [cs, cp1), for home tile h: mid-order range (c, h)
+    const int E = max(0, min(EMAX, (cp1 - cs) * nh));
+    for (int e = tid; e < E; e += blockDim.x) {
+        const int c = cs + e / nh, h = e % nh;
+        const int k = (sHx[h / nhy] * a.nty + sHy[h % nhy]) * a.nzc + c;
+        const int b = a.mstart[k];
+        sBeg[e] = b;
+        sPre[e + 1] = a.mstart[k + 1] - b;
+    }
+    __syncthreads();
+    if (warp == 0) {                                     // inclusive scan of the range lengths
+        int run = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            int v = e0 + lane < E ? sPre[e0 + lane + 1] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            if (e0 + lane < E) sPre[e0 + lane + 1] = run + v;
+            run += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) sPre[0] = 0;
+    }
+    __syncthreads();
+    const int total = sPre[E];
+    const int nbat = (total + B - 1) / B;
+
+    // stage candidate slots of batch `bi` into buffer bi & 1: two threads per particle
+    auto stage = [&](int bi) {
+        const int s = tid >> 1, role = tid & 1;
+        const int idx = bi * B + s;
+        if (s >= B) return;
+        double* rec = sRec + ((bi & 1) * B + s) * R::SIZE;
+        if (idx >= total) {
+            if (role == 0) sMask[bi & 1][s] = 0;
+            return;
+        }
+        int lo = 0, hi = E;                              // last e with sPre[e] <= idx
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sPre[mid] <= idx) lo = mid; else hi = mid;
+        }
+        const int c = cs + lo / nh;
+        const int k = sBeg[lo] + (idx - sPre[lo]);
+        const int4 in = a.minfo[k];
+        int dx = wrapc(in.y - X0, a.Ix), dy = wrapc(in.z - Y0, a.Iy);
+        unsigned mx = 0, my = 0;
+        if (!small) {
+            dx -= dx > a.Ix - P ? a.Ix : 0;              // signed start in [-(P-1), MZ_TX)
+            dy -= dy > a.Iy - P ? a.Iy : 0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) mx |= (dx <= 4 * g + 3 && dx + P - 1 >= 4 * g) ? 1u << g : 0u;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) my |= (dy <= 8 * g + 7 && dy + P - 1 >= 8 * g) ? 1u << g : 0u;
         } else {
 #pragma unroll
-            for (int z = 0; z < MT_Z; ++z)
-                if (z < nz) col[z] = acc[z];
+            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (wrapc(4 * g + i - dx, a.Ix) < P) mx |= 1u << g;
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (wrapc(8 * g + i - dy, a.Iy) < P) my |= 1u << g;
         }
+        unsigned mask = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+            if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
+        if (role == 0) {
+            sMask[bi & 1][s] = (unsigned char)mask;
+            *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, in.w - c * MZ_ZC, c);
+        }
+        if (!mask) return;
+        const d4 r = ld_d4(&a.mpos[k]);
+        if (role == 0) {
+            double wz[P];
+            window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
+#pragma unroll
+            for (int i = 0; i < P; ++i) rec[R::WZ + i] = wz[i];
+            rec[R::WZ + P] = 0.0;
+        } else {
+            double wx[P], wy[P];
+            window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
+            window_weights_rec<P, false>(r.y, in.z + p, a.hy, a.halfy, a.invH2Sy, a.gamma_y, wy, nullptr);
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                rec[R::WX + i] = r.w * wx[i];
+                rec[R::WY + i] = wy[i];
+            }
+        }
+    };
+
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+    int cur = cs;                                        // chunk held in acc[0, MZ_ZC)
+
+    if (nbat > 0) stage(0);
+    __syncthreads();
+    for (int bi = 0; bi < nbat; ++bi) {
+        if (bi + 1 < nbat) stage(bi + 1);
+        const int buf = bi & 1;
+        const int nb = min(B, total - bi * B);
+        int nmy = 0;                                     // this warp's particles, stream order
+        for (int s0 = 0; s0 < nb; s0 += 32) {
+            const int s = s0 + lane;
+            const bool mine = s < nb && ((sMask[buf][s] >> warp) & 1);
+            const unsigned bm = __ballot_sync(0xffffffffu, mine);
+            if (mine) sList[warp][nmy + __popc(bm & ((1u << lane) - 1))] = (unsigned short)s;
+            nmy += __popc(bm);
+        }
+        __syncwarp();
+        const double* base = sRec + buf * B * R::SIZE;
+        for (int i = 0; i < nmy; ++i) {
+            const double* rec = base + sList[warp][i] * R::SIZE;
+            const int4 hdr = *reinterpret_cast<const int4*>(rec + R::HDR);
+            while (cur < hdr.w) {                        // warp-uniform: entering a later chunk
+                spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
+                ++cur;
+            }
+            int u, v;
+            if (!small) { u = lx - hdr.x; v = ly - hdr.y; }
+            else { u = wrapc(lx - hdr.x, a.Ix); v = wrapc(ly - hdr.y, a.Iy); }
+            const bool in = (unsigned)u < (unsigned)P && (unsigned)v < (unsigned)P;
+            const double cc = in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : 0.0;
+            double wz[P + 1];
+            const double2* w2 = reinterpret_cast<const double2*>(rec + R::WZ);
+#pragma unroll
+            for (int k = 0; k < (P + 1) / 2; ++k) {
+                const double2 t = w2[k];
+                wz[2 * k] = t.x;
+                wz[2 * k + 1] = t.y;
+            }
+            switch (hdr.z) {
+                case 0: addz<P, 0>(acc, cc, wz); break;
+                case 1: addz<P, 1>(acc, cc, wz); break;
+                case 2: addz<P, 2>(acc, cc, wz); break;
+                case 3: addz<P, 3>(acc, cc, wz); break;
+                case 4: addz<P, 4>(acc, cc, wz); break;
+                case 5: addz<P, 5>(acc, cc, wz); break;
+                case 6: addz<P, 6>(acc, cc, wz); break;
+                default: addz<P, 7>(acc, cc, wz); break;
+            }
+        }
+        __syncthreads();
+    }
+    while (cur < ce) {
+        spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
+        ++cur;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// S7 gather: a CTA owns the particles whose stencil starts lie in its MZ_TX x MZ_TY tile and
+// one z segment.  It keeps a ring of Psi planes of the tile window (MZ_TX + P - 1) x
+// (MZ_TY + P - 1) in shared memory and advances it chunk by chunk; a warp gathers one
+// particle at a time, lanes over the P x P stencil columns (z contracted per lane, then the
+// separable x/y weights), and reduces the four values with shuffles.  Three lanes compute
+// the particle's separable weights (Gaussian recurrence, one axis each).
+template <int P>
+struct GRing {
+    static constexpr int WX = MZ_TX + P - 1, WY = MZ_TY + P - 1;
+    static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
+    static constexpr int PL = WX * WYP;                           // plane size (doubles)
+    static constexpr int D = MZ_ZC + P - 1;                       // planes in the ring
+    static constexpr int WSZ = 6 * P + 2;                         // per-warp weight scratch
+    static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
+    static constexpr size_t BYTES = sizeof(double) * (size_t(D) * PL + 8 * WSZ);
+    static constexpr bool FITS = BYTES <= 227 * 1024;
+    static constexpr int MINB = BYTES <= 113 * 1024 ? 2 : 1;     // CTAs per SM
+};
+
+template <int P>
+__global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a, const double* __restrict__ psi,
+                                                         d4* __restrict__ out) {
+    using G = GRing<P>;
+    constexpr int D = G::D, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
+    extern __shared__ __align__(16) double sm[];
+    double* ring = sm;                                   // [D][WX][WYP]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* wsc = sm + D * PL + warp * G::WSZ;           // Wx dWx Wy dWy Wz dWz
+    const int tile = blockIdx.x;
+    const int tx = tile / a.nty, ty = tile % a.nty;
+    const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
+    const int cb = a.c_lo + blockIdx.y * a.cps;
+    const int ce = min(cb + a.cps, a.c_hi + 1);
+    // this lane's stencil columns (a, b), row-major over P x P
+    int coff[NR], ca[NR], cbb[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int idx = lane + 32 * r;
+        ca[r] = idx < P * P ? idx / P : 0;
+        cbb[r] = idx < P * P ? idx - ca[r] * P : 0;
+        coff[r] = ca[r] * WYP + cbb[r];
+    }
+    // lane ax < 3: axis parameters for the weight recurrence
+    const int ax = min(lane, 2);
+    const double h = ax == 0 ? a.hx : (ax == 1 ? a.hy : a.hz);
+    const double half = ax == 0 ? a.halfx : (ax == 1 ? a.halfy : a.halfz);
+    const double al = ax == 0 ? a.invH2Sx : (ax == 1 ? a.invH2Sy : a.invH2Sz);
+    const double gam = ax == 0 ? a.gamma_x : (ax == 1 ? a.gamma_y : a.gamma_z);
+    int zl = 0, zh = 0;                                  // planes [zl, zh) resident
+    for (int c = cb; c < ce; ++c) {
+        const int key = tile * a.nzc + c;
+        const int k0 = a.mstart[key], k1 = a.mstart[key + 1];
+        if (k0 == k1) continue;
+        const int nlo = c * MZ_ZC, nhi = min(c * MZ_ZC + D, a.Izs);
+        const int from = (zh > nlo && zl <= nlo) ? zh : nlo;
+        __syncthreads();                                 // previous chunk's readers are done
+        {
+            constexpr int NPL = WX * WY;
+            const int nload = (nhi - from) * NPL;
+            for (int e0 = tid; e0 < nload; e0 += 4 * 256) {
+                double v[4];
+                int dst[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * 256;
+                    dst[u] = -1;
+                    if (e < nload) {
+                        const int pz = e / NPL, rem = e - pz * NPL;
+                        const int xr = rem / WY, yr = rem - xr * WY;
+                        const int plane = from + pz;
+                        const int gx = wrapc(X0 + xr, a.Ix), gy = wrapc(Y0 + yr, a.Iy);
+                        v[u] = __ldg(&psi[((size_t)plane * a.Ix + gx) * a.Iy + gy]);
+                        dst[u] = (plane % D) * PL + xr * WYP + yr;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (dst[u] >= 0) ring[dst[u]] = v[u];
+            }
+        }
+        zl = nlo;
+        zh = nhi;
+        __syncthreads();
+        for (int k = k0 + warp; k < k1; k += 8) {
+            const int4 in = a.minfo[k];
+            const d4 r = ld_d4(&a.mpos[k]);
+            if (lane < 3) {                              // weights of axis `lane` (recurrence)
+                const double x = lane == 0 ? r.x : (lane == 1 ? r.y : r.z);
+                const int s = lane == 0 ? in.y : (lane == 1 ? in.z : in.w);
+                const double d0 = ((double)s - half) * h - x;
+                double w = exp(-al * d0 * d0);
+                double q = exp(-al * h * (2.0 * d0 + h));
+                double* o = wsc + 2 * lane * P;
+#pragma unroll
+                for (int i = 0; i < P; ++i) {
+                    o[i] = w;
+                    o[P + i] = 2.0 * al * (d0 + i * h) * w;
+                    w *= q;
+                    q *= gam;
+                }
+            }
+            __syncwarp();
+            double wz[P], dwz[P];
+#pragma unroll
+            for (int i = 0; i < P; ++i) { wz[i] = wsc[4 * P + i]; dwz[i] = wsc[5 * P + i]; }
+            const int sxr = in.y - X0 + (in.y < 0 ? a.Ix : 0);   // start relative to the tile (in [0, MZ_TX))
+            const int syr = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
+            int pb[P];                                   // ring plane offsets of the P stencil planes
+            {
+                int zs = in.w % D;
+#pragma unroll
+                for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == D ? 0 : zs + 1; }
+            }
+            const double* base = ring + sxr * WYP + syr;
+            double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+            for (int rr = 0; rr < NR; ++rr) {
+                if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                const double* col = base + coff[rr];
+                double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+                for (int kz = 0; kz < P; ++kz) {
+                    const double v = col[pb[kz]];
+                    t0 = fma(wz[kz], v, t0);
+                    t1 = fma(dwz[kz], v, t1);
+                }
+                const double wx = wsc[ca[rr]], dwx = wsc[P + ca[rr]];
+                const double wy = wsc[2 * P + cbb[rr]], dwy = wsc[3 * P + cbb[rr]];
+                const double wxy = wx * wy;
+                phi = fma(wxy, t0, phi);
+                gz = fma(wxy, t1, gz);
+                gx = fma(dwx * wy, t0, gx);
+                gy = fma(wx * dwy, t0, gy);
+            }
+            // 4-value butterfly: after the first two levels each lane carries one value
+            {
+                const bool b1 = lane & 1;
+                double s0 = b1 ? phi : gx, s1 = b1 ? gy : gz;     // sent
+                double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;   // kept
+                k0v += __shfl_xor_sync(0xffffffffu, s0, 1);
+                k1v += __shfl_xor_sync(0xffffffffu, s1, 1);
+                const bool b2 = lane & 2;
+                double s = b2 ? k0v : k1v, kk = b2 ? k1v : k0v;
+                kk += __shfl_xor_sync(0xffffffffu, s, 2);
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
+                // lane&3: 0 -> phi, 1 -> gx, 2 -> gy, 3 -> gz (one 32-byte sector)
+                if (lane < 4) reinterpret_cast<double*>(&out[in.x])[lane] = a.Vh * kk;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+
+// S7 gather for wide windows whose plane ring does not fit in shared memory: same work split
+// (warp per particle, lanes over stencil columns) reading Psi through L1.
+template <int P>
+__global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* __restrict__ psi,
+                                                      d4* __restrict__ out, int nmid) {
+    __shared__ double wsm[8][6 * P + 2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* wsc = wsm[warp];
+    const int ax = min(lane, 2);
+    const double h = ax == 0 ? a.hx : (ax == 1 ? a.hy : a.hz);
+    const double half = ax == 0 ? a.halfx : (ax == 1 ? a.halfy : a.halfz);
+    const double al = ax == 0 ? a.invH2Sx : (ax == 1 ? a.invH2Sy : a.invH2Sz);
+    const double gam = ax == 0 ? a.gamma_x : (ax == 1 ? a.gamma_y : a.gamma_z);
+    const size_t plane = (size_t)a.Ix * a.Iy;
+    for (int k = blockIdx.x * 8 + warp; k < nmid; k += gridDim.x * 8) {
+        const int4 in = a.minfo[k];
+        const d4 r = ld_d4(&a.mpos[k]);
+        if (lane < 3) {
+            const double x = lane == 0 ? r.x : (lane == 1 ? r.y : r.z);
+            const int s = lane == 0 ? in.y : (lane == 1 ? in.z : in.w);
+            const double d0 = ((double)s - half) * h - x;
+            double w = exp(-al * d0 * d0);
+            double q = exp(-al * h * (2.0 * d0 + h));
+            double* o = wsc + 2 * lane * P;
+            for (int i = 0; i < P; ++i) {
+                o[i] = w;
+                o[P + i] = 2.0 * al * (d0 + i * h) * w;
+                w *= q;
+                q *= gam;
+            }
+        }
+        __syncwarp();
+        double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+        const double* zb = psi + (size_t)in.w * plane;
+        for (int idx = lane; idx < P * P; idx += 32) {
+            const int ai = idx / P, bi = idx - ai * P;
+            const int ix = wrapc(in.y + ai, a.Ix), iy = wrapc(in.z + bi, a.Iy);
+            const double* col = zb + (size_t)ix * a.Iy + iy;
+            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int kz = 0; kz < P; ++kz) {
+                const double v = __ldg(col + kz * plane);
+                t0 = fma(wsc[4 * P + kz], v, t0);
+                t1 = fma(wsc[5 * P + kz], v, t1);
+            }
+            const double wx = wsc[ai], dwx = wsc[P + ai], wy = wsc[2 * P + bi], dwy = wsc[3 * P + bi];
+            phi = fma(wx * wy, t0, phi);
+            gz = fma(wx * wy, t1, gz);
+            gx = fma(dwx * wy, t0, gx);
+            gy = fma(wx * dwy, t0, gy);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            phi += __shfl_xor_sync(0xffffffffu, phi, o);
+            gx += __shfl_xor_sync(0xffffffffu, gx, o);
+            gy += __shfl_xor_sync(0xffffffffu, gy, o);
+            gz += __shfl_xor_sync(0xffffffffu, gz, o);
+        }
+        if (lane == 0) st_d4(&out[in.x], d4{a.Vh * phi, a.Vh * gx, a.Vh * gy, a.Vh * gz});
+        __syncwarp();
+    }
+}
+
+// S5: multiply the half spectrum [Izs][Ix][Iy/2+1] by mult(k) = sum_{l<=m} A_l Tz[l][iz]
+// Tx[l][ix] Ty[l][iy].  A CTA owns MS_ROWS (iz, ix) rows: the per-row factors
+// A_l Tz Tx go to shared memory, each thread keeps Ty[l][iy] of its iy in registers.
+constexpr int MS_ROWS = 16;
+template <int LM>
+__global__ void __launch_bounds__(128) k_mid_scale(cuDoubleComplex* __restrict__ spec, int Ix, int Izs, int nyh, int L,
+                                                   const double* __restrict__ A, const double* __restrict__ Tx,
+                                                   const double* __restrict__ Ty, const double* __restrict__ Tz) {
+    __shared__ double sc[MS_ROWS][LM];
+    const int iy = blockIdx.x * blockDim.x + threadIdx.x;
+    const int row0 = blockIdx.y * MS_ROWS, nrows = Izs * Ix;
+    for (int e = threadIdx.x; e < MS_ROWS * LM; e += blockDim.x) {
+        const int r = e / LM, l = e - r * LM, row = row0 + r;
+        double v = 0.0;
+        if (row < nrows && l < L) {
+            const int iz = row / Ix, ix = row - iz * Ix;
+            v = A[l] * Tz[(size_t)l * Izs + iz] * Tx[(size_t)l * Ix + ix];
+        }
+        sc[r][l] = v;
+    }
+    __syncthreads();
+    if (iy >= nyh) return;
+    double ty[LM];
+#pragma unroll
+    for (int l = 0; l < LM; ++l) ty[l] = l < L ? Ty[(size_t)l * nyh + iy] : 0.0;
+    for (int r = 0; r < MS_ROWS && row0 + r < nrows; ++r) {
+        double m = 0.0;
+#pragma unroll
+        for (int l = 0; l < LM; ++l) m = fma(sc[r][l], ty[l], m);
+        const size_t idx = (size_t)(row0 + r) * nyh + iy;
+        const cuDoubleComplex v = spec[idx];
+        spec[idx] = make_cuDoubleComplex(v.x * m, v.y * m);
     }
 }
 

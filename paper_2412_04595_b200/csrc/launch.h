@@ -2,21 +2,32 @@
 // instantiations compile in parallel).  Return 0 on success, 1 for an unsupported template
 // parameter, 2 for a CUDA launch error (query cudaGetLastError()).
 #pragma once
+#include <cuComplex.h>
 #include <cuda_runtime.h>
 #include "kernels_common.cuh"
 
 namespace sog {
 struct MidArgs;
+struct MidSortArgs;
+struct MidZArgs;
 struct LongArgs;
 struct LongTileArgs;
-struct MidTileArgs;
-int launch_mid_spread_tile(const MidTileArgs& t, int P, const int4* g0, double* grid, cudaStream_t st);
 int launch_stencil_origins(const d4* pos, int N, const MidArgs& a, int has_mid, double lhx, double lhy, double lhpx,
                            double lhpy, int4* g0, cudaStream_t st);
+int launch_mid_sort_keys(const int4* g0, int N, const MidSortArgs& s, int* key, int* count, cudaStream_t st);
+int launch_mid_sort_place(const int* key, int N, int* cursor, int* tmp, const int* mstart, int nkeys, const d4* pos_s,
+                          const int4* g0, int p, d4* mpos, int4* minfo, cudaStream_t st);
+int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, double* grid, cudaStream_t st);
+int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st);
+size_t mid_gather_smem(int P);
+int mid_spread_emax();
+int launch_mid_scale(cuDoubleComplex* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx,
+                     const double* Ty, const double* Tz, cudaStream_t st);
 int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* psiT, d4* out, double gx, double gy,
                         cudaStream_t st);
 int long_pcmax(int Pc);
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
-int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, double gx, double gy, double gz,
-                      cudaStream_t st);
+// exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total); temp from scan_temp_bytes
+size_t scan_temp_bytes(int n);
+int launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes, cudaStream_t st);
 }  // namespace sog

@@ -6,38 +6,85 @@ namespace sog {
 
 #define SOG_ODD_P(M) M(5) M(7) M(9) M(11) M(13) M(15) M(17) M(19) M(21) M(23) M(25)
 
-int launch_mid_gather(const MidArgs& a, int P, const double* psi, d4* out, double gx, double gy, double gz,
-                      cudaStream_t st) {
-    int nb = (a.N + 127) / 128;
-    switch (P) {
-#define C_(P_) case P_: k_mid_gather<P_><<<nb, 128, 0, st>>>(a, psi, out, gx, gy, gz); break;
-        SOG_ODD_P(C_)
-#undef C_
-        default: return 1;
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
-}
-
-int launch_mid_spread_tile(const MidTileArgs& t, int P, const int4* g0, double* grid, cudaStream_t st) {
-    const int nblk = t.ntx * t.nty * t.ntz;
-    const size_t sh = sizeof(double) * MT_B * ((2 * P + 2 + MT_Z) & ~1);
-    switch (P) {
-#define C_(P_)                                                                                          \
-    case P_:                                                                                            \
-        if (cudaFuncSetAttribute(k_mid_spread_tile<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                 (int)sh) != cudaSuccess) return 2;                                     \
-        k_mid_spread_tile<P_><<<nblk, 256, sh, st>>>(t, g0, grid);                                      \
-        break;
-        SOG_ODD_P(C_)
-#undef C_
-        default: return 1;
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
-}
-
 int launch_stencil_origins(const d4* pos, int N, const MidArgs& a, int has_mid, double lhx, double lhy, double lhpx,
                            double lhpy, int4* g0, cudaStream_t st) {
     k_stencil_origins<<<(N + 255) / 256, 256, 0, st>>>(pos, N, a, has_mid, lhx, lhy, lhpx, lhpy, g0);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_mid_sort_keys(const int4* g0, int N, const MidSortArgs& s, int* key, int* count, cudaStream_t st) {
+    k_mid_key<<<(N + 255) / 256, 256, 0, st>>>(g0, N, s, key, count);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_mid_sort_place(const int* key, int N, int* cursor, int* tmp, const int* mstart, int nkeys, const d4* pos_s,
+                          const int4* g0, int p, d4* mpos, int4* minfo, cudaStream_t st) {
+    k_mid_scatter<<<(N + 255) / 256, 256, 0, st>>>(key, N, cursor, tmp);
+    k_mid_bucket<<<(int)(((long)nkeys * 32 + 255) / 256), 256, 0, st>>>(mstart, nkeys, tmp, pos_s, g0, p, mpos, minfo);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int P>
+int spread_go(const MidZArgs& a, int nseg, double* grid, cudaStream_t st) {
+    const size_t sh = SRec<P>::BYTES;
+    if (cudaFuncSetAttribute(k_mid_spread_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+        return 2;
+    k_mid_spread_z<P><<<dim3(a.ntx * a.nty, nseg), 256, sh, st>>>(a, grid);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, double* grid, cudaStream_t st) {
+    switch (P) {
+#define C_(P_) case P_: return spread_go<P_>(a, nseg, grid, st);
+        SOG_ODD_P(C_)
+#undef C_
+        default: return 1;
+    }
+}
+
+template <int P>
+int gather_go(const MidZArgs& a, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st) {
+    if constexpr (GRing<P>::FITS) {
+        const size_t sh = GRing<P>::BYTES;
+        if (cudaFuncSetAttribute(k_mid_gather_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+            return 2;
+        k_mid_gather_z<P><<<dim3(a.ntx * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+    } else {
+        k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st) {
+    switch (P) {
+#define C_(P_) case P_: return gather_go<P_>(a, nseg, nmid, psi, out, st);
+        SOG_ODD_P(C_)
+#undef C_
+        default: return 1;
+    }
+}
+
+int mid_spread_emax() { return SRec<11>::EMAX; }
+
+size_t mid_gather_smem(int P) {
+    switch (P) {
+#define C_(P_) case P_: return GRing<P_>::FITS ? GRing<P_>::BYTES : 1;
+        SOG_ODD_P(C_)
+#undef C_
+        default: return 0;
+    }
+}
+
+int launch_mid_scale(cuDoubleComplex* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx,
+                     const double* Ty, const double* Tz, cudaStream_t st) {
+    dim3 g((nyh + 127) / 128, (Izs * Ix + MS_ROWS - 1) / MS_ROWS);
+    if (L <= 8) k_mid_scale<8><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 16) k_mid_scale<16><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 24) k_mid_scale<24><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 32) k_mid_scale<32><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 48) k_mid_scale<48><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 64) k_mid_scale<64><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else return 1;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 

@@ -323,9 +323,10 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
                 T[size_t(l) * n + i] = p.S / (kPi * H * H) * std::exp(-e);
             }
     };
+    // spectrum layout [Izs][Ix][Iy/2+1]: y is the half (real-to-complex) axis
     axis(p.Ix, p.Lx, p.hx(), false, Tx);
-    axis(p.Iy, p.Ly, p.hy(), false, Ty);
-    axis(p.Izs, p.Lzs(), p.hz(), true, Tz);
+    axis(p.Iy, p.Ly, p.hy(), true, Ty);
+    axis(p.Izs, p.Lzs(), p.hz(), false, Tz);
 }
 
 void build_long_kernel(const Params& p, std::vector<double>& K) {

@@ -1,8 +1,9 @@
 // C ABI (include/sog.h) and the per-evaluation orchestration of the SOG hot path on B200.
 //
-//   S1 k_prepare -> k_scan -> k_scatter -> k_cellsort          (validate, canonicalise, cell sort)
-//   S2 k_near                                                   (near field + nothing else)
-//   S3-S7 k_mid_spread -> cuFFT D2Z -> k_mid_scale -> cuFFT Z2D -> k_mid_gather
+//   S1 k_prepare -> scan -> k_scatter -> k_cellsort             (validate, canonicalise, cell sort)
+//      k_stencil_origins -> k_mid_key -> scan -> k_mid_scatter -> k_mid_bucket   (mid order)
+//   S2 k_near3                                                  (near field + nothing else)
+//   S3-S7 k_mid_spread_z -> cuFFT D2Z -> k_mid_scale -> cuFFT Z2D -> k_mid_gather_z
 //   S8-S12 k_long_spread -> cuFFT D2Z (batched 2D) -> k_long_scale -> Z2D -> k_long_gather
 //   S13 k_combine                                               (self term, forces, unpermute, U)
 // cuFFT supplies only the butterflies.  All other steps are the kernels in kernels_*.cuh.
@@ -93,9 +94,17 @@ struct sog_plan {
     unsigned* dflags = nullptr;
     double* qsums = nullptr;   // [0] sum q, [1] sum |q|, [2] energy
     double *d_cF = nullptr, *d_cdF = nullptr;
-    // mid
+    // mid: S (spread output, its zero planes are never rewritten), Psi (inverse FFT output)
     double* mgrid = nullptr;
+    double* mpsi = nullptr;
     cuDoubleComplex* mspec = nullptr;
+    int *mkey = nullptr, *mcount = nullptr, *mstart = nullptr, *mcursor = nullptr, *mtmp = nullptr;
+    d4* mpos = nullptr;
+    int4* minfo = nullptr;
+    int nkeys = 0, nseg_s = 1, nseg_g = 1, mz_cps_g = 1;
+    MidZArgs mz{};
+    void* scan_tmp = nullptr;
+    size_t scan_bytes = 0;
     double *d_A = nullptr, *d_Tx = nullptr, *d_Ty = nullptr, *d_Tz = nullptr;
     cufftHandle mfwd = 0, minv = 0;
     bool has_mid = false;
@@ -152,7 +161,9 @@ void free_plan(sog_plan* pl) {
     void* ptrs[] = {pl->g0, pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
-                    pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force};
+                    pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
+                    pl->mpsi, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
+                    pl->scan_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -203,14 +214,57 @@ int setup(sog_plan* pl) {
     // mid range
     pl->has_mid = p.m >= 0;
     if (pl->has_mid) {
-        size_t G = (size_t)p.Ix * p.Iy * p.Izs, Gc = (size_t)p.Ix * p.Iy * (p.Izs / 2 + 1);
-        if ((rc = dalloc(pl, &pl->mgrid, G)) || (rc = dalloc(pl, &pl->mspec, Gc))) return rc;
+        size_t G = (size_t)p.Ix * p.Iy * p.Izs, Gc = (size_t)p.Izs * p.Ix * (p.Iy / 2 + 1);
+        if ((rc = dalloc(pl, &pl->mgrid, G)) || (rc = dalloc(pl, &pl->mpsi, G)) || (rc = dalloc(pl, &pl->mspec, Gc)))
+            return rc;
+        CK(cudaMemset(pl->mgrid, 0, G * sizeof(double)));
+        // mid order (S1) and the z-sweep geometry of the spread / gather
+        MidZArgs& z = pl->mz;
+        const int pp = (p.P - 1) / 2;
+        z.Ix = p.Ix; z.Iy = p.Iy; z.Izs = p.Izs;
+        z.hx = p.hx(); z.hy = p.hy(); z.hz = p.hz();
+        z.halfx = 0.5 * p.Ix; z.halfy = 0.5 * p.Iy; z.halfz = 0.5 * p.Izs;
+        auto inv = [&](double h) { double H = (p.P - 1) * h / 2.0; return p.S / (H * H); };
+        z.invH2Sx = inv(z.hx); z.invH2Sy = inv(z.hy); z.invH2Sz = inv(z.hz);
+        z.Vh = z.hx * z.hy * z.hz;
+        auto gam = [&](double h) { return std::exp(-2.0 * inv(h) * h * h); };
+        z.gamma_x = gam(z.hx); z.gamma_y = gam(z.hy); z.gamma_z = gam(z.hz);
+        z.ntx = (p.Ix + MZ_TX - 1) / MZ_TX; z.nty = (p.Iy + MZ_TY - 1) / MZ_TY; z.nzc = (p.Izs + MZ_ZC - 1) / MZ_ZC;
+        // stencil starts of particles with |z| <= Lz/2 (one point of rounding margin each side)
+        const int g_lo = std::max(pp, (int)std::floor(-0.5 * p.Lz / z.hz + 0.5 * p.Izs + 0.5) - 1);
+        const int g_hi = std::min(p.Izs - 1 - pp, (int)std::floor(0.5 * p.Lz / z.hz + 0.5 * p.Izs + 0.5) + 1);
+        z.c_lo = (g_lo - pp) / MZ_ZC;
+        z.c_hi = (g_hi - pp) / MZ_ZC;
+        z.c_hiw = std::min(z.nzc - 1, (g_hi - pp + p.P - 1) / MZ_ZC);
+        const int ntile = z.ntx * z.nty;
+        auto segs = [&](int nch, int& nseg, int cap) {
+            nseg = std::max(1, std::min(nch, (4 * 148 + ntile - 1) / ntile));
+            int cps = std::min(cap, (nch + nseg - 1) / nseg);
+            nseg = (nch + cps - 1) / cps;
+            return cps;
+        };
+        // spread: (chunks swept incl. warm-up) x (home tiles) must fit the CTA's range table
+        auto nhome = [&](int T, int I, int nt) { return std::min(8, T + p.P - 1 >= I ? nt : (p.P - 1 + T - 1) / T + 2); };
+        const int nh = nhome(MZ_TX, p.Ix, z.ntx) * nhome(MZ_TY, p.Iy, z.nty);
+        const int cap_s = mid_spread_emax() / nh - (p.P - 2 + MZ_ZC) / MZ_ZC;
+        if (cap_s < 1) return fail(SOG_EINVAL, "mid spread range table too small for this grid");
+        const int cps_s = segs(z.c_hiw - z.c_lo + 1, pl->nseg_s, cap_s);
+        const int cps_g = segs(z.c_hi - z.c_lo + 1, pl->nseg_g, 1 << 30);
+        z.cps = cps_s;
+        pl->mz_cps_g = cps_g;
+        pl->nkeys = ntile * z.nzc;
+        if ((rc = dalloc(pl, &pl->mkey, N)) || (rc = dalloc(pl, &pl->mtmp, N)) || (rc = dalloc(pl, &pl->mpos, N)) ||
+            (rc = dalloc(pl, &pl->minfo, N)) || (rc = dalloc(pl, &pl->mcount, pl->nkeys + 1)) ||
+            (rc = dalloc(pl, &pl->mstart, pl->nkeys + 1)) || (rc = dalloc(pl, &pl->mcursor, pl->nkeys + 1)))
+            return rc;
+        z.mpos = pl->mpos; z.minfo = pl->minfo; z.mstart = pl->mstart;
+        if (!mid_gather_smem(p.P)) return fail(SOG_EINVAL, "mid window support outside the compiled range");
         std::vector<double> A, Tx, Ty, Tz;
         build_mid_tables(p, A, Tx, Ty, Tz);
         if ((rc = upload(pl, &pl->d_A, A)) || (rc = upload(pl, &pl->d_Tx, Tx)) || (rc = upload(pl, &pl->d_Ty, Ty)) ||
             (rc = upload(pl, &pl->d_Tz, Tz)))
             return rc;
-        long long n[3] = {p.Ix, p.Iy, p.Izs};
+        long long n[3] = {p.Izs, p.Ix, p.Iy};   // z slowest, y fastest (half axis)
         size_t ws = 0;
         CKF(cufftCreate(&pl->mfwd));
         CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &ws));
@@ -260,6 +314,8 @@ int setup(sog_plan* pl) {
                                 (long long)p.Ilx * p.Ily, CUFFT_Z2D, p.Pc, &ws));
         pl->bytes += ws;
     }
+    pl->scan_bytes = std::max(scan_temp_bytes(pl->ncell), pl->nkeys ? scan_temp_bytes(pl->nkeys) : size_t(0));
+    if ((rc = dalloc(pl, (char**)&pl->scan_tmp, pl->scan_bytes))) return rc;
     for (auto& e : pl->ev) CK(cudaEventCreate(&e));
     return SOG_OK;
 }
@@ -327,7 +383,8 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     CK(cudaMemsetAsync(pl->qsums, 0, sizeof(double) * 4, st));
     int nb = (N + 255) / 256;
     k_prepare<<<nb, 256, 0, st>>>(xyz, q, N, pl->geo, pl->pos, pl->cell, pl->count, pl->dflags, pl->qsums);
-    k_scan<<<1, 1024, 0, st>>>(pl->count, pl->ncell, pl->start, pl->cursor);
+    if ((rc = lchk(launch_exclusive_scan(pl->count, pl->start, pl->ncell, pl->scan_tmp, pl->scan_bytes, st)))) return rc;
+    CK(cudaMemcpyAsync(pl->cursor, pl->start, sizeof(int) * pl->ncell, cudaMemcpyDeviceToDevice, st));
     k_scatter<<<nb, 256, 0, st>>>(pl->cell, N, pl->cursor, pl->tmp);
     k_cellsort<<<(pl->ncell * 32 + 255) / 256, 256, 0, st>>>(pl->start, pl->ncell, pl->tmp, pl->pos, pl->pos_s, pl->perm);
     {
@@ -337,6 +394,17 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         const double lhx = pp.hlx(), lhy = pp.hly();
         if ((rc = lchk(launch_stencil_origins(pl->pos_s, N, ma, pl->has_mid ? 1 : 0, lhx, lhy, 0.5 * pp.Ilx + 0.5,
                                               0.5 * pp.Ily + 0.5, pl->g0, st))))
+            return rc;
+    }
+    if (pl->has_mid) {   // mid order: bucket by (stencil-start tile, z chunk)
+        MidSortArgs ms{p.Ix, p.Iy, (p.P - 1) / 2, pl->mz.nty, pl->mz.nzc};
+        CK(cudaMemsetAsync(pl->mcount, 0, sizeof(int) * (pl->nkeys + 1), st));
+        if ((rc = lchk(launch_mid_sort_keys(pl->g0, N, ms, pl->mkey, pl->mcount, st)))) return rc;
+        if ((rc = lchk(launch_exclusive_scan(pl->mcount, pl->mstart, pl->nkeys, pl->scan_tmp, pl->scan_bytes, st))))
+            return rc;
+        CK(cudaMemcpyAsync(pl->mcursor, pl->mstart, sizeof(int) * pl->nkeys, cudaMemcpyDeviceToDevice, st));
+        if ((rc = lchk(launch_mid_sort_place(pl->mkey, N, pl->mcursor, pl->mtmp, pl->mstart, pl->nkeys, pl->pos_s,
+                                             pl->g0, (p.P - 1) / 2, pl->mpos, pl->minfo, st))))
             return rc;
     }
     CK(cudaGetLastError());
@@ -372,34 +440,22 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     mark(pl, 2);
     // S3-S7 mid range
     if (pl->has_mid && (stop_stage == 0 || stop_stage == 1 || stop_stage == 2)) {
-        MidTileArgs t;
-        t.a = mid_args(pl);
-        t.start = pl->start;
-        t.g = pl->geo;
-        auto gam = [&](double h) { double H = (p.P - 1) * h / 2.0; return std::exp(-2.0 * p.S / (H * H) * h * h); };
-        t.gamma_x = gam(p.hx()); t.gamma_y = gam(p.hy()); t.gamma_z = gam(p.hz());
-        t.ntx = (p.Ix + MT_X - 1) / MT_X; t.nty = (p.Iy + MT_Y - 1) / MT_Y; t.ntz = (p.Izs + MT_Z - 1) / MT_Z;
-        // stencil centres of particles with |z| <= Lz/2 (one extra point of margin each side)
-        t.gz_lo = (int)std::floor(-0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) - 1;
-        t.gz_hi = (int)std::floor(0.5 * p.Lz / p.hz() + 0.5 * p.Izs + 0.5) + 1;
-        if ((rc = lchk(launch_mid_spread_tile(t, p.P, pl->g0, pl->mgrid, st)))) return rc;
+        if ((rc = lchk(launch_mid_spread_z(pl->mz, p.P, pl->nseg_s, pl->mgrid, st)))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
         CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
         mark(pl, 4);
-        int nz = p.Izs / 2 + 1;
-        dim3 gs((nz + 127) / 128, p.Iy, p.Ix);
-        k_mid_scale<<<gs, 128, 0, st>>>(pl->mspec, p.Ix, p.Iy, nz, p.m + 1, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz);
-        CK(cudaGetLastError());
+        if ((rc = lchk(launch_mid_scale(pl->mspec, p.Ix, p.Izs, p.Iy / 2 + 1, p.m + 1, pl->d_A, pl->d_Tx, pl->d_Ty,
+                                        pl->d_Tz, st))))
+            return rc;
         mark(pl, 5);
-        CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mgrid));
+        CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mpsi));
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
         {
-            auto gam = [&](double h) { double H = (p.P - 1) * h / 2.0; return std::exp(-2.0 * p.S / (H * H) * h * h); };
-            if ((rc = lchk(launch_mid_gather(mid_args(pl), p.P, pl->mgrid, pl->o_mid, gam(p.hx()), gam(p.hy()),
-                                             gam(p.hz()), st))))
-                return rc;
+            MidZArgs g = pl->mz;
+            g.cps = pl->mz_cps_g;
+            if ((rc = lchk(launch_mid_gather_z(g, p.P, pl->nseg_g, N, pl->mpsi, pl->o_mid, st)))) return rc;
         }
     } else if (!pl->has_mid && !stop_stage) {
         CK(cudaMemsetAsync(pl->o_mid, 0, sizeof(d4) * N, st));
@@ -577,7 +633,7 @@ int sog_debug_stage(sog_plan* pl, int stage, const double* xyz, const double* q,
     if (stage == 1 || stage == 2) {
         if (!pl->has_mid) return fail(SOG_EINVAL, "plan has no mid-range part (m < 0)");
         need = (size_t)p.Ix * p.Iy * p.Izs;
-        src = pl->mgrid;
+        src = stage == 1 ? pl->mgrid : pl->mpsi;
     } else if (stage == 3 || stage == 4) {
         need = (size_t)p.Pc * p.Ilx * p.Ily;
         src = pl->lgrid;
@@ -636,8 +692,10 @@ int sog_set_stream(sog_plan* pl, void* s) {
 
 int sog_launches_per_eval(const sog_plan* pl) {
     if (!pl) return fail(SOG_EINVAL, "null plan");
-    // prepare, scan, scatter, cellsort, near, [mid: spread, scale, gather], long: spread, scale, gather, combine
-    return 4 + 1 + (pl->has_mid ? 3 : 0) + 3 + 1;
+    // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
+    // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
+    // transpose, gather, combine  (cuFFT launches are not counted)
+    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + 5 + 1;
 }
 
 }  // extern "C"

@@ -59,7 +59,8 @@ struct NearTable {
 };
 bool build_near_table(const Params& p, NearTable& t, std::string& err);
 
-// Mid-range scaling tables: mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz] (R12).
+// Mid-range scaling tables: mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz] (R12);
+// Ty covers the half axis iy < Iy/2+1, Tx and Tz the full axes (fftfreq order).
 void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<double>& Tx,
                       std::vector<double>& Ty, std::vector<double>& Tz);
 // Long-range kernel matrices K[mode][a][b], mode = ix*(Ily/2+1)+iy (R9, R10).

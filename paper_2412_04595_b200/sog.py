@@ -208,11 +208,12 @@ class Plan:
         return out
 
     def debug_stage(self, stage, xyz, q):
-        """Intermediate grid (1: mid spread, 2: mid Psi, 3: long proxies, 4: long Psi)."""
+        """Intermediate grid (1: mid spread, 2: mid Psi, both [Izs][Ix][Iy]; 3: long proxies,
+        4: long Psi, both [Pc][Ilx][Ily]) -- the library's device layouts, unchanged."""
         import torch
         d = self.describe()
         if stage in (1, 2):
-            shape = (d["Ix"], d["Iy"], d["Izs"])
+            shape = (d["Izs"], d["Ix"], d["Iy"])
         else:
             shape = (d["Pc"], d["Ilx"], d["Ily"])
         xyz, q = self._inputs(xyz, q)

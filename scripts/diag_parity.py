@@ -28,7 +28,7 @@ for c, nm in enumerate(("near", "mid", "long")):
           np.abs(po).max(), np.abs(comp[c][:, 0]).max()))
 S_o = O.mid_spread(op, x, q); Psi_o = O.mid_solve(op, S_o)
 Sl_o = O.long_spread(op, x, q); Psil_o = O.long_solve(op, Sl_o)
-for st, ref in ((1, S_o), (2, Psi_o), (3, Sl_o), (4, Psil_o)):
+for st, ref in ((1, S_o.transpose(2, 0, 1)), (2, Psi_o.transpose(2, 0, 1)), (3, Sl_o), (4, Psil_o)):
     g = pl.debug_stage(st, xd, qd).cpu().numpy()
     print("stage", st, "rel %.3e  |ref| %.3e |g| %.3e" % (rel(g, ref), np.abs(ref).max(), np.abs(g).max()))
 phi, F = pl.eval(xd, qd)

@@ -102,7 +102,8 @@ def test_c1_stages():
     Psi_o = O.mid_solve(op, S_o)
     Sl_o = O.long_spread(op, x, q)
     Psil_o = O.long_solve(op, Sl_o)
-    for stage, ref in ((1, S_o), (2, Psi_o), (3, Sl_o), (4, Psil_o)):
+    # the library's mid grids are [Izs][Ix][Iy] (z slowest); the oracle's are [Ix][Iy][Izs]
+    for stage, ref in ((1, S_o.transpose(2, 0, 1)), (2, Psi_o.transpose(2, 0, 1)), (3, Sl_o), (4, Psil_o)):
         g = pl.debug_stage(stage, xd, qd).cpu().numpy()
         assert g.shape == ref.shape
         assert rel(g, ref) <= TOL_FP64, (stage, rel(g, ref))
