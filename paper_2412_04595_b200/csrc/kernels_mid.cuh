@@ -126,11 +126,35 @@ struct MidZArgs {
 template <int P>
 struct SRec {
     static constexpr int WX = 0, WY = P, WZ = 2 * P, HDR = 3 * P + 1, SIZE = 3 * P + 3;
-    static constexpr int B = SIZE <= 42 ? 128 : 64;        // particles per staged batch
+    static constexpr int B = 64;                           // particles per staged batch
+    static constexpr int K = SIZE <= 42 ? 4 : 2;           // batch buffers in flight
     static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane
     static constexpr int EMAX = 1024;                      // (chunk, home tile) ranges per CTA
-    static constexpr size_t BYTES = sizeof(double) * 2 * B * SIZE + sizeof(int) * (2 * EMAX + 1);
+    static constexpr int NPROD = 2;                        // producer warps (32 particles each)
+    static constexpr int NTHR = 32 * (8 + NPROD);
+    static constexpr int MINB = P <= 15 ? 2 : 1;          // CTAs per SM (register budget)
+    static constexpr size_t BYTES = sizeof(double) * K * B * SIZE + sizeof(int) * (2 * EMAX + 1);
 };
+
+// mbarrier helpers (shared::cta)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
 
 template <int P, int O>
 __device__ __forceinline__ void addz(double (&acc)[SRec<P>::NACC], double c, const double (&wz)[P + 1]) {
@@ -153,23 +177,25 @@ __device__ __forceinline__ void spread_flush(double (&acc)[SRec<P>::NACC], int c
     for (int i = 0; i < SRec<P>::NACC; ++i) acc[i] = i + MZ_ZC < SRec<P>::NACC ? acc[i + MZ_ZC] : 0.0;
 }
 
+// Warp-specialised: NPROD producer warps stage the CTA's candidate stream (weights, relevance
+// masks) into K batch buffers; 8 consumer warps (one 4 x 8 column patch each) accumulate
+// their patch's particles.  full/empty mbarriers let consumer warps drift up to K batches
+// apart, so the per-batch imbalance between patches averages out.
 template <int P>
-__global__ void __launch_bounds__(256, 2) k_mid_spread_z(MidZArgs a, double* __restrict__ grid) {
+__global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(MidZArgs a, double* __restrict__ grid) {
     using R = SRec<P>;
-    constexpr int p = (P - 1) / 2, NACC = R::NACC, B = R::B, EMAX = R::EMAX;
-    extern __shared__ __align__(16) double sRec[];      // [2][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
-    int* sPre = reinterpret_cast<int*>(sRec + 2 * B * R::SIZE);
+    constexpr int p = (P - 1) / 2, NACC = R::NACC, B = R::B, K = R::K, EMAX = R::EMAX;
+    extern __shared__ __align__(16) double sRec[];      // [K][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
+    int* sPre = reinterpret_cast<int*>(sRec + K * B * R::SIZE);
     int* sBeg = sPre + EMAX + 1;
     __shared__ unsigned short sList[8][B];
-    __shared__ unsigned char sMask[2][B];
+    __shared__ unsigned char sMask[K][B];
+    __shared__ unsigned long long barFull[K], barEmpty[K];
     __shared__ int sHx[8], sHy[8], sNh[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const int tx = tile / a.nty, ty = tile % a.nty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
-    const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
-    const int cx = X0 + lx, cy = Y0 + ly;
-    const bool colok = cx < a.Ix && cy < a.Iy;
     // z segment: written chunks [cb, ce), sweep from cs (warm-up chunks are not written)
     const int cb = a.c_lo + blockIdx.y * a.cps;
     const int ce = min(cb + a.cps, a.c_hiw + 1);
@@ -195,12 +221,17 @@ __global__ void __launch_bounds__(256, 2) k_mid_spread_z(MidZArgs a, double* __r
             for (;;) { sHy[n++] = h; if (h == ty || n == 8) break; h = h + 1 == a.nty ? 0 : h + 1; }
         }
         sNh[1] = n;
+        for (int b = 0; b < K; ++b) {
+            mbar_init(&barFull[b], 32 * R::NPROD);
+            mbar_init(&barEmpty[b], 8 * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int nhx = sNh[0], nhy = sNh[1], nh = nhx * nhy;
     // candidate stream: for chunk c in [cs, cp1), for home tile h: mid-order range (c, h)
     const int E = max(0, min(EMAX, (cp1 - cs) * nh));
-    for (int e = tid; e < E; e += blockDim.x) {
+    for (int e = tid; e < E; e += R::NTHR) {
         const int c = cs + e / nh, h = e % nh;
         const int k = (sHx[h / nhy] * a.nty + sHy[h % nhy]) * a.nzc + c;
         const int b = a.mstart[k];
@@ -226,86 +257,85 @@ __global__ void __launch_bounds__(256, 2) k_mid_spread_z(MidZArgs a, double* __r
     const int total = sPre[E];
     const int nbat = (total + B - 1) / B;
 
-    // stage candidate slots of batch `bi` into buffer bi & 1: two threads per particle
-    auto stage = [&](int bi) {
-        const int s = tid >> 1, role = tid & 1;
-        const int idx = bi * B + s;
-        if (s >= B) return;
-        double* rec = sRec + ((bi & 1) * B + s) * R::SIZE;
-        if (idx >= total) {
-            if (role == 0) sMask[bi & 1][s] = 0;
-            return;
-        }
-        int lo = 0, hi = E;                              // last e with sPre[e] <= idx
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (sPre[mid] <= idx) lo = mid; else hi = mid;
-        }
-        const int c = cs + lo / nh;
-        const int k = sBeg[lo] + (idx - sPre[lo]);
-        const int4 in = a.minfo[k];
-        int dx = wrapc(in.y - X0, a.Ix), dy = wrapc(in.z - Y0, a.Iy);
-        unsigned mx = 0, my = 0;
-        if (!small) {
-            dx -= dx > a.Ix - P ? a.Ix : 0;              // signed start in [-(P-1), MZ_TX)
-            dy -= dy > a.Iy - P ? a.Iy : 0;
+    if (warp >= 8) {
+        // ---------------- producers: one particle per thread per batch ----------------
+        const int s = (warp - 8) * 32 + lane;
+        for (int bi = 0; bi < nbat; ++bi) {
+            const int buf = bi % K;
+            if (bi >= K) mbar_wait(&barEmpty[buf], ((bi / K) - 1) & 1);
+            const int idx = bi * B + s;
+            double* rec = sRec + (buf * B + s) * R::SIZE;
+            unsigned mask = 0;
+            if (idx < total) {
+                int lo = 0, hi = E;                      // last e with sPre[e] <= idx
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sPre[mid] <= idx) lo = mid; else hi = mid;
+                }
+                const int c = cs + lo / nh;
+                const int k = sBeg[lo] + (idx - sPre[lo]);
+                const int4 in = a.minfo[k];
+                int dx = wrapc(in.y - X0, a.Ix), dy = wrapc(in.z - Y0, a.Iy);
+                unsigned mx = 0, my = 0;
+                if (!small) {
+                    dx -= dx > a.Ix - P ? a.Ix : 0;      // signed start in [-(P-1), MZ_TX)
+                    dy -= dy > a.Iy - P ? a.Iy : 0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) mx |= (dx <= 4 * g + 3 && dx + P - 1 >= 4 * g) ? 1u << g : 0u;
+                    for (int g = 0; g < 4; ++g) mx |= (dx <= 4 * g + 3 && dx + P - 1 >= 4 * g) ? 1u << g : 0u;
 #pragma unroll
-            for (int g = 0; g < 2; ++g) my |= (dy <= 8 * g + 7 && dy + P - 1 >= 8 * g) ? 1u << g : 0u;
-        } else {
+                    for (int g = 0; g < 2; ++g) my |= (dy <= 8 * g + 7 && dy + P - 1 >= 8 * g) ? 1u << g : 0u;
+                } else {
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
+                    for (int g = 0; g < 4; ++g)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (wrapc(4 * g + i - dx, a.Ix) < P) mx |= 1u << g;
+                        for (int i = 0; i < 4; ++i)
+                            if (wrapc(4 * g + i - dx, a.Ix) < P) mx |= 1u << g;
 #pragma unroll
-            for (int g = 0; g < 2; ++g)
+                    for (int g = 0; g < 2; ++g)
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (wrapc(8 * g + i - dy, a.Iy) < P) my |= 1u << g;
-        }
-        unsigned mask = 0;
+                        for (int i = 0; i < 8; ++i)
+                            if (wrapc(8 * g + i - dy, a.Iy) < P) my |= 1u << g;
+                }
 #pragma unroll
-        for (int w = 0; w < 8; ++w)
-            if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
-        if (role == 0) {
-            sMask[bi & 1][s] = (unsigned char)mask;
-            *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, in.w - c * MZ_ZC, c);
-        }
-        if (!mask) return;
-        const d4 r = ld_d4(&a.mpos[k]);
-        if (role == 0) {
-            double wz[P];
-            window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
+                for (int w = 0; w < 8; ++w)
+                    if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
+                *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, in.w - c * MZ_ZC, c);
+                if (mask) {
+                    const d4 r = ld_d4(&a.mpos[k]);
+                    double wx[P], wy[P], wz[P];
+                    window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
+                    window_weights_rec<P, false>(r.y, in.z + p, a.hy, a.halfy, a.invH2Sy, a.gamma_y, wy, nullptr);
+                    window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
 #pragma unroll
-            for (int i = 0; i < P; ++i) rec[R::WZ + i] = wz[i];
-            rec[R::WZ + P] = 0.0;
-        } else {
-            double wx[P], wy[P];
-            window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
-            window_weights_rec<P, false>(r.y, in.z + p, a.hy, a.halfy, a.invH2Sy, a.gamma_y, wy, nullptr);
-#pragma unroll
-            for (int i = 0; i < P; ++i) {
-                rec[R::WX + i] = r.w * wx[i];
-                rec[R::WY + i] = wy[i];
+                    for (int i = 0; i < P; ++i) {
+                        rec[R::WX + i] = r.w * wx[i];
+                        rec[R::WY + i] = wy[i];
+                        rec[R::WZ + i] = wz[i];
+                    }
+                    rec[R::WZ + P] = 0.0;
+                }
             }
+            sMask[buf][s] = (unsigned char)mask;
+            mbar_arrive(&barFull[buf]);
         }
-    };
+        return;
+    }
 
+    // ---------------- consumers: warp = one 4 x 8 column patch ----------------
+    const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
+    const int cx = X0 + lx, cy = Y0 + ly;
+    const bool colok = cx < a.Ix && cy < a.Iy;
     double acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
     int cur = cs;                                        // chunk held in acc[0, MZ_ZC)
-
-    if (nbat > 0) stage(0);
-    __syncthreads();
     for (int bi = 0; bi < nbat; ++bi) {
-        if (bi + 1 < nbat) stage(bi + 1);
-        const int buf = bi & 1;
+        const int buf = bi % K;
+        mbar_wait(&barFull[buf], (bi / K) & 1);
         const int nb = min(B, total - bi * B);
         int nmy = 0;                                     // this warp's particles, stream order
-        for (int s0 = 0; s0 < nb; s0 += 32) {
+#pragma unroll
+        for (int s0 = 0; s0 < B; s0 += 32) {
             const int s = s0 + lane;
             const bool mine = s < nb && ((sMask[buf][s] >> warp) & 1);
             const unsigned bm = __ballot_sync(0xffffffffu, mine);
@@ -345,7 +375,8 @@ __global__ void __launch_bounds__(256, 2) k_mid_spread_z(MidZArgs a, double* __r
                 default: addz<P, 7>(acc, cc, wz); break;
             }
         }
-        __syncthreads();
+        __syncwarp();
+        mbar_arrive(&barEmpty[buf]);
     }
     while (cur < ce) {
         spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);

@@ -29,7 +29,7 @@ int spread_go(const MidZArgs& a, int nseg, double* grid, cudaStream_t st) {
     const size_t sh = SRec<P>::BYTES;
     if (cudaFuncSetAttribute(k_mid_spread_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
         return 2;
-    k_mid_spread_z<P><<<dim3(a.ntx * a.nty, nseg), 256, sh, st>>>(a, grid);
+    k_mid_spread_z<P><<<dim3(a.ntx * a.nty, nseg), SRec<P>::NTHR, sh, st>>>(a, grid);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 

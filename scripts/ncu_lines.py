@@ -43,3 +43,18 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def reasons(path, lines):
+    """Stall-reason breakdown of the given source line numbers."""
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    for r in rows:
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr and r and r[0] in lines and len(r) == len(hdr):
+            cols = [(h, float(v)) for h, v in zip(hdr, r) if h.startswith("stall_") and "Not Issued" not in h
+                    and v not in ("", "-")]
+            cols = sorted(cols, key=lambda t: -t[1])[:6]
+            print(r[0], r[1][:50], " ".join(f"{h[6:]}={v:.0f}" for h, v in cols))
