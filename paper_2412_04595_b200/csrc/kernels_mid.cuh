@@ -49,7 +49,7 @@ static __global__ void k_stencil_origins(const d4* __restrict__ pos, int N, MidA
     g0[i] = o;
 }
 
-constexpr int MZ_TX = 16, MZ_TY = 16, MZ_ZC = 8;
+constexpr int MZ_TX = 16, MZ_TY = 16, MZ_ZC = 4;
 
 // v mod n for v in (-2n, 2n) without integer division
 __device__ __forceinline__ int wrapc(int v, int n) {
@@ -120,15 +120,18 @@ struct MidZArgs {
     const int* mstart;                    // [ntx*nty*nzc + 1]
 };
 
-// spread record in shared memory: [q Wx (P)] [Wy (P)] [Wz (P, padded to P+1)] [hdr int4:
-// dx, dy, o = s_z - chunk base, chunk].  dx, dy are the stencil start relative to the tile
-// origin: signed in [-(P-1), MZ_TX) when the window does not wrap onto itself, else mod I.
+// spread record in shared memory: [q Wx (P)] [Wy (P)] [Wz placed at offset o = s_z - chunk
+// base inside the NACC-slot z window, zeros elsewhere (even length)] [hdr int4: dx, dy, -,
+// chunk].  dx, dy are the stencil start relative to the tile origin: signed in [-(P-1),
+// MZ_TX) when the window does not wrap onto itself, else mod I.
 template <int P>
 struct SRec {
-    static constexpr int WX = 0, WY = P, WZ = 2 * P, HDR = 3 * P + 1, SIZE = 3 * P + 3;
+    static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane (z planes)
+    static constexpr int NZP = (NACC + 1) & ~1;            // padded Wz slots
+    static constexpr int WX = 0, WY = P, WZ = 2 * P, HDR = 2 * P + NZP + ((2 * P + NZP) & 1);
+    static constexpr int SIZE = HDR + 2;
     static constexpr int B = 64;                           // particles per staged batch
-    static constexpr int K = SIZE <= 42 ? 4 : 2;           // batch buffers in flight
-    static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane
+    static constexpr int K = SIZE <= 48 ? 4 : 2;           // batch buffers in flight
     static constexpr int EMAX = 1024;                      // (chunk, home tile) ranges per CTA
     static constexpr int NPROD = 2;                        // producer warps (32 particles each)
     static constexpr int NTHR = 32 * (8 + NPROD);
@@ -154,12 +157,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
         "r"(parity)
         : "memory");
-}
-
-template <int P, int O>
-__device__ __forceinline__ void addz(double (&acc)[SRec<P>::NACC], double c, const double (&wz)[P + 1]) {
-#pragma unroll
-    for (int k = 0; k < P; ++k) acc[O + k] = fma(c, wz[k], acc[O + k]);
 }
 
 // lane flush of one chunk's MZ_ZC planes (written only for c >= cb), then slide the window
@@ -299,7 +296,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
 #pragma unroll
                 for (int w = 0; w < 8; ++w)
                     if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
-                *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, in.w - c * MZ_ZC, c);
+                *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, 0, c);
                 if (mask) {
                     const d4 r = ld_d4(&a.mpos[k]);
                     double wx[P], wy[P], wz[P];
@@ -310,9 +307,12 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
                     for (int i = 0; i < P; ++i) {
                         rec[R::WX + i] = r.w * wx[i];
                         rec[R::WY + i] = wy[i];
-                        rec[R::WZ + i] = wz[i];
                     }
-                    rec[R::WZ + P] = 0.0;
+                    const int o = in.w - c * MZ_ZC;      // z offset of the stencil in the window
+#pragma unroll
+                    for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = 0.0;
+#pragma unroll
+                    for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = wz[i];
                 }
             }
             sMask[buf][s] = (unsigned char)mask;
@@ -344,36 +344,39 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
         }
         __syncwarp();
         const double* base = sRec + buf * B * R::SIZE;
-        for (int i = 0; i < nmy; ++i) {
-            const double* rec = base + sList[warp][i] * R::SIZE;
-            const int4 hdr = *reinterpret_cast<const int4*>(rec + R::HDR);
-            while (cur < hdr.w) {                        // warp-uniform: entering a later chunk
-                spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
-                ++cur;
-            }
+        auto coef = [&](const double* rec, const int4& hdr) {
             int u, v;
             if (!small) { u = lx - hdr.x; v = ly - hdr.y; }
             else { u = wrapc(lx - hdr.x, a.Ix); v = wrapc(ly - hdr.y, a.Iy); }
             const bool in = (unsigned)u < (unsigned)P && (unsigned)v < (unsigned)P;
-            const double cc = in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : 0.0;
-            double wz[P + 1];
+            return in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : 0.0;
+        };
+        auto accum = [&](const double* rec, double cc) {
             const double2* w2 = reinterpret_cast<const double2*>(rec + R::WZ);
 #pragma unroll
-            for (int k = 0; k < (P + 1) / 2; ++k) {
+            for (int k = 0; k < R::NZP / 2; ++k) {
                 const double2 t = w2[k];
-                wz[2 * k] = t.x;
-                wz[2 * k + 1] = t.y;
+                if (2 * k < NACC) acc[2 * k] = fma(cc, t.x, acc[2 * k]);
+                if (2 * k + 1 < NACC) acc[2 * k + 1] = fma(cc, t.y, acc[2 * k + 1]);
             }
-            switch (hdr.z) {
-                case 0: addz<P, 0>(acc, cc, wz); break;
-                case 1: addz<P, 1>(acc, cc, wz); break;
-                case 2: addz<P, 2>(acc, cc, wz); break;
-                case 3: addz<P, 3>(acc, cc, wz); break;
-                case 4: addz<P, 4>(acc, cc, wz); break;
-                case 5: addz<P, 5>(acc, cc, wz); break;
-                case 6: addz<P, 6>(acc, cc, wz); break;
-                default: addz<P, 7>(acc, cc, wz); break;
+        };
+        int i = 0;
+        while (i < nmy) {                                // two particles per step when in one chunk
+            const double* ra = base + sList[warp][i] * R::SIZE;
+            const int4 ha = *reinterpret_cast<const int4*>(ra + R::HDR);
+            const bool two = i + 1 < nmy;
+            const double* rb = base + sList[warp][two ? i + 1 : i] * R::SIZE;
+            const int4 hb = *reinterpret_cast<const int4*>(rb + R::HDR);
+            while (cur < ha.w) {                         // warp-uniform: entering a later chunk
+                spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
+                ++cur;
             }
+            const double ca = coef(ra, ha);
+            const bool pair = two && hb.w == ha.w;
+            const double cbv = coef(rb, hb);
+            accum(ra, ca);
+            if (pair) accum(rb, cbv);
+            i += pair ? 2 : 1;
         }
         __syncwarp();
         mbar_arrive(&barEmpty[buf]);
