@@ -3,7 +3,13 @@
 //   S10 scaling        S'_a(k) = sum_b K_ab(k) S_b(k)                 (K from P:907/P:533, R10)
 //   S12 interpolation  phi_i = h_x h_y sum_g W W sum_a L_a(z_i) Psi_a[g]   (Eq. eq::SOGLong)
 // L_b(x) = sum_n C[b][n] T_n(x), x = 2 z / L_z, at first-kind Chebyshev nodes (App. A.2).
-// Proxy grids: [Pc][Ilx][Ily] real, spectra [Pc][Ilx][Ily/2+1].
+//
+// B200 form: the kernels work in the Chebyshev T basis instead of the Lagrange basis.  The
+// spread accumulates S~_n[g] = sum_j q_j T_n(z_j) W W (so S_b = sum_n C[b][n] S~_n), the
+// scaling applies K~(k) = C^T K(k) C (plan time, R9), and the gather evaluates
+// Psi~_m[g] = sum_a C[a][m] Psi_a[g] as phi = h_x h_y sum_g W W sum_m T_m(z) Psi~_m[g]:
+// the same linear maps, no P x P Lagrange evaluation per particle.
+// Proxy grids: [Pc][Ilx][Ily] real (T-basis layers), spectra [Pc][Ilx][Ily/2+1].
 #pragma once
 #include <cuComplex.h>
 #include "kernels_common.cuh"
@@ -13,42 +19,12 @@ namespace sog {
 struct LongArgs {
     const d4* pos;
     int N;
-    int Ilx, Ily, Pc;
+    int Ilx, Ily, Pc, Pl;
     double hx, hy, halfx, halfy, hpx, hpy, invH2Sx, invH2Sy;
     double two_over_Lz;
     double A;                 // h_x h_y
     const double* C;          // [Pc][Pc] Chebyshev -> Lagrange
 };
-
-template <int PCMAX>
-__device__ __forceinline__ void cheb_lagrange(double x, int Pc, const double* __restrict__ C, double* L,
-                                              double* dL) {
-    double T[PCMAX], dT[PCMAX];
-    T[0] = 1.0;
-    dT[0] = 0.0;
-    T[1] = x;
-    dT[1] = 1.0;
-#pragma unroll
-    for (int n = 1; n + 1 < PCMAX; ++n) {
-        T[n + 1] = 2.0 * x * T[n] - T[n - 1];
-        if (dL) dT[n + 1] = 2.0 * T[n] + 2.0 * x * dT[n] - dT[n - 1];
-    }
-#pragma unroll
-    for (int b = 0; b < PCMAX; ++b) {
-        double l = 0.0, dl = 0.0;
-        if (b < Pc) {
-#pragma unroll
-            for (int n = 0; n < PCMAX; ++n)
-                if (n < Pc) {
-                    double c = __ldg(&C[b * Pc + n]);
-                    l = fma(c, T[n], l);
-                    if (dL) dl = fma(c, dT[n], dl);
-                }
-        }
-        L[b] = l;
-        if (dL) dL[b] = dl;
-    }
-}
 
 // S10: one thread per (half mode, a).
 static __global__ void k_long_scale(const cuDoubleComplex* __restrict__ in, cuDoubleComplex* __restrict__ out,
@@ -107,7 +83,6 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
     const int tile = blockIdx.y, chunk = blockIdx.x;
     const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    for (int k = tid; k < Pc * Pc; k += nthr) sC[k] = a.C[k];
     // particle index ranges reaching this tile (1 or 2 ranges of x-slabs)
     int r0b = 0, r0e = a.N, r1b = 0, r1e = 0;
     if (!t.full_range) {
@@ -159,13 +134,10 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
             }
         }
         __syncthreads();
-        // L_b(z_j) = sum_n C[b][n] T_n(x_j), (j, b) pairs over all threads
+        // T-basis: the staged T_n(z_j) are the layer coefficients (S~_n)
         for (int q = tid; q < nb * PCMAX; q += nthr) {
-            int j = q / PCMAX, b = q % PCMAX;
-            double s = 0.0;
-            if (b < Pc)
-                for (int n = 0; n < Pc; ++n) s = fma(sC[b * Pc + n], sT[j * PCMAX + n], s);
-            sL[q] = s;
+            const int j = q / PCMAX, n = q % PCMAX;
+            sL[q] = n < Pc ? sT[j * PCMAX + n] : 0.0;
         }
         __syncthreads();
         if (own) {
@@ -231,9 +203,7 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
                                                       double gamma_x, double gamma_y, int SMEM) {
     extern __shared__ double sm[];
     const int Pc = a.Pc;
-    double* sC = sm;                                   // [Pc*Pc]
     double* sP = sm + PCMAX * PCMAX;                   // [Ilx*Ily*PCMAX]
-    for (int k = threadIdx.x; k < Pc * Pc; k += blockDim.x) sC[k] = a.C[k];
     if (SMEM) {
         const int n = a.Ilx * a.Ily * PCMAX;
         const double2* s2 = reinterpret_cast<const double2*>(psiT);
@@ -250,7 +220,7 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
     double wx[P], wy[P], dwx[P], dwy[P];
     window_weights_rec<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
     window_weights_rec<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
-    // Chebyshev T_n, T_n' at x = 2z/Lz, then L_b, L_b' (zero beyond Pc)
+    // Chebyshev T_n, T_n' at x = 2z/Lz (zero beyond Pc): the T-basis field Psi~ (see top)
     const double x = r.z * a.two_over_Lz;
     double L[PCMAX], dL[PCMAX];
     {
@@ -263,14 +233,8 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
         }
 #pragma unroll
         for (int b = 0; b < PCMAX; ++b) {
-            double l = 0.0, dl = 0.0;
-            if (b < Pc) {
-                const double* c = sC + b * Pc;
-#pragma unroll
-                for (int n = 0; n < PCMAX; ++n)
-                    if (n < Pc) { l = fma(c[n], T[n], l); dl = fma(c[n], dT[n], dl); }
-            }
-            L[b] = l; dL[b] = dl;
+            L[b] = b < Pc ? T[b] : 0.0;
+            dL[b] = b < Pc ? dT[b] : 0.0;
         }
     }
     double phi = 0, gx = 0, gy = 0, gz = 0;
@@ -301,6 +265,240 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
         gz = fma(wx[u], pdz, gz);
     }
     st_d4(&out[i], d4{a.A * phi, a.A * gx, a.A * gy, a.A * gz * a.two_over_Lz});
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Small long grids (Ilx <= 32, Ily <= 32, Ilx*Ily <= 256: every particle reaches most of the
+// grid).  S8 as a register-tiled product: a CTA keeps a private copy of the whole grid
+// S~[n][cx][cy] in registers (thread tile: 1 cx x 4 cy x 6 layers) and streams a slice of the
+// particles through shared memory as rotated, zero-padded weight rows
+//   Rx_j[cx] = q_j W(x_g - x_j) (stencil points only), Ry_j[cy], T_n(z_j);
+// a(cx,cy) = Rx[cx] Ry[cy] and S~ += a T: 24 FMAs per 4 DMULs and 6 shared loads.
+// Partials [block][n][cx][cy] are summed in a fixed order by k_long_sum (deterministic).
+constexpr int LG_KB = 64, LG_LT = 6, LG_RX = 32, LG_RY = 32;
+
+template <int PCP>
+__global__ void __launch_bounds__(512) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
+                                                          double gamma_y, int per, double* __restrict__ part) {
+    constexpr int NLG = PCP / LG_LT;
+    __shared__ __align__(16) double sRx[LG_KB][LG_RX];
+    __shared__ __align__(16) double sRy[LG_KB][LG_RY];
+    __shared__ __align__(16) double sT[LG_KB][PCP];
+    const int tid = threadIdx.x;
+    const int ncy4 = (a.Ily + 3) / 4;
+    const int lg = tid % NLG, cg = tid / NLG;
+    const int cx = cg / ncy4, cy0 = 4 * (cg % ncy4);
+    const bool own = cx < a.Ilx;
+    double acc[4][LG_LT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int l = 0; l < LG_LT; ++l) acc[i][l] = 0.0;
+    const int j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
+    const int P = a.Pl;
+    for (int base = j0; base < j1; base += LG_KB) {
+        const int nb = min(LG_KB, j1 - base);
+        __syncthreads();
+        for (int t = tid; t < LG_KB; t += blockDim.x) {
+            double* rx = sRx[t];
+            double* ry = sRy[t];
+            double* tt = sT[t];
+            for (int c = 0; c < LG_RX; ++c) rx[c] = 0.0;
+            for (int c = 0; c < LG_RY; ++c) ry[c] = 0.0;
+            for (int n = 0; n < PCP; ++n) tt[n] = 0.0;
+            if (t < nb) {
+                const int j = base + t;
+                const d4 r = ld_d4(&a.pos[j]);
+                const unsigned ow = (unsigned)g0[j].w;
+                const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
+                const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
+                // separable weights by the Gaussian recurrence (R6), placed at their columns
+                {
+                    const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
+                    double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
+                    int c = sx < 0 ? sx + a.Ilx : sx;
+                    for (int u = 0; u < P; ++u) {
+                        rx[c] = r.w * w;
+                        w *= q; q *= gamma_x;
+                        c = c + 1 == a.Ilx ? 0 : c + 1;
+                    }
+                }
+                {
+                    const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
+                    double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
+                    int c = sy < 0 ? sy + a.Ily : sy;
+                    for (int v = 0; v < P; ++v) {
+                        ry[c] = w;
+                        w *= q; q *= gamma_y;
+                        c = c + 1 == a.Ily ? 0 : c + 1;
+                    }
+                }
+                const double x = r.z * a.two_over_Lz;
+                double tm = 1.0, tc = x;
+                tt[0] = 1.0;
+                if (a.Pc > 1) tt[1] = x;
+                for (int n = 2; n < a.Pc; ++n) {
+                    const double tn = 2.0 * x * tc - tm;
+                    tt[n] = tn;
+                    tm = tc; tc = tn;
+                }
+            }
+        }
+        __syncthreads();
+        if (own) {
+#pragma unroll 2
+            for (int t = 0; t < nb; ++t) {
+                const double rx = sRx[t][cx];
+                const double2 y01 = *reinterpret_cast<const double2*>(&sRy[t][cy0]);
+                const double2 y23 = *reinterpret_cast<const double2*>(&sRy[t][cy0 + 2]);
+                double tl[LG_LT];
+#pragma unroll
+                for (int l = 0; l < LG_LT; l += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&sT[t][lg * LG_LT + l]);
+                    tl[l] = v.x; tl[l + 1] = v.y;
+                }
+                const double av[4] = {rx * y01.x, rx * y01.y, rx * y23.x, rx * y23.y};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int l = 0; l < LG_LT; ++l) acc[i][l] = fma(av[i], tl[l], acc[i][l]);
+            }
+        }
+    }
+    if (own) {
+        const size_t G = (size_t)a.Ilx * a.Ily;
+        double* o = part + (size_t)blockIdx.x * PCP * G;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int l = 0; l < LG_LT; ++l) {
+                const int cy = cy0 + i, n = lg * LG_LT + l;
+                if (cy < a.Ily) o[(size_t)n * G + (size_t)cx * a.Ily + cy] = acc[i][l];
+            }
+    }
+}
+
+// grid[n][g] = sum over blocks (fixed order) of part[block][n][g], n < Pc
+static __global__ void k_long_sum(const double* __restrict__ part, double* __restrict__ grid, int G, int Pc, int PCP,
+                                  int nblk) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * Pc) return;
+    const double* p = part + idx;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += p[(size_t)b * PCP * G];
+    grid[idx] = s;
+}
+
+// S12 for small long grids: one thread per particle, the whole T-basis field Psi~ in shared
+// memory as [cx][cy][PCP] and read with broadcast 128-bit loads (every thread walks the
+// columns in the same order).  Per column: V = sum_m T_m Psi~_m, V' = sum_m T'_m Psi~_m
+// (2 PCP FMAs) and 4 products with the rotated weights.  Rx / dRx rows live in shared
+// memory (dynamic cx), Ry / dRy in registers (static cy < NCY).
+template <int PCP, int NCY>
+__global__ void __launch_bounds__(128) k_long_gather_bc(LongArgs a, const int4* __restrict__ g0,
+                                                        const double* __restrict__ psi, d4* __restrict__ out) {
+    extern __shared__ __align__(16) double sm[];
+    const int G = a.Ilx * a.Ily;
+    double* sPsi = sm;                                  // [G][PCP]
+    double* sRx = sm + (size_t)G * PCP;                 // [Ilx][128]
+    double* sdRx = sRx + (size_t)a.Ilx * 128;           // [Ilx][128]
+    double* sRy = sdRx + (size_t)a.Ilx * 128;           // [NCY][128]
+    double* sdRy = sRy + (size_t)NCY * 128;             // [NCY][128]
+    for (int e = threadIdx.x; e < G * PCP; e += blockDim.x) {
+        const int g = e / PCP, n = e - g * PCP;
+        sPsi[e] = n < a.Pc ? psi[(size_t)n * G + g] : 0.0;
+    }
+    const int tid = threadIdx.x;
+    const int j = blockIdx.x * blockDim.x + tid;
+    const bool act = j < a.N;
+    const int P = a.Pl;
+    double T[PCP], dT[PCP];
+    double ry[NCY], dry[NCY];
+    {
+        for (int c = 0; c < a.Ilx; ++c) { sRx[c * 128 + tid] = 0.0; sdRx[c * 128 + tid] = 0.0; }
+#pragma unroll
+        for (int c = 0; c < NCY; ++c) { sRy[c * 128 + tid] = 0.0; sdRy[c * 128 + tid] = 0.0; }
+        d4 r{0.0, 0.0, 0.0, 0.0};
+        int sx = 0, sy = 0;
+        if (act) {
+            r = ld_d4(&a.pos[j]);
+            const unsigned ow = (unsigned)g0[j].w;
+            sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
+            sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
+            {
+                const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
+                double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
+                const double gam = exp(-2.0 * a.invH2Sx * a.hx * a.hx);
+                int c = sx < 0 ? sx + a.Ilx : sx;
+                for (int u = 0; u < P; ++u) {
+                    sRx[c * 128 + tid] = w;
+                    sdRx[c * 128 + tid] = 2.0 * a.invH2Sx * (d0 + u * a.hx) * w;
+                    w *= q; q *= gam;
+                    c = c + 1 == a.Ilx ? 0 : c + 1;
+                }
+            }
+            {
+                const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
+                double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
+                const double gam = exp(-2.0 * a.invH2Sy * a.hy * a.hy);
+                int c = sy < 0 ? sy + a.Ily : sy;
+                for (int v = 0; v < P; ++v) {
+                    sRy[c * 128 + tid] = w;
+                    sdRy[c * 128 + tid] = 2.0 * a.invH2Sy * (d0 + v * a.hy) * w;
+                    w *= q; q *= gam;
+                    c = c + 1 == a.Ily ? 0 : c + 1;
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCY; ++c) { ry[c] = sRy[c * 128 + tid]; dry[c] = sdRy[c * 128 + tid]; }
+        const double x = r.z * a.two_over_Lz;
+        T[0] = 1.0; dT[0] = 0.0;
+        T[1] = x; dT[1] = 1.0;
+#pragma unroll
+        for (int n = 1; n + 1 < PCP; ++n) {
+            T[n + 1] = 2.0 * x * T[n] - T[n - 1];
+            dT[n + 1] = 2.0 * T[n] + 2.0 * x * dT[n] - dT[n - 1];
+        }
+    }
+    __syncthreads();
+    double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int cx = 0; cx < a.Ilx; ++cx) {
+        const double rx = sRx[cx * 128 + tid], drx = sdRx[cx * 128 + tid];
+        const double* col = sPsi + (size_t)cx * a.Ily * PCP;
+#pragma unroll
+        for (int cy = 0; cy < NCY; ++cy) {
+            if (cy < a.Ily) {
+                const double2* c2 = reinterpret_cast<const double2*>(col + cy * PCP);
+                double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+                for (int n = 0; n < PCP; n += 2) {
+                    const double2 ps = c2[n / 2];
+                    v0 = fma(T[n], ps.x, v0); v0 = fma(T[n + 1], ps.y, v0);
+                    v1 = fma(dT[n], ps.x, v1); v1 = fma(dT[n + 1], ps.y, v1);
+                }
+                const double wxy = rx * ry[cy];
+                phi = fma(wxy, v0, phi);
+                gz = fma(wxy, v1, gz);
+                gx = fma(drx * ry[cy], v0, gx);
+                gy = fma(rx * dry[cy], v0, gy);
+            }
+        }
+    }
+    if (act) st_d4(&out[j], d4{a.A * phi, a.A * gx, a.A * gy, a.A * gz * a.two_over_Lz});
+}
+
+// Debug-stage conversions back to the paper's Lagrange (proxy-node) basis:
+//   S_b = sum_n C[b][n] S~_n,   Psi_a = sum_m T_m(x_a) Psi~_m  (x_a first-kind nodes).
+static __global__ void k_long_to_nodes(const double* __restrict__ in, double* __restrict__ out, int G, int Pc,
+                                       const double* __restrict__ M) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * Pc) return;
+    const int b = idx / G, g = idx - b * G;
+    double s = 0.0;
+    for (int n = 0; n < Pc; ++n) s = fma(M[b * Pc + n], in[(size_t)n * G + g], s);
+    out[idx] = s;
 }
 
 }  // namespace sog

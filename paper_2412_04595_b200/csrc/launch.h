@@ -27,6 +27,12 @@ int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* ps
                         cudaStream_t st);
 int long_pcmax(int Pc);
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
+bool long_small_ok(int Ilx, int Ily, int Pc);
+int long_small_pcp(int Pc);
+int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part,
+                            double* grid, cudaStream_t st);
+int launch_long_gather_bc(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st);
+int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const double* M, cudaStream_t st);
 // exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total); temp from scan_temp_bytes
 size_t scan_temp_bytes(int n);
 int launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes, cudaStream_t st);

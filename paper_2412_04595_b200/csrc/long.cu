@@ -79,3 +79,69 @@ int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* ps
 }
 
 }  // namespace sog
+
+namespace sog {
+
+// ---- small long grids (T-basis register-tiled spread, broadcast gather) ----
+int long_small_pcp(int Pc) { return Pc <= 30 ? ((Pc + LG_LT - 1) / LG_LT) * LG_LT : 0; }
+
+bool long_small_ok(int Ilx, int Ily, int Pc) {
+    return Ilx <= LG_RX && Ily <= LG_RY && Ilx * Ily <= 256 && long_small_pcp(Pc) > 0 && Ily <= 16;
+}
+
+template <int PCP>
+int spread_gemm_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part, double* grid,
+                   cudaStream_t st) {
+    const int nthr = ((a.Ilx * ((a.Ily + 3) / 4) * (PCP / LG_LT) + 31) / 32) * 32;
+    const int per = (a.N + nblk - 1) / nblk;
+    k_long_spread_gemm<PCP><<<nblk, nthr, 0, st>>>(a, g0, gx, gy, per, part);
+    const int G = a.Ilx * a.Ily;
+    k_long_sum<<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part,
+                            double* grid, cudaStream_t st) {
+    switch (long_small_pcp(a.Pc)) {
+        case 6: return spread_gemm_go<6>(a, g0, gx, gy, nblk, part, grid, st);
+        case 12: return spread_gemm_go<12>(a, g0, gx, gy, nblk, part, grid, st);
+        case 18: return spread_gemm_go<18>(a, g0, gx, gy, nblk, part, grid, st);
+        case 24: return spread_gemm_go<24>(a, g0, gx, gy, nblk, part, grid, st);
+        case 30: return spread_gemm_go<30>(a, g0, gx, gy, nblk, part, grid, st);
+    }
+    return 1;
+}
+
+template <int PCP, int NCY>
+int gather_bc_go(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
+    const size_t sh = sizeof(double) * ((size_t)a.Ilx * a.Ily * PCP + 2 * 128 * (size_t)a.Ilx + 2 * 128 * NCY);
+    auto k = k_long_gather_bc<PCP, NCY>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess) return 2;
+    k<<<(a.N + 127) / 128, 128, sh, st>>>(a, g0, psi, out);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int NCY>
+int gather_bc_p(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
+    // even PCP for 128-bit loads: Pc rounded up to even
+    switch ((a.Pc + 1) & ~1) {
+#define C_(M_) case M_: return gather_bc_go<M_, NCY>(a, g0, psi, out, st);
+        C_(2) C_(4) C_(6) C_(8) C_(10) C_(12) C_(14) C_(16) C_(18) C_(20) C_(22) C_(24) C_(26) C_(28) C_(30)
+#undef C_
+    }
+    return 1;
+}
+
+int launch_long_gather_bc(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
+    if (a.Ily <= 8) return gather_bc_p<8>(a, g0, psi, out, st);
+    if (a.Ily <= 12) return gather_bc_p<12>(a, g0, psi, out, st);
+    if (a.Ily <= 16) return gather_bc_p<16>(a, g0, psi, out, st);
+    return 1;
+}
+
+int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const double* M, cudaStream_t st) {
+    k_long_to_nodes<<<(G * Pc + 255) / 256, 256, 0, st>>>(in, out, G, Pc, M);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace sog

@@ -339,6 +339,8 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
     for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
     const double Hx = (p.Pl - 1) * p.hlx() / 2.0, Hy = (p.Pl - 1) * p.hly() / 2.0;
     K.assign(size_t(nx) * ny * P * P, 0.0);
+    std::vector<double> Cm;
+    build_cheb_matrix(P, Cm);
     for (int ix = 0; ix < nx; ++ix) {
         int fx = ix < (nx + 1) / 2 ? ix : ix - nx;
         double kx = 2.0 * kPi * fx / p.Lx;
@@ -367,9 +369,25 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
                     }
                     Km[a * P + b] = acc * dec;
                 }
+            // T basis (kernels_long.cuh): K~ = C^T K C with L_b(x) = sum_n C[b][n] T_n(x)
+            std::vector<long double> KC(size_t(P) * P, 0.0L);
+            for (int a = 0; a < P; ++a)
+                for (int n = 0; n < P; ++n) {
+                    long double t = 0.0L;
+                    for (int b = 0; b < P; ++b) t += (long double)Km[a * P + b] * Cm[size_t(b) * P + n];
+                    KC[size_t(a) * P + n] = t;
+                }
+            for (int m = 0; m < P; ++m)
+                for (int n = 0; n < P; ++n) {
+                    long double t = 0.0L;
+                    for (int a = 0; a < P; ++a) t += (long double)Cm[size_t(a) * P + m] * KC[size_t(a) * P + n];
+                    Km[m * P + n] = double(t);
+                }
         }
     }
 }
+
+void build_cheb_nodes(int Pc, std::vector<double>& Tn) { Tn = node_T(Pc); }
 
 void build_cheb_matrix(int Pc, std::vector<double>& C) {
     std::vector<double> Tn = node_T(Pc);

@@ -114,7 +114,11 @@ struct sog_plan {
     double* lpsiT = nullptr;        // long field, layer-fastest [Ilx][Ily][PCMAX]
     LongTileArgs lt{};
     cuDoubleComplex *lspec = nullptr, *lspec2 = nullptr;
-    double *d_K = nullptr, *d_C = nullptr;
+    double *d_K = nullptr, *d_C = nullptr, *d_Tn = nullptr;
+    bool long_small = false;        // small long grid: register-tiled spread + broadcast gather
+    int lg_nblk = 0;
+    double* lpart2 = nullptr;       // [lg_nblk][PCP][Ilx*Ily] spread partials
+    double* ldbg = nullptr;         // debug: T basis -> proxy-node basis
     cufftHandle lfwd = 0, linv = 0;
     // host-buffer path
     double *h_xyz = nullptr, *h_q = nullptr, *h_phi = nullptr, *h_force = nullptr;
@@ -162,7 +166,7 @@ void free_plan(sog_plan* pl) {
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
-                    pl->mpsi, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
+                    pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -281,7 +285,16 @@ int setup(sog_plan* pl) {
         std::vector<double> K, C;
         build_long_kernel(p, K);
         build_cheb_matrix(p.Pc, C);
-        if ((rc = upload(pl, &pl->d_K, K)) || (rc = upload(pl, &pl->d_C, C))) return rc;
+        std::vector<double> Tn;
+        build_cheb_nodes(p.Pc, Tn);
+        if ((rc = upload(pl, &pl->d_K, K)) || (rc = upload(pl, &pl->d_C, C)) || (rc = upload(pl, &pl->d_Tn, Tn)) ||
+            (rc = dalloc(pl, &pl->ldbg, G)))
+            return rc;
+        pl->long_small = long_small_ok(p.Ilx, p.Ily, p.Pc);
+        if (pl->long_small) {
+            pl->lg_nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (p.N + 255) / 256));
+            if ((rc = dalloc(pl, &pl->lpart2, (size_t)pl->lg_nblk * long_small_pcp(p.Pc) * p.Ilx * p.Ily))) return rc;
+        }
         // S8 tiling: one tile = whole grid when it fits one CTA, else 16x16 column tiles
         LongTileArgs& t = pl->lt;
         if (p.Ilx * p.Ily <= 256) { t.TX = p.Ilx; t.TY = p.Ily; }
@@ -347,7 +360,7 @@ LongArgs long_args(const sog_plan* pl) {
     LongArgs a;
     a.pos = pl->pos_s;
     a.N = int(p.N);
-    a.Ilx = p.Ilx; a.Ily = p.Ily; a.Pc = p.Pc;
+    a.Ilx = p.Ilx; a.Ily = p.Ily; a.Pc = p.Pc; a.Pl = p.Pl;
     a.hx = p.hlx(); a.hy = p.hly();
     a.halfx = 0.5 * p.Ilx; a.halfy = 0.5 * p.Ily;
     a.hpx = 0.5 * p.Ilx + 0.5; a.hpy = 0.5 * p.Ily + 0.5;
@@ -463,11 +476,17 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     mark(pl, 7);
     // S8-S12 long range
     if (stop_stage == 0 || stop_stage == 3 || stop_stage == 4) {
-        LongTileArgs t = pl->lt;
-        t.a = long_args(pl);
-        t.start = pl->start;
-        t.part = pl->lpart;
-        if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
+        if (pl->long_small) {
+            if ((rc = lchk(launch_long_spread_gemm(long_args(pl), pl->g0, pl->lt.gamma_x, pl->lt.gamma_y, pl->lg_nblk,
+                                                   pl->lpart2, pl->lgrid, st))))
+                return rc;
+        } else {
+            LongTileArgs t = pl->lt;
+            t.a = long_args(pl);
+            t.start = pl->start;
+            t.part = pl->lpart;
+            if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
+        }
         mark(pl, 8);
         if (stop_stage == 3) return SOG_OK;
         CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
@@ -477,9 +496,12 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
         mark(pl, 9);
         if (stop_stage == 4) return SOG_OK;
-        if ((rc = lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long, pl->lt.gamma_x,
-                                           pl->lt.gamma_y, st))))
+        if (pl->long_small) {
+            if ((rc = lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, st)))) return rc;
+        } else if ((rc = lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long,
+                                                  pl->lt.gamma_x, pl->lt.gamma_y, st)))) {
             return rc;
+        }
     }
     mark(pl, 10);
     return SOG_OK;
@@ -636,13 +658,18 @@ int sog_debug_stage(sog_plan* pl, int stage, const double* xyz, const double* q,
         src = stage == 1 ? pl->mgrid : pl->mpsi;
     } else if (stage == 3 || stage == 4) {
         need = (size_t)p.Pc * p.Ilx * p.Ily;
-        src = pl->lgrid;
+        src = pl->ldbg;                 // converted from the T basis below
     } else {
         return fail(SOG_EINVAL, "stage must be 1..4");
     }
     if (len < need) return fail(SOG_EINVAL, "output buffer too small");
     int rc = run_pipeline(pl, xyz, q, stage);
     if (rc) return rc;
+    if (stage >= 3) {   // T basis -> proxy nodes: S_b = sum_n C[b][n] S~_n, Psi_a = sum_m T_m(x_a) Psi~_m
+        if ((rc = lchk(launch_long_to_nodes(pl->lgrid, pl->ldbg, p.Ilx * p.Ily, p.Pc, stage == 3 ? pl->d_C : pl->d_Tn,
+                                            pl->stream))))
+            return rc;
+    }
     CK(cudaMemcpyAsync(out, src, need * sizeof(double), cudaMemcpyDeviceToDevice, pl->stream));
     return check_flags(pl);
 }
@@ -694,8 +721,8 @@ int sog_launches_per_eval(const sog_plan* pl) {
     if (!pl) return fail(SOG_EINVAL, "null plan");
     // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
     // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
-    // transpose, gather, combine  (cuFFT launches are not counted)
-    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + 5 + 1;
+    // [transpose,] gather, combine  (cuFFT launches are not counted)
+    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->long_small ? 4 : 5) + 1;
 }
 
 }  // extern "C"

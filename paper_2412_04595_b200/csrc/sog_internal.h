@@ -63,10 +63,13 @@ bool build_near_table(const Params& p, NearTable& t, std::string& err);
 // Ty covers the half axis iy < Iy/2+1, Tx and Tz the full axes (fftfreq order).
 void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<double>& Tx,
                       std::vector<double>& Ty, std::vector<double>& Tz);
-// Long-range kernel matrices K[mode][a][b], mode = ix*(Ily/2+1)+iy (R9, R10).
+// Long-range kernel matrices per half mode (mode = ix*(Ily/2+1)+iy), in the Chebyshev T
+// basis: K~[mode][m][n] = sum_ab C[a][m] K_ab C[b][n], K_ab from R9/R10.
 void build_long_kernel(const Params& p, std::vector<double>& K);
 // Chebyshev -> Lagrange coefficient matrix C[b][n]: L_b(x) = sum_n C[b][n] T_n(x).
 void build_cheb_matrix(int Pc, std::vector<double>& C);
+// Tn[a][m] = T_m(x_a) at the first-kind nodes x_a = cos((a+1/2) pi / Pc).
+void build_cheb_nodes(int Pc, std::vector<double>& Tn);
 
 std::string describe(const Params& p);
 
