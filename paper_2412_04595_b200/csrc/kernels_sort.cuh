@@ -96,8 +96,9 @@ __global__ void k_scatter(const int* __restrict__ cell, int N, int* __restrict__
     if (i < N) tmp[atomicAdd(&cursor[cell[i]], 1)] = i;
 }
 
-// One warp per cell: order the cell's members by original index (rank counting), gather
-// the sorted SoA and the permutation.  Makes the whole evaluation deterministic.
+// One warp per cell: order the cell's members by (z, original index) (rank counting), gather
+// the sorted SoA and the permutation.  Cells are z-major inside an (x,y) column, so every
+// column is z-sorted (the near-field z windows rely on it); the order is deterministic.
 __global__ void k_cellsort(const int* __restrict__ start, int ncell, const int* __restrict__ tmp,
                            const d4* __restrict__ pos, d4* __restrict__ pos_s, int* __restrict__ perm) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -106,11 +107,16 @@ __global__ void k_cellsort(const int* __restrict__ start, int ncell, const int* 
     int s = start[warp], n = start[warp + 1] - s;
     for (int e = lane; e < n; e += 32) {
         int my = tmp[s + e];
+        const double zm = pos[my].z;
         int rank = 0;
         if (n <= 4096) {
-            for (int f = 0; f < n; ++f) rank += (tmp[s + f] < my);
+            for (int f = 0; f < n; ++f) {
+                const int o = tmp[s + f];
+                const double zo = pos[o].z;
+                rank += (zo < zm || (zo == zm && o < my));
+            }
         } else {
-            rank = e;   // pathological clustering: keep arrival order
+            rank = e;   // pathological clustering: arrival order (z windows fall back to full columns)
         }
         perm[s + rank] = my;
         st_d4(&pos_s[s + rank], ld_d4(&pos[my]));

@@ -2,7 +2,7 @@
 //
 //   S1 k_prepare -> scan -> k_scatter -> k_cellsort             (validate, canonicalise, cell sort)
 //      k_stencil_origins -> k_mid_key -> scan -> k_mid_scatter -> k_mid_bucket   (mid order)
-//   S2 k_near3                                                  (near field + nothing else)
+//   S2 k_near3 (warp per target; k_near for tiny boxes)        (near field + nothing else)
 //   S3-S7 k_mid_spread_z -> cuFFT D2Z -> k_mid_scale -> cuFFT Z2D -> k_mid_gather_z
 //   S8-S12 k_long_spread -> cuFFT D2Z (batched 2D) -> k_long_scale -> Z2D -> k_long_gather
 //   S13 k_combine                                               (self term, forces, unpermute, U)
@@ -425,7 +425,7 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     // S2 near field
     if (!stop_stage) {
         const int D = pl->near.D;
-        if (D != 10) return fail(SOG_EINVAL, "near table degree");
+        if (D != NEAR_D) return fail(SOG_EINVAL, "near table degree");
         if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && p.N < (1 << 27)) {   // k_near3: warp per target
             Near3Args a;
             a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
@@ -435,8 +435,8 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
             a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
             size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
                         NEAR3_WARPS * 160 * sizeof(int) + sizeof(float4) * a.cap;
-            CK(cudaFuncSetAttribute(k_near3<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-            k_near3<10><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+            CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
         } else {
             NearArgs a;
             a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.cdF = pl->d_cdF; a.out = pl->o_near;
@@ -445,8 +445,8 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
             for (int i = 0; i < 3; ++i) { a.ox[i] = pl->offx[i]; a.oy[i] = pl->offy[i]; }
             a.noffx = pl->noffx; a.noffy = pl->noffy;
             size_t sh = 2 * sizeof(double) * pl->near.K * (D + 1);
-            CK(cudaFuncSetAttribute(k_near<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-            k_near<10><<<(N + 255) / 256, 256, sh, st>>>(a);
+            CK(cudaFuncSetAttribute(k_near<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_near<NEAR_D><<<(N + 255) / 256, 256, sh, st>>>(a);
         }
         CK(cudaGetLastError());
     }
