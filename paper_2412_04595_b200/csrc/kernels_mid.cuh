@@ -400,9 +400,10 @@ struct GRing {
     static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
     static constexpr int PL = WX * WYP;                           // plane size (doubles)
     static constexpr int D = MZ_ZC + P - 1;                       // planes in the ring
-    static constexpr int WSZ = 6 * P + 2;                         // per-warp weight scratch
+    static constexpr int WSZ = 6 * P + 2;                         // per-particle weight scratch
+    static constexpr int WB = 6;                                  // particles per warp batch (<= 10)
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
-    static constexpr size_t BYTES = sizeof(double) * (size_t(D) * PL + 8 * WSZ);
+    static constexpr size_t BYTES = sizeof(double) * (size_t(D) * PL + 8 * WB * WSZ);
     static constexpr bool FITS = BYTES <= 227 * 1024;
     static constexpr int MINB = BYTES <= 113 * 1024 ? 2 : 1;     // CTAs per SM
 };
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
     extern __shared__ __align__(16) double sm[];
     double* ring = sm;                                   // [D][WX][WYP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* wsc = sm + D * PL + warp * G::WSZ;           // Wx dWx Wy dWy Wz dWz
+    double* wsb = sm + D * PL + warp * G::WB * G::WSZ;   // per particle: Wx dWx Wy dWy Wz dWz, hdr
     const int tile = blockIdx.x;
     const int tx = tile / a.nty, ty = tile % a.nty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
@@ -430,12 +431,6 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
         cbb[r] = idx < P * P ? idx - ca[r] * P : 0;
         coff[r] = ca[r] * WYP + cbb[r];
     }
-    // lane ax < 3: axis parameters for the weight recurrence
-    const int ax = min(lane, 2);
-    const double h = ax == 0 ? a.hx : (ax == 1 ? a.hy : a.hz);
-    const double half = ax == 0 ? a.halfx : (ax == 1 ? a.halfy : a.halfz);
-    const double al = ax == 0 ? a.invH2Sx : (ax == 1 ? a.invH2Sy : a.invH2Sz);
-    const double gam = ax == 0 ? a.gamma_x : (ax == 1 ? a.gamma_y : a.gamma_z);
     int zl = 0, zh = 0;                                  // planes [zl, zh) resident
     for (int c = cb; c < ce; ++c) {
         const int key = tile * a.nzc + c;
@@ -471,37 +466,52 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
         zl = nlo;
         zh = nhi;
         __syncthreads();
-        for (int k = k0 + warp; k < k1; k += 8) {
-            const int4 in = a.minfo[k];
-            const d4 r = ld_d4(&a.mpos[k]);
-            if (lane < 3) {                              // weights of axis `lane` (recurrence)
-                const double x = lane == 0 ? r.x : (lane == 1 ? r.y : r.z);
-                const int s = lane == 0 ? in.y : (lane == 1 ? in.z : in.w);
-                const double d0 = ((double)s - half) * h - x;
-                double w = exp(-al * d0 * d0);
-                double q = exp(-al * h * (2.0 * d0 + h));
-                double* o = wsc + 2 * lane * P;
+        for (int kb = k0 + G::WB * warp; kb < k1; kb += G::WB * 8) {
+            const int nb = min(G::WB, k1 - kb);
+            // weights of WB particles at once: lane = (particle lane/3, axis lane%3), recurrence
+            if (lane < 3 * nb) {
+                const int pp = lane / 3, axl = lane - 3 * pp;
+                const int4 in = a.minfo[kb + pp];
+                const d4 r = ld_d4(&a.mpos[kb + pp]);
+                const double hh = axl == 0 ? a.hx : (axl == 1 ? a.hy : a.hz);
+                const double hf = axl == 0 ? a.halfx : (axl == 1 ? a.halfy : a.halfz);
+                const double aa = axl == 0 ? a.invH2Sx : (axl == 1 ? a.invH2Sy : a.invH2Sz);
+                const double gg = axl == 0 ? a.gamma_x : (axl == 1 ? a.gamma_y : a.gamma_z);
+                const double x = axl == 0 ? r.x : (axl == 1 ? r.y : r.z);
+                const int sa = axl == 0 ? in.y : (axl == 1 ? in.z : in.w);
+                const double d0 = ((double)sa - hf) * hh - x;
+                double w = exp(-aa * d0 * d0);
+                double q = exp(-aa * hh * (2.0 * d0 + hh));
+                double* o = wsb + pp * G::WSZ + 2 * axl * P;
 #pragma unroll
                 for (int i = 0; i < P; ++i) {
                     o[i] = w;
-                    o[P + i] = 2.0 * al * (d0 + i * h) * w;
+                    o[P + i] = 2.0 * aa * (d0 + i * hh) * w;
                     w *= q;
-                    q *= gam;
+                    q *= gg;
+                }
+                if (axl == 0) {
+                    int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + 6 * P);
+                    hd[0] = in.y - X0 + (in.y < 0 ? a.Ix : 0);          // start relative to the tile
+                    hd[1] = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
+                    hd[2] = in.w % D;                                    // ring slot of the first plane
+                    hd[3] = in.x;                                        // output (cell-sorted) index
                 }
             }
             __syncwarp();
+            for (int pp = 0; pp < nb; ++pp) {
+            const double* wsc = wsb + pp * G::WSZ;
+            const int4 hd = *reinterpret_cast<const int4*>(wsc + 6 * P);
             double wz[P], dwz[P];
 #pragma unroll
             for (int i = 0; i < P; ++i) { wz[i] = wsc[4 * P + i]; dwz[i] = wsc[5 * P + i]; }
-            const int sxr = in.y - X0 + (in.y < 0 ? a.Ix : 0);   // start relative to the tile (in [0, MZ_TX))
-            const int syr = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
             int pb[P];                                   // ring plane offsets of the P stencil planes
             {
-                int zs = in.w % D;
+                int zs = hd.z;
 #pragma unroll
                 for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == D ? 0 : zs + 1; }
             }
-            const double* base = ring + sxr * WYP + syr;
+            const double* base = ring + hd.x * WYP + hd.y;
             double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
             for (int rr = 0; rr < NR; ++rr) {
@@ -535,7 +545,8 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
 #pragma unroll
                 for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
                 // lane&3: 0 -> phi, 1 -> gx, 2 -> gy, 3 -> gz (one 32-byte sector)
-                if (lane < 4) reinterpret_cast<double*>(&out[in.x])[lane] = a.Vh * kk;
+                if (lane < 4) reinterpret_cast<double*>(&out[hd.w])[lane] = a.Vh * kk;
+            }
             }
             __syncwarp();
         }

@@ -245,9 +245,9 @@ bool build_near_table(const Params& p, NearTable& t, std::string& err) {
     sog_weights(p, w, s);
     const double s0sq = s[0] * s[0];
     const double umax = p.rc * p.rc;
-    // pieces with du / s_0^2 <= 1/16 and degree NEAR_D = 8: Taylor remainders at |d| <= du/2 of
-    // the narrowest Gaussian ~ (1/32)^9/9! ~ 1e-19 (F) and (1/32)^8/8! ~ 2e-17 (F')
-    t.K = std::max(1, int(std::ceil(16.0 * umax / s0sq)));
+    // pieces with du / (2 s_0^2) <= 1/8 and degree NEAR_D = 10: Taylor remainders at |d| <= du/2
+    // of the narrowest Gaussian ~1e-17 (F), ~3e-16 (F'); the table stays small (shared memory)
+    t.K = std::max(1, int(std::ceil(4.0 * umax / s0sq)));
     t.D = NEAR_D;
     t.du = umax / t.K;
     t.inv_du = t.K / umax;

@@ -51,7 +51,7 @@ double erfcinv_host(double y);
 
 // Near-field kernel table: F(u) and dF/du, u = r^2, piecewise Taylor polynomials (R16),
 // NEAR_D = polynomial degree (the kernels are instantiated for it).
-constexpr int NEAR_D = 8;
+constexpr int NEAR_D = 10;
 struct NearTable {
     int K = 0, D = 0;          // pieces, degree
     double du = 0, inv_du = 0; // piece width in u
