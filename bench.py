@@ -171,40 +171,61 @@ def run_reference(args, ws, rank):
     }), flush=True)
 
 
-def stage_roofline(plan, stages, N, clocks):
-    """Roofline of the dominant kernel stage from the plan's per-stage CUDA-event times."""
-    d = plan.describe()
+NEAR_FLOPS_PER_PAIR = 60.0   # r_ij (3), r^2 (5), F(u), F'(u) degree-10 joint Horner (40), 1/r (4), phi + grad (8)
+
+
+def stage_flops(d, N, L):
+    """Algorithmic FP64 flops per evaluation of each stencil/pair stage (DESIGN.md section 6;
+    FMA = 2 flops).  Near field: expected in-range pairs (4 pi / 3) r_c^3 rho per particle."""
     P, Pl, Pc = d["P"], d["Pl"], d["Pc"]
-    G = d["Ix"] * d["Iy"] * d["Izs"]
-    name = max((k for k in stages if k not in ("mid_fft_fwd", "mid_fft_inv", "long_fft_scale_ifft")),
-               key=lambda k: stages[k])
-    ms = stages[name]
-    # algorithmic FP64 flops per launch (DESIGN.md "Kernels"): FMA = 2 flops
-    flops = {
+    rho = N / (L[0] * L[1] * L[2])
+    pairs = 4.0 * math.pi / 3.0 * d["rc"] ** 3 * rho
+    return {
+        "near": N * pairs * NEAR_FLOPS_PER_PAIR,
         "mid_spread": N * (2.0 * P ** 3 + 2.0 * P * P),
         "mid_gather": N * (4.0 * P ** 3 + 6.0 * P * P + 8.0 * P),
-        "long_spread": N * (2.0 * Pl * Pl * Pc + 2.0 * Pc * Pc),
-        "long_gather": N * (4.0 * Pl * Pl * Pc + 6.0 * Pl * Pl + 4.0 * Pc * Pc),
-        "near": None, "sort": None, "mid_scale": None, "combine": None,
-    }.get(name)
-    bytes_ = {
-        "mid_spread": 32.0 * N + 8.0 * G, "mid_gather": 8.0 * G + 64.0 * N,
-        "mid_scale": 32.0 * G / 2, "sort": 150.0 * N, "combine": 160.0 * N,
-        "near": 64.0 * N,
-    }.get(name, 64.0 * N)
+        "long_spread": N * (2.0 * Pl * Pl * Pc + 2.0 * Pl * Pl),
+        "long_gather": N * (4.0 * Pl * Pl * Pc + 6.0 * Pl * Pl + 4.0 * Pc),
+    }
+
+
+def stage_roofline(plan, stages, N, L):
+    """Roofline of the dominant kernel stage (and of every stencil stage) from the plan's
+    per-stage CUDA-event times on the plan's stream."""
+    d = plan.describe()
+    G = d["Ix"] * d["Iy"] * d["Izs"]
     sm_mhz = 1965.0
     peak_fp64 = NUM_SMS * FP64_FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    if flops:
-        ach = flops / (ms * 1e-3) / 1e12
-        return name, {"bound": "alu", "kernel": name, "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
-                      "frac": ach / peak_fp64, "traffic": None,
-                      "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
-                      "algorithmic_flops": flops, "ms": ms}
-    ach = bytes_ / (ms * 1e-3) / 1e9
-    return name, {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                  "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_bytes": bytes_, "ms": ms}
+    flops = stage_flops(d, N, L)
+    per_stage = {}
+    for k, f in flops.items():
+        if stages.get(k):
+            ach = f / (stages[k] * 1e-3) / 1e12
+            per_stage[k] = {"bound": "alu", "achieved_tflops": ach, "frac": ach / peak_fp64, "ms": stages[k]}
+    # the mid scale and the FFTs are HBM-bound: read + write of the half spectrum (16 B / complex point)
+    spec_bytes = 2 * 16.0 * d["Izs"] * d["Ix"] * (d["Iy"] // 2 + 1)
+    if stages.get("mid_scale"):
+        ach = spec_bytes / (stages["mid_scale"] * 1e-3) / 1e9
+        per_stage["mid_scale"] = {"bound": "hbm", "achieved_gbs": ach, "frac": ach / peaks["hbm_gbs"],
+                                  "ms": stages["mid_scale"]}
+    name = max((k for k in stages if k not in ("mid_fft_fwd", "mid_fft_inv", "long_fft_scale_ifft")),
+               key=lambda k: stages[k])
+    ms = stages[name]
+    if name in flops:
+        ach = flops[name] / (ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": name, "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
+                "frac": ach / peak_fp64, "traffic": None,
+                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md, guide unit counts)",
+                "algorithmic_flops": flops[name], "ms": ms}
+    else:
+        bytes_ = {"mid_scale": spec_bytes, "sort": 150.0 * N, "combine": 160.0 * N}.get(name, 64.0 * N)
+        ach = bytes_ / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_bytes": bytes_, "ms": ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    return name, roof, per_stage
 
 
 def main():
@@ -253,7 +274,7 @@ def main():
         for k, v in plan.timings().items():
             acc[k] = acc.get(k, 0.0) + v / args.steps
     plan.set_flags(validate=False)
-    dom, roof = stage_roofline(plan, acc, N, clk.summary())
+    dom, roof, per_stage = stage_roofline(plan, acc, N, L)
     # end-to-end through the public host-buffer API (pinned host memory, copies in the timed region)
     e2e = None
     if not args.no_e2e:
@@ -292,6 +313,7 @@ def main():
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc")}},
         "stages_ms": acc,
         "roofline": roof,
+        "stage_roofline": per_stage,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": plan.launches_per_eval() * args.steps,

@@ -279,12 +279,12 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
 constexpr int LG_KB = 64, LG_LT = 6, LG_RX = 32, LG_RY = 32;
 
 template <int PCP>
-__global__ void __launch_bounds__(512) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
-                                                          double gamma_y, int per, double* __restrict__ part) {
+__global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
+                                                             double gamma_y, int per, double* __restrict__ part) {
     constexpr int NLG = PCP / LG_LT;
-    __shared__ __align__(16) double sRx[LG_KB][LG_RX];
-    __shared__ __align__(16) double sRy[LG_KB][LG_RY];
-    __shared__ __align__(16) double sT[LG_KB][PCP];
+    // double-buffered rows: [2][LG_KB][RXP + RYP + PCP], RXP = Ilx, RYP = Ily rounded up to 4
+    extern __shared__ __align__(16) double sm[];
+    const int RXP = a.Ilx, RYP = (a.Ily + 3) & ~3, RW = ((RXP + RYP + PCP) + 1) & ~1;
     const int tid = threadIdx.x;
     const int ncy4 = (a.Ily + 3) / 4;
     const int lg = tid % NLG, cg = tid / NLG;
@@ -297,65 +297,73 @@ __global__ void __launch_bounds__(512) k_long_spread_gemm(LongArgs a, const int4
         for (int l = 0; l < LG_LT; ++l) acc[i][l] = 0.0;
     const int j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
     const int P = a.Pl;
-    for (int base = j0; base < j1; base += LG_KB) {
-        const int nb = min(LG_KB, j1 - base);
-        __syncthreads();
-        for (int t = tid; t < LG_KB; t += blockDim.x) {
-            double* rx = sRx[t];
-            double* ry = sRy[t];
-            double* tt = sT[t];
-            for (int c = 0; c < LG_RX; ++c) rx[c] = 0.0;
-            for (int c = 0; c < LG_RY; ++c) ry[c] = 0.0;
+    // two threads per staged particle: role 0 -> Rx row and T row, role 1 -> Ry row
+    auto stage = [&](int base, int buf) {
+        const int t = tid >> 1, role = tid & 1;
+        if (t >= LG_KB) return;
+        double* row = sm + ((size_t)buf * LG_KB + t) * RW;
+        double* rx = row;
+        double* ry = row + RXP;
+        double* tt = row + RXP + RYP;
+        if (role == 0) {
+            for (int c = 0; c < RXP; ++c) rx[c] = 0.0;
             for (int n = 0; n < PCP; ++n) tt[n] = 0.0;
-            if (t < nb) {
-                const int j = base + t;
-                const d4 r = ld_d4(&a.pos[j]);
-                const unsigned ow = (unsigned)g0[j].w;
-                const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
-                const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
-                // separable weights by the Gaussian recurrence (R6), placed at their columns
-                {
-                    const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
-                    double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
-                    int c = sx < 0 ? sx + a.Ilx : sx;
-                    for (int u = 0; u < P; ++u) {
-                        rx[c] = r.w * w;
-                        w *= q; q *= gamma_x;
-                        c = c + 1 == a.Ilx ? 0 : c + 1;
-                    }
-                }
-                {
-                    const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
-                    double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
-                    int c = sy < 0 ? sy + a.Ily : sy;
-                    for (int v = 0; v < P; ++v) {
-                        ry[c] = w;
-                        w *= q; q *= gamma_y;
-                        c = c + 1 == a.Ily ? 0 : c + 1;
-                    }
-                }
-                const double x = r.z * a.two_over_Lz;
-                double tm = 1.0, tc = x;
-                tt[0] = 1.0;
-                if (a.Pc > 1) tt[1] = x;
-                for (int n = 2; n < a.Pc; ++n) {
-                    const double tn = 2.0 * x * tc - tm;
-                    tt[n] = tn;
-                    tm = tc; tc = tn;
-                }
+        } else {
+            for (int c = 0; c < RYP; ++c) ry[c] = 0.0;
+        }
+        const int j = base + t;
+        if (j >= j1) return;
+        const d4 r = ld_d4(&a.pos[j]);
+        const unsigned ow = (unsigned)g0[j].w;
+        if (role == 0) {
+            const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
+            const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
+            double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
+            int c = sx < 0 ? sx + a.Ilx : sx;
+            for (int u = 0; u < P; ++u) {
+                rx[c] = r.w * w;
+                w *= q; q *= gamma_x;
+                c = c + 1 == a.Ilx ? 0 : c + 1;
+            }
+            const double x = r.z * a.two_over_Lz;
+            double tm = 1.0, tc = x;
+            tt[0] = 1.0;
+            if (a.Pc > 1) tt[1] = x;
+            for (int n = 2; n < a.Pc; ++n) {
+                const double tn = 2.0 * x * tc - tm;
+                tt[n] = tn;
+                tm = tc; tc = tn;
+            }
+        } else {
+            const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
+            const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
+            double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
+            int c = sy < 0 ? sy + a.Ily : sy;
+            for (int v = 0; v < P; ++v) {
+                ry[c] = w;
+                w *= q; q *= gamma_y;
+                c = c + 1 == a.Ily ? 0 : c + 1;
             }
         }
-        __syncthreads();
+    };
+    if (j0 < j1) stage(j0, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int base = j0; base < j1; base += LG_KB, buf ^= 1) {
+        if (base + LG_KB < j1) stage(base + LG_KB, buf ^ 1);    // next batch while this one computes
+        const int nb = min(LG_KB, j1 - base);
         if (own) {
+            const double* rows = sm + (size_t)buf * LG_KB * RW;
 #pragma unroll 2
             for (int t = 0; t < nb; ++t) {
-                const double rx = sRx[t][cx];
-                const double2 y01 = *reinterpret_cast<const double2*>(&sRy[t][cy0]);
-                const double2 y23 = *reinterpret_cast<const double2*>(&sRy[t][cy0 + 2]);
+                const double* row = rows + (size_t)t * RW;
+                const double rx = row[cx];
+                const double2 y01 = *reinterpret_cast<const double2*>(row + RXP + cy0);
+                const double2 y23 = *reinterpret_cast<const double2*>(row + RXP + cy0 + 2);
                 double tl[LG_LT];
 #pragma unroll
                 for (int l = 0; l < LG_LT; l += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(&sT[t][lg * LG_LT + l]);
+                    const double2 v = *reinterpret_cast<const double2*>(row + RXP + RYP + lg * LG_LT + l);
                     tl[l] = v.x; tl[l + 1] = v.y;
                 }
                 const double av[4] = {rx * y01.x, rx * y01.y, rx * y23.x, rx * y23.y};
@@ -365,6 +373,7 @@ __global__ void __launch_bounds__(512) k_long_spread_gemm(LongArgs a, const int4
                     for (int l = 0; l < LG_LT; ++l) acc[i][l] = fma(av[i], tl[l], acc[i][l]);
             }
         }
+        __syncthreads();
     }
     if (own) {
         const size_t G = (size_t)a.Ilx * a.Ily;
@@ -396,7 +405,7 @@ static __global__ void k_long_sum(const double* __restrict__ part, double* __res
 // (2 PCP FMAs) and 4 products with the rotated weights.  Rx / dRx rows live in shared
 // memory (dynamic cx), Ry / dRy in registers (static cy < NCY).
 template <int PCP, int NCY>
-__global__ void __launch_bounds__(128) k_long_gather_bc(LongArgs a, const int4* __restrict__ g0,
+__global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int4* __restrict__ g0,
                                                         const double* __restrict__ psi, d4* __restrict__ out) {
     extern __shared__ __align__(16) double sm[];
     const int G = a.Ilx * a.Ily;
@@ -414,7 +423,6 @@ __global__ void __launch_bounds__(128) k_long_gather_bc(LongArgs a, const int4* 
     const bool act = j < a.N;
     const int P = a.Pl;
     double T[PCP], dT[PCP];
-    double ry[NCY], dry[NCY];
     {
         for (int c = 0; c < a.Ilx; ++c) { sRx[c * 128 + tid] = 0.0; sdRx[c * 128 + tid] = 0.0; }
 #pragma unroll
@@ -451,8 +459,6 @@ __global__ void __launch_bounds__(128) k_long_gather_bc(LongArgs a, const int4* 
                 }
             }
         }
-#pragma unroll
-        for (int c = 0; c < NCY; ++c) { ry[c] = sRy[c * 128 + tid]; dry[c] = sdRy[c * 128 + tid]; }
         const double x = r.z * a.two_over_Lz;
         T[0] = 1.0; dT[0] = 0.0;
         T[1] = x; dT[1] = 1.0;
@@ -478,11 +484,12 @@ __global__ void __launch_bounds__(128) k_long_gather_bc(LongArgs a, const int4* 
                     v0 = fma(T[n], ps.x, v0); v0 = fma(T[n + 1], ps.y, v0);
                     v1 = fma(dT[n], ps.x, v1); v1 = fma(dT[n + 1], ps.y, v1);
                 }
-                const double wxy = rx * ry[cy];
+                const double ry = sRy[cy * 128 + tid], dry = sdRy[cy * 128 + tid];
+                const double wxy = rx * ry;
                 phi = fma(wxy, v0, phi);
                 gz = fma(wxy, v1, gz);
-                gx = fma(drx * ry[cy], v0, gx);
-                gy = fma(rx * dry[cy], v0, gy);
+                gx = fma(drx * ry, v0, gx);
+                gy = fma(rx * dry, v0, gy);
             }
         }
     }

@@ -86,15 +86,22 @@ namespace sog {
 int long_small_pcp(int Pc) { return Pc <= 30 ? ((Pc + LG_LT - 1) / LG_LT) * LG_LT : 0; }
 
 bool long_small_ok(int Ilx, int Ily, int Pc) {
-    return Ilx <= LG_RX && Ily <= LG_RY && Ilx * Ily <= 256 && long_small_pcp(Pc) > 0 && Ily <= 16;
+    const int pcp = long_small_pcp(Pc);
+    return Ilx <= LG_RX && Ily <= 16 && pcp > 0 && Ilx * ((Ily + 3) / 4) * (pcp / LG_LT) <= 128;
 }
 
 template <int PCP>
 int spread_gemm_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part, double* grid,
                    cudaStream_t st) {
     const int nthr = ((a.Ilx * ((a.Ily + 3) / 4) * (PCP / LG_LT) + 31) / 32) * 32;
+    if (nthr > 128) return 1;
     const int per = (a.N + nblk - 1) / nblk;
-    k_long_spread_gemm<PCP><<<nblk, nthr, 0, st>>>(a, g0, gx, gy, per, part);
+    const int RW = ((a.Ilx + ((a.Ily + 3) & ~3) + PCP) + 1) & ~1;
+    const size_t sh = sizeof(double) * 2 * LG_KB * RW;
+    if (cudaFuncSetAttribute(k_long_spread_gemm<PCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+        cudaSuccess)
+        return 2;
+    k_long_spread_gemm<PCP><<<nblk, 128, sh, st>>>(a, g0, gx, gy, per, part);
     const int G = a.Ilx * a.Ily;
     k_long_sum<<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
