@@ -213,10 +213,16 @@ def stage_roofline(plan, stages, N, L):
     name = max((k for k in stages if k not in ("mid_fft_fwd", "mid_fft_inv", "long_fft_scale_ifft")),
                key=lambda k: stages[k])
     ms = stages[name]
+    # DRAM traffic of that kernel from the committed ncu --set full capture (per launch), if any
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get(name)
+        traffic = t["dram_bytes_per_launch"] if t else None
     if name in flops:
         ach = flops[name] / (ms * 1e-3) / 1e12
         roof = {"bound": "alu", "kernel": name, "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
-                "frac": ach / peak_fp64, "traffic": None,
+                "frac": ach / peak_fp64, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
                 "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md, guide unit counts)",
                 "algorithmic_flops": flops[name], "ms": ms}
     else:
