@@ -44,6 +44,7 @@ typedef enum {
     SOG_ENONFINITE = -4,    /* non-finite position or charge                                */
     SOG_EINFEASIBLE = -5,   /* tol outside [2e-14, 1e-1] (Table 1 force floor)       */
     SOG_ECUDA = -6,         /* CUDA runtime or cuFFT failure                                 */
+    SOG_ENCCL = -7,         /* NCCL unavailable or an NCCL call failed (x-slab ranks)        */
     SOG_ENOMEM = -8         /* device allocation failed                                      */
 } sog_status;
 
@@ -138,6 +139,45 @@ int sog_set_stream(sog_plan* p, void* cuda_stream);
 
 /* Number of kernel launches sog_eval enqueues (for the bench's gpu_launches). */
 int sog_launches_per_eval(const sog_plan* p);
+
+/* ---------------------------------------------------------------------------------------
+ * x-slab decomposition over R ranks (north_star "partitioned across the 8
+ * GPUs of one box by x-slabs").  Rank r owns the particles with canonical x in
+ *   [-Lx/2 + r Lx/R, -Lx/2 + (r+1) Lx/R)     (the last slab is closed at +Lx/2 by the wrap)
+ * and the mid-grid planes [r Ix/R, (r+1) Ix/R).  One evaluation exchanges: particle halos
+ * (particles within H = max(r_c, (p + 1.5) h_x) of a slab edge) with the two neighbours; the
+ * pencil all-to-all of the distributed 3D FFT (2D (z,y) FFTs per x plane, ky chunks, 1D FFT
+ * along x, and back); the Psi edge planes needed by the gather; and a sum of the long-range
+ * proxy grids (all-reduce).  The result equals the single-GPU evaluation up to rounding.
+ * The plan parameters are those of the global system of N_total particles (Ix rounded up to
+ * a multiple of R when the rules choose it); n_own_max bounds every rank's own count.
+ * --------------------------------------------------------------------------------------- */
+typedef struct sog_dist sog_dist;
+
+/* 128 bytes of ncclUniqueId for sog_dist_create (call on one rank, broadcast to the others,
+ * e.g. with torch.distributed).  SOG_ENCCL if libnccl.so.2 cannot be loaded. */
+int sog_nccl_unique_id(void* id128);
+
+/* One process per GPU (NCCL over NVLink): this process is `rank` of `nranks`.  Every rank
+ * calls it collectively with the same N_total, n_own_max, box, tol, opts and id. */
+sog_dist* sog_dist_create(int64_t N_total, int64_t n_own_max, double Lx, double Ly, double Lz, double tol,
+                          const sog_plan_opts* opts, int rank, int nranks, const void* nccl_id);
+
+/* All nranks ranks as virtual ranks of this process on the current device (exchanges are
+ * device-to-device copies): the same decomposition, for testing on one GPU. */
+sog_dist* sog_dist_create_loopback(int64_t N_total, int64_t n_own_max, double Lx, double Ly, double Lz, double tol,
+                                   const sog_plan_opts* opts, int nranks);
+
+/* Evaluate.  Arrays of length sog_dist_local_ranks(d) (1 for NCCL ranks, nranks for loopback);
+ * entry i: n_own[i] particles of local rank i, device arrays xyz (n x 3), q (n), outputs phi
+ * (n), force (n x 3) in that rank's own particle order.  Collective: every rank calls it.
+ * SOG_EINVAL if a particle is outside its rank's slab or a halo exceeds its capacity. */
+int sog_dist_eval(sog_dist* d, const int64_t* n_own, const double* const* xyz, const double* const* q,
+                  double* const* phi, double* const* force);
+
+int sog_dist_local_ranks(const sog_dist* d);
+int sog_dist_describe(const sog_dist* d, char* buf, size_t len);   /* plan + slab key=value lines */
+void sog_dist_destroy(sog_dist* d);                                 /* NULL-safe */
 
 #ifdef __cplusplus
 }

@@ -6,6 +6,6 @@ The Python layer only marshals arguments (ctypes); every step of the evaluation 
 libsog.so.  There is no CPU fallback: importing works without a GPU (plan creation and
 describe need none), but evaluation fails loudly without CUDA.
 """
-from .sog import Plan, SogError, choose_params, lib_path, load_library  # noqa: F401
+from .sog import DistPlan, Plan, SogError, choose_params, lib_path, load_library, redistribute, slab_owner  # noqa: F401
 
-__all__ = ["Plan", "SogError", "choose_params", "lib_path", "load_library"]
+__all__ = ["DistPlan", "Plan", "SogError", "choose_params", "lib_path", "load_library", "redistribute", "slab_owner"]

@@ -3,6 +3,13 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#ifdef SOG_ASSERTS
+#include <cassert>
+#define SOG_ASSERT(c) assert(c)
+#else
+#define SOG_ASSERT(c) ((void)0)
+#endif
+
 namespace sog {
 
 struct __align__(32) d4 {
@@ -23,12 +30,15 @@ __device__ __forceinline__ void st_d4(d4* p, d4 v) {
 // Validation flag bits written by k_prepare.
 enum : unsigned { FLAG_NONFINITE = 1u, FLAG_ZRANGE = 2u };
 
-// Geometry of the near-field cell grid (cells >= r_c; x,y periodic; z clamped).
+// Geometry of the near-field cell grid (cells >= r_c; y periodic; z clamped; x periodic for a
+// whole-box plan, or a non-periodic extended slab [x0, x0 + Lx) for an x-slab rank).
 struct CellGeo {
     double Lx, Ly, Lz;
     double invLx, invLy;
     int ncx, ncy, ncz;
     double sx, sy, sz;      // cells per unit length (nc / L)
+    double x0;              // x of the first cell edge (-Lx/2 for the whole box)
+    int px;                 // 1: x periodic (whole box), 0: x-slab (no x images)
 };
 
 // One axis of a window stencil on a uniform grid x_g = (g - I/2) h (R6):

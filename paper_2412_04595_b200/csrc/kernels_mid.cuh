@@ -64,6 +64,7 @@ __device__ __forceinline__ int wrapc(int v, int n) {
 // Mid-order bucket sort (part of S1).  k_mid_key -> scan -> k_mid_scatter -> k_mid_bucket.
 struct MidSortArgs {
     int Ix, Iy, p, nty, nzc;
+    int px, xorig;          // x periodic (whole box) or x-slab: local start = s_x - xorig (no wrap)
 };
 
 static __global__ void k_mid_key(const int4* __restrict__ g0, int N, MidSortArgs s, int* __restrict__ key,
@@ -71,7 +72,8 @@ static __global__ void k_mid_key(const int4* __restrict__ g0, int N, MidSortArgs
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     const int4 o = g0[j];
-    const int sx = wrapc(o.x - s.p, s.Ix), sy = wrapc(o.y - s.p, s.Iy), sz = o.z - s.p;
+    const int sx = s.px ? wrapc(o.x - s.p, s.Ix) : o.x - s.p - s.xorig, sy = wrapc(o.y - s.p, s.Iy), sz = o.z - s.p;
+    SOG_ASSERT(sx >= 0 && sy >= 0 && sz >= 0);
     const int k = ((sx / MZ_TX) * s.nty + sy / MZ_TY) * s.nzc + sz / MZ_ZC;
     key[j] = k;
     atomicAdd(&count[k], 1);
@@ -115,6 +117,8 @@ struct MidZArgs {
     int c_lo, c_hi;                       // chunks that can hold stencil starts
     int c_hiw;                            // last chunk with nonzero planes (spread writes [c_lo, c_hiw])
     int cps;                              // chunks per CTA z segment
+    int px, xorig, Ixk;                   // x periodic, or x-slab: local x = global - xorig, extent Ixk
+    int tlo, ntout;                       // x tiles processed: [tlo, tlo + ntout)
     const d4* mpos;
     const int4* minfo;                    // (cell-sorted index, s_x, s_y, s_z) unwrapped starts
     const int* mstart;                    // [ntx*nty*nzc + 1]
@@ -167,7 +171,8 @@ __device__ __forceinline__ void spread_flush(double (&acc)[SRec<P>::NACC], int c
 #pragma unroll
         for (int z = 0; z < MZ_ZC; ++z) {
             const int plane = c * MZ_ZC + z;
-            if (plane < a.Izs) grid[((size_t)plane * a.Ix + cx) * a.Iy + cy] = acc[z];
+            SOG_ASSERT(cx < a.Ixk && cy < a.Iy);
+            if (plane < a.Izs) grid[((size_t)plane * a.Ixk + cx) * a.Iy + cy] = acc[z];
         }
     }
 #pragma unroll
@@ -190,8 +195,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
     __shared__ unsigned long long barFull[K], barEmpty[K];
     __shared__ int sHx[8], sHy[8], sNh[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const int tx = tile / a.nty, ty = tile % a.nty;
+    const int tx = a.tlo + blockIdx.x / a.nty, ty = blockIdx.x % a.nty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
     // z segment: written chunks [cb, ce), sweep from cs (warm-up chunks are not written)
     const int cb = a.c_lo + blockIdx.y * a.cps;
@@ -199,11 +203,13 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
     if (cb >= ce) return;
     const int cs = max(a.c_lo, cb - (P - 2 + MZ_ZC) / MZ_ZC);
     const int cp1 = min(ce, a.c_hi + 1);                 // chunks [cs, cp1) hold particles
-    const bool small = (MZ_TX + P - 1 > a.Ix) || (MZ_TY + P - 1 > a.Iy);
+    const bool smallx = a.px && (MZ_TX + P - 1 > a.Ix), smally = MZ_TY + P - 1 > a.Iy;
     // home tiles whose particles can reach this tile (starts in [X0 - P + 1, X0 + TX - 1])
     if (tid == 0) {
         int n = 0;
-        if (MZ_TX + P - 1 >= a.Ix) {
+        if (!a.px) {
+            for (int h = max(0, (X0 - (P - 1)) / MZ_TX); h <= tx && n < 8; ++h) sHx[n++] = h;
+        } else if (MZ_TX + P - 1 >= a.Ix) {
             for (int h = 0; h < a.ntx && n < 8; ++h) sHx[n++] = h;
         } else {
             int h = wrapc(X0 - (P - 1), a.Ix) / MZ_TX;
@@ -231,6 +237,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
     for (int e = tid; e < E; e += R::NTHR) {
         const int c = cs + e / nh, h = e % nh;
         const int k = (sHx[h / nhy] * a.nty + sHy[h % nhy]) * a.nzc + c;
+        SOG_ASSERT(k >= 0 && k < a.ntx * a.nty * a.nzc);
         const int b = a.mstart[k];
         sBeg[e] = b;
         sPre[e + 1] = a.mstart[k + 1] - b;
@@ -271,22 +278,27 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
                 }
                 const int c = cs + lo / nh;
                 const int k = sBeg[lo] + (idx - sPre[lo]);
+                SOG_ASSERT(lo >= 0 && lo < E && k >= 0);
                 const int4 in = a.minfo[k];
-                int dx = wrapc(in.y - X0, a.Ix), dy = wrapc(in.z - Y0, a.Iy);
+                SOG_ASSERT(in.w - c * MZ_ZC >= 0 && in.w - c * MZ_ZC < MZ_ZC);
+                int dx = a.px ? wrapc(in.y - X0, a.Ix) : in.y - a.xorig - X0, dy = wrapc(in.z - Y0, a.Iy);
                 unsigned mx = 0, my = 0;
-                if (!small) {
-                    dx -= dx > a.Ix - P ? a.Ix : 0;      // signed start in [-(P-1), MZ_TX)
-                    dy -= dy > a.Iy - P ? a.Iy : 0;
+                if (!smallx) {
+                    if (a.px) dx -= dx > a.Ix - P ? a.Ix : 0;   // signed start in [-(P-1), MZ_TX)
 #pragma unroll
                     for (int g = 0; g < 4; ++g) mx |= (dx <= 4 * g + 3 && dx + P - 1 >= 4 * g) ? 1u << g : 0u;
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) my |= (dy <= 8 * g + 7 && dy + P - 1 >= 8 * g) ? 1u << g : 0u;
                 } else {
 #pragma unroll
                     for (int g = 0; g < 4; ++g)
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
                             if (wrapc(4 * g + i - dx, a.Ix) < P) mx |= 1u << g;
+                }
+                if (!smally) {
+                    dy -= dy > a.Iy - P ? a.Iy : 0;
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) my |= (dy <= 8 * g + 7 && dy + P - 1 >= 8 * g) ? 1u << g : 0u;
+                } else {
 #pragma unroll
                     for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
     // ---------------- consumers: warp = one 4 x 8 column patch ----------------
     const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
     const int cx = X0 + lx, cy = Y0 + ly;
-    const bool colok = cx < a.Ix && cy < a.Iy;
+    const bool colok = cx < a.Ixk && cy < a.Iy;
     double acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -345,9 +357,8 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
         __syncwarp();
         const double* base = sRec + buf * B * R::SIZE;
         auto coef = [&](const double* rec, const int4& hdr) {
-            int u, v;
-            if (!small) { u = lx - hdr.x; v = ly - hdr.y; }
-            else { u = wrapc(lx - hdr.x, a.Ix); v = wrapc(ly - hdr.y, a.Iy); }
+            const int u = smallx ? wrapc(lx - hdr.x, a.Ix) : lx - hdr.x;
+            const int v = smally ? wrapc(ly - hdr.y, a.Iy) : ly - hdr.y;
             const bool in = (unsigned)u < (unsigned)P && (unsigned)v < (unsigned)P;
             return in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : 0.0;
         };
@@ -417,8 +428,8 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
     double* ring = sm;                                   // [D][WX][WYP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* wsb = sm + D * PL + warp * G::WB * G::WSZ;   // per particle: Wx dWx Wy dWy Wz dWz, hdr
-    const int tile = blockIdx.x;
-    const int tx = tile / a.nty, ty = tile % a.nty;
+    const int tx = a.tlo + blockIdx.x / a.nty, ty = blockIdx.x % a.nty;
+    const int tile = tx * a.nty + ty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
     const int cb = a.c_lo + blockIdx.y * a.cps;
     const int ce = min(cb + a.cps, a.c_hi + 1);
@@ -453,8 +464,8 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
                         const int pz = e / NPL, rem = e - pz * NPL;
                         const int xr = rem / WY, yr = rem - xr * WY;
                         const int plane = from + pz;
-                        const int gx = wrapc(X0 + xr, a.Ix), gy = wrapc(Y0 + yr, a.Iy);
-                        v[u] = __ldg(&psi[((size_t)plane * a.Ix + gx) * a.Iy + gy]);
+                        const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr, gy = wrapc(Y0 + yr, a.Iy);
+                        v[u] = gx < a.Ixk ? __ldg(&psi[((size_t)plane * a.Ixk + gx) * a.Iy + gy]) : 0.0;
                         dst[u] = (plane % D) * PL + xr * WYP + yr;
                     }
                 }
@@ -492,7 +503,7 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
                 }
                 if (axl == 0) {
                     int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + 6 * P);
-                    hd[0] = in.y - X0 + (in.y < 0 ? a.Ix : 0);          // start relative to the tile
+                    hd[0] = a.px ? in.y - X0 + (in.y < 0 ? a.Ix : 0) : in.y - a.xorig - X0;   // relative to the tile
                     hd[1] = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
                     hd[2] = in.w % D;                                    // ring slot of the first plane
                     hd[3] = in.x;                                        // output (cell-sorted) index
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* 
     const double half = ax == 0 ? a.halfx : (ax == 1 ? a.halfy : a.halfz);
     const double al = ax == 0 ? a.invH2Sx : (ax == 1 ? a.invH2Sy : a.invH2Sz);
     const double gam = ax == 0 ? a.gamma_x : (ax == 1 ? a.gamma_y : a.gamma_z);
-    const size_t plane = (size_t)a.Ix * a.Iy;
+    const size_t plane = (size_t)a.Ixk * a.Iy;
     for (int k = blockIdx.x * 8 + warp; k < nmid; k += gridDim.x * 8) {
         const int4 in = a.minfo[k];
         const d4 r = ld_d4(&a.mpos[k]);
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* 
         const double* zb = psi + (size_t)in.w * plane;
         for (int idx = lane; idx < P * P; idx += 32) {
             const int ai = idx / P, bi = idx - ai * P;
-            const int ix = wrapc(in.y + ai, a.Ix), iy = wrapc(in.z + bi, a.Iy);
+            const int ix = a.px ? wrapc(in.y + ai, a.Ix) : min(in.y + ai - a.xorig, a.Ixk - 1), iy = wrapc(in.z + bi, a.Iy);
             const double* col = zb + (size_t)ix * a.Iy + iy;
             double t0 = 0.0, t1 = 0.0;
 #pragma unroll

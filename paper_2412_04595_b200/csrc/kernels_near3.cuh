@@ -66,14 +66,16 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
     for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = a.cF[t];
     if (threadIdx.x < 9) {
         const int k = threadIdx.x, ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
-        shift[k] = make_double2(ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0), uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0));
+        shift[k] = make_double2(!g.px ? 0.0 : (ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0)),
+                                uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0));
     }
-    const double ox = cx / g.sx - 0.5 * g.Lx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
+    const double ox = g.x0 + cx / g.sx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
     const int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
     int* wl = lists + warp * 160;
     int ns_total = 0;
     for (int k = 0; k < 9; ++k) {
         int nx = cx + k / 3 - 1, ny = cy + k % 3 - 1;
+        if (!g.px && (nx < 0 || nx >= g.ncx)) continue;           // x-slab: no x images
         nx += nx < 0 ? g.ncx : 0; nx -= nx >= g.ncx ? g.ncx : 0;
         ny += ny < 0 ? g.ncy : 0; ny -= ny >= g.ncy ? g.ncy : 0;
         const int cb = (nx * g.ncy + ny) * g.ncz;
@@ -88,9 +90,10 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
             int base = 0;
             for (int k = 0; k < 9; ++k) {
                 const int ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
+                if (!g.px && (ux < 0 || ux >= g.ncx)) continue;       // x-slab: no x images
                 const int nx = ux < 0 ? ux + g.ncx : (ux >= g.ncx ? ux - g.ncx : ux);
                 const int ny = uy < 0 ? uy + g.ncy : (uy >= g.ncy ? uy - g.ncy : uy);
-                const double sx = ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0);
+                const double sx = !g.px ? 0.0 : (ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0));
                 const double sy = uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0);
                 const int cb = (nx * g.ncy + ny) * g.ncz;
                 const int jb = a.start[cb + z0], n = a.start[cb + z1 + 1] - jb;

@@ -27,12 +27,12 @@ __global__ void k_prepare(const double* __restrict__ xyz, const double* __restri
         double qi = q[i];
         unsigned f = 0;
         if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(qi)) f |= FLAG_NONFINITE;
-        x = canon(x, g.Lx);
+        if (g.px) x = canon(x, g.Lx);   // x-slab ranks receive own + halo particles in the slab frame
         y = canon(y, g.Ly);
         if (!(fabs(z) <= 0.5 * g.Lz)) f |= FLAG_ZRANGE;
         int cx = 0, cy = 0, cz = 0;
         if (!f) {
-            cx = clampi((int)floor((x + 0.5 * g.Lx) * g.sx), 0, g.ncx - 1);
+            cx = clampi((int)floor((x - g.x0) * g.sx), 0, g.ncx - 1);
             cy = clampi((int)floor((y + 0.5 * g.Ly) * g.sy), 0, g.ncy - 1);
             cz = clampi((int)floor((z + 0.5 * g.Lz) * g.sz), 0, g.ncz - 1);
         }

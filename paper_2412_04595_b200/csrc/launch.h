@@ -36,4 +36,7 @@ int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const dou
 // exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total); temp from scan_temp_bytes
 size_t scan_temp_bytes(int n);
 int launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes, cudaStream_t st);
+size_t select_temp_bytes(int n);
+int launch_select_flagged(const d4* in, const int* flags, d4* out, int* nsel, int n, void* temp, size_t temp_bytes,
+                          cudaStream_t st);
 }  // namespace sog

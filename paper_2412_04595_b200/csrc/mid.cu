@@ -29,7 +29,7 @@ int spread_go(const MidZArgs& a, int nseg, double* grid, cudaStream_t st) {
     const size_t sh = SRec<P>::BYTES;
     if (cudaFuncSetAttribute(k_mid_spread_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
         return 2;
-    k_mid_spread_z<P><<<dim3(a.ntx * a.nty, nseg), SRec<P>::NTHR, sh, st>>>(a, grid);
+    k_mid_spread_z<P><<<dim3(a.ntout * a.nty, nseg), SRec<P>::NTHR, sh, st>>>(a, grid);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -48,7 +48,7 @@ int gather_go(const MidZArgs& a, int nseg, int nmid, const double* psi, d4* out,
         const size_t sh = GRing<P>::BYTES;
         if (cudaFuncSetAttribute(k_mid_gather_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
             return 2;
-        k_mid_gather_z<P><<<dim3(a.ntx * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+        k_mid_gather_z<P><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
     } else {
         k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
     }

@@ -20,3 +20,23 @@ int launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t tem
 }
 
 }  // namespace sog
+
+#include <cub/device/device_select.cuh>
+
+namespace sog {
+
+// stable compaction of the flagged particles (x-slab halos)
+size_t select_temp_bytes(int n) {
+    size_t bytes = 0;
+    cub::DeviceSelect::Flagged(nullptr, bytes, (const d4*)nullptr, (const int*)nullptr, (d4*)nullptr, (int*)nullptr, n);
+    return bytes;
+}
+
+int launch_select_flagged(const d4* in, const int* flags, d4* out, int* nsel, int n, void* temp, size_t temp_bytes,
+                          cudaStream_t st) {
+    size_t bytes = temp_bytes;
+    if (cub::DeviceSelect::Flagged(temp, bytes, in, flags, out, nsel, n, st) != cudaSuccess) return 2;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace sog

@@ -11,13 +11,16 @@
 #include <cufft.h>
 
 #include <cmath>
+#include <type_traits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/sog.h"
 #include "kernels_common.cuh"
+#include "kernels_dist.cuh"
 #include "kernels_long.cuh"
 #include "kernels_mid.cuh"
 #include "launch.h"
@@ -37,12 +40,13 @@ int fail(int code, const std::string& msg) {
 namespace sog {
 
 __global__ void k_combine(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
-                          const d4* __restrict__ pos, const int* __restrict__ perm, int N, double selfc,
+                          const d4* __restrict__ pos, const int* __restrict__ perm, int N, int nown, double selfc,
                           double* __restrict__ phi, double* __restrict__ force, double* __restrict__ energy) {
     // phi_i = Phi^N + Phi^mid + Phi^long - q_i sum_l w_l; F_i = -q_i grad phi
+    // (x-slab: only the nown own particles are written; halo entries have perm >= nown)
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0;
-    if (k < N) {
+    if (k < N && perm[k] < nown) {
         d4 a = ld_d4(&nearo[k]), b = ld_d4(&mido[k]), c = ld_d4(&longo[k]);
         double q = ld_d4(&pos[k]).w;
         double ph = a.x + b.x + c.x - q * selfc;
@@ -128,6 +132,24 @@ struct sog_plan {
     cudaEvent_t ev[16] = {};
     double timings[11] = {};
     size_t bytes = 0;
+    // ---- x-slab rank (R > 1); R == 1: the whole periodic box ----
+    int R = 1, rank = 0;
+    int Ncap = 0, Ncur = 0, Nown = 0;      // particle capacity / current local / own counts
+    double xs0 = 0, xs1 = 0, Hh = 0;       // slab [xs0, xs1) and particle halo width
+    int I0 = 0, Ixr = 0, XO = 0, Ixk = 0;  // interior planes [I0, I0+Ixr) at local x XO; local extent
+    int kc = 0, HP = 0;                    // ky chunk per rank; Psi halo planes per side
+    size_t blk = 0;                        // complex elements per all-to-all block
+    cuDoubleComplex *spec2 = nullptr, *specx = nullptr, *sbuf = nullptr, *rbuf = nullptr;
+    cufftHandle f2f = 0, f2i = 0, fxf = 0, fxi = 0;   // 2D (z,y) per x plane; 1D along x
+    double *hsb = nullptr, *hrb = nullptr;             // Psi halo planes [2][Izs][HP][Iy]
+    d4 *own = nullptr, *hsend = nullptr, *hrecv = nullptr, *pos_long = nullptr;
+    int *fl = nullptr, *fr = nullptr, *nsel = nullptr;
+    unsigned* dbad = nullptr;
+    double *lxyz = nullptr, *lq = nullptr;
+    void* sel_tmp = nullptr;
+    size_t sel_bytes = 0;
+    int halo_cap = 0;
+    int* pin_i = nullptr;                   // pinned [nl_send, nr_send, nl_recv, nr_recv, bad]
 };
 
 namespace {
@@ -167,11 +189,13 @@ void free_plan(sog_plan* pl) {
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
-                    pl->scan_tmp};
+                    pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
+                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
-    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv})
+    if (pl->pin_i) cudaFreeHost(pl->pin_i);
+    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi})
         if (h) cufftDestroy(h);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
@@ -181,7 +205,9 @@ void free_plan(sog_plan* pl) {
 int setup(sog_plan* pl) {
     Params& p = pl->p;
     CK(cudaGetDevice(&pl->device));
-    const int N = int(p.N);
+    if (pl->Ncap <= 0) pl->Ncap = int(p.N);
+    const int N = pl->Ncap;
+    const bool slab = pl->R > 1;
     std::vector<double> w, s;
     sog_weights(p, w, s);
     pl->selfc = 0;
@@ -190,11 +216,20 @@ int setup(sog_plan* pl) {
     CellGeo& g = pl->geo;
     g.Lx = p.Lx; g.Ly = p.Ly; g.Lz = p.Lz;
     g.invLx = 1.0 / p.Lx; g.invLy = 1.0 / p.Ly;
-    g.ncx = std::max(1, int(std::floor(p.Lx / p.rc)));
+    g.px = 1;
+    g.x0 = -0.5 * p.Lx;
+    if (slab) {   // non-periodic extended slab [xs0 - H, xs1 + H)
+        g.Lx = (pl->xs1 - pl->xs0) + 2.0 * pl->Hh;
+        g.invLx = 1.0 / g.Lx;
+        g.x0 = pl->xs0 - pl->Hh;
+        g.px = 0;
+    }
+    g.ncx = std::max(1, int(std::floor(g.Lx / p.rc)));
     g.ncy = std::max(1, int(std::floor(p.Ly / p.rc)));
     g.ncz = std::max(1, int(std::floor(p.Lz / p.rc)));
     while ((long)g.ncx * g.ncy * g.ncz > 64L * 1024 * 1024) { g.ncx = std::max(1, g.ncx / 2); g.ncy = std::max(1, g.ncy / 2); }
-    g.sx = g.ncx / p.Lx; g.sy = g.ncy / p.Ly; g.sz = g.ncz / p.Lz;
+    g.sx = g.ncx / g.Lx; g.sy = g.ncy / p.Ly; g.sz = g.ncz / p.Lz;
+    if (slab && (g.ncx < 3 || g.ncy < 3)) return fail(SOG_EINVAL, "x-slab needs >= 3 near cells per axis");
     pl->ncell = g.ncx * g.ncy * g.ncz;
     auto offs = [](int nc, int* o, int& n) {
         if (nc >= 3) { o[0] = -1; o[1] = 0; o[2] = 1; n = 3; }
@@ -218,10 +253,26 @@ int setup(sog_plan* pl) {
     // mid range
     pl->has_mid = p.m >= 0;
     if (pl->has_mid) {
-        size_t G = (size_t)p.Ix * p.Iy * p.Izs, Gc = (size_t)p.Izs * p.Ix * (p.Iy / 2 + 1);
+        const int nyh = p.Iy / 2 + 1;
+        if (slab) {   // local extended planes: [XO halo | Ixr interior (tile-padded) | XO + 16 halo]
+            pl->Ixr = p.Ix / pl->R;
+            pl->I0 = pl->rank * pl->Ixr;
+            // left/right local halo planes: every local particle (x within H of the slab) has its
+            // stencil start s_x in [I0 - ceil(H/h) - 1 - p, ...): XO covers it, tile aligned
+            const int hpl = int(std::ceil(pl->Hh / p.hx())) + 2 + p.P;
+            pl->XO = MZ_TX * ((hpl + MZ_TX - 1) / MZ_TX);
+            pl->Ixk = pl->XO + MZ_TX * ((pl->Ixr + MZ_TX - 1) / MZ_TX) + pl->XO + MZ_TX;
+            pl->HP = (p.P - 1) / 2 + 1;
+            pl->kc = (nyh + pl->R - 1) / pl->R;
+            pl->blk = (size_t)p.Izs * pl->Ixr * pl->kc;
+        } else {
+            pl->Ixk = p.Ix;
+        }
+        size_t G = (size_t)pl->Ixk * p.Iy * p.Izs, Gc = slab ? 1 : (size_t)p.Izs * p.Ix * nyh;
         if ((rc = dalloc(pl, &pl->mgrid, G)) || (rc = dalloc(pl, &pl->mpsi, G)) || (rc = dalloc(pl, &pl->mspec, Gc)))
             return rc;
         CK(cudaMemset(pl->mgrid, 0, G * sizeof(double)));
+        CK(cudaMemset(pl->mpsi, 0, G * sizeof(double)));
         // mid order (S1) and the z-sweep geometry of the spread / gather
         MidZArgs& z = pl->mz;
         const int pp = (p.P - 1) / 2;
@@ -233,14 +284,19 @@ int setup(sog_plan* pl) {
         z.Vh = z.hx * z.hy * z.hz;
         auto gam = [&](double h) { return std::exp(-2.0 * inv(h) * h * h); };
         z.gamma_x = gam(z.hx); z.gamma_y = gam(z.hy); z.gamma_z = gam(z.hz);
-        z.ntx = (p.Ix + MZ_TX - 1) / MZ_TX; z.nty = (p.Iy + MZ_TY - 1) / MZ_TY; z.nzc = (p.Izs + MZ_ZC - 1) / MZ_ZC;
+        z.ntx = (pl->Ixk + MZ_TX - 1) / MZ_TX; z.nty = (p.Iy + MZ_TY - 1) / MZ_TY; z.nzc = (p.Izs + MZ_ZC - 1) / MZ_ZC;
+        z.px = slab ? 0 : 1;
+        z.xorig = slab ? pl->I0 - pl->XO : 0;
+        z.Ixk = pl->Ixk;
+        z.tlo = slab ? pl->XO / MZ_TX : 0;
+        z.ntout = slab ? (pl->Ixr + MZ_TX - 1) / MZ_TX : z.ntx;
         // stencil starts of particles with |z| <= Lz/2 (one point of rounding margin each side)
         const int g_lo = std::max(pp, (int)std::floor(-0.5 * p.Lz / z.hz + 0.5 * p.Izs + 0.5) - 1);
         const int g_hi = std::min(p.Izs - 1 - pp, (int)std::floor(0.5 * p.Lz / z.hz + 0.5 * p.Izs + 0.5) + 1);
         z.c_lo = (g_lo - pp) / MZ_ZC;
         z.c_hi = (g_hi - pp) / MZ_ZC;
         z.c_hiw = std::min(z.nzc - 1, (g_hi - pp + p.P - 1) / MZ_ZC);
-        const int ntile = z.ntx * z.nty;
+        const int ntile = z.ntout * z.nty;
         auto segs = [&](int nch, int& nseg, int cap) {
             nseg = std::max(1, std::min(nch, (4 * 148 + ntile - 1) / ntile));
             int cps = std::min(cap, (nch + nseg - 1) / nseg);
@@ -249,14 +305,14 @@ int setup(sog_plan* pl) {
         };
         // spread: (chunks swept incl. warm-up) x (home tiles) must fit the CTA's range table
         auto nhome = [&](int T, int I, int nt) { return std::min(8, T + p.P - 1 >= I ? nt : (p.P - 1 + T - 1) / T + 2); };
-        const int nh = nhome(MZ_TX, p.Ix, z.ntx) * nhome(MZ_TY, p.Iy, z.nty);
+        const int nh = (slab ? (p.P - 1 + MZ_TX - 1) / MZ_TX + 1 : nhome(MZ_TX, p.Ix, z.ntx)) * nhome(MZ_TY, p.Iy, z.nty);
         const int cap_s = mid_spread_emax() / nh - (p.P - 2 + MZ_ZC) / MZ_ZC;
         if (cap_s < 1) return fail(SOG_EINVAL, "mid spread range table too small for this grid");
         const int cps_s = segs(z.c_hiw - z.c_lo + 1, pl->nseg_s, cap_s);
         const int cps_g = segs(z.c_hi - z.c_lo + 1, pl->nseg_g, 1 << 30);
         z.cps = cps_s;
         pl->mz_cps_g = cps_g;
-        pl->nkeys = ntile * z.nzc;
+        pl->nkeys = z.ntx * z.nty * z.nzc;
         if ((rc = dalloc(pl, &pl->mkey, N)) || (rc = dalloc(pl, &pl->mtmp, N)) || (rc = dalloc(pl, &pl->mpos, N)) ||
             (rc = dalloc(pl, &pl->minfo, N)) || (rc = dalloc(pl, &pl->mcount, pl->nkeys + 1)) ||
             (rc = dalloc(pl, &pl->mstart, pl->nkeys + 1)) || (rc = dalloc(pl, &pl->mcursor, pl->nkeys + 1)))
@@ -268,14 +324,38 @@ int setup(sog_plan* pl) {
         if ((rc = upload(pl, &pl->d_A, A)) || (rc = upload(pl, &pl->d_Tx, Tx)) || (rc = upload(pl, &pl->d_Ty, Ty)) ||
             (rc = upload(pl, &pl->d_Tz, Tz)))
             return rc;
-        long long n[3] = {p.Izs, p.Ix, p.Iy};   // z slowest, y fastest (half axis)
         size_t ws = 0;
-        CKF(cufftCreate(&pl->mfwd));
-        CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &ws));
-        pl->bytes += ws;
-        CKF(cufftCreate(&pl->minv));
-        CKF(cufftMakePlanMany64(pl->minv, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1, &ws));
-        pl->bytes += ws;
+        if (!slab) {
+            long long n[3] = {p.Izs, p.Ix, p.Iy};   // z slowest, y fastest (half axis)
+            CKF(cufftCreate(&pl->mfwd));
+            CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &ws));
+            pl->bytes += ws;
+            CKF(cufftCreate(&pl->minv));
+            CKF(cufftMakePlanMany64(pl->minv, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1, &ws));
+            pl->bytes += ws;
+        } else {
+            // distributed FFT: 2D (z, y) per interior x plane, all-to-all to ky chunks, 1D along x
+            long long n2[2] = {p.Izs, p.Iy};
+            long long ie[2] = {p.Izs, (long long)pl->Ixk * p.Iy}, oe[2] = {p.Izs, (long long)pl->Ixr * nyh};
+            CKF(cufftCreate(&pl->f2f));
+            CKF(cufftMakePlanMany64(pl->f2f, 2, n2, ie, 1, p.Iy, oe, 1, nyh, CUFFT_D2Z, pl->Ixr, &ws));
+            pl->bytes += ws;
+            CKF(cufftCreate(&pl->f2i));
+            CKF(cufftMakePlanMany64(pl->f2i, 2, n2, oe, 1, nyh, ie, 1, p.Iy, CUFFT_Z2D, pl->Ixr, &ws));
+            pl->bytes += ws;
+            long long n1[1] = {p.Ix};
+            CKF(cufftCreate(&pl->fxf));
+            CKF(cufftMakePlanMany64(pl->fxf, 1, n1, nullptr, 1, p.Ix, nullptr, 1, p.Ix, CUFFT_Z2Z,
+                                    (long long)p.Izs * pl->kc, &ws));
+            pl->bytes += ws;
+            const size_t nblk = pl->blk * pl->R;
+            if ((rc = dalloc(pl, &pl->spec2, (size_t)p.Izs * pl->Ixr * nyh)) ||
+                (rc = dalloc(pl, &pl->specx, (size_t)p.Izs * pl->kc * p.Ix)) || (rc = dalloc(pl, &pl->sbuf, nblk)) ||
+                (rc = dalloc(pl, &pl->rbuf, nblk)) ||
+                (rc = dalloc(pl, &pl->hsb, (size_t)2 * p.Izs * pl->HP * p.Iy)) ||
+                (rc = dalloc(pl, &pl->hrb, (size_t)2 * p.Izs * pl->HP * p.Iy)))
+                return rc;
+        }
     }
     // long range
     {
@@ -302,7 +382,7 @@ int setup(sog_plan* pl) {
         t.ntx = (p.Ilx + t.TX - 1) / t.TX;
         t.nty = (p.Ily + t.TY - 1) / t.TY;
         const int pl_half = (p.Pl - 1) / 2;
-        t.full_range = (t.TX + 2 * pl_half + 2 >= p.Ilx) ? 1 : 0;
+        t.full_range = (slab || t.TX + 2 * pl_half + 2 >= p.Ilx) ? 1 : 0;
         int ntile = t.ntx * t.nty;
         t.nchunk = std::max(1, std::min(4 * 148 / ntile + 1, int((p.N + 255) / 256)));
         if (!t.full_range) t.nchunk = std::max(1, t.nchunk * 3);
@@ -329,13 +409,24 @@ int setup(sog_plan* pl) {
     }
     pl->scan_bytes = std::max(scan_temp_bytes(pl->ncell), pl->nkeys ? scan_temp_bytes(pl->nkeys) : size_t(0));
     if ((rc = dalloc(pl, (char**)&pl->scan_tmp, pl->scan_bytes))) return rc;
+    if (slab) {   // particle halos
+        const int nown = pl->Ncap - 2 * pl->halo_cap;
+        pl->sel_bytes = select_temp_bytes(nown);
+        if ((rc = dalloc(pl, &pl->own, nown)) || (rc = dalloc(pl, &pl->hsend, 2 * pl->halo_cap)) ||
+            (rc = dalloc(pl, &pl->hrecv, 2 * pl->halo_cap)) || (rc = dalloc(pl, &pl->pos_long, N)) ||
+            (rc = dalloc(pl, &pl->fl, nown)) || (rc = dalloc(pl, &pl->fr, nown)) || (rc = dalloc(pl, &pl->nsel, 4)) ||
+            (rc = dalloc(pl, &pl->dbad, 1)) || (rc = dalloc(pl, &pl->lxyz, 3 * (size_t)N)) ||
+            (rc = dalloc(pl, &pl->lq, N)) || (rc = dalloc(pl, (char**)&pl->sel_tmp, pl->sel_bytes)))
+            return rc;
+        CK(cudaMallocHost((void**)&pl->pin_i, 8 * sizeof(int)));
+    }
     for (auto& e : pl->ev) CK(cudaEventCreate(&e));
     return SOG_OK;
 }
 
 int set_stream(sog_plan* pl, cudaStream_t s) {
     pl->stream = s;
-    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv})
+    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi})
         if (h) CKF(cufftSetStream(h, s));
     return SOG_OK;
 }
@@ -344,7 +435,7 @@ MidArgs mid_args(const sog_plan* pl) {
     const Params& p = pl->p;
     MidArgs a;
     a.pos = pl->pos_s;
-    a.N = int(p.N);
+    a.N = pl->Ncur;
     a.Ix = p.Ix; a.Iy = p.Iy; a.Izs = p.Izs;
     a.hx = p.hx(); a.hy = p.hy(); a.hz = p.hz();
     a.halfx = 0.5 * p.Ix; a.halfy = 0.5 * p.Iy; a.halfz = 0.5 * p.Izs;
@@ -359,7 +450,7 @@ LongArgs long_args(const sog_plan* pl) {
     const Params& p = pl->p;
     LongArgs a;
     a.pos = pl->pos_s;
-    a.N = int(p.N);
+    a.N = pl->Ncur;
     a.Ilx = p.Ilx; a.Ily = p.Ily; a.Pc = p.Pc; a.Pl = p.Pl;
     a.hx = p.hlx(); a.hy = p.hly();
     a.halfx = 0.5 * p.Ilx; a.halfy = 0.5 * p.Ily;
@@ -382,35 +473,36 @@ void mark(sog_plan* pl, int k) {
     if (pl->flags & SOG_TIMING) cudaEventRecord(pl->ev[k], pl->stream);
 }
 
-// Sort + all three components into o_near / o_mid / o_long (sorted order).  stop_stage > 0
-// returns early for sog_debug_stage.
-int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stage = 0) {
+// ---- pipeline stages (sorted order outputs o_near / o_mid / o_long) --------------------------
+
+// S1: validate, canonicalise, cell sort, stencil origins, mid order.  N = local particle count.
+int st_sort(sog_plan* pl, const double* xyz, const double* q, int N) {
     const Params& p = pl->p;
-    const int N = int(p.N);
     cudaStream_t st = pl->stream;
-    mark(pl, 0);
     int rc;
-    // S1
+    pl->Ncur = N;
     CK(cudaMemsetAsync(pl->count, 0, sizeof(int) * (pl->ncell + 1), st));
     CK(cudaMemsetAsync(pl->dflags, 0, sizeof(unsigned), st));
     CK(cudaMemsetAsync(pl->qsums, 0, sizeof(double) * 4, st));
-    int nb = (N + 255) / 256;
+    if (N == 0) {   // an empty slab: empty buckets everywhere
+        if (pl->has_mid) CK(cudaMemsetAsync(pl->mstart, 0, sizeof(int) * (pl->nkeys + 1), st));
+        return SOG_OK;
+    }
+    const int nb = (N + 255) / 256;
     k_prepare<<<nb, 256, 0, st>>>(xyz, q, N, pl->geo, pl->pos, pl->cell, pl->count, pl->dflags, pl->qsums);
     if ((rc = lchk(launch_exclusive_scan(pl->count, pl->start, pl->ncell, pl->scan_tmp, pl->scan_bytes, st)))) return rc;
     CK(cudaMemcpyAsync(pl->cursor, pl->start, sizeof(int) * pl->ncell, cudaMemcpyDeviceToDevice, st));
     k_scatter<<<nb, 256, 0, st>>>(pl->cell, N, pl->cursor, pl->tmp);
     k_cellsort<<<(pl->ncell * 32 + 255) / 256, 256, 0, st>>>(pl->start, pl->ncell, pl->tmp, pl->pos, pl->pos_s, pl->perm);
     {
-        const Params& pp = pl->p;
         MidArgs ma{};
         if (pl->has_mid) ma = mid_args(pl);
-        const double lhx = pp.hlx(), lhy = pp.hly();
-        if ((rc = lchk(launch_stencil_origins(pl->pos_s, N, ma, pl->has_mid ? 1 : 0, lhx, lhy, 0.5 * pp.Ilx + 0.5,
-                                              0.5 * pp.Ily + 0.5, pl->g0, st))))
+        if ((rc = lchk(launch_stencil_origins(pl->pos_s, N, ma, pl->has_mid ? 1 : 0, p.hlx(), p.hly(), 0.5 * p.Ilx + 0.5,
+                                              0.5 * p.Ily + 0.5, pl->g0, st))))
             return rc;
     }
     if (pl->has_mid) {   // mid order: bucket by (stencil-start tile, z chunk)
-        MidSortArgs ms{p.Ix, p.Iy, (p.P - 1) / 2, pl->mz.nty, pl->mz.nzc};
+        MidSortArgs ms{p.Ix, p.Iy, (p.P - 1) / 2, pl->mz.nty, pl->mz.nzc, pl->mz.px, pl->mz.xorig};
         CK(cudaMemsetAsync(pl->mcount, 0, sizeof(int) * (pl->nkeys + 1), st));
         if ((rc = lchk(launch_mid_sort_keys(pl->g0, N, ms, pl->mkey, pl->mcount, st)))) return rc;
         if ((rc = lchk(launch_exclusive_scan(pl->mcount, pl->mstart, pl->nkeys, pl->scan_tmp, pl->scan_bytes, st))))
@@ -421,39 +513,113 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
             return rc;
     }
     CK(cudaGetLastError());
-    mark(pl, 1);
-    // S2 near field
-    if (!stop_stage) {
-        const int D = pl->near.D;
-        if (D != NEAR_D) return fail(SOG_EINVAL, "near table degree");
-        if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && p.N < (1 << 27)) {   // k_near3: warp per target
-            Near3Args a;
-            a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
-            a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
-            a.g = pl->geo;
-            a.cap = 1536;
-            a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
-            size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
-                        NEAR3_WARPS * 160 * sizeof(int) + sizeof(float4) * a.cap;
-            CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-            k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
-        } else {
-            NearArgs a;
-            a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.cdF = pl->d_cdF; a.out = pl->o_near;
-            a.N = N; a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
-            a.g = pl->geo;
-            for (int i = 0; i < 3; ++i) { a.ox[i] = pl->offx[i]; a.oy[i] = pl->offy[i]; }
-            a.noffx = pl->noffx; a.noffy = pl->noffy;
-            size_t sh = 2 * sizeof(double) * pl->near.K * (D + 1);
-            CK(cudaFuncSetAttribute(k_near<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-            k_near<NEAR_D><<<(N + 255) / 256, 256, sh, st>>>(a);
-        }
-        CK(cudaGetLastError());
+    return SOG_OK;
+}
+
+// S2 near field (+ nothing else; the self term is removed in the combine)
+int st_near(sog_plan* pl) {
+    const Params& p = pl->p;
+    const int N = pl->Ncur;
+    cudaStream_t st = pl->stream;
+    if (N == 0) return SOG_OK;
+    const int D = pl->near.D;
+    if (D != NEAR_D) return fail(SOG_EINVAL, "near table degree");
+    if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && N < (1 << 27)) {   // k_near3: warp per target
+        Near3Args a;
+        a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
+        a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+        a.g = pl->geo;
+        a.cap = 1536;
+        a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+        size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
+                    NEAR3_WARPS * 160 * sizeof(int) + sizeof(float4) * a.cap;
+        CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+    } else {
+        if (!pl->geo.px) return fail(SOG_EINVAL, "x-slab needs >= 3 near cells per axis");
+        NearArgs a;
+        a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.cdF = pl->d_cdF; a.out = pl->o_near;
+        a.N = N; a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+        a.g = pl->geo;
+        for (int i = 0; i < 3; ++i) { a.ox[i] = pl->offx[i]; a.oy[i] = pl->offy[i]; }
+        a.noffx = pl->noffx; a.noffy = pl->noffy;
+        size_t sh = 2 * sizeof(double) * pl->near.K * (D + 1);
+        CK(cudaFuncSetAttribute(k_near<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_near<NEAR_D><<<(N + 255) / 256, 256, sh, st>>>(a);
     }
+    CK(cudaGetLastError());
+    return SOG_OK;
+}
+
+int st_mid_spread(sog_plan* pl) {
+    return lchk(launch_mid_spread_z(pl->mz, pl->p.P, pl->nseg_s, pl->mgrid, pl->stream));
+}
+
+int st_mid_gather(sog_plan* pl) {
+    MidZArgs g = pl->mz;
+    g.cps = pl->mz_cps_g;
+    if (pl->R > 1) { g.tlo -= 1; g.ntout += 1; }   // own particles near the left edge start in the halo tile
+    return lchk(launch_mid_gather_z(g, pl->p.P, pl->nseg_g, pl->Ncur, pl->mpsi, pl->o_mid, pl->stream));
+}
+
+// S8 (own particles only in an x-slab: the halo particles belong to the neighbours)
+int st_long_spread(sog_plan* pl) {
+    const Params& p = pl->p;
+    cudaStream_t st = pl->stream;
+    int rc;
+    LongArgs la = long_args(pl);
+    if (pl->R > 1) {
+        k_own_mask<<<(pl->Ncur + 255) / 256, 256, 0, st>>>(pl->pos_s, pl->perm, pl->Ncur, pl->Nown, pl->pos_long);
+        la.pos = pl->pos_long;
+    }
+    if (pl->long_small) {
+        if ((rc = lchk(launch_long_spread_gemm(la, pl->g0, pl->lt.gamma_x, pl->lt.gamma_y, pl->lg_nblk, pl->lpart2,
+                                               pl->lgrid, st))))
+            return rc;
+    } else {
+        LongTileArgs t = pl->lt;
+        t.a = la;
+        t.start = pl->start;
+        t.part = pl->lpart;
+        if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
+    }
+    return SOG_OK;
+}
+
+// S9-S11
+int st_long_solve(sog_plan* pl) {
+    const Params& p = pl->p;
+    cudaStream_t st = pl->stream;
+    CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
+    int nmode = p.Ilx * (p.Ily / 2 + 1);
+    k_long_scale<<<(nmode * p.Pc + 127) / 128, 128, 0, st>>>(pl->lspec, pl->lspec2, pl->d_K, nmode, p.Pc);
+    CK(cudaGetLastError());
+    CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
+    return SOG_OK;
+}
+
+// S12
+int st_long_gather(sog_plan* pl) {
+    const Params& p = pl->p;
+    if (pl->long_small) return lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, pl->stream));
+    return lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long, pl->lt.gamma_x,
+                                    pl->lt.gamma_y, pl->stream));
+}
+
+// Whole-box pipeline: sort + all three components (sorted order).  stop_stage > 0 returns
+// early for sog_debug_stage.
+int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stage = 0) {
+    const Params& p = pl->p;
+    cudaStream_t st = pl->stream;
+    mark(pl, 0);
+    int rc;
+    if ((rc = st_sort(pl, xyz, q, int(p.N)))) return rc;
+    mark(pl, 1);
+    if (!stop_stage && (rc = st_near(pl))) return rc;
     mark(pl, 2);
     // S3-S7 mid range
     if (pl->has_mid && (stop_stage == 0 || stop_stage == 1 || stop_stage == 2)) {
-        if ((rc = lchk(launch_mid_spread_z(pl->mz, p.P, pl->nseg_s, pl->mgrid, st)))) return rc;
+        if ((rc = st_mid_spread(pl))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
         CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
@@ -465,43 +631,20 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mpsi));
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
-        {
-            MidZArgs g = pl->mz;
-            g.cps = pl->mz_cps_g;
-            if ((rc = lchk(launch_mid_gather_z(g, p.P, pl->nseg_g, N, pl->mpsi, pl->o_mid, st)))) return rc;
-        }
+        if ((rc = st_mid_gather(pl))) return rc;
     } else if (!pl->has_mid && !stop_stage) {
-        CK(cudaMemsetAsync(pl->o_mid, 0, sizeof(d4) * N, st));
+        CK(cudaMemsetAsync(pl->o_mid, 0, sizeof(d4) * pl->Ncur, st));
     }
     mark(pl, 7);
     // S8-S12 long range
     if (stop_stage == 0 || stop_stage == 3 || stop_stage == 4) {
-        if (pl->long_small) {
-            if ((rc = lchk(launch_long_spread_gemm(long_args(pl), pl->g0, pl->lt.gamma_x, pl->lt.gamma_y, pl->lg_nblk,
-                                                   pl->lpart2, pl->lgrid, st))))
-                return rc;
-        } else {
-            LongTileArgs t = pl->lt;
-            t.a = long_args(pl);
-            t.start = pl->start;
-            t.part = pl->lpart;
-            if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
-        }
+        if ((rc = st_long_spread(pl))) return rc;
         mark(pl, 8);
         if (stop_stage == 3) return SOG_OK;
-        CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
-        int nmode = p.Ilx * (p.Ily / 2 + 1);
-        k_long_scale<<<(nmode * p.Pc + 127) / 128, 128, 0, st>>>(pl->lspec, pl->lspec2, pl->d_K, nmode, p.Pc);
-        CK(cudaGetLastError());
-        CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
+        if ((rc = st_long_solve(pl))) return rc;
         mark(pl, 9);
         if (stop_stage == 4) return SOG_OK;
-        if (pl->long_small) {
-            if ((rc = lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, st)))) return rc;
-        } else if ((rc = lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long,
-                                                  pl->lt.gamma_x, pl->lt.gamma_y, st)))) {
-            return rc;
-        }
+        if ((rc = st_long_gather(pl))) return rc;
     }
     mark(pl, 10);
     return SOG_OK;
@@ -609,7 +752,7 @@ int sog_eval(sog_plan* pl, const double* xyz, const double* q, double* phi, doub
     int rc = run_pipeline(pl, xyz, q);
     if (rc) return rc;
     const int N = int(pl->p.N);
-    k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N,
+    k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N, N,
                                                        pl->selfc, phi, force, pl->qsums + 2);
     CK(cudaGetLastError());
     mark(pl, 11);
@@ -723,6 +866,435 @@ int sog_launches_per_eval(const sog_plan* pl) {
     // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
     // [transpose,] gather, combine  (cuFFT launches are not counted)
     return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->long_small ? 4 : 5) + 1;
+}
+
+}  // extern "C"
+
+// =========================================================================================
+// x-slab distributed evaluation.  One sog_plan per rank in slab mode; the
+// exchange steps are expressed as per-rank send/receive lists and executed either by NCCL
+// (one process per GPU) or by a loopback backend (R virtual ranks of one process on one
+// device, device-to-device copies): the same decomposition runs in both.
+// =========================================================================================
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is resolved at run time (the process's already-loaded libnccl.so.2, e.g. torch's),
+// so libsog.so loads and runs single-GPU without it.
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    auto sym = [&](auto& fp, const char* name) { fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name)); return fp != nullptr; };
+    api.ok = sym(api.GetUniqueId, "ncclGetUniqueId") && sym(api.CommInitRank, "ncclCommInitRank") &&
+             sym(api.CommDestroy, "ncclCommDestroy") && sym(api.GroupStart, "ncclGroupStart") &&
+             sym(api.GroupEnd, "ncclGroupEnd") && sym(api.Send, "ncclSend") && sym(api.Recv, "ncclRecv") &&
+             sym(api.AllReduce, "ncclAllReduce") && sym(api.GetErrorString, "ncclGetErrorString");
+    return api;
+}
+
+struct Msg {
+    int peer;
+    void* ptr;
+    size_t bytes;
+};
+struct Exch {
+    std::vector<Msg> send, recv;
+};
+
+bool smooth7l(long n) {
+    for (long f : {2L, 3L, 5L, 7L})
+        while (n % f == 0) n /= f;
+    return n == 1;
+}
+
+}  // namespace
+
+struct sog_dist {
+    int R = 1;
+    bool loopback = false;
+    std::vector<sog_plan*> pl;           // loopback: all R ranks; NCCL: this process's rank
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+#define NCK(x)                                                                                     \
+    do {                                                                                           \
+        ncclResult_t r_ = (x);                                                                     \
+        if (r_ != ncclSuccess) return fail(SOG_ENCCL, std::string(#x ": ") + nccl().GetErrorString(r_)); \
+    } while (0)
+
+// execute one exchange step: ex[i] belongs to local plan i
+int run_exchange(sog_dist* d, std::vector<Exch>& ex) {
+    if (d->loopback) {
+        for (int r = 0; r < d->R; ++r) {
+            std::vector<int> used(d->R, 0);
+            for (const Msg& m : ex[r].send) {
+                // the k-th message r -> m.peer matches the k-th receive posted at m.peer from r
+                int k = used[m.peer]++, seen = 0;
+                const Msg* dst = nullptr;
+                for (const Msg& rv : ex[m.peer].recv)
+                    if (rv.peer == r && seen++ == k) { dst = &rv; break; }
+                if (!dst || dst->bytes < m.bytes) return fail(SOG_EINVAL, "loopback exchange: unmatched message");
+                if (m.bytes) CK(cudaMemcpyAsync(dst->ptr, m.ptr, m.bytes, cudaMemcpyDeviceToDevice, d->stream));
+            }
+        }
+        return SOG_OK;
+    }
+    NcclApi& api = nccl();
+    NCK(api.GroupStart());
+    for (const Msg& m : ex[0].send)
+        if (m.bytes) NCK(api.Send(m.ptr, m.bytes, ncclUint8, m.peer, d->comm, d->stream));
+    for (const Msg& m : ex[0].recv)
+        if (m.bytes) NCK(api.Recv(m.ptr, m.bytes, ncclUint8, m.peer, d->comm, d->stream));
+    NCK(api.GroupEnd());
+    return SOG_OK;
+}
+
+__global__ void k_sum_into(double* __restrict__ a, const double* __restrict__ b, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] += b[i];
+}
+
+// sum of the long-range proxy grids over ranks (S8 is linear in the charges)
+int run_allreduce(sog_dist* d, size_t n) {
+    if (d->loopback) {
+        double* a = d->pl[0]->lgrid;
+        for (int r = 1; r < d->R; ++r)
+            k_sum_into<<<(unsigned)((n + 255) / 256), 256, 0, d->stream>>>(a, d->pl[r]->lgrid, n);
+        for (int r = 1; r < d->R; ++r)
+            CK(cudaMemcpyAsync(d->pl[r]->lgrid, a, n * sizeof(double), cudaMemcpyDeviceToDevice, d->stream));
+        CK(cudaGetLastError());
+        return SOG_OK;
+    }
+    NCK(nccl().AllReduce(d->pl[0]->lgrid, d->pl[0]->lgrid, n, ncclFloat64, ncclSum, d->comm, d->stream));
+    return SOG_OK;
+}
+
+// SOG_DEBUG_SYNC=1: synchronise after every x-slab step and report the first failing one
+int dbg_sync(sog_dist* d, const char* what) {
+    static const bool on = std::getenv("SOG_DEBUG_SYNC") != nullptr;
+    if (!on) return SOG_OK;
+    cudaError_t e = cudaStreamSynchronize(d->stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SOG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return SOG_OK;
+}
+
+int kyc_of(const sog_plan* pl, int s) {
+    const int nyh = pl->p.Iy / 2 + 1;
+    return std::max(0, std::min(pl->kc, nyh - s * pl->kc));
+}
+
+int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const double* const* q, double* const* phi,
+              double* const* force) {
+    const int L = int(d->pl.size());
+    const int R = d->R;
+    std::vector<Exch> ex(L);
+    int rc;
+    auto left = [&](int r) { return (r + R - 1) % R; };
+    auto right = [&](int r) { return (r + 1) % R; };
+    // ---- particle halos: select, exchange counts, exchange particles ----
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        const Params& p = pl->p;
+        const int n = int(nown[i]);
+        if (n < 0 || n > pl->Ncap - 2 * pl->halo_cap) return fail(SOG_EINVAL, "own particle count exceeds the plan capacity");
+        pl->Nown = n;
+        cudaStream_t st = pl->stream;
+        CK(cudaMemsetAsync(pl->dbad, 0, sizeof(unsigned), st));
+        CK(cudaMemsetAsync(pl->nsel, 0, 4 * sizeof(int), st));
+        if (n > 0) {
+            k_slab_flags<<<(n + 255) / 256, 256, 0, st>>>(xyz[i], q[i], n, p.Lx, pl->xs0, pl->xs1, pl->Hh, pl->own, pl->fl,
+                                                         pl->fr, pl->dbad);
+            if ((rc = lchk(launch_select_flagged(pl->own, pl->fl, pl->hsend, pl->nsel, n, pl->sel_tmp, pl->sel_bytes, st))) ||
+                (rc = lchk(launch_select_flagged(pl->own, pl->fr, pl->hsend + pl->halo_cap, pl->nsel + 1, n, pl->sel_tmp,
+                                                 pl->sel_bytes, st))))
+                return rc;
+            // across the periodic seam the halo copies carry the image shift of the receiver's frame
+            if (pl->rank == 0)
+                k_shift_x<<<(pl->halo_cap + 255) / 256, 256, 0, st>>>(pl->hsend, pl->nsel, p.Lx);
+            if (pl->rank == R - 1)
+                k_shift_x<<<(pl->halo_cap + 255) / 256, 256, 0, st>>>(pl->hsend + pl->halo_cap, pl->nsel + 1, -p.Lx);
+        }
+        CK(cudaGetLastError());
+        const int r = pl->rank;
+        ex[i].send = {{left(r), pl->nsel, sizeof(int)}, {right(r), pl->nsel + 1, sizeof(int)}};
+        ex[i].recv = {{right(r), pl->nsel + 2, sizeof(int)}, {left(r), pl->nsel + 3, sizeof(int)}};
+    }
+    if ((rc = run_exchange(d, ex))) return rc;
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        CK(cudaMemcpyAsync(pl->pin_i, pl->nsel, 4 * sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+        CK(cudaMemcpyAsync(pl->pin_i + 4, pl->dbad, sizeof(unsigned), cudaMemcpyDeviceToHost, pl->stream));
+    }
+    CK(cudaStreamSynchronize(d->stream));
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        const int* c = pl->pin_i;
+        if (c[4]) return fail(SOG_EINVAL, "own particle outside the rank's x slab");
+        for (int k = 0; k < 4; ++k)
+            if (c[k] > pl->halo_cap) return fail(SOG_EINVAL, "x-slab halo exceeds its capacity (clustered input)");
+        const int r = pl->rank;
+        ex[i].send = {{left(r), pl->hsend, sizeof(d4) * c[0]}, {right(r), pl->hsend + pl->halo_cap, sizeof(d4) * c[1]}};
+        ex[i].recv = {{right(r), pl->hrecv + pl->halo_cap, sizeof(d4) * c[2]}, {left(r), pl->hrecv, sizeof(d4) * c[3]}};
+    }
+    if ((rc = run_exchange(d, ex))) return rc;
+    // ---- local particles: near field, mid spread, 2D FFTs, pack for the all-to-all ----
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        const Params& p = pl->p;
+        cudaStream_t st = pl->stream;
+        const int nl = pl->pin_i[3], nr = pl->pin_i[2], nloc = pl->Nown + nl + nr;
+        if (nloc > 0)
+            k_slab_local<<<(nloc + 255) / 256, 256, 0, st>>>(pl->own, pl->Nown, pl->hrecv, nl, pl->hrecv + pl->halo_cap, nr,
+                                                            pl->lxyz, pl->lq);
+        if ((rc = st_sort(pl, pl->lxyz, pl->lq, nloc)) || (rc = dbg_sync(d, "slab sort")) || (rc = st_near(pl)) ||
+            (rc = dbg_sync(d, "slab near")))
+            return rc;
+        if (!pl->has_mid) continue;
+        if ((rc = st_mid_spread(pl)) || (rc = dbg_sync(d, "slab spread"))) return rc;
+        CKF(cufftExecD2Z(pl->f2f, pl->mgrid + (size_t)pl->XO * p.Iy, pl->spec2));
+        if ((rc = dbg_sync(d, "2D FFT"))) return rc;
+        const size_t tot = (size_t)p.Izs * pl->Ixr * (p.Iy / 2 + 1);
+        k_pack_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->spec2, pl->sbuf, p.Izs, pl->Ixr, p.Iy / 2 + 1, pl->kc,
+                                                                  R, pl->blk);
+        CK(cudaGetLastError());
+        ex[i].send.clear();
+        ex[i].recv.clear();
+        const int r = pl->rank;
+        for (int s = 0; s < R; ++s) {
+            ex[i].send.push_back({s, pl->sbuf + s * pl->blk, sizeof(cuDoubleComplex) * p.Izs * pl->Ixr * kyc_of(pl, s)});
+            ex[i].recv.push_back({s, pl->rbuf + s * pl->blk, sizeof(cuDoubleComplex) * p.Izs * pl->Ixr * kyc_of(pl, r)});
+        }
+    }
+    const bool has_mid = d->pl[0]->has_mid;
+    if (has_mid) {
+        if ((rc = run_exchange(d, ex))) return rc;
+        // ---- x pencils: 1D FFT along x, S5 scaling, inverse, pack back ----
+        for (int i = 0; i < L; ++i) {
+            sog_plan* pl = d->pl[i];
+            const Params& p = pl->p;
+            cudaStream_t st = pl->stream;
+            const int r = pl->rank, kyc = kyc_of(pl, r);
+            const size_t tot = (size_t)p.Izs * kyc * p.Ix;
+            if (tot) {
+                k_unpack_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->rbuf, pl->specx, p.Izs, pl->Ixr, p.Ix, kyc,
+                                                                            pl->blk);
+                if ((rc = dbg_sync(d, "unpack fwd"))) return rc;
+                CKF(cufftExecZ2Z(pl->fxf, pl->specx, pl->specx, CUFFT_FORWARD));
+                k_scale_pencil<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->specx, p.Izs, kyc, p.Ix, r * pl->kc,
+                                                                              p.Iy / 2 + 1, p.m + 1, pl->d_A, pl->d_Tx,
+                                                                              pl->d_Ty, pl->d_Tz);
+                CKF(cufftExecZ2Z(pl->fxf, pl->specx, pl->specx, CUFFT_INVERSE));
+                k_pack_bwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->specx, pl->sbuf, p.Izs, pl->Ixr, p.Ix, kyc,
+                                                                          pl->blk);
+                CK(cudaGetLastError());
+            }
+            ex[i].send.clear();
+            ex[i].recv.clear();
+            for (int s = 0; s < R; ++s) {
+                ex[i].send.push_back({s, pl->sbuf + s * pl->blk, sizeof(cuDoubleComplex) * p.Izs * pl->Ixr * kyc});
+                ex[i].recv.push_back({s, pl->rbuf + s * pl->blk, sizeof(cuDoubleComplex) * p.Izs * pl->Ixr * kyc_of(pl, s)});
+            }
+        }
+        if ((rc = run_exchange(d, ex))) return rc;
+        // ---- inverse 2D FFTs into the interior planes of Psi; edge planes for the neighbours ----
+        for (int i = 0; i < L; ++i) {
+            sog_plan* pl = d->pl[i];
+            const Params& p = pl->p;
+            cudaStream_t st = pl->stream;
+            const size_t tot = (size_t)p.Izs * pl->Ixr * (p.Iy / 2 + 1);
+            k_unpack_bwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->rbuf, pl->spec2, p.Izs, pl->Ixr, p.Iy / 2 + 1,
+                                                                        pl->kc, R, pl->blk);
+            CKF(cufftExecZ2D(pl->f2i, pl->spec2, pl->mpsi + (size_t)pl->XO * p.Iy));
+            if ((rc = dbg_sync(d, "inverse 2D FFT"))) return rc;
+            const size_t hp = (size_t)p.Izs * pl->HP * p.Iy;
+            k_planes_pack<<<(unsigned)((hp + 255) / 256), 256, 0, st>>>(pl->mpsi, pl->hsb, p.Izs, pl->Ixk, p.Iy, pl->XO,
+                                                                        pl->HP);
+            k_planes_pack<<<(unsigned)((hp + 255) / 256), 256, 0, st>>>(pl->mpsi, pl->hsb + hp, p.Izs, pl->Ixk, p.Iy,
+                                                                        pl->XO + pl->Ixr - pl->HP, pl->HP);
+            CK(cudaGetLastError());
+            const int r = pl->rank;
+            ex[i].send = {{left(r), pl->hsb, sizeof(double) * hp}, {right(r), pl->hsb + hp, sizeof(double) * hp}};
+            ex[i].recv = {{right(r), pl->hrb + hp, sizeof(double) * hp}, {left(r), pl->hrb, sizeof(double) * hp}};
+        }
+        if ((rc = run_exchange(d, ex))) return rc;
+    }
+    // ---- halo planes in, mid gather, long spread of the own particles ----
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        const Params& p = pl->p;
+        cudaStream_t st = pl->stream;
+        if (pl->has_mid) {
+            const size_t hp = (size_t)p.Izs * pl->HP * p.Iy;
+            k_planes_unpack<<<(unsigned)((hp + 255) / 256), 256, 0, st>>>(pl->hrb, pl->mpsi, p.Izs, pl->Ixk, p.Iy,
+                                                                          pl->XO - pl->HP, pl->HP);
+            k_planes_unpack<<<(unsigned)((hp + 255) / 256), 256, 0, st>>>(pl->hrb + hp, pl->mpsi, p.Izs, pl->Ixk, p.Iy,
+                                                                          pl->XO + pl->Ixr, pl->HP);
+            CK(cudaGetLastError());
+            if ((rc = dbg_sync(d, "psi halo"))) return rc;
+            if (pl->Ncur && ((rc = st_mid_gather(pl)) || (rc = dbg_sync(d, "slab gather")))) return rc;
+        } else if (pl->Ncur) {
+            CK(cudaMemsetAsync(pl->o_mid, 0, sizeof(d4) * pl->Ncur, st));
+        }
+        if (pl->Ncur) {
+            if ((rc = st_long_spread(pl))) return rc;
+        } else {
+            CK(cudaMemsetAsync(pl->lgrid, 0, sizeof(double) * p.Pc * p.Ilx * p.Ily, st));
+        }
+    }
+    {
+        const Params& p = d->pl[0]->p;
+        if ((rc = dbg_sync(d, "long spread")) || (rc = run_allreduce(d, (size_t)p.Pc * p.Ilx * p.Ily)) ||
+            (rc = dbg_sync(d, "long allreduce")))
+            return rc;
+    }
+    // ---- long solve (redundant per rank: small grid), long gather, combine ----
+    for (int i = 0; i < L; ++i) {
+        sog_plan* pl = d->pl[i];
+        if ((rc = st_long_solve(pl))) return rc;
+        if (!pl->Ncur) continue;
+        if ((rc = st_long_gather(pl))) return rc;
+        const int N = pl->Ncur;
+        CK(cudaMemsetAsync(pl->qsums + 2, 0, sizeof(double), pl->stream));
+        k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N,
+                                                           pl->Nown, pl->selfc, phi[i], force[i], pl->qsums + 2);
+        CK(cudaGetLastError());
+    }
+    return SOG_OK;
+}
+
+// plan of one x-slab rank (slab geometry, capacities); p holds the global parameters
+int dist_plan_setup(sog_plan* pl, int rank, int R, int64_t nown_max) {
+    const Params& p = pl->p;
+    pl->R = R;
+    pl->rank = rank;
+    pl->xs0 = -0.5 * p.Lx + p.Lx * rank / R;
+    pl->xs1 = (rank == R - 1) ? 0.5 * p.Lx : -0.5 * p.Lx + p.Lx * (rank + 1) / R;
+    const double hx = p.Lx / p.Ix;
+    pl->Hh = std::max(p.rc, ((p.P - 1) / 2 + 1.5) * hx) * (1.0 + 1e-9);
+    if (p.Lx / R < pl->Hh) return fail(SOG_EINVAL, "x slab narrower than the halo (r_c / window): use fewer ranks");
+    if (p.Ix % R) return fail(SOG_EINVAL, "mid grid Ix must be a multiple of the rank count");
+    if (p.Iy / 2 + 1 < R) return fail(SOG_EINVAL, "mid grid too small for the pencil transpose");
+    const double frac = pl->Hh / (p.Lx / R);
+    pl->halo_cap = int(std::min<double>(double(nown_max), std::ceil(double(nown_max) * frac * 1.5 + 1024.0)));
+    pl->Ncap = int(nown_max + 2 * int64_t(pl->halo_cap));
+    return setup(pl);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sog_nccl_unique_id(void* id128) {
+    if (!id128) return fail(SOG_EINVAL, "null argument");
+    if (!nccl().ok) return fail(SOG_ENCCL, "libnccl.so.2 not available");
+    ncclUniqueId id;
+    NCK(nccl().GetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+    return SOG_OK;
+}
+
+static sog_dist* dist_create(int64_t N_total, int64_t nown_max, double Lx, double Ly, double Lz, double tol,
+                             const sog_plan_opts* o, int R, int first, int count, bool loopback, const void* id128) {
+    if (R < 2 || nown_max < 1) { fail(SOG_EINVAL, "x-slab needs >= 2 ranks and a positive capacity"); return nullptr; }
+    sog_dist* d = new sog_dist();
+    d->R = R;
+    d->loopback = loopback;
+    d->stream = o ? (cudaStream_t)o->cuda_stream : nullptr;
+    Params p;
+    RuleKnobs k;
+    if (make_params(p, k, N_total, Lx, Ly, Lz, tol, o) != SOG_OK) { delete d; return nullptr; }
+    if (!(o && o->explicit_params) && p.m >= 0) {   // Ix a multiple of R (even, FFT friendly)
+        long n = p.Ix;
+        while (n % R || (n & 1) || !smooth7l(n)) ++n;
+        p.Ix = int(n);
+    }
+    for (int r = first; r < first + count; ++r) {
+        sog_plan* pl = new sog_plan();
+        pl->p = p;
+        pl->knobs = k;
+        if (o) pl->flags = o->flags;
+        d->pl.push_back(pl);
+        int rc = dist_plan_setup(pl, r, R, nown_max);
+        if (rc == SOG_OK) rc = set_stream(pl, d->stream);
+        if (rc != SOG_OK) { std::string keep = g_err; sog_dist_destroy(d); g_err = keep; return nullptr; }
+    }
+    if (!loopback) {
+        if (!nccl().ok) { fail(SOG_ENCCL, "libnccl.so.2 not available"); sog_dist_destroy(d); return nullptr; }
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        ncclResult_t r = nccl().CommInitRank(&d->comm, R, id, first);
+        if (r != ncclSuccess) {
+            fail(SOG_ENCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+            sog_dist_destroy(d);
+            return nullptr;
+        }
+    }
+    return d;
+}
+
+sog_dist* sog_dist_create(int64_t N_total, int64_t nown_max, double Lx, double Ly, double Lz, double tol,
+                          const sog_plan_opts* opts, int rank, int nranks, const void* nccl_id) {
+    if (!nccl_id || rank < 0 || rank >= nranks) { fail(SOG_EINVAL, "bad rank / NCCL id"); return nullptr; }
+    return dist_create(N_total, nown_max, Lx, Ly, Lz, tol, opts, nranks, rank, 1, false, nccl_id);
+}
+
+sog_dist* sog_dist_create_loopback(int64_t N_total, int64_t nown_max, double Lx, double Ly, double Lz, double tol,
+                                   const sog_plan_opts* opts, int nranks) {
+    return dist_create(N_total, nown_max, Lx, Ly, Lz, tol, opts, nranks, 0, nranks, true, nullptr);
+}
+
+int sog_dist_eval(sog_dist* d, const int64_t* n_own, const double* const* xyz, const double* const* q,
+                  double* const* phi, double* const* force) {
+    if (!d || !n_own || !xyz || !q || !phi || !force) return fail(SOG_EINVAL, "null argument");
+    return dist_eval(d, n_own, xyz, q, phi, force);
+}
+
+int sog_dist_local_ranks(const sog_dist* d) { return d ? int(d->pl.size()) : fail(SOG_EINVAL, "null"); }
+
+int sog_dist_describe(const sog_dist* d, char* buf, size_t len) {
+    if (!d || d->pl.empty()) return fail(SOG_EINVAL, "null");
+    const sog_plan* pl = d->pl[0];
+    std::string s = describe(pl->p);
+    char extra[512];
+    std::snprintf(extra, sizeof extra, "ranks=%d\nslab_planes=%d\nhalo=%.17g\nhalo_capacity=%d\nlocal_capacity=%d\n",
+                  d->R, pl->Ixr, pl->Hh, pl->halo_cap, pl->Ncap);
+    s += extra;
+    if (buf && len) {
+        size_t n = std::min(len - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return int(s.size());
+}
+
+void sog_dist_destroy(sog_dist* d) {
+    if (!d) return;
+    if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+    for (sog_plan* pl : d->pl) free_plan(pl);
+    delete d;
 }
 
 }  // extern "C"

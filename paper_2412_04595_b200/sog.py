@@ -10,12 +10,14 @@ _LIB = None
 SOG_NO_VALIDATE = 1
 SOG_TIMING = 2
 STATUS = {0: "SOG_OK", -1: "SOG_EINVAL", -2: "SOG_ENONNEUTRAL", -3: "SOG_EZRANGE",
-          -4: "SOG_ENONFINITE", -5: "SOG_EINFEASIBLE", -6: "SOG_ECUDA", -8: "SOG_ENOMEM"}
+          -4: "SOG_ENONFINITE", -5: "SOG_EINFEASIBLE", -6: "SOG_ECUDA", -7: "SOG_ENCCL", -8: "SOG_ENOMEM"}
 TIMING_NAMES = ["sort", "near", "mid_spread", "mid_fft_fwd", "mid_scale", "mid_fft_inv", "mid_gather",
                 "long_spread", "long_fft_scale_ifft", "long_gather", "combine"]
 EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval", "sog_eval_host", "sog_eval_components",
            "sog_debug_stage", "sog_last_energy", "sog_plan_destroy", "sog_last_error", "sog_plan_describe",
-           "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval"]
+           "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval",
+           "sog_nccl_unique_id", "sog_dist_create", "sog_dist_create_loopback", "sog_dist_eval",
+           "sog_dist_local_ranks", "sog_dist_describe", "sog_dist_destroy"]
 
 
 class SogError(RuntimeError):
@@ -77,6 +79,21 @@ def load_library():
     lib.sog_set_stream.argtypes = [P, P]
     lib.sog_launches_per_eval.restype = I
     lib.sog_launches_per_eval.argtypes = [P]
+    I64 = ctypes.c_int64
+    lib.sog_nccl_unique_id.restype = I
+    lib.sog_nccl_unique_id.argtypes = [P]
+    lib.sog_dist_create.restype = P
+    lib.sog_dist_create.argtypes = [I64, I64, D, D, D, D, ctypes.POINTER(Opts), I, I, P]
+    lib.sog_dist_create_loopback.restype = P
+    lib.sog_dist_create_loopback.argtypes = [I64, I64, D, D, D, D, ctypes.POINTER(Opts), I]
+    lib.sog_dist_eval.restype = I
+    lib.sog_dist_eval.argtypes = [P, P, P, P, P, P]
+    lib.sog_dist_local_ranks.restype = I
+    lib.sog_dist_local_ranks.argtypes = [P]
+    lib.sog_dist_describe.restype = I
+    lib.sog_dist_describe.argtypes = [P, ctypes.c_char_p, S]
+    lib.sog_dist_destroy.restype = None
+    lib.sog_dist_destroy.argtypes = [P]
     _LIB = lib
     return lib
 
@@ -266,3 +283,129 @@ def _host_ptr(a):
     if a.is_cuda or not a.is_contiguous():
         raise ValueError("host tensors must be contiguous CPU tensors")
     return a.data_ptr()
+
+
+def slab_owner(x, Lx, R):
+    """Rank owning canonical x under the x-slab rule of include/sog.h (host-side helper, numpy)."""
+    import numpy as np
+    x = np.asarray(x, dtype=np.float64)
+    xc = x - Lx * np.floor((x + 0.5 * Lx) / Lx)
+    xc = np.where(xc >= 0.5 * Lx, xc - Lx, xc)
+    r = np.floor((xc + 0.5 * Lx) * R / Lx).astype(np.int64)
+    # the library's slab edges are -Lx/2 + r Lx / R evaluated in fp64: settle ties exactly
+    lo = -0.5 * Lx + Lx * r / R
+    r = np.where(xc < lo, r - 1, r)
+    hi = np.where(r + 1 == R, 0.5 * Lx, -0.5 * Lx + Lx * (r + 1) / R)
+    r = np.where(xc >= hi, r + 1, r)
+    return np.clip(r, 0, R - 1)
+
+
+class DistPlan:
+    """x-slab decomposition over R ranks (include/sog.h).
+
+    loopback=True: all R ranks as virtual ranks of this process on the current GPU;
+    eval() then takes lists of per-rank tensors.  loopback=False: one rank per process over
+    NCCL; pass rank, nranks and the 128-byte NCCL id (see nccl_unique_id / from_process_group).
+    """
+
+    def __init__(self, N_total, n_own_max, L, tol, R, rank=0, nccl_id=None, loopback=False, params=None,
+                 stream=None):
+        self.lib = load_library()
+        self.L = tuple(float(v) for v in L)
+        self.R = int(R)
+        o = Opts()
+        if params is not None:
+            o.explicit_params = 1
+            for k in PLAN_FIELDS:
+                setattr(o, k, type(getattr(o, k))(params[k]))
+        o.flags = SOG_NO_VALIDATE
+        o.cuda_stream = _stream_handle(stream)
+        if loopback:
+            h = self.lib.sog_dist_create_loopback(int(N_total), int(n_own_max), *self.L, float(tol), ctypes.byref(o),
+                                                  self.R)
+        else:
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            h = self.lib.sog_dist_create(int(N_total), int(n_own_max), *self.L, float(tol), ctypes.byref(o),
+                                         int(rank), self.R, buf)
+        if not h:
+            raise SogError(-1, self.lib.sog_last_error().decode())
+        self.h = h
+        self.nlocal = self.lib.sog_dist_local_ranks(h)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = load_library()
+        buf = ctypes.create_string_buffer(128)
+        rc = lib.sog_nccl_unique_id(buf)
+        if rc:
+            raise _err(lib, rc)
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, N_total, n_own_max, L, tol, **kw):
+        """One rank per process: the NCCL id is created on rank 0 and broadcast with torch.distributed."""
+        import torch.distributed as dist
+        rank, R = dist.get_rank(), dist.get_world_size()
+        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(N_total, n_own_max, L, tol, R, rank=rank, nccl_id=obj[0], **kw)
+
+    def describe(self) -> dict:
+        n = self.lib.sog_dist_describe(self.h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        self.lib.sog_dist_describe(self.h, buf, n + 1)
+        return _parse(buf.value.decode())
+
+    def eval(self, xyz, q, phi=None, force=None):
+        """xyz, q: (lists of, for loopback) CUDA float64 tensors of this rank's own particles."""
+        import torch
+        single = not isinstance(xyz, (list, tuple))
+        xs, qs = ([xyz], [q]) if single else (list(xyz), list(q))
+        if len(xs) != self.nlocal:
+            raise ValueError(f"expected {self.nlocal} per-rank inputs")
+        xs = [x.contiguous() for x in xs]
+        qs = [v.contiguous() for v in qs]
+        phis = [torch.empty(len(v), dtype=torch.float64, device=v.device) for v in qs] if phi is None else (
+            [phi] if single else list(phi))
+        fs = [torch.empty(len(v), 3, dtype=torch.float64, device=v.device) for v in qs] if force is None else (
+            [force] if single else list(force))
+        n = (ctypes.c_int64 * self.nlocal)(*[len(v) for v in qs])
+        P = ctypes.c_void_p * self.nlocal
+        rc = self.lib.sog_dist_eval(self.h, n, P(*[x.data_ptr() for x in xs]), P(*[v.data_ptr() for v in qs]),
+                                    P(*[v.data_ptr() for v in phis]), P(*[v.data_ptr() for v in fs]))
+        if rc:
+            raise _err(self.lib, rc)
+        return (phis[0], fs[0]) if single else (phis, fs)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sog_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def redistribute(xyz, q, L, group=None):
+    """Move every particle to the rank owning its x slab (torch.distributed, any backend):
+    returns this rank's (xyz, q, origin) where origin = (source rank, source index) per
+    particle, so results can be sent back.  Host-side marshalling for sog_dist_eval."""
+    import torch
+    import torch.distributed as dist
+    R, me = dist.get_world_size(group), dist.get_rank(group)
+    dev = xyz.device
+    owner = torch.from_numpy(slab_owner(xyz[:, 0].detach().cpu().numpy(), float(L[0]), R)).to(dev)
+    order = torch.argsort(owner, stable=True)
+    counts = torch.bincount(owner, minlength=R)
+    rcounts = torch.empty_like(counts)
+    dist.all_to_all_single(rcounts, counts, group=group)
+    sc, rc = counts.tolist(), rcounts.tolist()
+    idx = torch.arange(len(q), device=dev, dtype=torch.float64)
+    rank_col = torch.full((len(q),), float(me), device=dev, dtype=torch.float64)
+    send = torch.cat([xyz, q[:, None], rank_col[:, None], idx[:, None]], dim=1)[order].contiguous()
+    recv = torch.empty(sum(rc), 6, dtype=torch.float64, device=dev)
+    dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    return recv[:, :3].contiguous(), recv[:, 3].contiguous(), recv[:, 4:].to(torch.int64)

@@ -1,0 +1,102 @@
+"""x-slab decomposition on one GPU: R virtual ranks in one process (loopback
+exchange backend), same kernels and exchange steps as the NCCL path.  The assembled result
+must equal the single-GPU evaluation (same plan) to rounding and the oracle within 1e-12."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import sog as O
+from oracle.plan import TABLE1, make_plan
+from synth import config_system
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+def slab_plan(name, N, R, tol=1e-6, half=False):
+    xyz, q, L = config_system(name, N=N)
+    if half:   # every particle in the lower half of x: the upper ranks own nothing
+        xyz = xyz.copy()
+        xyz[:, 0] = -0.5 * L[0] + 0.5 * (xyz[:, 0] + 0.5 * L[0])
+    op = make_plan(len(q), *L, tol)
+    if op.m >= 0 and op.Ix % R:
+        ix = op.Ix
+        while ix % R or ix % 2:
+            ix += 1
+        op = dataclasses.replace(op, Ix=ix)
+    params = dataclasses.asdict(op)
+    params["row"] = [r[0] for r in TABLE1].index(op.b)
+    return xyz, q, L, op, params
+
+
+def run_slabs(xyz, q, L, op, params, R):
+    from paper_2412_04595_b200 import DistPlan, Plan, slab_owner
+    owner = slab_owner(xyz[:, 0], L[0], R)
+    idx = [np.nonzero(owner == r)[0] for r in range(R)]
+    nmax = max(1, max(len(i) for i in idx))
+    dp = DistPlan(len(q), nmax, L, op.tol, R, loopback=True, params=params)
+    xs = [torch.from_numpy(np.ascontiguousarray(xyz[i])).cuda() for i in idx]
+    qs = [torch.from_numpy(np.ascontiguousarray(q[i])).cuda() for i in idx]
+    phis, fs = dp.eval(xs, qs)
+    torch.cuda.synchronize()
+    phi = np.empty(len(q))
+    F = np.empty((len(q), 3))
+    for r in range(R):
+        phi[idx[r]] = phis[r].cpu().numpy()
+        F[idx[r]] = fs[r].cpu().numpy()
+    pl = Plan(len(q), L, op.tol, params=params)
+    p1, F1 = pl.eval(torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda())
+    torch.cuda.synchronize()
+    d = dp.describe()
+    dp.close()
+    pl.close()
+    return phi, F, p1.cpu().numpy(), F1.cpu().numpy(), d
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_loopback_cube_matches_single_and_oracle(R):
+    xyz, q, L, op, params = slab_plan("c5", 20000, R)
+    phi, F, p1, F1, d = run_slabs(xyz, q, L, op, params, R)
+    assert d["ranks"] == R and d["slab_planes"] * R == d["Ix"]
+    assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
+    phi_o, F_o = O.evaluate(op, xyz, q)
+    assert rel(phi, phi_o) <= 1e-12 and rel(F, F_o) <= 1e-12, (rel(phi, phi_o), rel(F, F_o))
+
+
+def test_loopback_slab_box_two_ranks():
+    """c3 shape (thin slab, wide in x,y): two ranks, long-range proxies exercised."""
+    xyz, q, L, op, params = slab_plan("c3", 8000, 2)
+    phi, F, p1, F1, _ = run_slabs(xyz, q, L, op, params, 2)
+    assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
+
+
+def test_loopback_empty_ranks():
+    """Every particle in the lower half of x: ranks 2, 3 of 4 own nothing (halo only)."""
+    xyz, q, L, op, params = slab_plan("c5", 12000, 4, half=True)
+    phi, F, p1, F1, _ = run_slabs(xyz, q, L, op, params, 4)
+    assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
+
+
+def test_particle_outside_its_slab_is_rejected():
+    from paper_2412_04595_b200 import DistPlan, SogError
+    xyz, q, L, op, params = slab_plan("c5", 4000, 2)
+    dp = DistPlan(len(q), len(q), L, op.tol, 2, loopback=True, params=params)
+    x = torch.from_numpy(xyz).cuda()
+    qq = torch.from_numpy(q).cuda()
+    empty_x = torch.empty(0, 3, dtype=torch.float64, device="cuda")
+    empty_q = torch.empty(0, dtype=torch.float64, device="cuda")
+    with pytest.raises(SogError):       # all particles handed to rank 0
+        dp.eval([x, empty_x], [qq, empty_q])
+    dp.close()
