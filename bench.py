@@ -5,9 +5,11 @@
 
 Workload (BASELINE.json metric "particles/s per potential+force eval (fp64, tol 1e-6)"): the
 c5 configuration, N = 1e7 neutral +-1 charges uniform in a 215^3 box (periodic x,y, free z),
-tol 1e-6, synthetic seeded inputs (synth/).  Each rank evaluates its own system (weak
-scaling; the x-slab decomposition is a later row).  The working set (mid grid 4.3 GB) is far
-larger than L2, so no explicit flush is needed between steps.
+tol 1e-6, synthetic seeded inputs (synth/).  N = 1: one GPU evaluates the whole system.
+N > 1 (torchrun): the same system split into x slabs over the ranks (include/sog.h
+sog_dist_*: particle halos, pencil all-to-all FFT, Psi edge planes, long-grid all-reduce over
+NCCL), strong scaling; --parallelism replicas runs independent systems instead (weak).  The
+working set (mid grid 3.5 GB) is far larger than L2, so no explicit flush is needed.
 
 --impl reference times the CPU oracle (oracle/, the only other place bench.py runs it) on
 a bounded sample of the same workload, on rank 0 only.
@@ -45,6 +47,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallelism", default="xslab", choices=["xslab", "replicas"],
+                    help="N>1: x-slab decomposition of one system (strong scaling, NCCL) or replicas")
     return ap.parse_args()
 
 
@@ -234,11 +238,88 @@ def stage_roofline(plan, stages, N, L):
     return name, roof, per_stage
 
 
+def run_xslab(args, ws, rank, local):
+    """N>1: one c5 system split into x slabs over the ranks (NCCL over NVLink; strong scaling)."""
+    import torch
+    from paper_2412_04595_b200 import DistPlan, slab_owner
+    c = CONFIGS[args.config]
+    tol = args.tol or c.tol
+    xyz, q, L = config_system(args.config)          # every rank generates the same seeded system
+    N = len(q)
+    owner = slab_owner(xyz[:, 0], L[0], ws)
+    counts = np.bincount(owner, minlength=ws)
+    mine = np.nonzero(owner == rank)[0]
+    stream = torch.cuda.current_stream()
+    plan = DistPlan.from_process_group(N, int(counts.max()), L, tol, stream=stream)
+    xd = torch.from_numpy(np.ascontiguousarray(xyz[mine])).cuda()
+    qd = torch.from_numpy(np.ascontiguousarray(q[mine])).cuda()
+    phi = torch.empty(len(mine), dtype=torch.float64, device="cuda")
+    F = torch.empty(len(mine), 3, dtype=torch.float64, device="cuda")
+    for _ in range(max(1, args.warmup)):
+        plan.eval(xd, qd, phi, F)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.eval(xd, qd, phi, F)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    # end to end: pinned host -> device copies of this rank's particles and results back
+    hx = torch.from_numpy(np.ascontiguousarray(xyz[mine])).pin_memory()
+    hq = torch.from_numpy(np.ascontiguousarray(q[mine])).pin_memory()
+    hphi = torch.empty(len(mine), dtype=torch.float64).pin_memory()
+    hF = torch.empty(len(mine), 3, dtype=torch.float64).pin_memory()
+    barrier(ws)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(hx, non_blocking=True)
+        qd.copy_(hq, non_blocking=True)
+        plan.eval(xd, qd, phi, F)
+        hphi.copy_(phi, non_blocking=True)
+        hF.copy_(F, non_blocking=True)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(g0.elapsed_time(g1) / args.steps, ws)
+    d = plan.describe()
+    out = {
+        "metric": METRIC, "value": N / (ms * 1e-3), "unit": "particles/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: N={N} neutral +-1 charges uniform in "
+                               f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
+                   "N": N, "tol": tol, "parallelism": f"xslab{ws} (NCCL: particle halos, pencil all-to-all "
+                                                    f"FFT, Psi edge planes, long-grid all-reduce)",
+                   "l2": "working set >> 126 MB L2; no flush",
+                   "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc",
+                                              "slab_planes", "halo")}},
+        "roofline": None,
+        "cpu_baseline": None,
+        "e2e": {"value": N / (e2e_ms * 1e-3), "unit": "particles/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(32 * N), "d2h_bytes_per_step": int(32 * N)},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    plan.close()
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if ws > 1 and args.parallelism == "xslab":
+        run_xslab(args, ws, rank, local)
         return
     import torch
     from paper_2412_04595_b200 import Plan
