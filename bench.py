@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
     ap.add_argument("--parallelism", default="xslab", choices=["xslab", "replicas"],
                     help="N>1: x-slab decomposition of one system (strong scaling, NCCL) or replicas")
     return ap.parse_args()
@@ -328,7 +330,7 @@ def main():
     xyz, q, L = config_system(args.config, seed_offset=rank)
     N = len(q)
     stream = torch.cuda.current_stream()
-    plan = Plan(N, L, tol, stream=stream, validate=False)
+    plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision)
     xd = torch.from_numpy(xyz).cuda()
     qd = torch.from_numpy(q).cuda()
     phi = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -392,7 +394,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: N={N} neutral +-1 charges uniform in "
                                f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
                    "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",

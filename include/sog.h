@@ -77,6 +77,9 @@ typedef struct {
     int Pc;
     void* cuda_stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream */
     unsigned flags;         /* SOG_NO_VALIDATE ... */
+    int precision;          /* 0: fp64 (default); 1: fp32 mode (S2-S12 in fp32 storage and
+                               arithmetic, positions/outputs fp64 at the boundary; tol >= 1e-5,
+                               whole-box plans with small long grids; parity bar 1e-5) */
 } sog_plan_opts;
 
 /* Build a plan for N particles in the box (Lx,Ly,Lz) at tolerance tol on the current

@@ -12,6 +12,7 @@
 // Proxy grids: [Pc][Ilx][Ily] real (T-basis layers), spectra [Pc][Ilx][Ily/2+1].
 #pragma once
 #include <cuComplex.h>
+#include <type_traits>
 #include "kernels_common.cuh"
 
 namespace sog {
@@ -27,19 +28,23 @@ struct LongArgs {
 };
 
 // S10: one thread per (half mode, a).
-static __global__ void k_long_scale(const cuDoubleComplex* __restrict__ in, cuDoubleComplex* __restrict__ out,
-                             const double* __restrict__ K, int nmode, int Pc) {
+template <typename C = cuDoubleComplex>
+__global__ void k_long_scale(const C* __restrict__ in, C* __restrict__ out, const double* __restrict__ K, int nmode,
+                             int Pc) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nmode * Pc) return;
     int mode = t / Pc, aa = t % Pc;
     const double* Km = K + ((size_t)mode * Pc + aa) * Pc;
     double re = 0, im = 0;
     for (int b = 0; b < Pc; ++b) {
-        cuDoubleComplex v = in[(size_t)b * nmode + mode];
-        re = fma(Km[b], v.x, re);
-        im = fma(Km[b], v.y, im);
+        const C v = in[(size_t)b * nmode + mode];
+        re = fma(Km[b], (double)v.x, re);
+        im = fma(Km[b], (double)v.y, im);
     }
-    out[(size_t)aa * nmode + mode] = make_cuDoubleComplex(re, im);
+    C o;
+    o.x = re;
+    o.y = im;
+    out[(size_t)aa * nmode + mode] = o;
 }
 
 }  // namespace sog
@@ -278,19 +283,21 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
 // Partials [block][n][cx][cy] are summed in a fixed order by k_long_sum (deterministic).
 constexpr int LG_KB = 64, LG_LT = 6, LG_RX = 32, LG_RY = 32;
 
-template <int PCP>
+template <int PCP, typename T = double>
 __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
-                                                             double gamma_y, int per, double* __restrict__ part) {
+                                                             double gamma_y, int per, T* __restrict__ part) {
     constexpr int NLG = PCP / LG_LT;
     // double-buffered rows: [2][LG_KB][RXP + RYP + PCP], RXP = Ilx, RYP = Ily rounded up to 4
-    extern __shared__ __align__(16) double sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
     const int RXP = a.Ilx, RYP = (a.Ily + 3) & ~3, RW = ((RXP + RYP + PCP) + 1) & ~1;
     const int tid = threadIdx.x;
     const int ncy4 = (a.Ily + 3) / 4;
     const int lg = tid % NLG, cg = tid / NLG;
     const int cx = cg / ncy4, cy0 = 4 * (cg % ncy4);
     const bool own = cx < a.Ilx;
-    double acc[4][LG_LT];
+    T acc[4][LG_LT];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -301,15 +308,15 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
     auto stage = [&](int base, int buf) {
         const int t = tid >> 1, role = tid & 1;
         if (t >= LG_KB) return;
-        double* row = sm + ((size_t)buf * LG_KB + t) * RW;
-        double* rx = row;
-        double* ry = row + RXP;
-        double* tt = row + RXP + RYP;
+        T* row = sm + ((size_t)buf * LG_KB + t) * RW;
+        T* rx = row;
+        T* ry = row + RXP;
+        T* tt = row + RXP + RYP;
         if (role == 0) {
-            for (int c = 0; c < RXP; ++c) rx[c] = 0.0;
-            for (int n = 0; n < PCP; ++n) tt[n] = 0.0;
+            for (int c = 0; c < RXP; ++c) rx[c] = T(0);
+            for (int n = 0; n < PCP; ++n) tt[n] = T(0);
         } else {
-            for (int c = 0; c < RYP; ++c) ry[c] = 0.0;
+            for (int c = 0; c < RYP; ++c) ry[c] = T(0);
         }
         const int j = base + t;
         if (j >= j1) return;
@@ -321,17 +328,17 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
             double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
             int c = sx < 0 ? sx + a.Ilx : sx;
             for (int u = 0; u < P; ++u) {
-                rx[c] = r.w * w;
+                rx[c] = T(r.w * w);
                 w *= q; q *= gamma_x;
                 c = c + 1 == a.Ilx ? 0 : c + 1;
             }
             const double x = r.z * a.two_over_Lz;
             double tm = 1.0, tc = x;
-            tt[0] = 1.0;
-            if (a.Pc > 1) tt[1] = x;
+            tt[0] = T(1);
+            if (a.Pc > 1) tt[1] = T(x);
             for (int n = 2; n < a.Pc; ++n) {
                 const double tn = 2.0 * x * tc - tm;
-                tt[n] = tn;
+                tt[n] = T(tn);
                 tm = tc; tc = tn;
             }
         } else {
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
             double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
             int c = sy < 0 ? sy + a.Ily : sy;
             for (int v = 0; v < P; ++v) {
-                ry[c] = w;
+                ry[c] = T(w);
                 w *= q; q *= gamma_y;
                 c = c + 1 == a.Ily ? 0 : c + 1;
             }
@@ -353,20 +360,20 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
         if (base + LG_KB < j1) stage(base + LG_KB, buf ^ 1);    // next batch while this one computes
         const int nb = min(LG_KB, j1 - base);
         if (own) {
-            const double* rows = sm + (size_t)buf * LG_KB * RW;
+            const T* rows = sm + (size_t)buf * LG_KB * RW;
 #pragma unroll 2
             for (int t = 0; t < nb; ++t) {
-                const double* row = rows + (size_t)t * RW;
-                const double rx = row[cx];
-                const double2 y01 = *reinterpret_cast<const double2*>(row + RXP + cy0);
-                const double2 y23 = *reinterpret_cast<const double2*>(row + RXP + cy0 + 2);
-                double tl[LG_LT];
+                const T* row = rows + (size_t)t * RW;
+                const T rx = row[cx];
+                const V2 y01 = *reinterpret_cast<const V2*>(row + RXP + cy0);
+                const V2 y23 = *reinterpret_cast<const V2*>(row + RXP + cy0 + 2);
+                T tl[LG_LT];
 #pragma unroll
                 for (int l = 0; l < LG_LT; l += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(row + RXP + RYP + lg * LG_LT + l);
+                    const V2 v = *reinterpret_cast<const V2*>(row + RXP + RYP + lg * LG_LT + l);
                     tl[l] = v.x; tl[l + 1] = v.y;
                 }
-                const double av[4] = {rx * y01.x, rx * y01.y, rx * y23.x, rx * y23.y};
+                const T av[4] = {rx * y01.x, rx * y01.y, rx * y23.x, rx * y23.y};
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
     }
     if (own) {
         const size_t G = (size_t)a.Ilx * a.Ily;
-        double* o = part + (size_t)blockIdx.x * PCP * G;
+        T* o = part + (size_t)blockIdx.x * PCP * G;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -389,14 +396,15 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
 }
 
 // grid[n][g] = sum over blocks (fixed order) of part[block][n][g], n < Pc
-static __global__ void k_long_sum(const double* __restrict__ part, double* __restrict__ grid, int G, int Pc, int PCP,
+template <typename T>
+__global__ void k_long_sum(const T* __restrict__ part, T* __restrict__ grid, int G, int Pc, int PCP,
                                   int nblk) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= G * Pc) return;
-    const double* p = part + idx;
+    const T* p = part + idx;
     double s = 0.0;
     for (int b = 0; b < nblk; ++b) s += p[(size_t)b * PCP * G];
-    grid[idx] = s;
+    grid[idx] = T(s);
 }
 
 // S12 for small long grids: one thread per particle, the whole T-basis field Psi~ in shared
@@ -404,29 +412,31 @@ static __global__ void k_long_sum(const double* __restrict__ part, double* __res
 // columns in the same order).  Per column: V = sum_m T_m Psi~_m, V' = sum_m T'_m Psi~_m
 // (2 PCP FMAs) and 4 products with the rotated weights.  Rx / dRx rows live in shared
 // memory (dynamic cx), Ry / dRy in registers (static cy < NCY).
-template <int PCP, int NCY>
+template <int PCP, int NCY, typename T = double>
 __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int4* __restrict__ g0,
-                                                        const double* __restrict__ psi, d4* __restrict__ out) {
-    extern __shared__ __align__(16) double sm[];
+                                                        const T* __restrict__ psi, d4* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
     const int G = a.Ilx * a.Ily;
-    double* sPsi = sm;                                  // [G][PCP]
-    double* sRx = sm + (size_t)G * PCP;                 // [Ilx][128]
-    double* sdRx = sRx + (size_t)a.Ilx * 128;           // [Ilx][128]
-    double* sRy = sdRx + (size_t)a.Ilx * 128;           // [NCY][128]
-    double* sdRy = sRy + (size_t)NCY * 128;             // [NCY][128]
+    T* sPsi = sm;                                  // [G][PCP]
+    T* sRx = sm + (size_t)G * PCP;                 // [Ilx][128]
+    T* sdRx = sRx + (size_t)a.Ilx * 128;           // [Ilx][128]
+    T* sRy = sdRx + (size_t)a.Ilx * 128;           // [NCY][128]
+    T* sdRy = sRy + (size_t)NCY * 128;             // [NCY][128]
     for (int e = threadIdx.x; e < G * PCP; e += blockDim.x) {
         const int g = e / PCP, n = e - g * PCP;
-        sPsi[e] = n < a.Pc ? psi[(size_t)n * G + g] : 0.0;
+        sPsi[e] = n < a.Pc ? psi[(size_t)n * G + g] : T(0);
     }
     const int tid = threadIdx.x;
     const int j = blockIdx.x * blockDim.x + tid;
     const bool act = j < a.N;
     const int P = a.Pl;
-    double T[PCP], dT[PCP];
+    T Tn[PCP], dT[PCP];
     {
-        for (int c = 0; c < a.Ilx; ++c) { sRx[c * 128 + tid] = 0.0; sdRx[c * 128 + tid] = 0.0; }
+        for (int c = 0; c < a.Ilx; ++c) { sRx[c * 128 + tid] = T(0); sdRx[c * 128 + tid] = T(0); }
 #pragma unroll
-        for (int c = 0; c < NCY; ++c) { sRy[c * 128 + tid] = 0.0; sdRy[c * 128 + tid] = 0.0; }
+        for (int c = 0; c < NCY; ++c) { sRy[c * 128 + tid] = T(0); sdRy[c * 128 + tid] = T(0); }
         d4 r{0.0, 0.0, 0.0, 0.0};
         int sx = 0, sy = 0;
         if (act) {
@@ -440,8 +450,8 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
                 const double gam = exp(-2.0 * a.invH2Sx * a.hx * a.hx);
                 int c = sx < 0 ? sx + a.Ilx : sx;
                 for (int u = 0; u < P; ++u) {
-                    sRx[c * 128 + tid] = w;
-                    sdRx[c * 128 + tid] = 2.0 * a.invH2Sx * (d0 + u * a.hx) * w;
+                    sRx[c * 128 + tid] = T(w);
+                    sdRx[c * 128 + tid] = T(2.0 * a.invH2Sx * (d0 + u * a.hx) * w);
                     w *= q; q *= gam;
                     c = c + 1 == a.Ilx ? 0 : c + 1;
                 }
@@ -452,40 +462,42 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
                 const double gam = exp(-2.0 * a.invH2Sy * a.hy * a.hy);
                 int c = sy < 0 ? sy + a.Ily : sy;
                 for (int v = 0; v < P; ++v) {
-                    sRy[c * 128 + tid] = w;
-                    sdRy[c * 128 + tid] = 2.0 * a.invH2Sy * (d0 + v * a.hy) * w;
+                    sRy[c * 128 + tid] = T(w);
+                    sdRy[c * 128 + tid] = T(2.0 * a.invH2Sy * (d0 + v * a.hy) * w);
                     w *= q; q *= gam;
                     c = c + 1 == a.Ily ? 0 : c + 1;
                 }
             }
         }
         const double x = r.z * a.two_over_Lz;
-        T[0] = 1.0; dT[0] = 0.0;
-        T[1] = x; dT[1] = 1.0;
+        double t0 = 1.0, t1 = x, d0v = 0.0, d1v = 1.0;   // Chebyshev T_n, T_n' in fp64, stored as T
+        Tn[0] = T(t0); dT[0] = T(d0v);
+        if (PCP > 1) { Tn[1] = T(t1); dT[1] = T(d1v); }
 #pragma unroll
         for (int n = 1; n + 1 < PCP; ++n) {
-            T[n + 1] = 2.0 * x * T[n] - T[n - 1];
-            dT[n + 1] = 2.0 * T[n] + 2.0 * x * dT[n] - dT[n - 1];
+            const double t2 = 2.0 * x * t1 - t0, d2 = 2.0 * t1 + 2.0 * x * d1v - d0v;
+            Tn[n + 1] = T(t2); dT[n + 1] = T(d2);
+            t0 = t1; t1 = t2; d0v = d1v; d1v = d2;
         }
     }
     __syncthreads();
-    double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    T phi = 0, gx = 0, gy = 0, gz = 0;
     for (int cx = 0; cx < a.Ilx; ++cx) {
-        const double rx = sRx[cx * 128 + tid], drx = sdRx[cx * 128 + tid];
-        const double* col = sPsi + (size_t)cx * a.Ily * PCP;
+        const T rx = sRx[cx * 128 + tid], drx = sdRx[cx * 128 + tid];
+        const T* col = sPsi + (size_t)cx * a.Ily * PCP;
 #pragma unroll
         for (int cy = 0; cy < NCY; ++cy) {
             if (cy < a.Ily) {
-                const double2* c2 = reinterpret_cast<const double2*>(col + cy * PCP);
-                double v0 = 0.0, v1 = 0.0;
+                const V2* c2 = reinterpret_cast<const V2*>(col + cy * PCP);
+                T v0 = 0, v1 = 0;
 #pragma unroll
                 for (int n = 0; n < PCP; n += 2) {
-                    const double2 ps = c2[n / 2];
-                    v0 = fma(T[n], ps.x, v0); v0 = fma(T[n + 1], ps.y, v0);
+                    const V2 ps = c2[n / 2];
+                    v0 = fma(Tn[n], ps.x, v0); v0 = fma(Tn[n + 1], ps.y, v0);
                     v1 = fma(dT[n], ps.x, v1); v1 = fma(dT[n + 1], ps.y, v1);
                 }
-                const double ry = sRy[cy * 128 + tid], dry = sdRy[cy * 128 + tid];
-                const double wxy = rx * ry;
+                const T ry = sRy[cy * 128 + tid], dry = sdRy[cy * 128 + tid];
+                const T wxy = rx * ry;
                 phi = fma(wxy, v0, phi);
                 gz = fma(wxy, v1, gz);
                 gx = fma(drx * ry, v0, gx);
@@ -493,7 +505,7 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
             }
         }
     }
-    if (act) st_d4(&out[j], d4{a.A * phi, a.A * gx, a.A * gy, a.A * gz * a.two_over_Lz});
+    if (act) st_d4(&out[j], d4{a.A * double(phi), a.A * double(gx), a.A * double(gy), a.A * double(gz) * a.two_over_Lz});
 }
 
 // Debug-stage conversions back to the paper's Lagrange (proxy-node) basis:

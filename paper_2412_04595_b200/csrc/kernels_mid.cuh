@@ -14,6 +14,7 @@
 // multiply-adds per touched column, and every grid point is written exactly once.
 #pragma once
 #include <cuComplex.h>
+#include <type_traits>
 #include "kernels_common.cuh"
 
 namespace sog {
@@ -128,19 +129,21 @@ struct MidZArgs {
 // base inside the NACC-slot z window, zeros elsewhere (even length)] [hdr int4: dx, dy, -,
 // chunk].  dx, dy are the stencil start relative to the tile origin: signed in [-(P-1),
 // MZ_TX) when the window does not wrap onto itself, else mod I.
-template <int P>
+template <int P, typename T = double>
 struct SRec {
+    static constexpr int AL = 16 / int(sizeof(T));         // elements per 16 bytes
     static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane (z planes)
     static constexpr int NZP = (NACC + 1) & ~1;            // padded Wz slots
-    static constexpr int WX = 0, WY = P, WZ = 2 * P, HDR = 2 * P + NZP + ((2 * P + NZP) & 1);
-    static constexpr int SIZE = HDR + 2;
+    static constexpr int WX = 0, WY = P, WZ = ((2 * P + AL - 1) / AL) * AL;
+    static constexpr int HDR = ((WZ + NZP + AL - 1) / AL) * AL;   // int4 header, 16-byte aligned
+    static constexpr int SIZE = HDR + AL;
     static constexpr int B = 64;                           // particles per staged batch
-    static constexpr int K = SIZE <= 48 ? 4 : 2;           // batch buffers in flight
+    static constexpr int K = SIZE * int(sizeof(T)) <= 48 * 8 ? 4 : 2;   // batch buffers in flight
     static constexpr int EMAX = 1024;                      // (chunk, home tile) ranges per CTA
     static constexpr int NPROD = 2;                        // producer warps (32 particles each)
     static constexpr int NTHR = 32 * (8 + NPROD);
-    static constexpr int MINB = P <= 15 ? 2 : 1;          // CTAs per SM (register budget)
-    static constexpr size_t BYTES = sizeof(double) * K * B * SIZE + sizeof(int) * (2 * EMAX + 1);
+    static constexpr int MINB = P <= 15 || sizeof(T) == 4 ? 2 : 1;   // CTAs per SM (register budget)
+    static constexpr size_t BYTES = sizeof(T) * K * B * SIZE + sizeof(int) * (2 * EMAX + 1);
 };
 
 // mbarrier helpers (shared::cta)
@@ -164,9 +167,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 }
 
 // lane flush of one chunk's MZ_ZC planes (written only for c >= cb), then slide the window
-template <int P>
-__device__ __forceinline__ void spread_flush(double (&acc)[SRec<P>::NACC], int c, int cb, bool colok, int cx, int cy,
-                                             const MidZArgs& a, double* __restrict__ grid) {
+template <int P, typename T>
+__device__ __forceinline__ void spread_flush(T (&acc)[SRec<P, T>::NACC], int c, int cb, bool colok, int cx, int cy,
+                                             const MidZArgs& a, T* __restrict__ grid) {
     if (c >= cb && colok) {
 #pragma unroll
         for (int z = 0; z < MZ_ZC; ++z) {
@@ -176,18 +179,20 @@ __device__ __forceinline__ void spread_flush(double (&acc)[SRec<P>::NACC], int c
         }
     }
 #pragma unroll
-    for (int i = 0; i < SRec<P>::NACC; ++i) acc[i] = i + MZ_ZC < SRec<P>::NACC ? acc[i + MZ_ZC] : 0.0;
+    for (int i = 0; i < SRec<P, T>::NACC; ++i) acc[i] = i + MZ_ZC < SRec<P, T>::NACC ? acc[i + MZ_ZC] : T(0);
 }
 
 // Warp-specialised: NPROD producer warps stage the CTA's candidate stream (weights, relevance
 // masks) into K batch buffers; 8 consumer warps (one 4 x 8 column patch each) accumulate
 // their patch's particles.  full/empty mbarriers let consumer warps drift up to K batches
 // apart, so the per-batch imbalance between patches averages out.
-template <int P>
-__global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(MidZArgs a, double* __restrict__ grid) {
-    using R = SRec<P>;
+template <int P, typename T = double>
+__global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spread_z(MidZArgs a, T* __restrict__ grid) {
+    using R = SRec<P, T>;
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
     constexpr int p = (P - 1) / 2, NACC = R::NACC, B = R::B, K = R::K, EMAX = R::EMAX;
-    extern __shared__ __align__(16) double sRec[];      // [K][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sRec = reinterpret_cast<T*>(smraw);      // [K][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
     int* sPre = reinterpret_cast<int*>(sRec + K * B * R::SIZE);
     int* sBeg = sPre + EMAX + 1;
     __shared__ unsigned short sList[8][B];
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
             const int buf = bi % K;
             if (bi >= K) mbar_wait(&barEmpty[buf], ((bi / K) - 1) & 1);
             const int idx = bi * B + s;
-            double* rec = sRec + (buf * B + s) * R::SIZE;
+            T* rec = sRec + (buf * B + s) * R::SIZE;
             unsigned mask = 0;
             if (idx < total) {
                 int lo = 0, hi = E;                      // last e with sPre[e] <= idx
@@ -317,14 +322,14 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
                     window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
 #pragma unroll
                     for (int i = 0; i < P; ++i) {
-                        rec[R::WX + i] = r.w * wx[i];
-                        rec[R::WY + i] = wy[i];
+                        rec[R::WX + i] = T(r.w * wx[i]);
+                        rec[R::WY + i] = T(wy[i]);
                     }
                     const int o = in.w - c * MZ_ZC;      // z offset of the stencil in the window
 #pragma unroll
-                    for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = 0.0;
+                    for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
 #pragma unroll
-                    for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = wz[i];
+                    for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(wz[i]);
                 }
             }
             sMask[buf][s] = (unsigned char)mask;
@@ -337,9 +342,9 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
     const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
     const int cx = X0 + lx, cy = Y0 + ly;
     const bool colok = cx < a.Ixk && cy < a.Iy;
-    double acc[NACC];
+    T acc[NACC];
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NACC; ++i) acc[i] = T(0);
     int cur = cs;                                        // chunk held in acc[0, MZ_ZC)
     for (int bi = 0; bi < nbat; ++bi) {
         const int buf = bi % K;
@@ -355,36 +360,36 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
             nmy += __popc(bm);
         }
         __syncwarp();
-        const double* base = sRec + buf * B * R::SIZE;
-        auto coef = [&](const double* rec, const int4& hdr) {
+        const T* base = sRec + buf * B * R::SIZE;
+        auto coef = [&](const T* rec, const int4& hdr) {
             const int u = smallx ? wrapc(lx - hdr.x, a.Ix) : lx - hdr.x;
             const int v = smally ? wrapc(ly - hdr.y, a.Iy) : ly - hdr.y;
             const bool in = (unsigned)u < (unsigned)P && (unsigned)v < (unsigned)P;
-            return in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : 0.0;
+            return in ? rec[R::WX + min((unsigned)u, P - 1u)] * rec[R::WY + min((unsigned)v, P - 1u)] : T(0);
         };
-        auto accum = [&](const double* rec, double cc) {
-            const double2* w2 = reinterpret_cast<const double2*>(rec + R::WZ);
+        auto accum = [&](const T* rec, T cc) {
+            const V2* w2 = reinterpret_cast<const V2*>(rec + R::WZ);
 #pragma unroll
             for (int k = 0; k < R::NZP / 2; ++k) {
-                const double2 t = w2[k];
+                const V2 t = w2[k];
                 if (2 * k < NACC) acc[2 * k] = fma(cc, t.x, acc[2 * k]);
                 if (2 * k + 1 < NACC) acc[2 * k + 1] = fma(cc, t.y, acc[2 * k + 1]);
             }
         };
         int i = 0;
         while (i < nmy) {                                // two particles per step when in one chunk
-            const double* ra = base + sList[warp][i] * R::SIZE;
+            const T* ra = base + sList[warp][i] * R::SIZE;
             const int4 ha = *reinterpret_cast<const int4*>(ra + R::HDR);
             const bool two = i + 1 < nmy;
-            const double* rb = base + sList[warp][two ? i + 1 : i] * R::SIZE;
+            const T* rb = base + sList[warp][two ? i + 1 : i] * R::SIZE;
             const int4 hb = *reinterpret_cast<const int4*>(rb + R::HDR);
             while (cur < ha.w) {                         // warp-uniform: entering a later chunk
-                spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
+                spread_flush<P, T>(acc, cur, cb, colok, cx, cy, a, grid);
                 ++cur;
             }
-            const double ca = coef(ra, ha);
+            const T ca = coef(ra, ha);
             const bool pair = two && hb.w == ha.w;
-            const double cbv = coef(rb, hb);
+            const T cbv = coef(rb, hb);
             accum(ra, ca);
             if (pair) accum(rb, cbv);
             i += pair ? 2 : 1;
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
         mbar_arrive(&barEmpty[buf]);
     }
     while (cur < ce) {
-        spread_flush<P>(acc, cur, cb, colok, cx, cy, a, grid);
+        spread_flush<P, T>(acc, cur, cb, colok, cx, cy, a, grid);
         ++cur;
     }
 }
@@ -405,29 +410,31 @@ __global__ void __launch_bounds__(SRec<P>::NTHR, SRec<P>::MINB) k_mid_spread_z(M
 // particle at a time, lanes over the P x P stencil columns (z contracted per lane, then the
 // separable x/y weights), and reduces the four values with shuffles.  Three lanes compute
 // the particle's separable weights (Gaussian recurrence, one axis each).
-template <int P>
+template <int P, typename T = double>
 struct GRing {
     static constexpr int WX = MZ_TX + P - 1, WY = MZ_TY + P - 1;
     static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
     static constexpr int PL = WX * WYP;                           // plane size (doubles)
     static constexpr int D = MZ_ZC + P - 1;                       // planes in the ring
-    static constexpr int WSZ = 6 * P + 2;                         // per-particle weight scratch
+    static constexpr int AL = 16 / int(sizeof(T)), HOFF = ((6 * P + AL - 1) / AL) * AL;
+    static constexpr int WSZ = HOFF + AL;                         // per-particle weight scratch
     static constexpr int WB = 6;                                  // particles per warp batch (<= 10)
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
-    static constexpr size_t BYTES = sizeof(double) * (size_t(D) * PL + 8 * WB * WSZ);
+    static constexpr size_t BYTES = sizeof(T) * (size_t(D) * PL + 8 * WB * WSZ);
     static constexpr bool FITS = BYTES <= 227 * 1024;
     static constexpr int MINB = BYTES <= 113 * 1024 ? 2 : 1;     // CTAs per SM
 };
 
-template <int P>
-__global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a, const double* __restrict__ psi,
+template <int P, typename T = double>
+__global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArgs a, const T* __restrict__ psi,
                                                          d4* __restrict__ out) {
-    using G = GRing<P>;
+    using G = GRing<P, T>;
     constexpr int D = G::D, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
-    extern __shared__ __align__(16) double sm[];
-    double* ring = sm;                                   // [D][WX][WYP]
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
+    T* ring = sm;                                   // [D][WX][WYP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* wsb = sm + D * PL + warp * G::WB * G::WSZ;   // per particle: Wx dWx Wy dWy Wz dWz, hdr
+    T* wsb = sm + D * PL + warp * G::WB * G::WSZ;   // per particle: Wx dWx Wy dWy Wz dWz, hdr
     const int tx = a.tlo + blockIdx.x / a.nty, ty = blockIdx.x % a.nty;
     const int tile = tx * a.nty + ty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
@@ -454,7 +461,7 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
             constexpr int NPL = WX * WY;
             const int nload = (nhi - from) * NPL;
             for (int e0 = tid; e0 < nload; e0 += 4 * 256) {
-                double v[4];
+                T v[4];
                 int dst[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
                         const int xr = rem / WY, yr = rem - xr * WY;
                         const int plane = from + pz;
                         const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr, gy = wrapc(Y0 + yr, a.Iy);
-                        v[u] = gx < a.Ixk ? __ldg(&psi[((size_t)plane * a.Ixk + gx) * a.Iy + gy]) : 0.0;
+                        v[u] = gx < a.Ixk ? __ldg(&psi[((size_t)plane * a.Ixk + gx) * a.Iy + gy]) : T(0);
                         dst[u] = (plane % D) * PL + xr * WYP + yr;
                     }
                 }
@@ -493,16 +500,16 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
                 const double d0 = ((double)sa - hf) * hh - x;
                 double w = exp(-aa * d0 * d0);
                 double q = exp(-aa * hh * (2.0 * d0 + hh));
-                double* o = wsb + pp * G::WSZ + 2 * axl * P;
+                T* o = wsb + pp * G::WSZ + 2 * axl * P;
 #pragma unroll
                 for (int i = 0; i < P; ++i) {
-                    o[i] = w;
-                    o[P + i] = 2.0 * aa * (d0 + i * hh) * w;
+                    o[i] = T(w);
+                    o[P + i] = T(2.0 * aa * (d0 + i * hh) * w);
                     w *= q;
                     q *= gg;
                 }
                 if (axl == 0) {
-                    int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + 6 * P);
+                    int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + G::HOFF);
                     hd[0] = a.px ? in.y - X0 + (in.y < 0 ? a.Ix : 0) : in.y - a.xorig - X0;   // relative to the tile
                     hd[1] = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
                     hd[2] = in.w % D;                                    // ring slot of the first plane
@@ -511,9 +518,9 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
             }
             __syncwarp();
             for (int pp = 0; pp < nb; ++pp) {
-            const double* wsc = wsb + pp * G::WSZ;
-            const int4 hd = *reinterpret_cast<const int4*>(wsc + 6 * P);
-            double wz[P], dwz[P];
+            const T* wsc = wsb + pp * G::WSZ;
+            const int4 hd = *reinterpret_cast<const int4*>(wsc + G::HOFF);
+            T wz[P], dwz[P];
 #pragma unroll
             for (int i = 0; i < P; ++i) { wz[i] = wsc[4 * P + i]; dwz[i] = wsc[5 * P + i]; }
             int pb[P];                                   // ring plane offsets of the P stencil planes
@@ -522,22 +529,22 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
 #pragma unroll
                 for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == D ? 0 : zs + 1; }
             }
-            const double* base = ring + hd.x * WYP + hd.y;
-            double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+            const T* base = ring + hd.x * WYP + hd.y;
+            T phi = 0, gx = 0, gy = 0, gz = 0;
 #pragma unroll
             for (int rr = 0; rr < NR; ++rr) {
                 if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
-                const double* col = base + coff[rr];
-                double t0 = 0.0, t1 = 0.0;
+                const T* col = base + coff[rr];
+                T t0 = 0, t1 = 0;
 #pragma unroll
                 for (int kz = 0; kz < P; ++kz) {
-                    const double v = col[pb[kz]];
+                    const T v = col[pb[kz]];
                     t0 = fma(wz[kz], v, t0);
                     t1 = fma(dwz[kz], v, t1);
                 }
-                const double wx = wsc[ca[rr]], dwx = wsc[P + ca[rr]];
-                const double wy = wsc[2 * P + cbb[rr]], dwy = wsc[3 * P + cbb[rr]];
-                const double wxy = wx * wy;
+                const T wx = wsc[ca[rr]], dwx = wsc[P + ca[rr]];
+                const T wy = wsc[2 * P + cbb[rr]], dwy = wsc[3 * P + cbb[rr]];
+                const T wxy = wx * wy;
                 phi = fma(wxy, t0, phi);
                 gz = fma(wxy, t1, gz);
                 gx = fma(dwx * wy, t0, gx);
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(256, GRing<P>::MINB) k_mid_gather_z(MidZArgs a
             // 4-value butterfly: after the first two levels each lane carries one value
             {
                 const bool b1 = lane & 1;
-                double s0 = b1 ? phi : gx, s1 = b1 ? gy : gz;     // sent
+                double s0 = b1 ? phi : gx, s1 = b1 ? gy : gz;  // reduction in fp64     // sent
                 double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;   // kept
                 k0v += __shfl_xor_sync(0xffffffffu, s0, 1);
                 k1v += __shfl_xor_sync(0xffffffffu, s1, 1);
@@ -632,8 +639,8 @@ __global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* 
 // Tx[l][ix] Ty[l][iy].  A CTA owns MS_ROWS (iz, ix) rows: the per-row factors
 // A_l Tz Tx go to shared memory, each thread keeps Ty[l][iy] of its iy in registers.
 constexpr int MS_ROWS = 16;
-template <int LM>
-__global__ void __launch_bounds__(128) k_mid_scale(cuDoubleComplex* __restrict__ spec, int Ix, int Izs, int nyh, int L,
+template <int LM, typename C = cuDoubleComplex>
+__global__ void __launch_bounds__(128) k_mid_scale(C* __restrict__ spec, int Ix, int Izs, int nyh, int L,
                                                    const double* __restrict__ A, const double* __restrict__ Tx,
                                                    const double* __restrict__ Ty, const double* __restrict__ Tz) {
     __shared__ double sc[MS_ROWS][LM];
@@ -658,8 +665,10 @@ __global__ void __launch_bounds__(128) k_mid_scale(cuDoubleComplex* __restrict__
 #pragma unroll
         for (int l = 0; l < LM; ++l) m = fma(sc[r][l], ty[l], m);
         const size_t idx = (size_t)(row0 + r) * nyh + iy;
-        const cuDoubleComplex v = spec[idx];
-        spec[idx] = make_cuDoubleComplex(v.x * m, v.y * m);
+        C v = spec[idx];
+        v.x *= m;
+        v.y *= m;
+        spec[idx] = v;
     }
 }
 

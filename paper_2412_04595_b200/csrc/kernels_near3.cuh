@@ -164,3 +164,133 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
 }
 
 }  // namespace sog
+
+namespace sog {
+
+// fp32 mode (c4 at tol 1e-4, parity bar 1e-5): the staged cell-relative fp32 coordinates are
+// the evaluation coordinates; F(u) from the same table rounded to fp32, 1/r by rsqrtf, lane
+// partial sums in fp32, the warp reduction in fp64.
+template <int D>
+__global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3f(Near3Args a) {
+    extern __shared__ __align__(16) float smf[];
+    float* tab = smf;                                                   // [K*(D+1)]
+    int* lists = reinterpret_cast<int*>(smf + ((a.K * (D + 1) + 3) & ~3));   // [warps][160]
+    float4* src = reinterpret_cast<float4*>(lists + NEAR3_WARPS * 160);      // [cap]: rel. xyz + q
+    const CellGeo& g = a.g;
+    const int c = blockIdx.x;
+    const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+    const int t0 = a.start[c], t1 = a.start[c + 1];
+    if (t0 == t1) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = (float)a.cF[t];
+    const double ox = g.x0 + cx / g.sx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
+    const int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
+    int* wl = lists + warp * 160;
+    int ns_total = 0;
+    for (int k = 0; k < 9; ++k) {
+        int nx = cx + k / 3 - 1, ny = cy + k % 3 - 1;
+        if (!g.px && (nx < 0 || nx >= g.ncx)) continue;
+        nx += nx < 0 ? g.ncx : 0; nx -= nx >= g.ncx ? g.ncx : 0;
+        ny += ny < 0 ? g.ncy : 0; ny -= ny >= g.ncy ? g.ncy : 0;
+        const int cb = (nx * g.ncy + ny) * g.ncz;
+        ns_total += a.start[cb + z1 + 1] - a.start[cb + z0];
+    }
+    const float rc2 = (float)a.rc2, du = (float)a.du, inv_du = (float)a.inv_du;
+    for (int sbeg = 0; sbeg < ns_total; sbeg += a.cap) {
+        const int send = min(ns_total, sbeg + a.cap);
+        __syncthreads();
+        {
+            int base = 0;
+            for (int k = 0; k < 9; ++k) {
+                const int ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
+                if (!g.px && (ux < 0 || ux >= g.ncx)) continue;
+                const int nx = ux < 0 ? ux + g.ncx : (ux >= g.ncx ? ux - g.ncx : ux);
+                const int ny = uy < 0 ? uy + g.ncy : (uy >= g.ncy ? uy - g.ncy : uy);
+                const double sx = !g.px ? 0.0 : (ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0));
+                const double sy = uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0);
+                const int cb = (nx * g.ncy + ny) * g.ncz;
+                const int jb = a.start[cb + z0], n = a.start[cb + z1 + 1] - jb;
+                const int lo = max(sbeg, base), hi = min(send, base + n);
+                for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+                    const d4 s = ld_d4(&a.pos[jb + (q - base)]);
+                    src[q - sbeg] = make_float4((float)(s.x + sx - ox), (float)(s.y + sy - oy), (float)(s.z - oz),
+                                                (float)s.w);
+                }
+                base += n;
+            }
+        }
+        __syncthreads();
+        const int nsrc = send - sbeg;
+        for (int it = t0 + warp; it < t1; it += NEAR3_WARPS) {
+            const d4 pi = ld_d4(&a.pos[it]);
+            const float xi = (float)(pi.x - ox), yi = (float)(pi.y - oy), zi = (float)(pi.z - oz);
+            float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+            int npend = 0;
+            auto pair = [&](int q) {
+                const float4 s = src[q];
+                const float dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
+                const float u = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (!(u < rc2 && u > 0.f)) return;
+                const int kk = min(a.K - 1, (int)(u * inv_du));
+                const float d = u - (kk + 0.5f) * du;
+                const float* cf = tab + kk * (D + 1);
+                float F = cf[D], dF = 0.f;
+#pragma unroll
+                for (int n = D - 1; n >= 0; --n) {
+                    dF = fmaf(dF, d, F);
+                    F = fmaf(F, d, cf[n]);
+                }
+                const float rinv = rsqrtf(u);
+                phi = fmaf(s.w, rinv - F, phi);
+                const float cc = s.w * (-rinv * rinv * rinv - 2.f * dF);
+                gx = fmaf(cc, dx, gx);
+                gy = fmaf(cc, dy, gy);
+                gz = fmaf(cc, dz, gz);
+            };
+            for (int q0 = 0; q0 < nsrc; q0 += 128) {
+                bool pass[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int q = q0 + 32 * r + lane;
+                    pass[r] = false;
+                    if (q < nsrc) {
+                        const float4 s = src[q];
+                        const float dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
+                        pass[r] = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rc2;
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned m = __ballot_sync(0xffffffffu, pass[r]);
+                    if (pass[r]) wl[npend + __popc(m & ((1u << lane) - 1))] = q0 + 32 * r + lane;
+                    npend += __popc(m);
+                }
+                __syncwarp();
+                while (npend >= 32) {
+                    npend -= 32;
+                    pair(wl[npend + lane]);
+                }
+                __syncwarp();
+            }
+            if (lane < npend) pair(wl[lane]);
+            double p = phi, x = gx, y = gy, z = gz;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                p += __shfl_xor_sync(0xffffffffu, p, o);
+                x += __shfl_xor_sync(0xffffffffu, x, o);
+                y += __shfl_xor_sync(0xffffffffu, y, o);
+                z += __shfl_xor_sync(0xffffffffu, z, o);
+            }
+            if (lane == 0) {
+                if (sbeg == 0) st_d4(&a.out[it], d4{p, x, y, z});
+                else {
+                    d4 o = a.out[it];
+                    st_d4(&a.out[it], d4{o.x + p, o.y + x, o.z + y, o.w + z});
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace sog

@@ -17,21 +17,23 @@ int launch_stencil_origins(const d4* pos, int N, const MidArgs& a, int has_mid, 
 int launch_mid_sort_keys(const int4* g0, int N, const MidSortArgs& s, int* key, int* count, cudaStream_t st);
 int launch_mid_sort_place(const int* key, int N, int* cursor, int* tmp, const int* mstart, int nkeys, const d4* pos_s,
                           const int4* g0, int p, d4* mpos, int4* minfo, cudaStream_t st);
-int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, double* grid, cudaStream_t st);
-int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st);
+int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32, cudaStream_t st);
+int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void* psi, d4* out, bool f32,
+                        cudaStream_t st);
 size_t mid_gather_smem(int P);
 int mid_spread_emax();
-int launch_mid_scale(cuDoubleComplex* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx,
-                     const double* Ty, const double* Tz, cudaStream_t st);
+int launch_mid_scale(void* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx, const double* Ty,
+                     const double* Tz, bool f32, cudaStream_t st);
 int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* psiT, d4* out, double gx, double gy,
                         cudaStream_t st);
 int long_pcmax(int Pc);
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
 bool long_small_ok(int Ilx, int Ily, int Pc);
 int long_small_pcp(int Pc);
-int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part,
-                            double* grid, cudaStream_t st);
-int launch_long_gather_bc(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st);
+int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, void* part, void* grid,
+                            bool f32, cudaStream_t st);
+int launch_long_gather_bc(const LongArgs& a, const int4* g0, const void* psi, d4* out, bool f32, cudaStream_t st);
+int launch_long_scale(const void* in, void* out, const double* K, int nmode, int Pc, bool f32, cudaStream_t st);
 int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const double* M, cudaStream_t st);
 // exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total); temp from scan_temp_bytes
 size_t scan_temp_bytes(int n);

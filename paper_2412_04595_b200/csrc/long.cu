@@ -90,60 +90,79 @@ bool long_small_ok(int Ilx, int Ily, int Pc) {
     return Ilx <= LG_RX && Ily <= 16 && pcp > 0 && Ilx * ((Ily + 3) / 4) * (pcp / LG_LT) <= 128;
 }
 
-template <int PCP>
-int spread_gemm_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part, double* grid,
+template <int PCP, typename T>
+int spread_gemm_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, T* part, T* grid,
                    cudaStream_t st) {
     const int nthr = ((a.Ilx * ((a.Ily + 3) / 4) * (PCP / LG_LT) + 31) / 32) * 32;
     if (nthr > 128) return 1;
     const int per = (a.N + nblk - 1) / nblk;
     const int RW = ((a.Ilx + ((a.Ily + 3) & ~3) + PCP) + 1) & ~1;
-    const size_t sh = sizeof(double) * 2 * LG_KB * RW;
-    if (cudaFuncSetAttribute(k_long_spread_gemm<PCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+    const size_t sh = sizeof(T) * 2 * LG_KB * RW;
+    if (cudaFuncSetAttribute(k_long_spread_gemm<PCP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
         cudaSuccess)
         return 2;
-    k_long_spread_gemm<PCP><<<nblk, 128, sh, st>>>(a, g0, gx, gy, per, part);
+    k_long_spread_gemm<PCP, T><<<nblk, 128, sh, st>>>(a, g0, gx, gy, per, part);
     const int G = a.Ilx * a.Ily;
-    k_long_sum<<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
+    k_long_sum<T><<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part,
-                            double* grid, cudaStream_t st) {
+template <typename T>
+int spread_gemm_t(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, T* part, T* grid,
+                  cudaStream_t st) {
     switch (long_small_pcp(a.Pc)) {
-        case 6: return spread_gemm_go<6>(a, g0, gx, gy, nblk, part, grid, st);
-        case 12: return spread_gemm_go<12>(a, g0, gx, gy, nblk, part, grid, st);
-        case 18: return spread_gemm_go<18>(a, g0, gx, gy, nblk, part, grid, st);
-        case 24: return spread_gemm_go<24>(a, g0, gx, gy, nblk, part, grid, st);
-        case 30: return spread_gemm_go<30>(a, g0, gx, gy, nblk, part, grid, st);
+        case 6: return spread_gemm_go<6, T>(a, g0, gx, gy, nblk, part, grid, st);
+        case 12: return spread_gemm_go<12, T>(a, g0, gx, gy, nblk, part, grid, st);
+        case 18: return spread_gemm_go<18, T>(a, g0, gx, gy, nblk, part, grid, st);
+        case 24: return spread_gemm_go<24, T>(a, g0, gx, gy, nblk, part, grid, st);
+        case 30: return spread_gemm_go<30, T>(a, g0, gx, gy, nblk, part, grid, st);
     }
     return 1;
 }
 
-template <int PCP, int NCY>
-int gather_bc_go(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
-    const size_t sh = sizeof(double) * ((size_t)a.Ilx * a.Ily * PCP + 2 * 128 * (size_t)a.Ilx + 2 * 128 * NCY);
-    auto k = k_long_gather_bc<PCP, NCY>;
+int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, void* part, void* grid,
+                            bool f32, cudaStream_t st) {
+    return f32 ? spread_gemm_t(a, g0, gx, gy, nblk, (float*)part, (float*)grid, st)
+               : spread_gemm_t(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st);
+}
+
+template <int PCP, int NCY, typename T>
+int gather_bc_go(const LongArgs& a, const int4* g0, const T* psi, d4* out, cudaStream_t st) {
+    const size_t sh = sizeof(T) * ((size_t)a.Ilx * a.Ily * PCP + 2 * 128 * (size_t)a.Ilx + 2 * 128 * NCY);
+    auto k = k_long_gather_bc<PCP, NCY, T>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess) return 2;
     k<<<(a.N + 127) / 128, 128, sh, st>>>(a, g0, psi, out);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-template <int NCY>
-int gather_bc_p(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
-    // even PCP for 128-bit loads: Pc rounded up to even
+template <int NCY, typename T>
+int gather_bc_p(const LongArgs& a, const int4* g0, const T* psi, d4* out, cudaStream_t st) {
+    // even PCP for 2-wide loads: Pc rounded up to even
     switch ((a.Pc + 1) & ~1) {
-#define C_(M_) case M_: return gather_bc_go<M_, NCY>(a, g0, psi, out, st);
+#define C_(M_) case M_: return gather_bc_go<M_, NCY, T>(a, g0, psi, out, st);
         C_(2) C_(4) C_(6) C_(8) C_(10) C_(12) C_(14) C_(16) C_(18) C_(20) C_(22) C_(24) C_(26) C_(28) C_(30)
 #undef C_
     }
     return 1;
 }
 
-int launch_long_gather_bc(const LongArgs& a, const int4* g0, const double* psi, d4* out, cudaStream_t st) {
-    if (a.Ily <= 8) return gather_bc_p<8>(a, g0, psi, out, st);
-    if (a.Ily <= 12) return gather_bc_p<12>(a, g0, psi, out, st);
-    if (a.Ily <= 16) return gather_bc_p<16>(a, g0, psi, out, st);
+template <typename T>
+int gather_bc_t(const LongArgs& a, const int4* g0, const T* psi, d4* out, cudaStream_t st) {
+    if (a.Ily <= 8) return gather_bc_p<8, T>(a, g0, psi, out, st);
+    if (a.Ily <= 12) return gather_bc_p<12, T>(a, g0, psi, out, st);
+    if (a.Ily <= 16) return gather_bc_p<16, T>(a, g0, psi, out, st);
     return 1;
+}
+
+int launch_long_gather_bc(const LongArgs& a, const int4* g0, const void* psi, d4* out, bool f32, cudaStream_t st) {
+    return f32 ? gather_bc_t(a, g0, (const float*)psi, out, st) : gather_bc_t(a, g0, (const double*)psi, out, st);
+}
+
+int launch_long_scale(const void* in, void* out, const double* K, int nmode, int Pc, bool f32, cudaStream_t st) {
+    const int nb = (nmode * Pc + 127) / 128;
+    if (f32) k_long_scale<cuComplex><<<nb, 128, 0, st>>>((const cuComplex*)in, (cuComplex*)out, K, nmode, Pc);
+    else k_long_scale<cuDoubleComplex><<<nb, 128, 0, st>>>((const cuDoubleComplex*)in, (cuDoubleComplex*)out, K, nmode, Pc);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
 int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const double* M, cudaStream_t st) {

@@ -24,40 +24,48 @@ int launch_mid_sort_place(const int* key, int N, int* cursor, int* tmp, const in
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-template <int P>
-int spread_go(const MidZArgs& a, int nseg, double* grid, cudaStream_t st) {
-    const size_t sh = SRec<P>::BYTES;
-    if (cudaFuncSetAttribute(k_mid_spread_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+template <int P, typename T>
+int spread_go(const MidZArgs& a, int nseg, T* grid, cudaStream_t st) {
+    const size_t sh = SRec<P, T>::BYTES;
+    if (cudaFuncSetAttribute(k_mid_spread_z<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
         return 2;
-    k_mid_spread_z<P><<<dim3(a.ntout * a.nty, nseg), SRec<P>::NTHR, sh, st>>>(a, grid);
+    k_mid_spread_z<P, T><<<dim3(a.ntout * a.nty, nseg), SRec<P, T>::NTHR, sh, st>>>(a, grid);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, double* grid, cudaStream_t st) {
+int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32, cudaStream_t st) {
     switch (P) {
-#define C_(P_) case P_: return spread_go<P_>(a, nseg, grid, st);
+#define C_(P_)                                                                                  \
+    case P_:                                                                                    \
+        return f32 ? spread_go<P_, float>(a, nseg, (float*)grid, st) : spread_go<P_, double>(a, nseg, (double*)grid, st);
         SOG_ODD_P(C_)
 #undef C_
         default: return 1;
     }
 }
 
-template <int P>
-int gather_go(const MidZArgs& a, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st) {
-    if constexpr (GRing<P>::FITS) {
-        const size_t sh = GRing<P>::BYTES;
-        if (cudaFuncSetAttribute(k_mid_gather_z<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+template <int P, typename T>
+int gather_go(const MidZArgs& a, int nseg, int nmid, const T* psi, d4* out, cudaStream_t st) {
+    if constexpr (GRing<P, T>::FITS) {
+        const size_t sh = GRing<P, T>::BYTES;
+        if (cudaFuncSetAttribute(k_mid_gather_z<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+            cudaSuccess)
             return 2;
-        k_mid_gather_z<P><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+        k_mid_gather_z<P, T><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
     } else {
-        k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
+        if constexpr (sizeof(T) == 4) return 1;   // fp32 mode: ring gather only
+        else k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const double* psi, d4* out, cudaStream_t st) {
+int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void* psi, d4* out, bool f32,
+                        cudaStream_t st) {
     switch (P) {
-#define C_(P_) case P_: return gather_go<P_>(a, nseg, nmid, psi, out, st);
+#define C_(P_)                                                                                             \
+    case P_:                                                                                               \
+        return f32 ? gather_go<P_, float>(a, nseg, nmid, (const float*)psi, out, st)                      \
+                   : gather_go<P_, double>(a, nseg, nmid, (const double*)psi, out, st);
         SOG_ODD_P(C_)
 #undef C_
         default: return 1;
@@ -75,17 +83,24 @@ size_t mid_gather_smem(int P) {
     }
 }
 
-int launch_mid_scale(cuDoubleComplex* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx,
-                     const double* Ty, const double* Tz, cudaStream_t st) {
+template <typename C>
+int mid_scale_go(C* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx, const double* Ty,
+                 const double* Tz, cudaStream_t st) {
     dim3 g((nyh + 127) / 128, (Izs * Ix + MS_ROWS - 1) / MS_ROWS);
-    if (L <= 8) k_mid_scale<8><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
-    else if (L <= 16) k_mid_scale<16><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
-    else if (L <= 24) k_mid_scale<24><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
-    else if (L <= 32) k_mid_scale<32><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
-    else if (L <= 48) k_mid_scale<48><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
-    else if (L <= 64) k_mid_scale<64><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    if (L <= 8) k_mid_scale<8, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 16) k_mid_scale<16, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 24) k_mid_scale<24, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 32) k_mid_scale<32, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 48) k_mid_scale<48, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
+    else if (L <= 64) k_mid_scale<64, C><<<g, 128, 0, st>>>(spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz);
     else return 1;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_mid_scale(void* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx, const double* Ty,
+                     const double* Tz, bool f32, cudaStream_t st) {
+    return f32 ? mid_scale_go((cuComplex*)spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz, st)
+               : mid_scale_go((cuDoubleComplex*)spec, Ix, Izs, nyh, L, A, Tx, Ty, Tz, st);
 }
 
 }  // namespace sog

@@ -133,6 +133,7 @@ struct sog_plan {
     double timings[11] = {};
     size_t bytes = 0;
     // ---- x-slab rank (R > 1); R == 1: the whole periodic box ----
+    bool f32 = false;                      // fp32 mode (S2-S12 in fp32; grids hold floats)
     int R = 1, rank = 0;
     int Ncap = 0, Ncur = 0, Nown = 0;      // particle capacity / current local / own counts
     double xs0 = 0, xs1 = 0, Hh = 0;       // slab [xs0, xs1) and particle halo width
@@ -328,10 +329,10 @@ int setup(sog_plan* pl) {
         if (!slab) {
             long long n[3] = {p.Izs, p.Ix, p.Iy};   // z slowest, y fastest (half axis)
             CKF(cufftCreate(&pl->mfwd));
-            CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &ws));
+            CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, pl->f32 ? CUFFT_R2C : CUFFT_D2Z, 1, &ws));
             pl->bytes += ws;
             CKF(cufftCreate(&pl->minv));
-            CKF(cufftMakePlanMany64(pl->minv, 3, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1, &ws));
+            CKF(cufftMakePlanMany64(pl->minv, 3, n, nullptr, 1, 0, nullptr, 1, 0, pl->f32 ? CUFFT_C2R : CUFFT_Z2D, 1, &ws));
             pl->bytes += ws;
         } else {
             // distributed FFT: 2D (z, y) per interior x plane, all-to-all to ky chunks, 1D along x
@@ -400,11 +401,11 @@ int setup(sog_plan* pl) {
         size_t ws = 0;
         CKF(cufftCreate(&pl->lfwd));
         CKF(cufftMakePlanMany64(pl->lfwd, 2, n, nullptr, 1, (long long)p.Ilx * p.Ily, nullptr, 1,
-                                (long long)p.Ilx * (p.Ily / 2 + 1), CUFFT_D2Z, p.Pc, &ws));
+                                (long long)p.Ilx * (p.Ily / 2 + 1), pl->f32 ? CUFFT_R2C : CUFFT_D2Z, p.Pc, &ws));
         pl->bytes += ws;
         CKF(cufftCreate(&pl->linv));
         CKF(cufftMakePlanMany64(pl->linv, 2, n, nullptr, 1, (long long)p.Ilx * (p.Ily / 2 + 1), nullptr, 1,
-                                (long long)p.Ilx * p.Ily, CUFFT_Z2D, p.Pc, &ws));
+                                (long long)p.Ilx * p.Ily, pl->f32 ? CUFFT_C2R : CUFFT_Z2D, p.Pc, &ws));
         pl->bytes += ws;
     }
     pl->scan_bytes = std::max(scan_temp_bytes(pl->ncell), pl->nkeys ? scan_temp_bytes(pl->nkeys) : size_t(0));
@@ -524,7 +525,18 @@ int st_near(sog_plan* pl) {
     if (N == 0) return SOG_OK;
     const int D = pl->near.D;
     if (D != NEAR_D) return fail(SOG_EINVAL, "near table degree");
-    if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && N < (1 << 27)) {   // k_near3: warp per target
+    if (pl->f32 && pl->geo.ncx >= 3 && pl->geo.ncy >= 3) {   // fp32 mode: cell-relative fp32 (k_near3f)
+        // (boxes with < 3 cells per periodic axis use the generic fp64 kernel below)
+        Near3Args a;
+        a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
+        a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+        a.g = pl->geo;
+        a.cap = 2048;
+        size_t sh = sizeof(float) * ((pl->near.K * (D + 1) + 3) & ~3) + NEAR3_WARPS * 160 * sizeof(int) +
+                    sizeof(float4) * a.cap;
+        CK(cudaFuncSetAttribute(k_near3f<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_near3f<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+    } else if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && N < (1 << 27)) {   // k_near3: warp per target
         Near3Args a;
         a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
         a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
@@ -552,14 +564,14 @@ int st_near(sog_plan* pl) {
 }
 
 int st_mid_spread(sog_plan* pl) {
-    return lchk(launch_mid_spread_z(pl->mz, pl->p.P, pl->nseg_s, pl->mgrid, pl->stream));
+    return lchk(launch_mid_spread_z(pl->mz, pl->p.P, pl->nseg_s, pl->mgrid, pl->f32, pl->stream));
 }
 
 int st_mid_gather(sog_plan* pl) {
     MidZArgs g = pl->mz;
     g.cps = pl->mz_cps_g;
     if (pl->R > 1) { g.tlo -= 1; g.ntout += 1; }   // own particles near the left edge start in the halo tile
-    return lchk(launch_mid_gather_z(g, pl->p.P, pl->nseg_g, pl->Ncur, pl->mpsi, pl->o_mid, pl->stream));
+    return lchk(launch_mid_gather_z(g, pl->p.P, pl->nseg_g, pl->Ncur, pl->mpsi, pl->o_mid, pl->f32, pl->stream));
 }
 
 // S8 (own particles only in an x-slab: the halo particles belong to the neighbours)
@@ -574,9 +586,10 @@ int st_long_spread(sog_plan* pl) {
     }
     if (pl->long_small) {
         if ((rc = lchk(launch_long_spread_gemm(la, pl->g0, pl->lt.gamma_x, pl->lt.gamma_y, pl->lg_nblk, pl->lpart2,
-                                               pl->lgrid, st))))
+                                               pl->lgrid, pl->f32, st))))
             return rc;
     } else {
+        if (pl->f32) return fail(SOG_EINVAL, "fp32 mode needs a small long grid (register-tiled path)");
         LongTileArgs t = pl->lt;
         t.a = la;
         t.start = pl->start;
@@ -590,18 +603,26 @@ int st_long_spread(sog_plan* pl) {
 int st_long_solve(sog_plan* pl) {
     const Params& p = pl->p;
     cudaStream_t st = pl->stream;
-    CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
-    int nmode = p.Ilx * (p.Ily / 2 + 1);
-    k_long_scale<<<(nmode * p.Pc + 127) / 128, 128, 0, st>>>(pl->lspec, pl->lspec2, pl->d_K, nmode, p.Pc);
-    CK(cudaGetLastError());
-    CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
+    int rc;
+    const int nmode = p.Ilx * (p.Ily / 2 + 1);
+    if (pl->f32) {
+        CKF(cufftExecR2C(pl->lfwd, (float*)pl->lgrid, (cufftComplex*)pl->lspec));
+        if ((rc = lchk(launch_long_scale(pl->lspec, pl->lspec2, pl->d_K, nmode, p.Pc, true, st)))) return rc;
+        CKF(cufftExecC2R(pl->linv, (cufftComplex*)pl->lspec2, (float*)pl->lgrid));
+    } else {
+        CKF(cufftExecD2Z(pl->lfwd, pl->lgrid, pl->lspec));
+        if ((rc = lchk(launch_long_scale(pl->lspec, pl->lspec2, pl->d_K, nmode, p.Pc, false, st)))) return rc;
+        CKF(cufftExecZ2D(pl->linv, pl->lspec2, pl->lgrid));
+    }
     return SOG_OK;
 }
 
 // S12
 int st_long_gather(sog_plan* pl) {
     const Params& p = pl->p;
-    if (pl->long_small) return lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, pl->stream));
+    if (pl->long_small)
+        return lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, pl->f32, pl->stream));
+    if (pl->f32) return fail(SOG_EINVAL, "fp32 mode needs a small long grid (register-tiled path)");
     return lchk(launch_long_gather2(long_args(pl), p.Pl, pl->lgrid, pl->lpsiT, pl->o_long, pl->lt.gamma_x,
                                     pl->lt.gamma_y, pl->stream));
 }
@@ -622,13 +643,15 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         if ((rc = st_mid_spread(pl))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
-        CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
+        if (pl->f32) CKF(cufftExecR2C(pl->mfwd, (float*)pl->mgrid, (cufftComplex*)pl->mspec));
+        else CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
         mark(pl, 4);
         if ((rc = lchk(launch_mid_scale(pl->mspec, p.Ix, p.Izs, p.Iy / 2 + 1, p.m + 1, pl->d_A, pl->d_Tx, pl->d_Ty,
-                                        pl->d_Tz, st))))
+                                        pl->d_Tz, pl->f32, st))))
             return rc;
         mark(pl, 5);
-        CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mpsi));
+        if (pl->f32) CKF(cufftExecC2R(pl->minv, (cufftComplex*)pl->mspec, (float*)pl->mpsi));
+        else CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mpsi));
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
         if ((rc = st_mid_gather(pl))) return rc;
@@ -693,6 +716,8 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
         return fail(SOG_EINVAL, "box lengths must be positive and finite");
     if (!(tol >= 2e-14 && tol <= 1e-1)) return fail(SOG_EINFEASIBLE, "tol outside [2e-14, 1e-1]");
     p.N = N; p.Lx = Lx; p.Ly = Ly; p.Lz = Lz; p.tol = tol;
+    if (o && o->precision != 0 && o->precision != 1) return fail(SOG_EINVAL, "precision must be 0 (fp64) or 1 (fp32)");
+    if (o && o->precision == 1 && tol < 1e-5) return fail(SOG_EINFEASIBLE, "fp32 mode supports tol >= 1e-5");
     std::string err;
     if (o && o->explicit_params) {
         static const double tb[6][3] = {{2.0, 1.9892536839080267, 0.9944464927622323},
@@ -735,6 +760,7 @@ sog_plan* sog_plan_create_ex(int64_t N, double Lx, double Ly, double Lz, double 
     sog_plan* pl = new sog_plan();
     if (make_params(pl->p, pl->knobs, N, Lx, Ly, Lz, tol, o) != SOG_OK) { delete pl; return nullptr; }
     if (o) pl->flags = o->flags;
+    pl->f32 = o && o->precision == 1;
     int rc = setup(pl);
     if (rc == SOG_OK) rc = set_stream(pl, o ? (cudaStream_t)o->cuda_stream : nullptr);
     if (rc != SOG_OK) { std::string keep = g_err; free_plan(pl); g_err = keep; return nullptr; }
@@ -792,6 +818,7 @@ int sog_eval_components(sog_plan* pl, const double* xyz, const double* q, double
 
 int sog_debug_stage(sog_plan* pl, int stage, const double* xyz, const double* q, double* out, size_t len) {
     if (!pl || !xyz || !q || !out) return fail(SOG_EINVAL, "null argument");
+    if (pl->f32) return fail(SOG_EINVAL, "debug stages are available in fp64 mode only");
     const Params& p = pl->p;
     size_t need;
     const double* src;
@@ -1219,6 +1246,7 @@ int sog_nccl_unique_id(void* id128) {
 static sog_dist* dist_create(int64_t N_total, int64_t nown_max, double Lx, double Ly, double Lz, double tol,
                              const sog_plan_opts* o, int R, int first, int count, bool loopback, const void* id128) {
     if (R < 2 || nown_max < 1) { fail(SOG_EINVAL, "x-slab needs >= 2 ranks and a positive capacity"); return nullptr; }
+    if (o && o->precision == 1) { fail(SOG_EINVAL, "x-slab ranks run in fp64"); return nullptr; }
     sog_dist* d = new sog_dist();
     d->R = R;
     d->loopback = loopback;

@@ -33,7 +33,8 @@ class Opts(ctypes.Structure):
                 ("Ix", ctypes.c_int), ("Iy", ctypes.c_int), ("Iz", ctypes.c_int), ("Izs", ctypes.c_int),
                 ("P", ctypes.c_int), ("S", ctypes.c_double),
                 ("Ilx", ctypes.c_int), ("Ily", ctypes.c_int), ("Pl", ctypes.c_int), ("Sl", ctypes.c_double),
-                ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint)]
+                ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint),
+                ("precision", ctypes.c_int)]
 
 
 def lib_path() -> str:
@@ -113,7 +114,7 @@ class Plan:
     """
 
     def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
-                 validate=True, timing=False):
+                 validate=True, timing=False, precision="fp64"):
         self.lib = load_library()
         self.N = int(N)
         self.L = tuple(float(v) for v in L)
@@ -127,6 +128,7 @@ class Plan:
                 setattr(o, k, type(getattr(o, k))(params[k]))
         o.flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
         o.cuda_stream = _stream_handle(stream)
+        o.precision = {"fp64": 0, "fp32": 1}[precision]
         h = self.lib.sog_plan_create_ex(self.N, *self.L, self.tol, ctypes.byref(o))
         if not h:
             raise SogError(-1, self.lib.sog_last_error().decode())

@@ -267,3 +267,29 @@ def test_full_size_c5_properties():
     p4, _ = pl.eval(xd, 2.0 * qd)
     assert rel(p4.cpu().numpy(), 2.0 * phi0) <= 1e-14
     assert np.linalg.norm(F0.sum(0)) <= 1e-6 * np.abs(F0).max() * math.sqrt(len(q))
+
+
+TOL_FP32 = 1e-5      # north_star: <= 1e-5 relative L2 vs the fp64 oracle in fp32 mode
+
+
+@pytest.mark.parametrize("name,N", [("c4", 4000), ("c1", 1000), ("c5", 20000), ("c2", 3000)])
+def test_fp32_mode_vs_fp64_oracle(name, N):
+    """fp32 mode (BASELINE config c4 at its fp32 tolerance 1e-4): S2-S12 in fp32, same plan as
+    the fp64 oracle; relative L2 of phi and F <= 1e-5."""
+    xyz, q, L = config_system(name, N=N)
+    op = make_plan(len(q), *L, 1e-4)
+    pl = gpu_plan(op, precision="fp32")
+    x, qq = to_dev(xyz, q)
+    phi, F = pl.eval(x, qq)
+    torch.cuda.synchronize()
+    phi_o, F_o = O.evaluate(op, xyz, q)
+    e_phi, e_F = rel(phi.cpu().numpy(), phi_o), rel(F.cpu().numpy(), F_o)
+    pl.close()
+    assert e_phi <= TOL_FP32 and e_F <= TOL_FP32, (e_phi, e_F)
+    assert e_phi > 1e-12, "fp32 mode must actually compute in fp32"
+
+
+def test_fp32_mode_rejects_tight_tolerance():
+    from paper_2412_04595_b200 import Plan, SogError
+    with pytest.raises(SogError):
+        Plan(1000, (10.0, 10.0, 10.0), 1e-8, precision="fp32")
