@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eta", type=float, default=None, help="override rule R4's eta (plan knob)")
+    ap.add_argument("--rc-factor", type=float, default=None, help="override rule R2's r_c factor (plan knob)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
     ap.add_argument("--parallelism", default="xslab", choices=["xslab", "replicas"],
@@ -330,7 +332,8 @@ def main():
     xyz, q, L = config_system(args.config, seed_offset=rank)
     N = len(q)
     stream = torch.cuda.current_stream()
-    plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision)
+    plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision, eta=args.eta,
+                rc_factor=args.rc_factor)
     xd = torch.from_numpy(xyz).cuda()
     qd = torch.from_numpy(q).cuda()
     phi = torch.empty(N, dtype=torch.float64, device="cuda")

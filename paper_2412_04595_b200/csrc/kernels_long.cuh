@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
 constexpr int LG_KB = 64, LG_LT = 6, LG_RX = 32, LG_RY = 32;
 
 template <int PCP, typename T = double>
-__global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
+__global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const int4* __restrict__ g0, double gamma_x,
                                                              double gamma_y, int per, T* __restrict__ part) {
     constexpr int NLG = PCP / LG_LT;
     // double-buffered rows: [2][LG_KB][RXP + RYP + PCP], RXP = Ilx, RYP = Ily rounded up to 4
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(128, 4) k_long_spread_gemm(LongArgs a, const i
     // two threads per staged particle: role 0 -> Rx row and T row, role 1 -> Ry row
     auto stage = [&](int base, int buf) {
         const int t = tid >> 1, role = tid & 1;
-        if (t >= LG_KB) return;
+        if (t >= LG_KB) return;   // blockDim >= 2 * LG_KB = 128
         T* row = sm + ((size_t)buf * LG_KB + t) * RW;
         T* rx = row;
         T* ry = row + RXP;

@@ -87,21 +87,22 @@ int long_small_pcp(int Pc) { return Pc <= 30 ? ((Pc + LG_LT - 1) / LG_LT) * LG_L
 
 bool long_small_ok(int Ilx, int Ily, int Pc) {
     const int pcp = long_small_pcp(Pc);
-    return Ilx <= LG_RX && Ily <= 16 && pcp > 0 && Ilx * ((Ily + 3) / 4) * (pcp / LG_LT) <= 128;
+    return Ilx <= LG_RX && Ily <= 16 && pcp > 0 && Ilx * ((Ily + 3) / 4) * (pcp / LG_LT) <= 256;
 }
 
 template <int PCP, typename T>
 int spread_gemm_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, T* part, T* grid,
                    cudaStream_t st) {
-    const int nthr = ((a.Ilx * ((a.Ily + 3) / 4) * (PCP / LG_LT) + 31) / 32) * 32;
-    if (nthr > 128) return 1;
+    int nthr = ((a.Ilx * ((a.Ily + 3) / 4) * (PCP / LG_LT) + 31) / 32) * 32;
+    if (nthr > 256) return 1;
+    nthr = nthr <= 128 ? 128 : 256;
     const int per = (a.N + nblk - 1) / nblk;
     const int RW = ((a.Ilx + ((a.Ily + 3) & ~3) + PCP) + 1) & ~1;
     const size_t sh = sizeof(T) * 2 * LG_KB * RW;
     if (cudaFuncSetAttribute(k_long_spread_gemm<PCP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
         cudaSuccess)
         return 2;
-    k_long_spread_gemm<PCP, T><<<nblk, 128, sh, st>>>(a, g0, gx, gy, per, part);
+    k_long_spread_gemm<PCP, T><<<nblk, nthr, sh, st>>>(a, g0, gx, gy, per, part);
     const int G = a.Ilx * a.Ily;
     k_long_sum<T><<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
