@@ -414,27 +414,46 @@ template <int P, typename T = double>
 struct GRing {
     static constexpr int WX = MZ_TX + P - 1, WY = MZ_TY + P - 1;
     static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
-    static constexpr int PL = WX * WYP;                           // plane size (doubles)
-    static constexpr int D = MZ_ZC + P - 1;                       // planes in the ring
-    static constexpr int AL = 16 / int(sizeof(T)), HOFF = ((6 * P + AL - 1) / AL) * AL;
+    static constexpr int PL = WX * WYP;                           // plane size (elements)
+    static constexpr int D = MZ_ZC + P - 1;                       // planes a chunk reads
+    static constexpr int DR = D + MZ_ZC;                          // ring: + the next chunk's planes (prefetch)
+    static constexpr int AL = 16 / int(sizeof(T));
+    static constexpr int HOFF = ((3 * P + 3 + AL - 1) / AL) * AL; // [Wx Wy Wz | d0x d0y d0z] then hdr
     static constexpr int WSZ = HOFF + AL;                         // per-particle weight scratch
-    static constexpr int WB = 6;                                  // particles per warp batch (<= 10)
+    static constexpr int WB = 4;                                  // particles per warp batch
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
-    static constexpr size_t BYTES = sizeof(T) * (size_t(D) * PL + 8 * WB * WSZ);
+    static constexpr size_t BYTES = sizeof(T) * (size_t(DR) * PL + 8 * WB * WSZ);
     static constexpr bool FITS = BYTES <= 227 * 1024;
-    static constexpr int MINB = BYTES <= 113 * 1024 ? 2 : 1;     // CTAs per SM
+    static constexpr int MINB = BYTES <= 112 * 1024 ? 2 : 1;     // CTAs per SM
 };
 
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// S7: a CTA owns the particles whose stencil starts lie in its MZ_TX x MZ_TY tile and one z
+// segment.  A ring of DR Psi planes of the tile window (MZ_TX + P - 1) x (MZ_TY + P - 1) lives in
+// shared memory; while a chunk's particles are gathered, the MZ_ZC planes of the next chunk are
+// already on their way (cp.async), so plane loads overlap the gather.  A warp computes the
+// separable weights of WB particles at once (lane = particle x axis, Gaussian recurrence) and
+// gathers them one at a time, lanes over the P x P columns (z contracted per lane, W' from the
+// stored W), 4-value butterfly reduction.
 template <int P, typename T = double>
 __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArgs a, const T* __restrict__ psi,
-                                                         d4* __restrict__ out) {
+                                                                          d4* __restrict__ out) {
     using G = GRing<P, T>;
-    constexpr int D = G::D, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
+    constexpr int DR = G::DR, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
     extern __shared__ __align__(16) unsigned char smraw[];
     T* sm = reinterpret_cast<T*>(smraw);
-    T* ring = sm;                                   // [D][WX][WYP]
+    T* ring = sm;                                        // [DR][WX][WYP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    T* wsb = sm + D * PL + warp * G::WB * G::WSZ;   // per particle: Wx dWx Wy dWy Wz dWz, hdr
+    T* wsb = sm + DR * PL + warp * G::WB * G::WSZ;
     const int tx = a.tlo + blockIdx.x / a.nty, ty = blockIdx.x % a.nty;
     const int tile = tx * a.nty + ty;
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
@@ -449,48 +468,53 @@ __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArg
         cbb[r] = idx < P * P ? idx - ca[r] * P : 0;
         coff[r] = ca[r] * WYP + cbb[r];
     }
-    int zl = 0, zh = 0;                                  // planes [zl, zh) resident
+    // issue async copies of planes [p0, p1) of the window into their ring slots
+    auto load_planes = [&](int p0, int p1) {
+        constexpr int NPL = WX * WY;
+        const int nload = (p1 - p0) * NPL;
+        for (int e = tid; e < nload; e += 256) {
+            const int pz = e / NPL, rem = e - pz * NPL;
+            const int xr = rem / WY, yr = rem - xr * WY;
+            const int plane = p0 + pz;
+            const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr, gy = wrapc(Y0 + yr, a.Iy);
+            T* dst = ring + (plane % DR) * PL + xr * WYP + yr;
+            if (gx < a.Ixk) {
+                const T* srcp = psi + ((size_t)plane * a.Ixk + gx) * a.Iy + gy;
+                if (sizeof(T) == 8) cp_async8(dst, srcp); else cp_async4(dst, srcp);
+            } else {
+                *dst = T(0);
+            }
+        }
+    };
+    int zh = 0, zl = 0;                                  // planes [zl, zh) resident or in flight
     for (int c = cb; c < ce; ++c) {
         const int key = tile * a.nzc + c;
         const int k0 = a.mstart[key], k1 = a.mstart[key + 1];
         if (k0 == k1) continue;
-        const int nlo = c * MZ_ZC, nhi = min(c * MZ_ZC + D, a.Izs);
-        const int from = (zh > nlo && zl <= nlo) ? zh : nlo;
+        const int nlo = c * MZ_ZC, nhi = min(c * MZ_ZC + G::D, a.Izs);
         __syncthreads();                                 // previous chunk's readers are done
-        {
-            constexpr int NPL = WX * WY;
-            const int nload = (nhi - from) * NPL;
-            for (int e0 = tid; e0 < nload; e0 += 4 * 256) {
-                T v[4];
-                int dst[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * 256;
-                    dst[u] = -1;
-                    if (e < nload) {
-                        const int pz = e / NPL, rem = e - pz * NPL;
-                        const int xr = rem / WY, yr = rem - xr * WY;
-                        const int plane = from + pz;
-                        const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr, gy = wrapc(Y0 + yr, a.Iy);
-                        v[u] = gx < a.Ixk ? __ldg(&psi[((size_t)plane * a.Ixk + gx) * a.Iy + gy]) : T(0);
-                        dst[u] = (plane % D) * PL + xr * WYP + yr;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (dst[u] >= 0) ring[dst[u]] = v[u];
-            }
+        if (!(zl <= nlo && zh >= nhi)) {                 // not prefetched (first chunk or a jump)
+            const int from = (zl <= nlo && zh > nlo) ? zh : nlo;
+            load_planes(from, nhi);
+            zl = nlo;
+            zh = nhi;
         }
-        zl = nlo;
-        zh = nhi;
+        cp_async_wait_all();
         __syncthreads();
-        for (int kb = k0 + G::WB * warp; kb < k1; kb += G::WB * 8) {
-            const int nb = min(G::WB, k1 - kb);
+        // prefetch the next chunk's new planes into the slots of planes < nlo (no longer read)
+        {
+            const int p1 = min(nhi + MZ_ZC, a.Izs);
+            if (p1 > zh) { load_planes(zh, p1); zh = p1; }
+            zl = max(zl, zh - DR);
+        }
+        // particles of the chunk dealt round-robin over the 8 warps (k0 + warp + 8 i), WB at a time
+        for (int kb = k0 + warp; kb < k1; kb += G::WB * 8) {
+            const int nb = min(G::WB, (k1 - kb + 7) / 8);
             // weights of WB particles at once: lane = (particle lane/3, axis lane%3), recurrence
             if (lane < 3 * nb) {
                 const int pp = lane / 3, axl = lane - 3 * pp;
-                const int4 in = a.minfo[kb + pp];
-                const d4 r = ld_d4(&a.mpos[kb + pp]);
+                const int4 in = a.minfo[kb + 8 * pp];
+                const d4 r = ld_d4(&a.mpos[kb + 8 * pp]);
                 const double hh = axl == 0 ? a.hx : (axl == 1 ? a.hy : a.hz);
                 const double hf = axl == 0 ? a.halfx : (axl == 1 ? a.halfy : a.halfz);
                 const double aa = axl == 0 ? a.invH2Sx : (axl == 1 ? a.invH2Sy : a.invH2Sz);
@@ -500,77 +524,82 @@ __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArg
                 const double d0 = ((double)sa - hf) * hh - x;
                 double w = exp(-aa * d0 * d0);
                 double q = exp(-aa * hh * (2.0 * d0 + hh));
-                T* o = wsb + pp * G::WSZ + 2 * axl * P;
+                T* o = wsb + pp * G::WSZ + axl * P;
 #pragma unroll
                 for (int i = 0; i < P; ++i) {
                     o[i] = T(w);
-                    o[P + i] = T(2.0 * aa * (d0 + i * hh) * w);
                     w *= q;
                     q *= gg;
                 }
+                wsb[pp * G::WSZ + 3 * P + axl] = T(d0);       // for W' = 2 a (d0 + i h) W
                 if (axl == 0) {
                     int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + G::HOFF);
                     hd[0] = a.px ? in.y - X0 + (in.y < 0 ? a.Ix : 0) : in.y - a.xorig - X0;   // relative to the tile
                     hd[1] = in.z - Y0 + (in.z < 0 ? a.Iy : 0);
-                    hd[2] = in.w % D;                                    // ring slot of the first plane
+                    hd[2] = in.w % DR;                                   // ring slot of the first plane
                     hd[3] = in.x;                                        // output (cell-sorted) index
                 }
             }
             __syncwarp();
+            const T ax2 = T(2.0 * a.invH2Sx), ay2 = T(2.0 * a.invH2Sy), az2 = T(2.0 * a.invH2Sz);
+            const T hxT = T(a.hx), hyT = T(a.hy), hzT = T(a.hz);
             for (int pp = 0; pp < nb; ++pp) {
-            const T* wsc = wsb + pp * G::WSZ;
-            const int4 hd = *reinterpret_cast<const int4*>(wsc + G::HOFF);
-            T wz[P], dwz[P];
+                const T* wsc = wsb + pp * G::WSZ;
+                const int4 hd = *reinterpret_cast<const int4*>(wsc + G::HOFF);
+                const T d0x = wsc[3 * P], d0y = wsc[3 * P + 1], d0z = wsc[3 * P + 2];
+                T wz[P], dwz[P];
 #pragma unroll
-            for (int i = 0; i < P; ++i) { wz[i] = wsc[4 * P + i]; dwz[i] = wsc[5 * P + i]; }
-            int pb[P];                                   // ring plane offsets of the P stencil planes
-            {
-                int zs = hd.z;
-#pragma unroll
-                for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == D ? 0 : zs + 1; }
-            }
-            const T* base = ring + hd.x * WYP + hd.y;
-            T phi = 0, gx = 0, gy = 0, gz = 0;
-#pragma unroll
-            for (int rr = 0; rr < NR; ++rr) {
-                if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
-                const T* col = base + coff[rr];
-                T t0 = 0, t1 = 0;
-#pragma unroll
-                for (int kz = 0; kz < P; ++kz) {
-                    const T v = col[pb[kz]];
-                    t0 = fma(wz[kz], v, t0);
-                    t1 = fma(dwz[kz], v, t1);
+                for (int i = 0; i < P; ++i) {
+                    wz[i] = wsc[2 * P + i];
+                    dwz[i] = az2 * (d0z + T(i) * hzT) * wz[i];
                 }
-                const T wx = wsc[ca[rr]], dwx = wsc[P + ca[rr]];
-                const T wy = wsc[2 * P + cbb[rr]], dwy = wsc[3 * P + cbb[rr]];
-                const T wxy = wx * wy;
-                phi = fma(wxy, t0, phi);
-                gz = fma(wxy, t1, gz);
-                gx = fma(dwx * wy, t0, gx);
-                gy = fma(wx * dwy, t0, gy);
-            }
-            // 4-value butterfly: after the first two levels each lane carries one value
-            {
+                int pb[P];                               // ring plane offsets of the P stencil planes
+                {
+                    int zs = hd.z;
+#pragma unroll
+                    for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == DR ? 0 : zs + 1; }
+                }
+                const T* base = ring + hd.x * WYP + hd.y;
+                T phi = 0, gx = 0, gy = 0, gz = 0;
+#pragma unroll
+                for (int rr = 0; rr < NR; ++rr) {
+                    if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                    const T* col = base + coff[rr];
+                    T t0 = 0, t1 = 0;
+#pragma unroll
+                    for (int kz = 0; kz < P; ++kz) {
+                        const T v = col[pb[kz]];
+                        t0 = fma(wz[kz], v, t0);
+                        t1 = fma(dwz[kz], v, t1);
+                    }
+                    const T wx = wsc[ca[rr]], wy = wsc[P + cbb[rr]];
+                    const T dwx = ax2 * (d0x + T(ca[rr]) * hxT) * wx;
+                    const T dwy = ay2 * (d0y + T(cbb[rr]) * hyT) * wy;
+                    const T wxy = wx * wy;
+                    phi = fma(wxy, t0, phi);
+                    gz = fma(wxy, t1, gz);
+                    gx = fma(dwx * wy, t0, gx);
+                    gy = fma(wx * dwy, t0, gy);
+                }
+                // 4-value butterfly (fp64): after two levels each lane carries one value
                 const bool b1 = lane & 1;
-                double s0 = b1 ? phi : gx, s1 = b1 ? gy : gz;  // reduction in fp64     // sent
-                double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;   // kept
-                k0v += __shfl_xor_sync(0xffffffffu, s0, 1);
-                k1v += __shfl_xor_sync(0xffffffffu, s1, 1);
+                const double vphi = phi, vgx = gx, vgy = gy, vgz = gz;
+                double k0v = b1 ? vgx : vphi, k1v = b1 ? vgz : vgy;
+                k0v += __shfl_xor_sync(0xffffffffu, b1 ? vphi : vgx, 1);
+                k1v += __shfl_xor_sync(0xffffffffu, b1 ? vgy : vgz, 1);
                 const bool b2 = lane & 2;
-                double s = b2 ? k0v : k1v, kk = b2 ? k1v : k0v;
-                kk += __shfl_xor_sync(0xffffffffu, s, 2);
+                double kk = b2 ? k1v : k0v;
+                kk += __shfl_xor_sync(0xffffffffu, b2 ? k0v : k1v, 2);
 #pragma unroll
                 for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
                 // lane&3: 0 -> phi, 1 -> gx, 2 -> gy, 3 -> gz (one 32-byte sector)
                 if (lane < 4) reinterpret_cast<double*>(&out[hd.w])[lane] = a.Vh * kk;
             }
-            }
             __syncwarp();
         }
     }
+    cp_async_wait_all();                                 // no copy may outlive the CTA
 }
-
 
 // S7 gather for wide windows whose plane ring does not fit in shared memory: same work split
 // (warp per particle, lanes over stencil columns) reading Psi through L1.
