@@ -702,3 +702,96 @@ __global__ void __launch_bounds__(128) k_mid_scale(C* __restrict__ spec, int Ix,
 }
 
 }  // namespace sog
+
+namespace sog {
+
+// ---------------------------------------------------------------------------------------
+// z-pruned mid FFT (whole box).  S is zero outside the planes the spread writes, and the
+// gather reads Psi only on the planes the particles' stencils reach, so:
+//   2D D2Z over the nonzero planes  X[z][m], m = x * nyh + ky        (cuFFT, batched)
+//   transpose into zero-padded pencils Y[m][Izs] (z contiguous)       (k_tr_xz)
+//   1D Z2Z along z, S5 scaling on [m][kz], inverse 1D Z2Z               (cuFFT + k_scale_pencil_z)
+//   transpose the gather's planes back X'[z][m], 2D Z2D into Psi       (k_tr_zx, cuFFT)
+// The normalisation is unchanged (cuFFT 2D x 1D unnormalised = 3D).
+constexpr int TR_T = 32;
+
+// X [nz][M] (complex) -> Y [M][Izs] rows, columns z0 .. z0 + nz
+template <typename C>
+__global__ void __launch_bounds__(TR_T * 8) k_tr_xz(const C* __restrict__ X, C* __restrict__ Y, int nz, long long M,
+                                                     int Izs, int z0) {
+    __shared__ C tile[TR_T][TR_T + 1];
+    const long long m0 = (long long)blockIdx.x * TR_T;
+    const int zb = blockIdx.y * TR_T;
+    const int tx = threadIdx.x & (TR_T - 1), ty = threadIdx.x / TR_T;   // 32 x 8 threads
+    for (int r = ty; r < TR_T; r += 8) {
+        const int z = zb + r;
+        const long long m = m0 + tx;
+        if (z < nz && m < M) tile[r][tx] = X[(size_t)z * M + m];
+    }
+    __syncthreads();
+    for (int r = ty; r < TR_T; r += 8) {
+        const long long m = m0 + r;
+        const int z = zb + tx;
+        if (z < nz && m < M) Y[(size_t)m * Izs + z0 + z] = tile[tx][r];
+    }
+}
+
+// Y [M][Izs] columns z0 .. z0 + nz -> X [nz][M]
+template <typename C>
+__global__ void __launch_bounds__(TR_T * 8) k_tr_zx(const C* __restrict__ Y, C* __restrict__ X, int nz, long long M,
+                                                     int Izs, int z0) {
+    __shared__ C tile[TR_T][TR_T + 1];
+    const long long m0 = (long long)blockIdx.x * TR_T;
+    const int zb = blockIdx.y * TR_T;
+    const int tx = threadIdx.x & (TR_T - 1), ty = threadIdx.x / TR_T;
+    for (int r = ty; r < TR_T; r += 8) {
+        const long long m = m0 + r;
+        const int z = zb + tx;
+        if (z < nz && m < M) tile[r][tx] = Y[(size_t)m * Izs + z0 + z];
+    }
+    __syncthreads();
+    for (int r = ty; r < TR_T; r += 8) {
+        const int z = zb + r;
+        const long long m = m0 + tx;
+        if (z < nz && m < M) X[(size_t)z * M + m] = tile[tx][r];
+    }
+}
+
+// S5 on z pencils W [m = x * nyh + ky][Izs]: a CTA owns MS_ROWS pencils (per-pencil factors
+// A_l Tx Ty in shared memory), each thread keeps Tz[l][z] of its z in registers.
+template <int LM, typename C>
+__global__ void __launch_bounds__(128) k_scale_pencil_z(C* __restrict__ W, int Ix, int nyh, int Izs, int L,
+                                                        const double* __restrict__ A, const double* __restrict__ Tx,
+                                                        const double* __restrict__ Ty, const double* __restrict__ Tz) {
+    __shared__ double sc[MS_ROWS][LM];
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long M = (long long)Ix * nyh;
+    const long long row0 = (long long)blockIdx.y * MS_ROWS;
+    for (int e = threadIdx.x; e < MS_ROWS * LM; e += blockDim.x) {
+        const int r = e / LM, l = e - r * LM;
+        const long long m = row0 + r;
+        double v = 0.0;
+        if (m < M && l < L) {
+            const int x = int(m / nyh), ky = int(m - (long long)x * nyh);
+            v = A[l] * Tx[(size_t)l * Ix + x] * Ty[(size_t)l * nyh + ky];
+        }
+        sc[r][l] = v;
+    }
+    __syncthreads();
+    if (z >= Izs) return;
+    double tz[LM];
+#pragma unroll
+    for (int l = 0; l < LM; ++l) tz[l] = l < L ? Tz[(size_t)l * Izs + z] : 0.0;
+    for (int r = 0; r < MS_ROWS && row0 + r < M; ++r) {
+        double m = 0.0;
+#pragma unroll
+        for (int l = 0; l < LM; ++l) m = fma(sc[r][l], tz[l], m);
+        const size_t idx = (size_t)(row0 + r) * Izs + z;
+        C v = W[idx];
+        v.x *= m;
+        v.y *= m;
+        W[idx] = v;
+    }
+}
+
+}  // namespace sog

@@ -21,6 +21,10 @@ int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32
 int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void* psi, d4* out, bool f32,
                         cudaStream_t st);
 size_t mid_gather_smem(int P);
+int launch_zfft_transpose(const void* in, void* out, int nz, long long M, int Izs, int z0, bool fwd, bool f32,
+                          cudaStream_t st);
+int launch_scale_pencil_z(void* W, int Ix, int nyh, int Izs, int L, const double* A, const double* Tx,
+                          const double* Ty, const double* Tz, bool f32, cudaStream_t st);
 int mid_spread_emax();
 int launch_mid_scale(void* spec, int Ix, int Izs, int nyh, int L, const double* A, const double* Tx, const double* Ty,
                      const double* Tz, bool f32, cudaStream_t st);

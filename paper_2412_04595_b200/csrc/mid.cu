@@ -104,3 +104,42 @@ int launch_mid_scale(void* spec, int Ix, int Izs, int nyh, int L, const double* 
 }
 
 }  // namespace sog
+
+namespace sog {
+
+template <typename C>
+int zfft_tr_go(const C* in, C* out, int nz, long long M, int Izs, int z0, bool fwd, cudaStream_t st) {
+    dim3 g((unsigned)((M + TR_T - 1) / TR_T), (nz + TR_T - 1) / TR_T);
+    if (fwd) k_tr_xz<C><<<g, TR_T * 8, 0, st>>>(in, out, nz, M, Izs, z0);
+    else k_tr_zx<C><<<g, TR_T * 8, 0, st>>>(in, out, nz, M, Izs, z0);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_zfft_transpose(const void* in, void* out, int nz, long long M, int Izs, int z0, bool fwd, bool f32,
+                          cudaStream_t st) {
+    return f32 ? zfft_tr_go((const cuComplex*)in, (cuComplex*)out, nz, M, Izs, z0, fwd, st)
+               : zfft_tr_go((const cuDoubleComplex*)in, (cuDoubleComplex*)out, nz, M, Izs, z0, fwd, st);
+}
+
+template <typename C>
+int scale_z_go(C* W, int Ix, int nyh, int Izs, int L, const double* A, const double* Tx, const double* Ty,
+               const double* Tz, cudaStream_t st) {
+    const long long M = (long long)Ix * nyh;
+    dim3 g((Izs + 127) / 128, (unsigned)((M + MS_ROWS - 1) / MS_ROWS));
+    if (L <= 8) k_scale_pencil_z<8, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else if (L <= 16) k_scale_pencil_z<16, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else if (L <= 24) k_scale_pencil_z<24, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else if (L <= 32) k_scale_pencil_z<32, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else if (L <= 48) k_scale_pencil_z<48, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else if (L <= 64) k_scale_pencil_z<64, C><<<g, 128, 0, st>>>(W, Ix, nyh, Izs, L, A, Tx, Ty, Tz);
+    else return 1;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_scale_pencil_z(void* W, int Ix, int nyh, int Izs, int L, const double* A, const double* Tx,
+                          const double* Ty, const double* Tz, bool f32, cudaStream_t st) {
+    return f32 ? scale_z_go((cuComplex*)W, Ix, nyh, Izs, L, A, Tx, Ty, Tz, st)
+               : scale_z_go((cuDoubleComplex*)W, Ix, nyh, Izs, L, A, Tx, Ty, Tz, st);
+}
+
+}  // namespace sog

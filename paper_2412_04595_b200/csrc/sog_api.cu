@@ -110,7 +110,10 @@ struct sog_plan {
     void* scan_tmp = nullptr;
     size_t scan_bytes = 0;
     double *d_A = nullptr, *d_Tx = nullptr, *d_Ty = nullptr, *d_Tz = nullptr;
-    cufftHandle mfwd = 0, minv = 0;
+    cufftHandle mfwd = 0, minv = 0;     // z-pruned FFT: 2D over the written / read planes
+    cufftHandle minv_full = 0, mzfft = 0;  // 2D inverse over all planes (debug stage 2); 1D along z
+    cuDoubleComplex *mX = nullptr, *mY = nullptr;   // [planes][Ix*nyh] and zero-padded pencils [Ix*nyh][Izs]
+    int zs0 = 0, nzf = 0, zg0 = 0, nzg = 0;         // spread-written planes, gather-read planes
     bool has_mid = false;
     // long
     double* lgrid = nullptr;
@@ -196,8 +199,11 @@ void free_plan(sog_plan* pl) {
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
     if (pl->pin_i) cudaFreeHost(pl->pin_i);
-    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi})
+    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
+                          pl->mzfft})
         if (h) cufftDestroy(h);
+    for (void* p : {(void*)pl->mX, (void*)pl->mY})
+        if (p) cudaFree(p);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
     delete pl;
@@ -327,12 +333,33 @@ int setup(sog_plan* pl) {
             return rc;
         size_t ws = 0;
         if (!slab) {
-            long long n[3] = {p.Izs, p.Ix, p.Iy};   // z slowest, y fastest (half axis)
+            // z-pruned 3D FFT: 2D (x,y) over the planes the spread writes, 1D along z on zero-padded
+            // z-contiguous pencils, 2D inverse over the planes the gather reads
+            pl->zs0 = z.c_lo * MZ_ZC;
+            pl->nzf = std::min(p.Izs, (z.c_hiw + 1) * MZ_ZC) - pl->zs0;
+            pl->zg0 = z.c_lo * MZ_ZC;
+            pl->nzg = std::min(p.Izs, (z.c_hi + 1) * MZ_ZC + p.P) - pl->zg0;
+            const long long M = (long long)p.Ix * nyh;
+            const size_t csz = pl->f32 ? sizeof(cuComplex) : sizeof(cuDoubleComplex);
+            CK(cudaMalloc((void**)&pl->mX, csz * (size_t)M * p.Izs));
+            CK(cudaMalloc((void**)&pl->mY, csz * (size_t)M * p.Izs));
+            CK(cudaMemset(pl->mY, 0, csz * (size_t)M * p.Izs));   // z padding of the pencils stays zero
+            pl->bytes += 2 * csz * (size_t)M * p.Izs;
+            long long n2[2] = {p.Ix, p.Iy}, n1[1] = {p.Izs};
+            const cufftType r2c = pl->f32 ? CUFFT_R2C : CUFFT_D2Z, c2r = pl->f32 ? CUFFT_C2R : CUFFT_Z2D;
+            const cufftType c2c = pl->f32 ? CUFFT_C2C : CUFFT_Z2Z;
             CKF(cufftCreate(&pl->mfwd));
-            CKF(cufftMakePlanMany64(pl->mfwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, pl->f32 ? CUFFT_R2C : CUFFT_D2Z, 1, &ws));
+            CKF(cufftMakePlanMany64(pl->mfwd, 2, n2, nullptr, 1, (long long)p.Ix * p.Iy, nullptr, 1, M, r2c, pl->nzf, &ws));
             pl->bytes += ws;
             CKF(cufftCreate(&pl->minv));
-            CKF(cufftMakePlanMany64(pl->minv, 3, n, nullptr, 1, 0, nullptr, 1, 0, pl->f32 ? CUFFT_C2R : CUFFT_Z2D, 1, &ws));
+            CKF(cufftMakePlanMany64(pl->minv, 2, n2, nullptr, 1, M, nullptr, 1, (long long)p.Ix * p.Iy, c2r, pl->nzg, &ws));
+            pl->bytes += ws;
+            CKF(cufftCreate(&pl->minv_full));
+            CKF(cufftMakePlanMany64(pl->minv_full, 2, n2, nullptr, 1, M, nullptr, 1, (long long)p.Ix * p.Iy, c2r, p.Izs,
+                                    &ws));
+            pl->bytes += ws;
+            CKF(cufftCreate(&pl->mzfft));
+            CKF(cufftMakePlanMany64(pl->mzfft, 1, n1, nullptr, 1, p.Izs, nullptr, 1, p.Izs, c2c, M, &ws));
             pl->bytes += ws;
         } else {
             // distributed FFT: 2D (z, y) per interior x plane, all-to-all to ky chunks, 1D along x
@@ -427,7 +454,8 @@ int setup(sog_plan* pl) {
 
 int set_stream(sog_plan* pl, cudaStream_t s) {
     pl->stream = s;
-    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi})
+    for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
+                          pl->mzfft})
         if (h) CKF(cufftSetStream(h, s));
     return SOG_OK;
 }
@@ -643,15 +671,33 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         if ((rc = st_mid_spread(pl))) return rc;
         mark(pl, 3);
         if (stop_stage == 1) return SOG_OK;
-        if (pl->f32) CKF(cufftExecR2C(pl->mfwd, (float*)pl->mgrid, (cufftComplex*)pl->mspec));
-        else CKF(cufftExecD2Z(pl->mfwd, pl->mgrid, pl->mspec));
+        // S4: 2D FFTs of the written planes, transpose to zero-padded z pencils, FFT along z
+        const int nyh = p.Iy / 2 + 1;
+        const long long M = (long long)p.Ix * nyh;
+        const size_t gp = (size_t)p.Ix * p.Iy;
+        if (pl->f32) {
+            CKF(cufftExecR2C(pl->mfwd, (float*)pl->mgrid + gp * pl->zs0, (cufftComplex*)pl->mX));
+        } else {
+            CKF(cufftExecD2Z(pl->mfwd, pl->mgrid + gp * pl->zs0, pl->mX));
+        }
+        if ((rc = lchk(launch_zfft_transpose(pl->mX, pl->mY, pl->nzf, M, p.Izs, pl->zs0, true, pl->f32, st)))) return rc;
+        if (pl->f32) CKF(cufftExecC2C(pl->mzfft, (cufftComplex*)pl->mY, (cufftComplex*)pl->mspec, CUFFT_FORWARD));
+        else CKF(cufftExecZ2Z(pl->mzfft, pl->mY, pl->mspec, CUFFT_FORWARD));
         mark(pl, 4);
-        if ((rc = lchk(launch_mid_scale(pl->mspec, p.Ix, p.Izs, p.Iy / 2 + 1, p.m + 1, pl->d_A, pl->d_Tx, pl->d_Ty,
-                                        pl->d_Tz, pl->f32, st))))
+        // S5 on the z pencils
+        if ((rc = lchk(launch_scale_pencil_z(pl->mspec, p.Ix, nyh, p.Izs, p.m + 1, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz,
+                                             pl->f32, st))))
             return rc;
         mark(pl, 5);
-        if (pl->f32) CKF(cufftExecC2R(pl->minv, (cufftComplex*)pl->mspec, (float*)pl->mpsi));
-        else CKF(cufftExecZ2D(pl->minv, pl->mspec, pl->mpsi));
+        // S6: inverse along z, back to planes (only those the gather reads; all for the debug stage)
+        if (pl->f32) CKF(cufftExecC2C(pl->mzfft, (cufftComplex*)pl->mspec, (cufftComplex*)pl->mspec, CUFFT_INVERSE));
+        else CKF(cufftExecZ2Z(pl->mzfft, pl->mspec, pl->mspec, CUFFT_INVERSE));
+        const bool full = stop_stage == 2;
+        const int z0 = full ? 0 : pl->zg0, nz = full ? p.Izs : pl->nzg;
+        if ((rc = lchk(launch_zfft_transpose(pl->mspec, pl->mX, nz, M, p.Izs, z0, false, pl->f32, st)))) return rc;
+        const cufftHandle inv = full ? pl->minv_full : pl->minv;
+        if (pl->f32) CKF(cufftExecC2R(inv, (cufftComplex*)pl->mX, (float*)pl->mpsi + gp * z0));
+        else CKF(cufftExecZ2D(inv, pl->mX, pl->mpsi + gp * z0));
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
         if ((rc = st_mid_gather(pl))) return rc;
