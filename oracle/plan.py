@@ -27,15 +27,15 @@ TABLE1 = (
 )
 
 # ---- plan constants (R2, R4-R9); tuned on B200 / calibrated vs Ewald2D ----
-RC_FACTOR = 3.5      # R2: r_c = RC_FACTOR * rho^(-1/3)
+RC_FACTOR = 3.25     # R2: r_c = RC_FACTOR * rho^(-1/3)  (GPU-tuned plan knob, R2)
 ETA = 0.3            # R4: range-splitting factor
 KAPPA = 1.15         # R5/R8: Nyquist safety, h <= pi s /(2 KAPPA sqrt(ln 1/tol))
 WIN_C = 0.3          # R6: window error target eps_w = WIN_C * tol
 PAD_C = 10.0         # R7: z padding  s_m * sqrt(ln(PAD_C/tol))
 CHEB_C = 0.1         # R9: Chebyshev two-variable interpolation target CHEB_C * tol
 CHEB_FLOOR = 5e-14   # R9: rounding floor of the interpolation test
-FFT_COST = 43.0      # R6: cost of one FFT grid point in units of one stencil point (B200 model)
-LONG_FFT_COST = 43.0
+FFT_COST = 30.0      # R6: cost of one FFT grid point in units of one stencil point (B200-measured model)
+LONG_FFT_COST = 30.0
 TOL_MIN = 2e-14      # Table 1 force floor 1.98e-14
 TOL_MAX = 1e-1
 
