@@ -8,4 +8,4 @@ tail -1 gpurun_out/bench_full.log
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain_bench.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu_launch=$?
 python scripts/profile_eval.py c5 2 > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_near3|k_mid_gather_z|k_mid_spread_z|k_long_gather_bc|k_long_spread_gemm" -s 0 -c 5 -o gpurun_out/prof_round python scripts/profile_eval.py c5 1 > gpurun_out/ncu_round.log 2>&1; echo ncu_full=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_near3|k_mid_gather_z|k_mid_spread_z|k_long_gather_bc|k_long_spread_gemm|k_tr_xz|k_scale_pencil_z" -s 0 -c 7 -o gpurun_out/prof_round python scripts/profile_eval.py c5 1 > gpurun_out/ncu_round.log 2>&1; echo ncu_full=$?
