@@ -56,7 +56,12 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
     double* tab = sm;                                                   // [K*(D+1)]
     double2* shift = reinterpret_cast<double2*>(sm + ((a.K * (D + 1) + 1) & ~1));   // [9]
     int* lists = reinterpret_cast<int*>(shift + 10);                    // [warps][160]
-    float4* src = reinterpret_cast<float4*>(lists + NEAR3_WARPS * 160); // [cap]: rel. xyz + code
+    // staged sources in 64-wide blocks, candidate q = 64 b + 32 h + l stored as
+    //   sxy[b][l] = (x_h0, x_h1, y_h0, y_h1), sz[b][l] = (z_h0, z_h1), sc[b][l] = (code_h0, code_h1)
+    // so that one lane tests two candidates with packed fp32x2 arithmetic
+    float4* sxy = reinterpret_cast<float4*>(lists + NEAR3_WARPS * 160); // [cap/64][32]
+    float2* sz = reinterpret_cast<float2*>(sxy + a.cap / 2);             // [cap/64][32]
+    int2* sc = reinterpret_cast<int2*>(sz + a.cap / 2);                  // [cap/64][32]
     const CellGeo& g = a.g;
     const int c = blockIdx.x;
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
@@ -81,9 +86,21 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
         const int cb = (nx * g.ncy + ny) * g.ncz;
         ns_total += a.start[cb + z1 + 1] - a.start[cb + z0];
     }
+    float* sxyf = reinterpret_cast<float*>(sxy);
+    float* szf = reinterpret_cast<float*>(sz);
+    int* scf = reinterpret_cast<int*>(sc);
+    auto put = [&](int q, float x, float y, float z, int code) {
+        const int b = q >> 6, h = (q >> 5) & 1, l = q & 31, e = b * 32 + l;
+        sxyf[4 * e + h] = x;
+        sxyf[4 * e + 2 + h] = y;
+        szf[2 * e + h] = z;
+        scf[2 * e + h] = code;
+    };
+    const float rc2f = a.rc2f;
     // process the neighbourhood in capacity-sized pieces (usually one)
     for (int sbeg = 0; sbeg < ns_total; sbeg += a.cap) {
         const int send = min(ns_total, sbeg + a.cap);
+        const int nsrc = send - sbeg, npad = (nsrc + 127) & ~127;
         __syncthreads();
         // stage sources [sbeg, send) of the concatenated 9-column list with image shifts
         {
@@ -101,34 +118,38 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
                 for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) {
                     const int j = jb + (q - base);
                     const d4 s = ld_d4(&a.pos[j]);
-                    src[q - sbeg] = make_float4((float)(s.x + sx - ox), (float)(s.y + sy - oy), (float)(s.z - oz),
-                                                __int_as_float((j << 4) | k));
+                    put(q - sbeg, (float)(s.x + sx - ox), (float)(s.y + sy - oy), (float)(s.z - oz), (j << 4) | k);
                 }
                 base += n;
             }
+            for (int q = nsrc + threadIdx.x; q < npad; q += blockDim.x) put(q, 1e18f, 0.f, 0.f, 0);   // sentinels
         }
         __syncthreads();
-        const int nsrc = send - sbeg;
         for (int it = t0 + warp; it < t1; it += NEAR3_WARPS) {
             const d4 pi = ld_d4(&a.pos[it]);
             const float xi = (float)(pi.x - ox), yi = (float)(pi.y - oy), zi = (float)(pi.z - oz);
+            const float2 xi2 = make_float2(xi, xi), yi2 = make_float2(yi, yi), zi2 = make_float2(zi, zi);
+            const float2 m1 = make_float2(-1.f, -1.f);
             double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
             int npend = 0;
-            for (int q0 = 0; q0 < nsrc; q0 += 128) {
-                // fp32 pre-test of 4 x 32 sources (independent chains)
+            for (int q0 = 0; q0 < npad; q0 += 128) {
+                // fp32 pre-test of 4 x 32 sources, two per packed fp32x2 operation
                 bool pass[4];
                 int code[4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int q = q0 + 32 * r + lane;
-                    pass[r] = false;
-                    code[r] = 0;
-                    if (q < nsrc) {
-                        const float4 s = src[q];
-                        const float dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
-                        pass[r] = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < a.rc2f;
-                        code[r] = __float_as_int(s.w);
-                    }
+                for (int r = 0; r < 2; ++r) {
+                    const int e = (q0 >> 6) * 32 + r * 32 + lane;
+                    const float4 xy = sxy[e];
+                    const float2 zz = sz[e];
+                    const int2 cc = sc[e];
+                    const float2 dx = __ffma2_rn(make_float2(xy.x, xy.y), m1, xi2);
+                    const float2 dy = __ffma2_rn(make_float2(xy.z, xy.w), m1, yi2);
+                    const float2 dz = __ffma2_rn(zz, m1, zi2);
+                    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+                    pass[2 * r] = r2.x < rc2f;
+                    pass[2 * r + 1] = r2.y < rc2f;
+                    code[2 * r] = cc.x;
+                    code[2 * r + 1] = cc.y;
                 }
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -144,19 +165,19 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
                 __syncwarp();
             }
             if (lane < npend) near_pair<D>(tab, a, pi, wl[lane], shift, phi, gx, gy, gz);
+            // 4-value butterfly; lanes 0..3 hold phi, gx, gy, gz
+            const bool b1 = lane & 1;
+            double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;
+            k0v += __shfl_xor_sync(0xffffffffu, b1 ? phi : gx, 1);
+            k1v += __shfl_xor_sync(0xffffffffu, b1 ? gy : gz, 1);
+            const bool b2 = lane & 2;
+            double kk = b2 ? k1v : k0v;
+            kk += __shfl_xor_sync(0xffffffffu, b2 ? k0v : k1v, 2);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                phi += __shfl_xor_sync(0xffffffffu, phi, o);
-                gx += __shfl_xor_sync(0xffffffffu, gx, o);
-                gy += __shfl_xor_sync(0xffffffffu, gy, o);
-                gz += __shfl_xor_sync(0xffffffffu, gz, o);
-            }
-            if (lane == 0) {
-                if (sbeg == 0) st_d4(&a.out[it], d4{phi, gx, gy, gz});
-                else {
-                    d4 o = a.out[it];
-                    st_d4(&a.out[it], d4{o.x + phi, o.y + gx, o.z + gy, o.w + gz});
-                }
+            for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
+            if (lane < 4) {
+                double* o = reinterpret_cast<double*>(&a.out[it]);
+                o[lane] = sbeg == 0 ? kk : o[lane] + kk;
             }
             __syncwarp();
         }

@@ -569,10 +569,10 @@ int st_near(sog_plan* pl) {
         a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
         a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
         a.g = pl->geo;
-        a.cap = 1536;
+        a.cap = 1536;                            // multiple of 128 (packed staging layout)
         a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
         size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
-                    NEAR3_WARPS * 160 * sizeof(int) + sizeof(float4) * a.cap;
+                    NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;
         CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
     } else {
