@@ -36,6 +36,9 @@ CHEB_C = 0.1         # R9: Chebyshev two-variable interpolation target CHEB_C * 
 CHEB_FLOOR = 5e-14   # R9: rounding floor of the interpolation test
 FFT_COST = 30.0      # R6: cost of one FFT grid point in units of one stencil point (B200-measured model)
 LONG_FFT_COST = 30.0
+KB_BETA = 2.2        # R6-KB: Kaiser-Bessel shape beta = KB_BETA * P (R6-KB; cf. beta = 2.5 P)
+KB_NU_EXTRA = 3      # R6-KB: polynomial degree nu = P + KB_NU_EXTRA of the Chebyshev-interpolated window
+KB_RATE = (0.4, 0.92)  # R6-KB: window error ~ 10^(a - b P) at h = h_Nyquist (calibrated)
 TOL_MIN = 2e-14      # Table 1 force floor 1.98e-14
 TOL_MAX = 1e-1
 
@@ -109,6 +112,18 @@ def choose_window(s: float, eps_w: float, tol: float, cost_fn):
     return best[1], S, best[2]
 
 
+def choose_window_kb(s: float, eps_w: float, tol: float):
+    """R6-KB: Kaiser-Bessel window (Remark rmk::PWindow, P:477-480), shape beta = KB_BETA P,
+    support P = the smallest odd P >= 5 with 10^(a - b P) <= eps_w, mesh size at the Nyquist
+    bound of R5 (the window does not constrain h).  Returns (P, beta, h, nu)."""
+    a, b = KB_RATE
+    P = 5
+    while 10.0 ** (a - b * P) > eps_w:
+        P += 2
+    h = math.pi * s / (2.0 * KAPPA * math.sqrt(math.log(1.0 / tol)))
+    return P, KB_BETA * P, h, P + KB_NU_EXTRA
+
+
 def cheb_nodes(P: int) -> np.ndarray:
     """First-kind Chebyshev nodes x_i = cos((i-1/2) pi / P), i=1..P."""
     i = np.arange(1, P + 1, dtype=np.float64)
@@ -175,13 +190,16 @@ class Plan:
     Iz: int = 0           # interior z count, h_z = Lz / Iz
     Izs: int = 0          # extended z grid count I_z^*
     P: int = 0            # window support (odd)
-    S: float = 0.0        # window shape
+    S: float = 0.0        # window shape: S (Gaussian) or beta (Kaiser-Bessel)
     # long-range (R8-R9)
     Ilx: int = 0
     Ily: int = 0
     Pl: int = 0
     Sl: float = 0.0
     Pc: int = 0           # Chebyshev proxy layers
+    window: str = "gs"    # "gs": Gaussian (Eq. eq::GS); "kb": Kaiser-Bessel, polynomial weights (R6-KB)
+    nu: int = 0           # KB: degree of the Chebyshev-interpolated window polynomials (mid)
+    nul: int = 0          # KB: same for the long-range window
 
     # derived quantities (recomputed, never stored separately)
     @property
@@ -224,6 +242,9 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     row = over.pop("row", None) or select_row(tol)
     b, r0, omega = row[0], row[1], row[2]
     rc_factor = over.pop("rc_factor", RC_FACTOR)
+    window = over.pop("window", "gs")
+    if window not in ("gs", "kb"):
+        raise ValueError("window must be 'gs' or 'kb'")
     eta = over.pop("eta", ETA)
     rho = N / (Lx * Ly * Lz)
     rc = over.pop("rc", None)
@@ -249,7 +270,7 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
                 m = ell
     m = min(m, M - 1)                                        # keep >= 1 long-range Gaussian
     p = Plan(N=N, Lx=Lx, Ly=Ly, Lz=Lz, tol=tol, b=b, r0=r0, omega=omega, rc=rc,
-             sigma=sigma, M=M, m=m)
+             sigma=sigma, M=M, m=m, window=window)
     eps_w = WIN_C * tol
     if m >= 0:
         sm = s0 * b ** m
@@ -258,7 +279,10 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
             pad = max(2.0 * ((P - 1) * h / 2.0 + h), sm * math.sqrt(math.log(PAD_C / tol)))
             return P ** 3 + FFT_COST * (Lx * Ly * (Lz + pad)) / (N * h ** 3)
 
-        P, S, h = choose_window(s0, eps_w, tol, cost_mid)
+        if window == "kb":
+            P, S, h, p.nu = choose_window_kb(s0, eps_w, tol)
+        else:
+            P, S, h = choose_window(s0, eps_w, tol, cost_mid)
         p.P, p.S = P, S
         p.Ix = friendly_even(math.ceil(Lx / h))
         p.Iy = friendly_even(math.ceil(Ly / h))
@@ -271,7 +295,10 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     def cost_long(P, h):
         return P ** 2 + LONG_FFT_COST * (Lx * Ly) / (N * h ** 2)
 
-    Pl, Sl, hl = choose_window(sl, eps_w, tol, cost_long)          # R8
+    if window == "kb":
+        Pl, Sl, hl, p.nul = choose_window_kb(sl, eps_w, tol)      # R8 with R6-KB
+    else:
+        Pl, Sl, hl = choose_window(sl, eps_w, tol, cost_long)      # R8
     p.Pl, p.Sl = Pl, Sl
     p.Ilx = max(friendly_even(math.ceil(Lx / hl)), friendly_even(Pl))
     p.Ily = max(friendly_even(math.ceil(Ly / hl)), friendly_even(Pl))

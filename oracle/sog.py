@@ -18,6 +18,8 @@ import math
 
 import numpy as np
 import scipy.fft
+import scipy.special
+from numpy.polynomial import chebyshev as npcheb
 from scipy.spatial import cKDTree
 
 from .plan import Plan, cheb_T, cheb_nodes
@@ -129,18 +131,71 @@ def gaussian_window_hat(k, H: float, S: float):
     return math.sqrt(math.pi / S) * H * np.exp(-(np.asarray(k) ** 2) * H * H / (4.0 * S))
 
 
-def stencil(x: np.ndarray, I: int, h: float, P: int, S: float, periodic: bool):
+def kb_window(d, H: float, beta: float):
+    """Kaiser-Bessel window W_KB(x) = I0(beta sqrt(1 - (x/H)^2)) / I0(beta) for |x| <= H,
+    0 otherwise (Remark rmk::PWindow, P:477-480; Kaiser 1980)."""
+    d = np.asarray(d, dtype=np.float64)
+    t = np.clip(1.0 - (d / H) ** 2, 0.0, None)
+    return np.where(np.abs(d) <= H, scipy.special.i0(beta * np.sqrt(t)) / scipy.special.i0(beta), 0.0)
+
+
+def kb_window_hat(k, H: float, beta: float):
+    """Fourier transform of W_KB: 2H sinh(sqrt(beta^2 - (kH)^2)) / (I0(beta) sqrt(beta^2 - (kH)^2))
+    (sin / sqrt form for kH > beta), used for deconvolution as the Gaussian's closed form is."""
+    a = beta * beta - (np.asarray(k, dtype=np.float64) * H) ** 2
+    r = np.sqrt(np.abs(a))
+    rs = np.where(r == 0.0, 1.0, r)
+    f = np.where(a > 0.0, np.sinh(r) / rs, np.where(r == 0.0, 1.0, np.sin(r) / rs))
+    return 2.0 * H * f / scipy.special.i0(beta)
+
+
+def window_half_width(window: str, P: int, h: float) -> float:
+    """Support half-width H: (P-1)h/2 for the Gaussian (Eq. eq::GS, P:676); P h/2 for KB
+    (R6-KB: every one of the P stencil points stays inside the support for all particle
+    offsets, so each stencil point's weight is analytic in the offset)."""
+    return (P * h if window == "kb" else (P - 1) * h) / 2.0
+
+
+def kb_stencil_polys(P: int, beta: float, nu: int):
+    """R6-KB (the paper's polynomial windows, Remark rmk::PWindow P:477-480): for stencil
+    point j = 0..P-1 and the particle's offset u = x/h + I/2 - g0 in [-1/2, 1/2), the weight
+    W_KB((j - p - u) h) is replaced by its degree-nu interpolant at the nu+1 first-kind
+    Chebyshev points of u in [-1/2, 1/2] (Chebyshev series in t = 2u).  h cancels (the window
+    scales with H = P h / 2).  Returns the (P, nu+1) Chebyshev coefficients."""
+    p = (P - 1) // 2
+    C = np.empty((P, nu + 1))
+    for j in range(P):
+        C[j] = npcheb.chebinterpolate(lambda t: kb_window((j - p - 0.5 * t), 0.5 * P, beta), nu)
+    return C
+
+
+def window_hat(plan: Plan, k, H: float, long: bool = False):
+    """Closed-form window transform for the deconvolution (R6 / R6-KB)."""
+    shape = plan.Sl if long else plan.S
+    if plan.window == "kb":
+        return kb_window_hat(k, H, shape)
+    return gaussian_window_hat(k, H, shape)
+
+
+def stencil(x: np.ndarray, I: int, h: float, P: int, S: float, periodic: bool, window: str = "gs", nu: int = 0):
     """R6: the P (odd) consecutive grid points centred at the nearest grid point
     g0 = floor(x/h + I/2 + 1/2) of the grid x_g = (g - I/2) h; window
     W(x_g - x) = exp(-S ((x_g - x)/H)^2), H = (P-1)h/2 (Eq. eq::GS, P:676),
-    evaluated at all P points.  Returns (flat index, W, dW/dx_particle)."""
+    evaluated at all P points; window == "kb": the polynomial Kaiser-Bessel weights of
+    kb_stencil_polys.  Returns (flat index, W, dW/dx_particle)."""
     p = (P - 1) // 2
-    H = (P - 1) * h / 2.0
+    H = window_half_width(window, P, h)
     g0 = np.floor(x / h + (I / 2.0 + 0.5)).astype(np.int64)
     g = g0[:, None] + np.arange(-p, p + 1)[None, :]
-    d = (g - I / 2.0) * h - x[:, None]
-    W = np.exp(-S * (d / H) ** 2)
-    dW = 2.0 * S * d / (H * H) * W          # d/dx_i W(x_i - x_g)  (R11)
+    if window == "kb":
+        u = x / h + I / 2.0 - g0                 # in [-1/2, 1/2)
+        C = kb_stencil_polys(P, S, nu)
+        W = np.stack([npcheb.chebval(2.0 * u, C[j]) for j in range(P)], axis=1)
+        dW = np.stack([npcheb.chebval(2.0 * u, npcheb.chebder(C[j])) * 2.0 / h for j in range(P)], axis=1)
+    else:
+        d = (g - I / 2.0) * h - x[:, None]
+        W = np.exp(-S * (d / H) ** 2)
+        dW = 2.0 * S * d / (H * H) * W          # d/dx_i W(x_i - x_g)  (R11)
     if periodic:
         g = np.mod(g, I)
     elif np.any(g < 0) or np.any(g >= I):
@@ -162,17 +217,17 @@ def mid_multiplier(plan: Plan) -> np.ndarray:
     tau = np.zeros_like(k2)
     for ell in range(plan.m + 1):
         tau += w[ell] * s[ell] ** 3 * np.exp(-s[ell] ** 2 * k2 / 4.0)
-    Hx, Hy, Hz = ((plan.P - 1) * h / 2.0 for h in (plan.hx, plan.hy, plan.hz))
-    What = (gaussian_window_hat(kx, Hx, plan.S)[:, None, None]
-            * gaussian_window_hat(ky, Hy, plan.S)[None, :, None]
-            * gaussian_window_hat(kz, Hz, plan.S)[None, None, :])
+    Hx, Hy, Hz = (window_half_width(plan.window, plan.P, h) for h in (plan.hx, plan.hy, plan.hz))
+    What = (window_hat(plan, kx, Hx)[:, None, None]
+            * window_hat(plan, ky, Hy)[None, :, None]
+            * window_hat(plan, kz, Hz)[None, None, :])
     return math.pi ** 1.5 * tau / What ** 2
 
 
 def mid_stencils(plan: Plan, xyz):
-    sx = stencil(xyz[:, 0], plan.Ix, plan.hx, plan.P, plan.S, True)
-    sy = stencil(xyz[:, 1], plan.Iy, plan.hy, plan.P, plan.S, True)
-    sz = stencil(xyz[:, 2], plan.Izs, plan.hz, plan.P, plan.S, False)
+    sx = stencil(xyz[:, 0], plan.Ix, plan.hx, plan.P, plan.S, True, plan.window, plan.nu)
+    sy = stencil(xyz[:, 1], plan.Iy, plan.hy, plan.P, plan.S, True, plan.window, plan.nu)
+    sz = stencil(xyz[:, 2], plan.Izs, plan.hz, plan.P, plan.S, False, plan.window, plan.nu)
     return sx, sy, sz
 
 
@@ -251,9 +306,9 @@ def long_kernel(plan: Plan) -> np.ndarray:
         K += E[:, :, None, None] * spec[None, None]
         K0 += w[ell] * s[ell] ** 2 * np.expm1(-d2 / s[ell] ** 2)
     K[:, :, 0, 0] = K0
-    Hx = (plan.Pl - 1) * plan.hlx / 2.0
-    Hy = (plan.Pl - 1) * plan.hly / 2.0
-    What = gaussian_window_hat(kx, Hx, plan.Sl)[:, None] * gaussian_window_hat(ky, Hy, plan.Sl)[None, :]
+    Hx = window_half_width(plan.window, plan.Pl, plan.hlx)
+    Hy = window_half_width(plan.window, plan.Pl, plan.hly)
+    What = window_hat(plan, kx, Hx, long=True)[:, None] * window_hat(plan, ky, Hy, long=True)[None, :]
     return math.pi * K / What[None, None] ** 2
 
 
@@ -273,8 +328,8 @@ def long_basis(plan: Plan, z: np.ndarray):
 
 
 def long_stencils(plan: Plan, xyz):
-    sx = stencil(xyz[:, 0], plan.Ilx, plan.hlx, plan.Pl, plan.Sl, True)
-    sy = stencil(xyz[:, 1], plan.Ily, plan.hly, plan.Pl, plan.Sl, True)
+    sx = stencil(xyz[:, 0], plan.Ilx, plan.hlx, plan.Pl, plan.Sl, True, plan.window, plan.nul)
+    sy = stencil(xyz[:, 1], plan.Ily, plan.hly, plan.Pl, plan.Sl, True, plan.window, plan.nul)
     return sx, sy
 
 

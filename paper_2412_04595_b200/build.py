@@ -14,6 +14,19 @@ FLAGS = (["-DSOG_ASSERTS"] if os.environ.get("SOG_ASSERTS") else []) + ["-O3", "
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
+def _obj_stale(src: str, obj: str) -> bool:
+    """An object is stale when it, or its nvcc -MD dependency file, is older than any dependency."""
+    dep = obj + ".d"
+    if not (os.path.exists(obj) and os.path.exists(dep)):
+        return True
+    t = os.path.getmtime(obj)
+    with open(dep) as f:
+        text = f.read().replace("\\\n", " ")
+    files = [w for w in text.split(":", 1)[-1].split() if w]
+    files.append(os.path.join(CSRC, src))
+    return any(not os.path.exists(d) or os.path.getmtime(d) > t for d in files)
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -26,17 +39,25 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    stamp = os.path.join(HERE, "lib", "obj", "flags.txt")
+    flags = " ".join(FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True               # compiler flags changed (e.g. SOG_ASSERTS): rebuild everything
     if not force and not _stale():
         return LIB
     os.makedirs(os.path.join(HERE, "lib", "obj"), exist_ok=True)
+    with open(stamp, "w") as f:
+        f.write(flags)
     objs, procs = [], []
-    for src in SOURCES:            # one nvcc per translation unit, in parallel
+    for src in SOURCES:            # one nvcc per stale translation unit, in parallel
         obj = os.path.join(HERE, "lib", "obj", src + ".o")
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        objs.append(obj)
+        if not force and not _obj_stale(src, obj):
+            continue
+        cmd = [NVCC, *FLAGS, "-MD", "-MF", obj + ".d", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), cmd))
-        objs.append(obj)
     for pr, cmd in procs:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)

@@ -65,6 +65,18 @@ bool choose_window(double s, double eps_w, double tol, double kappa, Cost cost, 
     return found;
 }
 
+// R6-KB: support P = smallest odd >= 5 with 10^(a - b P) <= eps_w, beta = kb_beta P, the mesh at
+// the Nyquist bound (the window does not constrain h), nu = P + kb_nu_extra
+void choose_window_kb(double s, double eps_w, double tol, const RuleKnobs& k, int& Pout, double& beta, double& h,
+                      int& nu) {
+    int P = 5;
+    while (std::pow(10.0, k.kb_rate_a - k.kb_rate_b * P) > eps_w) P += 2;
+    Pout = P;
+    beta = k.kb_beta * P;
+    h = kPi * s / (2.0 * k.kappa * std::sqrt(std::log(1.0 / tol)));
+    nu = P + k.kb_nu_extra;
+}
+
 // Chebyshev T_n(x), n < P
 void cheb_T(double x, int P, double* T) {
     T[0] = 1.0;
@@ -188,7 +200,9 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
             return double(P) * P * P + k.fft_cost * (p.Lx * p.Ly * (p.Lz + pad)) / (N * h * h * h);
         };
         double h;
-        if (!choose_window(s0, eps_w, p.tol, k.kappa, cost_mid, p.P, p.S, h)) { err = "no mid window"; return false; }
+        if (p.window == 1)
+            choose_window_kb(s0, eps_w, p.tol, k, p.P, p.S, h, p.nu);
+        else if (!choose_window(s0, eps_w, p.tol, k.kappa, cost_mid, p.P, p.S, h)) { err = "no mid window"; return false; }
         p.Ix = friendly_even(long(std::ceil(p.Lx / h)));
         p.Iy = friendly_even(long(std::ceil(p.Ly / h)));
         p.Iz = std::max(1L, long(std::ceil(p.Lz / h)));
@@ -202,7 +216,9 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
         return double(P) * P + k.long_fft_cost * (p.Lx * p.Ly) / (N * h * h);
     };
     double hl;
-    if (!choose_window(sl, eps_w, p.tol, k.kappa, cost_long, p.Pl, p.Sl, hl)) { err = "no long window"; return false; }
+    if (p.window == 1)
+        choose_window_kb(sl, eps_w, p.tol, k, p.Pl, p.Sl, hl, p.nul);
+    else if (!choose_window(sl, eps_w, p.tol, k.kappa, cost_long, p.Pl, p.Sl, hl)) { err = "no long window"; return false; }
     p.Ilx = std::max(friendly_even(long(std::ceil(p.Lx / hl))), friendly_even(p.Pl));
     p.Ily = std::max(friendly_even(long(std::ceil(p.Ly / hl))), friendly_even(p.Pl));
     // R9
@@ -235,6 +251,15 @@ bool validate_params(const Params& p, std::string& err) {
     if (!(p.Sl > 0)) return bad("bad long window shape");
     if (p.Ilx < p.Pl || p.Ily < p.Pl) return bad("long grid smaller than the window support");
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
+    if (p.window != 0 && p.window != 1) return bad("window must be 0 (Gaussian) or 1 (Kaiser-Bessel)");
+    if (p.window == 1) {
+        if (p.m >= 0 && (p.nu < 2 || p.nu > p.P + 3)) return bad("KB mid polynomial degree nu must be in [2, P+3]");
+        if (p.nul < 2 || p.nul > p.Pl + 3) return bad("KB long polynomial degree nul must be in [2, Pl+3]");
+        // deconvolution divides by the window transform: keep every grid mode inside its
+        // positive (sinh) branch, k_max H = pi P / 2 < beta
+        if (p.m >= 0 && !(p.S > 0.5 * kPi * p.P)) return bad("KB mid shape beta must exceed pi P / 2");
+        if (!(p.Sl > 0.5 * kPi * p.Pl)) return bad("KB long shape beta must exceed pi Pl / 2");
+    }
     return true;
 }
 
@@ -315,11 +340,16 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
     auto axis = [&](int I, double Lper, double h, bool half, std::vector<double>& T) {
         int n = half ? I / 2 + 1 : I;
         T.resize(size_t(L) * n);
-        double H = (p.P - 1) * h / 2.0;
+        double H = (p.window == 1 ? p.P : p.P - 1) * h / 2.0;
         for (int l = 0; l < L; ++l)
             for (int i = 0; i < n; ++i) {
                 int f = (half || i < (I + 1) / 2) ? i : i - I;   // numpy fftfreq ordering
                 double kk = 2.0 * kPi * f / Lper;
+                if (p.window == 1) {   // R6-KB: exp(-k^2 s_l^2/4) / W_KB(k)^2
+                    const double wh = kb_hat(kk, H, p.S);
+                    T[size_t(l) * n + i] = std::exp(-kk * kk * s[l] * s[l] / 4.0) / (wh * wh);
+                    continue;
+                }
                 double e = kk * kk * (s[l] * s[l] / 4.0 - H * H / (2.0 * p.S));
                 T[size_t(l) * n + i] = p.S / (kPi * H * H) * std::exp(-e);
             }
@@ -338,7 +368,8 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
     const int P = p.Pc, nx = p.Ilx, ny = p.Ily / 2 + 1;
     std::vector<double> za(P);
     for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
-    const double Hx = (p.Pl - 1) * p.hlx() / 2.0, Hy = (p.Pl - 1) * p.hly() / 2.0;
+    const int Pw = p.window == 1 ? p.Pl : p.Pl - 1;   // support width in mesh steps (R6 / R6-KB)
+    const double Hx = Pw * p.hlx() / 2.0, Hy = Pw * p.hly() / 2.0;
     K.assign(size_t(nx) * ny * P * P, 0.0);
     std::vector<double> Cm;
     build_cheb_matrix(P, Cm);
@@ -349,8 +380,10 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
             double ky = 2.0 * kPi * iy / p.Ly;
             double k2 = kx * kx + ky * ky;
             // 1 / (W_x W_y)^2
-            double Wx = std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
-            double Wy = std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
+            double Wx = p.window == 1 ? kb_hat(kx, Hx, p.Sl)
+                                      : std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
+            double Wy = p.window == 1 ? kb_hat(ky, Hy, p.Sl)
+                                      : std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
             // 1/(Ilx Ily) of the (unnormalised) cuFFT inverse is folded in here (R12)
             double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
             double* Km = &K[(size_t(ix) * ny + iy) * P * P];
@@ -390,6 +423,52 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
 
 void build_cheb_nodes(int Pc, std::vector<double>& Tn) { Tn = node_T(Pc); }
 
+double kb_hat(double k, double H, double beta) {
+    // int_{-H}^{H} I0(beta sqrt(1 - (x/H)^2)) / I0(beta) e^{-ikx} dx
+    //   = 2H sinh(sqrt(beta^2 - (kH)^2)) / (I0(beta) sqrt(beta^2 - (kH)^2))   (sin form past kH = beta)
+    const double a = beta * beta - (k * H) * (k * H);
+    const double r = std::sqrt(std::fabs(a));
+    const double f = r == 0.0 ? 1.0 : (a > 0.0 ? std::sinh(r) / r : std::sin(r) / r);
+    return 2.0 * H * f / std::cyl_bessel_i(0.0, beta);
+}
+
+void build_kb_poly(int P, double beta, int nu, std::vector<double>& c) {
+    // Chebyshev interpolation in t = 2u at the nu+1 first-kind points (discrete orthogonality),
+    // then the series sum_n a_n T_n(2u) re-expanded in powers of u, all in long double.
+    const int p = (P - 1) / 2, n1 = nu + 1;
+    const long double half_w = 0.5L * P, pi = 3.141592653589793238462643383279502884L;
+    const long double i0b = std::cyl_bessel_il(0.0L, (long double)beta);
+    c.assign(size_t(n1) * P, 0.0);
+    std::vector<long double> f(n1), a(n1), Tm(n1), Tc(n1), Tn(n1), mono(n1);
+    for (int j = 0; j < P; ++j) {
+        for (int i = 0; i < n1; ++i) {
+            const long double t = std::cos((i + 0.5L) * pi / n1);
+            const long double x = (long double)(j - p) - 0.5L * t;      // (x_g - x) / h
+            const long double r = 1.0L - (x / half_w) * (x / half_w);
+            f[i] = r < 0 ? 0.0L : std::cyl_bessel_il(0.0L, (long double)beta * std::sqrt(r)) / i0b;
+        }
+        for (int n = 0; n < n1; ++n) {
+            long double acc = 0;
+            for (int i = 0; i < n1; ++i) acc += f[i] * std::cos(n * (i + 0.5L) * pi / n1);
+            a[n] = acc * (n == 0 ? 1.0L : 2.0L) / n1;
+        }
+        // T_n(2u) as monomials in u: T_0 = 1, T_1 = 2u, T_{n+1} = 4u T_n - T_{n-1}
+        std::fill(mono.begin(), mono.end(), 0.0L);
+        std::fill(Tm.begin(), Tm.end(), 0.0L);
+        std::fill(Tc.begin(), Tc.end(), 0.0L);
+        Tm[0] = 1.0L;
+        mono[0] += a[0];
+        if (n1 > 1) { Tc[1] = 2.0L; mono[1] += 2.0L * a[1]; }
+        for (int n = 2; n < n1; ++n) {
+            for (int e = 0; e < n1; ++e) Tn[e] = (e > 0 ? 4.0L * Tc[e - 1] : 0.0L) - Tm[e];
+            for (int e = 0; e < n1; ++e) mono[e] += a[n] * Tn[e];
+            Tm.swap(Tc);
+            Tc.swap(Tn);
+        }
+        for (int e = 0; e < n1; ++e) c[size_t(e) * P + j] = double(mono[e]);
+    }
+}
+
 void build_cheb_matrix(int Pc, std::vector<double>& C) {
     std::vector<double> Tn = node_T(Pc);
     C.resize(size_t(Pc) * Pc);
@@ -405,7 +484,8 @@ std::string describe(const Params& p) {
       << "\nrc=" << p.rc << "\nsigma=" << p.sigma << "\nM=" << p.M << "\nm=" << p.m
       << "\nIx=" << p.Ix << "\nIy=" << p.Iy << "\nIz=" << p.Iz << "\nIzs=" << p.Izs
       << "\nP=" << p.P << "\nS=" << p.S << "\nIlx=" << p.Ilx << "\nIly=" << p.Ily
-      << "\nPl=" << p.Pl << "\nSl=" << p.Sl << "\nPc=" << p.Pc << "\n";
+      << "\nPl=" << p.Pl << "\nSl=" << p.Sl << "\nPc=" << p.Pc << "\nwindow=" << p.window
+      << "\nnu=" << p.nu << "\nnul=" << p.nul << "\n";
     return o.str();
 }
 

@@ -23,6 +23,9 @@ struct Params {
     int Ilx = 0, Ily = 0, Pl = 0;
     double Sl = 0;
     int Pc = 0;
+    // window (R6 / R6-KB): 0 = Gaussian (Eq. eq::GS), 1 = Kaiser-Bessel as per-stencil-point
+    // polynomials of degree nu (mid) / nul (long); S, Sl hold beta for KB
+    int window = 0, nu = 0, nul = 0;
     // derived
     double hx() const { return Lx / Ix; }
     double hy() const { return Ly / Iy; }
@@ -41,6 +44,9 @@ struct RuleKnobs {
     double cheb_c = 0.1;      // R9
     double fft_cost = 30.0;   // R6 cost model (grid point vs stencil point, B200-measured)
     double long_fft_cost = 30.0;
+    double kb_beta = 2.2;     // R6-KB: beta = kb_beta * P
+    int kb_nu_extra = 3;      // R6-KB: nu = P + kb_nu_extra
+    double kb_rate_a = 0.4, kb_rate_b = 0.92;   // R6-KB: window error ~ 10^(a - b P)
 };
 
 // plan.cpp
@@ -68,6 +74,11 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
 // Long-range kernel matrices per half mode (mode = ix*(Ily/2+1)+iy), in the Chebyshev T
 // basis: K~[mode][m][n] = sum_ab C[a][m] K_ab C[b][n], K_ab from R9/R10.
 void build_long_kernel(const Params& p, std::vector<double>& K);
+// R6-KB: monomial coefficients c[n * P + j] (n = 0..nu) in u = x/h + I/2 - g0 of the degree-nu
+// Chebyshev interpolant of W_KB((j - p - u) h), H = P h / 2 (Remark rmk::PWindow)
+void build_kb_poly(int P, double beta, int nu, std::vector<double>& c);
+// Fourier transform of the KB window of half-width H (sinh / sin branches)
+double kb_hat(double k, double H, double beta);
 // Chebyshev -> Lagrange coefficient matrix C[b][n]: L_b(x) = sum_n C[b][n] T_n(x).
 void build_cheb_matrix(int Pc, std::vector<double>& C);
 // Tn[a][m] = T_m(x_a) at the first-kind nodes x_a = cos((a+1/2) pi / Pc).

@@ -34,7 +34,19 @@ class Opts(ctypes.Structure):
                 ("P", ctypes.c_int), ("S", ctypes.c_double),
                 ("Ilx", ctypes.c_int), ("Ily", ctypes.c_int), ("Pl", ctypes.c_int), ("Sl", ctypes.c_double),
                 ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint),
-                ("precision", ctypes.c_int)]
+                ("precision", ctypes.c_int), ("window", ctypes.c_int), ("nu", ctypes.c_int),
+                ("nul", ctypes.c_int)]
+
+WINDOWS = {"gs": 0, "kb": 1}
+
+
+def _set_window(o, window, params):
+    """Window choice: explicit params carry their own (oracle Plan: "gs"/"kb"), else `window`."""
+    w = params.get("window", window) if params is not None else window
+    o.window = WINDOWS[w] if isinstance(w, str) else int(w)
+    if params is not None:
+        o.nu = int(params.get("nu", 0))
+        o.nul = int(params.get("nul", 0))
 
 
 def lib_path() -> str:
@@ -114,7 +126,7 @@ class Plan:
     """
 
     def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
-                 validate=True, timing=False, precision="fp64"):
+                 validate=True, timing=False, precision="fp64", window="gs"):
         self.lib = load_library()
         self.N = int(N)
         self.L = tuple(float(v) for v in L)
@@ -129,6 +141,7 @@ class Plan:
         o.flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
         o.cuda_stream = _stream_handle(stream)
         o.precision = {"fp64": 0, "fp32": 1}[precision]
+        _set_window(o, window, params)
         h = self.lib.sog_plan_create_ex(self.N, *self.L, self.tol, ctypes.byref(o))
         if not h:
             raise SogError(-1, self.lib.sog_last_error().decode())
@@ -253,12 +266,13 @@ def _parse(text):
     return out
 
 
-def choose_params(N, L, tol, rc_factor=None, eta=None) -> dict:
+def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs") -> dict:
     """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU)."""
     lib = load_library()
     o = Opts()
     o.rc_factor = float(rc_factor or 0.0)
     o.eta = float(eta or 0.0)
+    _set_window(o, window, None)
     n = lib.sog_plan_choose(int(N), *[float(v) for v in L], float(tol), ctypes.byref(o), None, 0)
     if n < 0:
         raise _err(lib, n)
@@ -311,7 +325,7 @@ class DistPlan:
     """
 
     def __init__(self, N_total, n_own_max, L, tol, R, rank=0, nccl_id=None, loopback=False, params=None,
-                 stream=None):
+                 stream=None, window="gs"):
         self.lib = load_library()
         self.L = tuple(float(v) for v in L)
         self.R = int(R)
@@ -322,6 +336,7 @@ class DistPlan:
                 setattr(o, k, type(getattr(o, k))(params[k]))
         o.flags = SOG_NO_VALIDATE
         o.cuda_stream = _stream_handle(stream)
+        _set_window(o, window, params)
         if loopback:
             h = self.lib.sog_dist_create_loopback(int(N_total), int(n_own_max), *self.L, float(tol), ctypes.byref(o),
                                                   self.R)

@@ -41,12 +41,15 @@ CASES += [("tiny", 2, (20.0, 20.0, 20.0), 1e-6), ("confined", 5000, (60.0, 60.0,
           ("tall", 3000, (6.0, 7.0, 90.0), 1e-4), ("dense", 100000, (10.0, 10.0, 10.0), 1e-8)]
 
 
+@pytest.mark.parametrize("window", ["gs", "kb"])
 @pytest.mark.parametrize("name,N,L,tol", CASES)
-def test_plan_rules_match_oracle(name, N, L, tol):
-    lib_p = B.choose_params(N, L, tol)
-    ora = dataclasses.asdict(make_plan(N, *L, tol))
+def test_plan_rules_match_oracle(name, N, L, tol, window):
+    lib_p = B.choose_params(N, L, tol, window=window)
+    ora = dataclasses.asdict(make_plan(N, *L, tol, window=window))
     for k, v in ora.items():
-        if isinstance(v, int):
+        if k == "window":
+            assert lib_p[k] == B.WINDOWS[v]
+        elif isinstance(v, int):
             assert lib_p[k] == v, (k, lib_p[k], v)
         else:
             assert abs(lib_p[k] - v) <= 1e-13 * abs(v), (k, lib_p[k], v)
