@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--rc-factor", type=float, default=None, help="override rule R2's r_c factor (plan knob)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
+    ap.add_argument("--window", default="gs", choices=["gs", "kb"],
+                    help="mid/long window: Gaussian (Eq. eq::GS) or Kaiser-Bessel polynomials (DESIGN.md R6-KB)")
     ap.add_argument("--parallelism", default="xslab", choices=["xslab", "replicas"],
                     help="N>1: x-slab decomposition of one system (strong scaling, NCCL) or replicas")
     return ap.parse_args()
@@ -132,7 +134,7 @@ def barrier(ws):
         dist.barrier()
 
 
-def oracle_sample(cfg, tol, target_seconds=15.0):
+def oracle_sample(cfg, tol, target_seconds=15.0, window="gs"):
     """The oracle as it stands on a bounded sample of the workload: a system of the same
     density and aspect ratio, N chosen so one evaluation takes ~target_seconds."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -142,7 +144,7 @@ def oracle_sample(cfg, tol, target_seconds=15.0):
     n = 2000
     while True:
         xyz, q, L = config_system(cfg, N=n)
-        op = make_plan(n, *L, tol)
+        op = make_plan(n, *L, tol, window=window)
         t0 = time.perf_counter()
         O.evaluate(op, xyz, q)
         dt = time.perf_counter() - t0
@@ -156,11 +158,11 @@ def run_reference(args, ws, rank):
         return
     c = CONFIGS[args.config]
     tol = args.tol or c.tol
-    n, dt0, L = oracle_sample(args.config, tol)
+    n, dt0, L = oracle_sample(args.config, tol, window=args.window)
     import oracle.sog as O
     from oracle.plan import make_plan
     xyz, q, L = config_system(args.config, N=n)
-    op = make_plan(n, *L, tol)
+    op = make_plan(n, *L, tol, window=args.window)
     for _ in range(min(args.warmup, 1)):
         O.evaluate(op, xyz, q)
     t0 = time.perf_counter()
@@ -254,7 +256,7 @@ def run_xslab(args, ws, rank, local):
     counts = np.bincount(owner, minlength=ws)
     mine = np.nonzero(owner == rank)[0]
     stream = torch.cuda.current_stream()
-    plan = DistPlan.from_process_group(N, int(counts.max()), L, tol, stream=stream)
+    plan = DistPlan.from_process_group(N, int(counts.max()), L, tol, stream=stream, window=args.window)
     xd = torch.from_numpy(np.ascontiguousarray(xyz[mine])).cuda()
     qd = torch.from_numpy(np.ascontiguousarray(q[mine])).cuda()
     phi = torch.empty(len(mine), dtype=torch.float64, device="cuda")
@@ -300,6 +302,7 @@ def run_xslab(args, ws, rank, local):
                    "N": N, "tol": tol, "parallelism": f"xslab{ws} (NCCL: particle halos, pencil all-to-all "
                                                     f"FFT, Psi edge planes, long-grid all-reduce)",
                    "l2": "working set >> 126 MB L2; no flush",
+                   "window": args.window,
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc",
                                               "slab_planes", "halo")}},
         "roofline": None,
@@ -333,7 +336,7 @@ def main():
     N = len(q)
     stream = torch.cuda.current_stream()
     plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision, eta=args.eta,
-                rc_factor=args.rc_factor)
+                rc_factor=args.rc_factor, window=args.window)
     xd = torch.from_numpy(xyz).cuda()
     qd = torch.from_numpy(q).cuda()
     phi = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -389,7 +392,7 @@ def main():
                "host_wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n, dt, Ls = oracle_sample(args.config, tol)
+        n, dt, Ls = oracle_sample(args.config, tol, window=args.window)
         cpu = {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "oracle",
                "sample": f"one full oracle evaluation of a {args.config}-density system, N={n}, "
                          f"box {Ls[0]:.2f}x{Ls[1]:.2f}x{Ls[2]:.2f}, tol {tol:g}, 1 host thread"}
@@ -402,6 +405,7 @@ def main():
                                f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
                    "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",
                    "l2": "working set (mid grid %.1f GB) >> 126 MB L2; no flush" % (d["Ix"] * d["Iy"] * d["Izs"] * 8 / 1e9),
+                   "window": args.window,
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc")}},
         "stages_ms": acc,
         "roofline": roof,

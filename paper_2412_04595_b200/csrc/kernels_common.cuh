@@ -82,6 +82,42 @@ __device__ __forceinline__ void window_weights_rec(double x, int g0, double h, d
     }
 }
 
+// R6-KB (Kaiser-Bessel window as polynomials, Remark rmk::PWindow P:477-480): the particle's
+// offset from its nearest grid point u = x/h + I/2 - g0 in [-1/2, 1/2], rounded as the oracle does
+__device__ __forceinline__ double kb_offset(double x, double h, double halfI, int g0) {
+    return __dsub_rn(__dadd_rn(__ddiv_rn(x, h), halfI), (double)g0);
+}
+
+// W_j(u) = sum_n c[n P + j] u^n at the P stencil points (Horner, P independent chains) and
+// dW_j/du; c is the plan's monomial table (host build_kb_poly), read as uniform loads.
+template <int P, bool GRAD>
+__device__ __forceinline__ void kb_weights(double u, const double* __restrict__ c, int nu, double* W, double* dW) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        W[j] = __ldg(c + nu * P + j);
+        if (GRAD) dW[j] = 0.0;
+    }
+    for (int n = nu - 1; n >= 0; --n) {
+        const double* cn = c + n * P;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            if (GRAD) dW[j] = fma(dW[j], u, W[j]);
+            W[j] = fma(W[j], u, __ldg(cn + j));
+        }
+    }
+}
+
+// one stencil point of a runtime-P table: W_j(u), dW_j/du in *dw
+__device__ __forceinline__ double kb_point(const double* __restrict__ c, int P, int nu, int j, double u, double* dw) {
+    double w = __ldg(c + nu * P + j), d = 0.0;
+    for (int n = nu - 1; n >= 0; --n) {
+        d = fma(d, u, w);
+        w = fma(w, u, __ldg(c + n * P + j));
+    }
+    if (dw) *dw = d;
+    return w;
+}
+
 __device__ __forceinline__ int wrap(int g, int I) {
     g %= I;
     return g < 0 ? g + I : g;

@@ -25,7 +25,26 @@ struct LongArgs {
     double two_over_Lz;
     double A;                 // h_x h_y
     const double* C;          // [Pc][Pc] Chebyshev -> Lagrange
+    const double* kbc;        // R6-KB monomial table [nu + 1][Pl] (window = KB), else null
+    int nu, kb;               // KB polynomial degree; kb = 1 for the KB window
 };
+
+// x or y weights of the long window at the Pl points g0-p..g0+p: Gaussian recurrence or the
+// KB polynomials (dW/dx = dW/du / h)
+template <int P, bool GRAD>
+__device__ __forceinline__ void long_weights(const LongArgs& a, double x, int g0, double h, double half,
+                                             double invH2S, double gamma, double* W, double* dW) {
+    if (a.kb) {
+        kb_weights<P, GRAD>(kb_offset(x, h, half, g0), a.kbc, a.nu, W, dW);
+        if (GRAD) {
+            const double ih = 1.0 / h;
+#pragma unroll
+            for (int j = 0; j < P; ++j) dW[j] *= ih;
+        }
+    } else {
+        window_weights_rec<P, GRAD>(x, g0, h, half, invH2S, gamma, W, dW);
+    }
+}
 
 // S10: one thread per (half mode, a).
 template <typename C = cuDoubleComplex>
@@ -121,8 +140,8 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
             d4 r = ld_d4(&a.pos[j]);
             int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
             double wx[P], wy[P];
-            window_weights_rec<P, false>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
-            window_weights_rec<P, false>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
+            long_weights<P, false>(a, r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
+            long_weights<P, false>(a, r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
 #pragma unroll
             for (int u = 0; u < P; ++u) { sW[tid * 2 * P + u] = wx[u]; sW[tid * 2 * P + P + u] = wy[u]; }
             sQ[tid] = r.w;
@@ -223,8 +242,8 @@ __global__ void __launch_bounds__(128) k_long_gather2(LongArgs a, const double* 
     d4 r = ld_d4(&a.pos[i]);
     const int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
     double wx[P], wy[P], dwx[P], dwy[P];
-    window_weights_rec<P, true>(r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
-    window_weights_rec<P, true>(r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
+    long_weights<P, true>(a, r.x, gx0, a.hx, a.halfx, a.invH2Sx, gamma_x, wx, dwx);
+    long_weights<P, true>(a, r.y, gy0, a.hy, a.halfy, a.invH2Sy, gamma_y, wy, dwy);
     // Chebyshev T_n, T_n' at x = 2z/Lz (zero beyond Pc): the T-basis field Psi~ (see top)
     const double x = r.z * a.two_over_Lz;
     double L[PCMAX], dL[PCMAX];
@@ -324,13 +343,21 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
         const unsigned ow = (unsigned)g0[j].w;
         if (role == 0) {
             const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
-            const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
-            double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
             int c = sx < 0 ? sx + a.Ilx : sx;
-            for (int u = 0; u < P; ++u) {
-                rx[c] = T(r.w * w);
-                w *= q; q *= gamma_x;
-                c = c + 1 == a.Ilx ? 0 : c + 1;
+            if (a.kb) {
+                const double u0 = kb_offset(r.x, a.hx, a.halfx, sx + (P - 1) / 2);
+                for (int u = 0; u < P; ++u) {
+                    rx[c] = T(r.w * kb_point(a.kbc, P, a.nu, u, u0, nullptr));
+                    c = c + 1 == a.Ilx ? 0 : c + 1;
+                }
+            } else {
+                const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
+                double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
+                for (int u = 0; u < P; ++u) {
+                    rx[c] = T(r.w * w);
+                    w *= q; q *= gamma_x;
+                    c = c + 1 == a.Ilx ? 0 : c + 1;
+                }
             }
             const double x = r.z * a.two_over_Lz;
             double tm = 1.0, tc = x;
@@ -343,13 +370,21 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
             }
         } else {
             const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
-            const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
-            double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
             int c = sy < 0 ? sy + a.Ily : sy;
-            for (int v = 0; v < P; ++v) {
-                ry[c] = T(w);
-                w *= q; q *= gamma_y;
-                c = c + 1 == a.Ily ? 0 : c + 1;
+            if (a.kb) {
+                const double u0 = kb_offset(r.y, a.hy, a.halfy, sy + (P - 1) / 2);
+                for (int v = 0; v < P; ++v) {
+                    ry[c] = T(kb_point(a.kbc, P, a.nu, v, u0, nullptr));
+                    c = c + 1 == a.Ily ? 0 : c + 1;
+                }
+            } else {
+                const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
+                double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
+                for (int v = 0; v < P; ++v) {
+                    ry[c] = T(w);
+                    w *= q; q *= gamma_y;
+                    c = c + 1 == a.Ily ? 0 : c + 1;
+                }
             }
         }
     };
@@ -444,6 +479,25 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
             const unsigned ow = (unsigned)g0[j].w;
             sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
             sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
+            if (a.kb) {
+                const double ux = kb_offset(r.x, a.hx, a.halfx, sx + (P - 1) / 2);
+                const double uy = kb_offset(r.y, a.hy, a.halfy, sy + (P - 1) / 2);
+                const double ihx = 1.0 / a.hx, ihy = 1.0 / a.hy;
+                int c = sx < 0 ? sx + a.Ilx : sx;
+                for (int u = 0; u < P; ++u) {
+                    double dw;
+                    sRx[c * 128 + tid] = T(kb_point(a.kbc, P, a.nu, u, ux, &dw));
+                    sdRx[c * 128 + tid] = T(dw * ihx);
+                    c = c + 1 == a.Ilx ? 0 : c + 1;
+                }
+                c = sy < 0 ? sy + a.Ily : sy;
+                for (int v = 0; v < P; ++v) {
+                    double dw;
+                    sRy[c * 128 + tid] = T(kb_point(a.kbc, P, a.nu, v, uy, &dw));
+                    sdRy[c * 128 + tid] = T(dw * ihy);
+                    c = c + 1 == a.Ily ? 0 : c + 1;
+                }
+            } else {
             {
                 const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
                 double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
@@ -467,6 +521,7 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
                     w *= q; q *= gam;
                     c = c + 1 == a.Ily ? 0 : c + 1;
                 }
+            }
             }
         }
         const double x = r.z * a.two_over_Lz;

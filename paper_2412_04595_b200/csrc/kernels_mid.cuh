@@ -123,6 +123,8 @@ struct MidZArgs {
     const d4* mpos;
     const int4* minfo;                    // (cell-sorted index, s_x, s_y, s_z) unwrapped starts
     const int* mstart;                    // [ntx*nty*nzc + 1]
+    const double* kbc;                    // R6-KB monomial table [nu + 1][P] (window = KB), else null
+    int nu, kb;                           // KB polynomial degree; kb = 1 for the KB window
 };
 
 // spread record in shared memory: [q Wx (P)] [Wy (P)] [Wz placed at offset o = s_z - chunk
@@ -186,7 +188,7 @@ __device__ __forceinline__ void spread_flush(T (&acc)[SRec<P, T>::NACC], int c, 
 // masks) into K batch buffers; 8 consumer warps (one 4 x 8 column patch each) accumulate
 // their patch's particles.  full/empty mbarriers let consumer warps drift up to K batches
 // apart, so the per-batch imbalance between patches averages out.
-template <int P, typename T = double>
+template <int P, typename T = double, bool KB = false>
 __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spread_z(MidZArgs a, T* __restrict__ grid) {
     using R = SRec<P, T>;
     using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
@@ -316,20 +318,36 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                 *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, 0, c);
                 if (mask) {
                     const d4 r = ld_d4(&a.mpos[k]);
-                    double wx[P], wy[P], wz[P];
-                    window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
-                    window_weights_rec<P, false>(r.y, in.z + p, a.hy, a.halfy, a.invH2Sy, a.gamma_y, wy, nullptr);
-                    window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
-#pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        rec[R::WX + i] = T(r.w * wx[i]);
-                        rec[R::WY + i] = T(wy[i]);
-                    }
                     const int o = in.w - c * MZ_ZC;      // z offset of the stencil in the window
+                    if constexpr (KB) {
+                        // one axis at a time (P live weights, no spills at wide supports)
+                        double w[P];
+                        kb_weights<P, false>(kb_offset(r.x, a.hx, a.halfx, in.y + p), a.kbc, a.nu, w, nullptr);
 #pragma unroll
-                    for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
+                        for (int i = 0; i < P; ++i) rec[R::WX + i] = T(r.w * w[i]);
+                        kb_weights<P, false>(kb_offset(r.y, a.hy, a.halfy, in.z + p), a.kbc, a.nu, w, nullptr);
 #pragma unroll
-                    for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(wz[i]);
+                        for (int i = 0; i < P; ++i) rec[R::WY + i] = T(w[i]);
+#pragma unroll
+                        for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
+                        kb_weights<P, false>(kb_offset(r.z, a.hz, a.halfz, in.w + p), a.kbc, a.nu, w, nullptr);
+#pragma unroll
+                        for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(w[i]);
+                    } else {
+                        double wx[P], wy[P], wz[P];
+                        window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
+                        window_weights_rec<P, false>(r.y, in.z + p, a.hy, a.halfy, a.invH2Sy, a.gamma_y, wy, nullptr);
+                        window_weights_rec<P, false>(r.z, in.w + p, a.hz, a.halfz, a.invH2Sz, a.gamma_z, wz, nullptr);
+#pragma unroll
+                        for (int i = 0; i < P; ++i) {
+                            rec[R::WX + i] = T(r.w * wx[i]);
+                            rec[R::WY + i] = T(wy[i]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
+#pragma unroll
+                        for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(wz[i]);
+                    }
                 }
             }
             sMask[buf][s] = (unsigned char)mask;
@@ -410,7 +428,7 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
 // particle at a time, lanes over the P x P stencil columns (z contracted per lane, then the
 // separable x/y weights), and reduces the four values with shuffles.  Three lanes compute
 // the particle's separable weights (Gaussian recurrence, one axis each).
-template <int P, typename T = double>
+template <int P, typename T = double, bool KB = false>
 struct GRing {
     static constexpr int WX = MZ_TX + P - 1, WY = MZ_TY + P - 1;
     static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
@@ -418,7 +436,8 @@ struct GRing {
     static constexpr int D = MZ_ZC + P - 1;                       // planes a chunk reads
     static constexpr int DR = D + MZ_ZC;                          // ring: + the next chunk's planes (prefetch)
     static constexpr int AL = 16 / int(sizeof(T));
-    static constexpr int HOFF = ((3 * P + 3 + AL - 1) / AL) * AL; // [Wx Wy Wz | d0x d0y d0z] then hdr
+    // [Wx Wy Wz | d0x d0y d0z] (Gaussian: W' from W and d0) or [Wx Wy Wz | W'x W'y W'z] (KB), then hdr
+    static constexpr int HOFF = (((KB ? 6 * P : 3 * P + 3) + AL - 1) / AL) * AL;
     static constexpr int WSZ = HOFF + AL;                         // per-particle weight scratch
     static constexpr int WB = 4;                                  // particles per warp batch
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
@@ -444,10 +463,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // separable weights of WB particles at once (lane = particle x axis, Gaussian recurrence) and
 // gathers them one at a time, lanes over the P x P columns (z contracted per lane, W' from the
 // stored W), 4-value butterfly reduction.
-template <int P, typename T = double>
-__global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArgs a, const T* __restrict__ psi,
-                                                                          d4* __restrict__ out) {
-    using G = GRing<P, T>;
+template <int P, typename T = double, bool KB = false>
+__global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(MidZArgs a, const T* __restrict__ psi,
+                                                                              d4* __restrict__ out) {
+    using G = GRing<P, T, KB>;
     constexpr int DR = G::DR, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
     extern __shared__ __align__(16) unsigned char smraw[];
     T* sm = reinterpret_cast<T*>(smraw);
@@ -521,17 +540,28 @@ __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArg
                 const double gg = axl == 0 ? a.gamma_x : (axl == 1 ? a.gamma_y : a.gamma_z);
                 const double x = axl == 0 ? r.x : (axl == 1 ? r.y : r.z);
                 const int sa = axl == 0 ? in.y : (axl == 1 ? in.z : in.w);
-                const double d0 = ((double)sa - hf) * hh - x;
-                double w = exp(-aa * d0 * d0);
-                double q = exp(-aa * hh * (2.0 * d0 + hh));
                 T* o = wsb + pp * G::WSZ + axl * P;
+                if constexpr (KB) {
+                    double w[P], dw[P];
+                    kb_weights<P, true>(kb_offset(x, hh, hf, sa + (P - 1) / 2), a.kbc, a.nu, w, dw);
+                    const double ih = 1.0 / hh;
 #pragma unroll
-                for (int i = 0; i < P; ++i) {
-                    o[i] = T(w);
-                    w *= q;
-                    q *= gg;
+                    for (int i = 0; i < P; ++i) {
+                        o[i] = T(w[i]);
+                        o[3 * P + i] = T(dw[i] * ih);          // dW/dx = dW/du / h
+                    }
+                } else {
+                    const double d0 = ((double)sa - hf) * hh - x;
+                    double w = exp(-aa * d0 * d0);
+                    double q = exp(-aa * hh * (2.0 * d0 + hh));
+#pragma unroll
+                    for (int i = 0; i < P; ++i) {
+                        o[i] = T(w);
+                        w *= q;
+                        q *= gg;
+                    }
+                    wsb[pp * G::WSZ + 3 * P + axl] = T(d0);   // for W' = 2 a (d0 + i h) W
                 }
-                wsb[pp * G::WSZ + 3 * P + axl] = T(d0);       // for W' = 2 a (d0 + i h) W
                 if (axl == 0) {
                     int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + G::HOFF);
                     hd[0] = a.px ? in.y - X0 + (in.y < 0 ? a.Ix : 0) : in.y - a.xorig - X0;   // relative to the tile
@@ -551,7 +581,7 @@ __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArg
 #pragma unroll
                 for (int i = 0; i < P; ++i) {
                     wz[i] = wsc[2 * P + i];
-                    dwz[i] = az2 * (d0z + T(i) * hzT) * wz[i];
+                    dwz[i] = KB ? wsc[5 * P + i] : az2 * (d0z + T(i) * hzT) * wz[i];
                 }
                 int pb[P];                               // ring plane offsets of the P stencil planes
                 {
@@ -573,8 +603,8 @@ __global__ void __launch_bounds__(256, GRing<P, T>::MINB) k_mid_gather_z(MidZArg
                         t1 = fma(dwz[kz], v, t1);
                     }
                     const T wx = wsc[ca[rr]], wy = wsc[P + cbb[rr]];
-                    const T dwx = ax2 * (d0x + T(ca[rr]) * hxT) * wx;
-                    const T dwy = ay2 * (d0y + T(cbb[rr]) * hyT) * wy;
+                    const T dwx = KB ? wsc[3 * P + ca[rr]] : ax2 * (d0x + T(ca[rr]) * hxT) * wx;
+                    const T dwy = KB ? wsc[4 * P + cbb[rr]] : ay2 * (d0y + T(cbb[rr]) * hyT) * wy;
                     const T wxy = wx * wy;
                     phi = fma(wxy, t0, phi);
                     gz = fma(wxy, t1, gz);
@@ -621,15 +651,24 @@ __global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* 
         if (lane < 3) {
             const double x = lane == 0 ? r.x : (lane == 1 ? r.y : r.z);
             const int s = lane == 0 ? in.y : (lane == 1 ? in.z : in.w);
-            const double d0 = ((double)s - half) * h - x;
-            double w = exp(-al * d0 * d0);
-            double q = exp(-al * h * (2.0 * d0 + h));
             double* o = wsc + 2 * lane * P;
-            for (int i = 0; i < P; ++i) {
-                o[i] = w;
-                o[P + i] = 2.0 * al * (d0 + i * h) * w;
-                w *= q;
-                q *= gam;
+            if (a.kb) {
+                double w[P], dw[P];
+                kb_weights<P, true>(kb_offset(x, h, half, s + (P - 1) / 2), a.kbc, a.nu, w, dw);
+                for (int i = 0; i < P; ++i) {
+                    o[i] = w[i];
+                    o[P + i] = dw[i] / h;
+                }
+            } else {
+                const double d0 = ((double)s - half) * h - x;
+                double w = exp(-al * d0 * d0);
+                double q = exp(-al * h * (2.0 * d0 + h));
+                for (int i = 0; i < P; ++i) {
+                    o[i] = w;
+                    o[P + i] = 2.0 * al * (d0 + i * h) * w;
+                    w *= q;
+                    q *= gam;
+                }
             }
         }
         __syncwarp();

@@ -24,13 +24,26 @@ int launch_mid_sort_place(const int* key, int N, int* cursor, int* tmp, const in
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
+// KB-window instantiations (R6-KB): supports up to 17 in fp64 (tol >= 2e-14 needs P <= 17),
+// up to 11 in fp32 mode (tol >= 1e-5)
+template <int P, typename T>
+constexpr bool kb_compiled() { return sizeof(T) == 8 ? P <= 17 : P <= 11; }
+
+template <int P, typename T, bool KB>
+int spread_go_w(const MidZArgs& a, int nseg, T* grid, cudaStream_t st) {
+    const size_t sh = SRec<P, T>::BYTES;
+    if (cudaFuncSetAttribute(k_mid_spread_z<P, T, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+        cudaSuccess)
+        return 2;
+    k_mid_spread_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), SRec<P, T>::NTHR, sh, st>>>(a, grid);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
 template <int P, typename T>
 int spread_go(const MidZArgs& a, int nseg, T* grid, cudaStream_t st) {
-    const size_t sh = SRec<P, T>::BYTES;
-    if (cudaFuncSetAttribute(k_mid_spread_z<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
-        return 2;
-    k_mid_spread_z<P, T><<<dim3(a.ntout * a.nty, nseg), SRec<P, T>::NTHR, sh, st>>>(a, grid);
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+    if (!a.kb) return spread_go_w<P, T, false>(a, nseg, grid, st);
+    if constexpr (kb_compiled<P, T>()) return spread_go_w<P, T, true>(a, nseg, grid, st);
+    return 1;
 }
 
 int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32, cudaStream_t st) {
@@ -44,19 +57,29 @@ int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32
     }
 }
 
+template <int P, typename T, bool KB>
+int gather_ring(const MidZArgs& a, int nseg, const T* psi, d4* out, cudaStream_t st) {
+    const size_t sh = GRing<P, T, KB>::BYTES;
+    if (cudaFuncSetAttribute(k_mid_gather_z<P, T, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+        cudaSuccess)
+        return 2;
+    k_mid_gather_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
 template <int P, typename T>
 int gather_go(const MidZArgs& a, int nseg, int nmid, const T* psi, d4* out, cudaStream_t st) {
-    if constexpr (GRing<P, T>::FITS) {
-        const size_t sh = GRing<P, T>::BYTES;
-        if (cudaFuncSetAttribute(k_mid_gather_z<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
-            cudaSuccess)
-            return 2;
-        k_mid_gather_z<P, T><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+    if (!a.kb) {
+        if constexpr (GRing<P, T, false>::FITS) return gather_ring<P, T, false>(a, nseg, psi, out, st);
     } else {
-        if constexpr (sizeof(T) == 4) return 1;   // fp32 mode: ring gather only
-        else k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
+        if constexpr (kb_compiled<P, T>() && GRing<P, T, true>::FITS) return gather_ring<P, T, true>(a, nseg, psi, out, st);
     }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+    if constexpr (sizeof(T) == 4) {
+        return 1;   // fp32 mode: ring gather only
+    } else {
+        k_mid_gather_g<P><<<148 * 8, 256, 0, st>>>(a, psi, out, nmid);
+        return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+    }
 }
 
 int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void* psi, d4* out, bool f32,

@@ -25,12 +25,12 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
 
 
-def slab_plan(name, N, R, tol=1e-6, half=False):
+def slab_plan(name, N, R, tol=1e-6, half=False, window="gs"):
     xyz, q, L = config_system(name, N=N)
     if half:   # every particle in the lower half of x: the upper ranks own nothing
         xyz = xyz.copy()
         xyz[:, 0] = -0.5 * L[0] + 0.5 * (xyz[:, 0] + 0.5 * L[0])
-    op = make_plan(len(q), *L, tol)
+    op = make_plan(len(q), *L, tol, window=window)
     if op.m >= 0 and op.Ix % R:
         ix = op.Ix
         while ix % R or ix % 2:
@@ -70,6 +70,15 @@ def test_loopback_cube_matches_single_and_oracle(R):
     xyz, q, L, op, params = slab_plan("c5", 20000, R)
     phi, F, p1, F1, d = run_slabs(xyz, q, L, op, params, R)
     assert d["ranks"] == R and d["slab_planes"] * R == d["Ix"]
+    assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
+    phi_o, F_o = O.evaluate(op, xyz, q)
+    assert rel(phi, phi_o) <= 1e-12 and rel(F, F_o) <= 1e-12, (rel(phi, phi_o), rel(F, F_o))
+
+
+def test_loopback_kb_window_three_ranks():
+    """x-slab path with the Kaiser-Bessel window (R6-KB): equals the single-GPU plan and the oracle."""
+    xyz, q, L, op, params = slab_plan("c5", 20000, 3, window="kb")
+    phi, F, p1, F1, _ = run_slabs(xyz, q, L, op, params, 3)
     assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
     phi_o, F_o = O.evaluate(op, xyz, q)
     assert rel(phi, phi_o) <= 1e-12 and rel(F, F_o) <= 1e-12, (rel(phi, phi_o), rel(F, F_o))
