@@ -88,34 +88,55 @@ __device__ __forceinline__ double kb_offset(double x, double h, double halfI, in
     return __dsub_rn(__dadd_rn(__ddiv_rn(x, h), halfI), (double)g0);
 }
 
-// W_j(u) = sum_n c[n P + j] u^n at the P stencil points (Horner, P independent chains) and
-// dW_j/du; c is the plan's monomial table (host build_kb_poly), read as uniform loads.
+// R6-KB monomial table, carried by value in the kernel arguments (constant bank): c[n P + j] is
+// the u^n coefficient of stencil point j, n = 0..P+3 (degrees nu < P + 3 are zero-padded), so
+// with P a compile-time constant every coefficient is an immediate constant-bank operand.
+constexpr int KB_PMAX = 17;
+constexpr int KB_TAB = KB_PMAX * (KB_PMAX + 4);
+struct KBTab {
+    double c[KB_TAB];
+};
+
+// W_j(u) = sum_n c[n P + j] u^n at the P stencil points (Horner, P independent chains) and dW_j/du
 template <int P, bool GRAD>
-__device__ __forceinline__ void kb_weights(double u, const double* __restrict__ c, int nu, double* W, double* dW) {
+__device__ __forceinline__ void kb_weights(double u, const KBTab& t, double* W, double* dW) {
+    static_assert(P <= KB_PMAX, "KB window support above KB_PMAX");
+    constexpr int NU = P + 3;
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-        W[j] = __ldg(c + nu * P + j);
+        W[j] = t.c[NU * P + j];
         if (GRAD) dW[j] = 0.0;
     }
-    for (int n = nu - 1; n >= 0; --n) {
-        const double* cn = c + n * P;
+#pragma unroll
+    for (int n = NU - 1; n >= 0; --n) {
 #pragma unroll
         for (int j = 0; j < P; ++j) {
             if (GRAD) dW[j] = fma(dW[j], u, W[j]);
-            W[j] = fma(W[j], u, __ldg(cn + j));
+            W[j] = fma(W[j], u, t.c[n * P + j]);
         }
     }
 }
 
-// one stencil point of a runtime-P table: W_j(u), dW_j/du in *dw
-__device__ __forceinline__ double kb_point(const double* __restrict__ c, int P, int nu, int j, double u, double* dw) {
-    double w = __ldg(c + nu * P + j), d = 0.0;
-    for (int n = nu - 1; n >= 0; --n) {
-        d = fma(d, u, w);
-        w = fma(w, u, __ldg(c + n * P + j));
+// runtime-P front end: f(j, W_j, dW_j/du) for j < P (P odd in [5, KB_PMAX])
+template <int P, bool GRAD, class F>
+__device__ __forceinline__ void kb_emit(double u, const KBTab& t, F& f) {
+    double W[P], dW[P];
+    kb_weights<P, GRAD>(u, t, W, dW);
+#pragma unroll
+    for (int j = 0; j < P; ++j) f(j, W[j], GRAD ? dW[j] : 0.0);
+}
+template <bool GRAD, class F>
+__device__ __forceinline__ void kb_emit_rt(int P, double u, const KBTab& t, F& f) {
+    switch (P) {
+        case 5: kb_emit<5, GRAD>(u, t, f); break;
+        case 7: kb_emit<7, GRAD>(u, t, f); break;
+        case 9: kb_emit<9, GRAD>(u, t, f); break;
+        case 11: kb_emit<11, GRAD>(u, t, f); break;
+        case 13: kb_emit<13, GRAD>(u, t, f); break;
+        case 15: kb_emit<15, GRAD>(u, t, f); break;
+        case 17: kb_emit<17, GRAD>(u, t, f); break;
+        default: break;
     }
-    if (dw) *dw = d;
-    return w;
 }
 
 __device__ __forceinline__ int wrap(int g, int I) {

@@ -25,8 +25,8 @@ struct LongArgs {
     double two_over_Lz;
     double A;                 // h_x h_y
     const double* C;          // [Pc][Pc] Chebyshev -> Lagrange
-    const double* kbc;        // R6-KB monomial table [nu + 1][Pl] (window = KB), else null
-    int nu, kb;               // KB polynomial degree; kb = 1 for the KB window
+    int kb;                   // 1: Kaiser-Bessel window (R6-KB), table kt
+    KBTab kt;
 };
 
 // x or y weights of the long window at the Pl points g0-p..g0+p: Gaussian recurrence or the
@@ -35,7 +35,7 @@ template <int P, bool GRAD>
 __device__ __forceinline__ void long_weights(const LongArgs& a, double x, int g0, double h, double half,
                                              double invH2S, double gamma, double* W, double* dW) {
     if (a.kb) {
-        kb_weights<P, GRAD>(kb_offset(x, h, half, g0), a.kbc, a.nu, W, dW);
+        if constexpr (P <= KB_PMAX) kb_weights<P, GRAD>(kb_offset(x, h, half, g0), a.kt, W, dW);
         if (GRAD) {
             const double ih = 1.0 / h;
 #pragma unroll
@@ -345,11 +345,13 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
             const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
             int c = sx < 0 ? sx + a.Ilx : sx;
             if (a.kb) {
-                const double u0 = kb_offset(r.x, a.hx, a.halfx, sx + (P - 1) / 2);
-                for (int u = 0; u < P; ++u) {
-                    rx[c] = T(r.w * kb_point(a.kbc, P, a.nu, u, u0, nullptr));
-                    c = c + 1 == a.Ilx ? 0 : c + 1;
-                }
+                const double qw = r.w;
+                const int Il = a.Ilx;
+                auto put = [&](int u, double w, double) {
+                    const int cc = c + u;
+                    rx[cc >= Il ? cc - Il : cc] = T(qw * w);
+                };
+                kb_emit_rt<false>(P, kb_offset(r.x, a.hx, a.halfx, sx + (P - 1) / 2), a.kt, put);
             } else {
                 const double d0 = ((double)sx - a.halfx) * a.hx - r.x;
                 double w = exp(-a.invH2Sx * d0 * d0), q = exp(-a.invH2Sx * a.hx * (2.0 * d0 + a.hx));
@@ -372,11 +374,12 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
             const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
             int c = sy < 0 ? sy + a.Ily : sy;
             if (a.kb) {
-                const double u0 = kb_offset(r.y, a.hy, a.halfy, sy + (P - 1) / 2);
-                for (int v = 0; v < P; ++v) {
-                    ry[c] = T(kb_point(a.kbc, P, a.nu, v, u0, nullptr));
-                    c = c + 1 == a.Ily ? 0 : c + 1;
-                }
+                const int Il = a.Ily;
+                auto put = [&](int v, double w, double) {
+                    const int cc = c + v;
+                    ry[cc >= Il ? cc - Il : cc] = T(w);
+                };
+                kb_emit_rt<false>(P, kb_offset(r.y, a.hy, a.halfy, sy + (P - 1) / 2), a.kt, put);
             } else {
                 const double d0 = ((double)sy - a.halfy) * a.hy - r.y;
                 double w = exp(-a.invH2Sy * d0 * d0), q = exp(-a.invH2Sy * a.hy * (2.0 * d0 + a.hy));
@@ -483,20 +486,20 @@ __global__ void __launch_bounds__(128, 4) k_long_gather_bc(LongArgs a, const int
                 const double ux = kb_offset(r.x, a.hx, a.halfx, sx + (P - 1) / 2);
                 const double uy = kb_offset(r.y, a.hy, a.halfy, sy + (P - 1) / 2);
                 const double ihx = 1.0 / a.hx, ihy = 1.0 / a.hy;
-                int c = sx < 0 ? sx + a.Ilx : sx;
-                for (int u = 0; u < P; ++u) {
-                    double dw;
-                    sRx[c * 128 + tid] = T(kb_point(a.kbc, P, a.nu, u, ux, &dw));
-                    sdRx[c * 128 + tid] = T(dw * ihx);
-                    c = c + 1 == a.Ilx ? 0 : c + 1;
-                }
-                c = sy < 0 ? sy + a.Ily : sy;
-                for (int v = 0; v < P; ++v) {
-                    double dw;
-                    sRy[c * 128 + tid] = T(kb_point(a.kbc, P, a.nu, v, uy, &dw));
-                    sdRy[c * 128 + tid] = T(dw * ihy);
-                    c = c + 1 == a.Ily ? 0 : c + 1;
-                }
+                const int cx0 = sx < 0 ? sx + a.Ilx : sx, cy0 = sy < 0 ? sy + a.Ily : sy;
+                const int Ilx = a.Ilx, Ily = a.Ily;
+                auto putx = [&](int u, double w, double dw) {
+                    const int cc = cx0 + u >= Ilx ? cx0 + u - Ilx : cx0 + u;
+                    sRx[cc * 128 + tid] = T(w);
+                    sdRx[cc * 128 + tid] = T(dw * ihx);
+                };
+                auto puty = [&](int v, double w, double dw) {
+                    const int cc = cy0 + v >= Ily ? cy0 + v - Ily : cy0 + v;
+                    sRy[cc * 128 + tid] = T(w);
+                    sdRy[cc * 128 + tid] = T(dw * ihy);
+                };
+                kb_emit_rt<true>(P, ux, a.kt, putx);
+                kb_emit_rt<true>(P, uy, a.kt, puty);
             } else {
             {
                 const double d0 = ((double)sx - a.halfx) * a.hx - r.x;

@@ -123,8 +123,8 @@ struct MidZArgs {
     const d4* mpos;
     const int4* minfo;                    // (cell-sorted index, s_x, s_y, s_z) unwrapped starts
     const int* mstart;                    // [ntx*nty*nzc + 1]
-    const double* kbc;                    // R6-KB monomial table [nu + 1][P] (window = KB), else null
-    int nu, kb;                           // KB polynomial degree; kb = 1 for the KB window
+    int kb;                               // 1: Kaiser-Bessel window (R6-KB), table kt
+    KBTab kt;
 };
 
 // spread record in shared memory: [q Wx (P)] [Wy (P)] [Wz placed at offset o = s_z - chunk
@@ -322,15 +322,15 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                     if constexpr (KB) {
                         // one axis at a time (P live weights, no spills at wide supports)
                         double w[P];
-                        kb_weights<P, false>(kb_offset(r.x, a.hx, a.halfx, in.y + p), a.kbc, a.nu, w, nullptr);
+                        kb_weights<P, false>(kb_offset(r.x, a.hx, a.halfx, in.y + p), a.kt, w, nullptr);
 #pragma unroll
                         for (int i = 0; i < P; ++i) rec[R::WX + i] = T(r.w * w[i]);
-                        kb_weights<P, false>(kb_offset(r.y, a.hy, a.halfy, in.z + p), a.kbc, a.nu, w, nullptr);
+                        kb_weights<P, false>(kb_offset(r.y, a.hy, a.halfy, in.z + p), a.kt, w, nullptr);
 #pragma unroll
                         for (int i = 0; i < P; ++i) rec[R::WY + i] = T(w[i]);
 #pragma unroll
                         for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
-                        kb_weights<P, false>(kb_offset(r.z, a.hz, a.halfz, in.w + p), a.kbc, a.nu, w, nullptr);
+                        kb_weights<P, false>(kb_offset(r.z, a.hz, a.halfz, in.w + p), a.kt, w, nullptr);
 #pragma unroll
                         for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(w[i]);
                     } else {
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                 T* o = wsb + pp * G::WSZ + axl * P;
                 if constexpr (KB) {
                     double w[P], dw[P];
-                    kb_weights<P, true>(kb_offset(x, hh, hf, sa + (P - 1) / 2), a.kbc, a.nu, w, dw);
+                    kb_weights<P, true>(kb_offset(x, hh, hf, sa + (P - 1) / 2), a.kt, w, dw);
                     const double ih = 1.0 / hh;
 #pragma unroll
                     for (int i = 0; i < P; ++i) {
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(256) k_mid_gather_g(MidZArgs a, const double* 
             double* o = wsc + 2 * lane * P;
             if (a.kb) {
                 double w[P], dw[P];
-                kb_weights<P, true>(kb_offset(x, h, half, s + (P - 1) / 2), a.kbc, a.nu, w, dw);
+                if constexpr (P <= KB_PMAX) kb_weights<P, true>(kb_offset(x, h, half, s + (P - 1) / 2), a.kt, w, dw);
                 for (int i = 0; i < P; ++i) {
                     o[i] = w[i];
                     o[P + i] = dw[i] / h;

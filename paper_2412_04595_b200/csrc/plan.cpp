@@ -253,6 +253,7 @@ bool validate_params(const Params& p, std::string& err) {
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
     if (p.window != 0 && p.window != 1) return bad("window must be 0 (Gaussian) or 1 (Kaiser-Bessel)");
     if (p.window == 1) {
+        if ((p.m >= 0 && p.P > 17) || p.Pl > 17) return bad("KB window support must be <= 17");
         if (p.m >= 0 && (p.nu < 2 || p.nu > p.P + 3)) return bad("KB mid polynomial degree nu must be in [2, P+3]");
         if (p.nul < 2 || p.nul > p.Pl + 3) return bad("KB long polynomial degree nul must be in [2, Pl+3]");
         // deconvolution divides by the window transform: keep every grid mode inside its

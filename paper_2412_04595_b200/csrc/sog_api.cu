@@ -122,7 +122,7 @@ struct sog_plan {
     LongTileArgs lt{};
     cuDoubleComplex *lspec = nullptr, *lspec2 = nullptr;
     double *d_K = nullptr, *d_C = nullptr, *d_Tn = nullptr;
-    double *d_kbm = nullptr, *d_kbl = nullptr;   // R6-KB polynomial tables (mid, long)
+    KBTab kbl{};                                 // R6-KB long-window table (mid: in mz)
     bool long_small = false;        // small long grid: register-tiled spread + broadcast gather
     int lg_nblk = 0;
     double* lpart2 = nullptr;       // [lg_nblk][PCP][Ilx*Ily] spread partials
@@ -195,8 +195,7 @@ void free_plan(sog_plan* pl) {
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
-                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp,
-                    pl->d_kbm, pl->d_kbl};
+                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -210,6 +209,8 @@ void free_plan(sog_plan* pl) {
         if (e) cudaEventDestroy(e);
     delete pl;
 }
+
+void kb_table(int P, double beta, int nu, KBTab& t);
 
 int setup(sog_plan* pl) {
     Params& p = pl->p;
@@ -334,14 +335,7 @@ int setup(sog_plan* pl) {
             (rc = upload(pl, &pl->d_Tz, Tz)))
             return rc;
         z.kb = p.window == 1 ? 1 : 0;
-        z.nu = p.nu;
-        z.kbc = nullptr;
-        if (z.kb) {
-            std::vector<double> c;
-            build_kb_poly(p.P, p.S, p.nu, c);
-            if ((rc = upload(pl, &pl->d_kbm, c))) return rc;
-            z.kbc = pl->d_kbm;
-        }
+        if (z.kb) kb_table(p.P, p.S, p.nu, z.kt);
         size_t ws = 0;
         if (!slab) {
             // z-pruned 3D FFT: 2D (x,y) over the planes the spread writes, 1D along z on zero-padded
@@ -432,11 +426,7 @@ int setup(sog_plan* pl) {
         auto gam = [&](double h) { double H = (p.Pl - 1) * h / 2.0; return std::exp(-2.0 * p.Sl / (H * H) * h * h); };
         t.gamma_x = gam(p.hlx());
         t.gamma_y = gam(p.hly());
-        if (p.window == 1) {
-            std::vector<double> c;
-            build_kb_poly(p.Pl, p.Sl, p.nul, c);
-            if ((rc = upload(pl, &pl->d_kbl, c))) return rc;
-        }
+        if (p.window == 1) kb_table(p.Pl, p.Sl, p.nul, pl->kbl);
         int pcmax = p.Pc <= 16 ? 16 : 32;
         if ((rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
         if ((rc = dalloc(pl, &pl->lpsiT, (size_t)p.Ilx * p.Ily * 32))) return rc;
@@ -491,6 +481,15 @@ MidArgs mid_args(const sog_plan* pl) {
     return a;
 }
 
+// R6-KB table: the degree-nu monomial coefficients, zero-padded to degree P + 3 (kernels_common.cuh)
+void kb_table(int P, double beta, int nu, KBTab& t) {
+    std::vector<double> c;
+    build_kb_poly(P, beta, nu, c);
+    for (int i = 0; i < KB_TAB; ++i) t.c[i] = 0.0;
+    for (int n = 0; n <= nu; ++n)
+        for (int j = 0; j < P; ++j) t.c[n * P + j] = c[size_t(n) * P + j];
+}
+
 LongArgs long_args(const sog_plan* pl) {
     const Params& p = pl->p;
     LongArgs a;
@@ -506,8 +505,7 @@ LongArgs long_args(const sog_plan* pl) {
     a.A = a.hx * a.hy;
     a.C = pl->d_C;
     a.kb = p.window == 1 ? 1 : 0;
-    a.nu = p.nul;
-    a.kbc = pl->d_kbl;
+    a.kt = pl->kbl;
     return a;
 }
 
