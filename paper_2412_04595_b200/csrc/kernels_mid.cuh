@@ -394,23 +394,31 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                 if (2 * k + 1 < NACC) acc[2 * k + 1] = fma(cc, t.y, acc[2 * k + 1]);
             }
         };
+        // runs of same-chunk particles, two per step; the chunk flush (a register-window shift)
+        // stays outside the run loop so the accumulators keep fixed registers inside it
         int i = 0;
-        while (i < nmy) {                                // two particles per step when in one chunk
+        while (i < nmy) {
             const T* ra = base + sList[warp][i] * R::SIZE;
-            const int4 ha = *reinterpret_cast<const int4*>(ra + R::HDR);
-            const bool two = i + 1 < nmy;
-            const T* rb = base + sList[warp][two ? i + 1 : i] * R::SIZE;
-            const int4 hb = *reinterpret_cast<const int4*>(rb + R::HDR);
+            int4 ha = *reinterpret_cast<const int4*>(ra + R::HDR);
             while (cur < ha.w) {                         // warp-uniform: entering a later chunk
                 spread_flush<P, T>(acc, cur, cb, colok, cx, cy, a, grid);
                 ++cur;
             }
-            const T ca = coef(ra, ha);
-            const bool pair = two && hb.w == ha.w;
-            const T cbv = coef(rb, hb);
-            accum(ra, ca);
-            if (pair) accum(rb, cbv);
-            i += pair ? 2 : 1;
+            for (;;) {
+                const bool two = i + 1 < nmy;
+                const T* rb = base + sList[warp][two ? i + 1 : i] * R::SIZE;
+                const int4 hb = *reinterpret_cast<const int4*>(rb + R::HDR);
+                const bool pair = two && hb.w == cur;
+                const T ca = coef(ra, ha);
+                const T cbv = pair ? coef(rb, hb) : T(0);   // branch-free: zero weight when unpaired
+                accum(ra, ca);
+                accum(rb, cbv);
+                i += pair ? 2 : 1;
+                if (i >= nmy) break;
+                ra = base + sList[warp][i] * R::SIZE;
+                ha = *reinterpret_cast<const int4*>(ra + R::HDR);
+                if (ha.w != cur) break;
+            }
         }
         __syncwarp();
         mbar_arrive(&barEmpty[buf]);

@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kb.py tests/test_gpu_parity.py -x -q -m gpu -k "c1 or c2_tol or shapes or fp32 or edge or determinism" > gpurun_out/kb_tests.log 2>&1; echo tests=$?; tail -3 gpurun_out/kb_tests.log
+for w in gs kb; do
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --window $w > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?
+  python -c "import json;d=json.loads(open('gpurun_out/bench_$w.log').read().strip().splitlines()[-1]);print('$w', d['ms_per_step'], {k:round(v,2) for k,v in d['stages_ms'].items()})"
+done
