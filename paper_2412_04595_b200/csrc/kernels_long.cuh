@@ -323,25 +323,39 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
         for (int l = 0; l < LG_LT; ++l) acc[i][l] = 0.0;
     const int j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
     const int P = a.Pl;
-    // two threads per staged particle: role 0 -> Rx row and T row, role 1 -> Ry row
+    // threads per staged particle: 4 with >= 256 threads (Rx row, Ry row, T row, idle), else 2
+    // (Rx and T rows, Ry row)
+    const bool four = blockDim.x >= 4 * LG_KB;
     auto stage = [&](int base, int buf) {
-        const int t = tid >> 1, role = tid & 1;
+        const int t = four ? tid >> 2 : tid >> 1, role = four ? tid & 3 : tid & 1;
         if (t >= LG_KB) return;   // blockDim >= 2 * LG_KB = 128
+        const bool doX = role == 0, doY = role == 1, doT = four ? role == 2 : role == 0;
         T* row = sm + ((size_t)buf * LG_KB + t) * RW;
         T* rx = row;
         T* ry = row + RXP;
         T* tt = row + RXP + RYP;
-        if (role == 0) {
+        if (doX)
             for (int c = 0; c < RXP; ++c) rx[c] = T(0);
+        if (doT)
             for (int n = 0; n < PCP; ++n) tt[n] = T(0);
-        } else {
+        if (doY)
             for (int c = 0; c < RYP; ++c) ry[c] = T(0);
-        }
         const int j = base + t;
-        if (j >= j1) return;
+        if (j >= j1 || !(doX || doY || doT)) return;
         const d4 r = ld_d4(&a.pos[j]);
         const unsigned ow = (unsigned)g0[j].w;
-        if (role == 0) {
+        if (doT) {
+            const double x = r.z * a.two_over_Lz;
+            double tm = 1.0, tc = x;
+            tt[0] = T(1);
+            if (a.Pc > 1) tt[1] = T(x);
+            for (int n = 2; n < a.Pc; ++n) {
+                const double tn = 2.0 * x * tc - tm;
+                tt[n] = T(tn);
+                tm = tc; tc = tn;
+            }
+        }
+        if (doX) {
             const int sx = (int)(ow & 0xffffu) - 32768 - (P - 1) / 2;
             int c = sx < 0 ? sx + a.Ilx : sx;
             if (a.kb) {
@@ -361,16 +375,7 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
                     c = c + 1 == a.Ilx ? 0 : c + 1;
                 }
             }
-            const double x = r.z * a.two_over_Lz;
-            double tm = 1.0, tc = x;
-            tt[0] = T(1);
-            if (a.Pc > 1) tt[1] = T(x);
-            for (int n = 2; n < a.Pc; ++n) {
-                const double tn = 2.0 * x * tc - tm;
-                tt[n] = T(tn);
-                tm = tc; tc = tn;
-            }
-        } else {
+        } else if (doY) {
             const int sy = (int)(ow >> 16) - 32768 - (P - 1) / 2;
             int c = sy < 0 ? sy + a.Ily : sy;
             if (a.kb) {

@@ -271,22 +271,41 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
     if (warp >= 8) {
         // ---------------- producers: one particle per thread per batch ----------------
         const int s = (warp - 8) * 32 + lane;
+        // software pipeline: the candidate of batch bi + 1 is located and its (minfo, mpos) loads
+        // are in flight while batch bi's weights are computed
+        auto locate = [&](int idx, int& c) {
+            int lo = 0, hi = E;                          // last e with sPre[e] <= idx
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (sPre[mid] <= idx) lo = mid; else hi = mid;
+            }
+            c = cs + lo / nh;
+            SOG_ASSERT(lo >= 0 && lo < E);
+            return sBeg[lo] + (idx - sPre[lo]);
+        };
+        int4 in_n = make_int4(0, 0, 0, 0);
+        d4 r_n{0.0, 0.0, 0.0, 0.0};
+        int c_n = 0;
+        if (s < total) {
+            const int k = locate(s, c_n);
+            in_n = a.minfo[k];
+            r_n = ld_d4(&a.mpos[k]);
+        }
         for (int bi = 0; bi < nbat; ++bi) {
             const int buf = bi % K;
-            if (bi >= K) mbar_wait(&barEmpty[buf], ((bi / K) - 1) & 1);
             const int idx = bi * B + s;
+            const int4 in = in_n;
+            const d4 r = r_n;
+            const int c = c_n;
+            if (idx + B < total) {
+                const int k = locate(idx + B, c_n);
+                in_n = a.minfo[k];
+                r_n = ld_d4(&a.mpos[k]);
+            }
+            if (bi >= K) mbar_wait(&barEmpty[buf], ((bi / K) - 1) & 1);
             T* rec = sRec + (buf * B + s) * R::SIZE;
             unsigned mask = 0;
             if (idx < total) {
-                int lo = 0, hi = E;                      // last e with sPre[e] <= idx
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sPre[mid] <= idx) lo = mid; else hi = mid;
-                }
-                const int c = cs + lo / nh;
-                const int k = sBeg[lo] + (idx - sPre[lo]);
-                SOG_ASSERT(lo >= 0 && lo < E && k >= 0);
-                const int4 in = a.minfo[k];
                 SOG_ASSERT(in.w - c * MZ_ZC >= 0 && in.w - c * MZ_ZC < MZ_ZC);
                 int dx = a.px ? wrapc(in.y - X0, a.Ix) : in.y - a.xorig - X0, dy = wrapc(in.z - Y0, a.Iy);
                 unsigned mx = 0, my = 0;
@@ -317,7 +336,6 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                     if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
                 *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, 0, c);
                 if (mask) {
-                    const d4 r = ld_d4(&a.mpos[k]);
                     const int o = in.w - c * MZ_ZC;      // z offset of the stencil in the window
                     if constexpr (KB) {
                         // one axis at a time (P live weights, no spills at wide supports)
@@ -411,12 +429,16 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                 const bool pair = two && hb.w == cur;
                 const T ca = coef(ra, ha);
                 const T cbv = pair ? coef(rb, hb) : T(0);   // branch-free: zero weight when unpaired
+                i += pair ? 2 : 1;
+                // next step's record and header are loaded before this step's FMAs
+                const bool more = i < nmy;
+                const T* rn = base + sList[warp][more ? i : 0] * R::SIZE;
+                const int4 hn = *reinterpret_cast<const int4*>(rn + R::HDR);
                 accum(ra, ca);
                 accum(rb, cbv);
-                i += pair ? 2 : 1;
-                if (i >= nmy) break;
-                ra = base + sList[warp][i] * R::SIZE;
-                ha = *reinterpret_cast<const int4*>(ra + R::HDR);
+                if (!more) break;
+                ra = rn;
+                ha = hn;
                 if (ha.w != cur) break;
             }
         }
