@@ -84,8 +84,10 @@ struct LongTileArgs {
     int full_range;          // 1: every particle reaches every tile (small periodic grid)
     const int* start;        // cell start offsets (sorted order), for x-slab particle ranges
     int ncx, cells_per_x;    // near-cell grid: ncx slabs of cells_per_x = ncy*ncz cells
-    double cell_w;           // Lx / ncx
-    double Lx;
+    int ncy, ncz;
+    double cell_w, cell_wy;  // Lx / ncx, Ly / ncy
+    double Lx, Ly;
+    double* grid;            // nchunk == 1: tiles own their columns, written directly (no reduce)
     double gamma_x, gamma_y; // window recurrence constants exp(-2 a h^2)
     double* part;
 };
@@ -107,22 +109,53 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
     const int tile = blockIdx.y, chunk = blockIdx.x;
     const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    // particle index ranges reaching this tile (1 or 2 ranges of x-slabs)
-    int r0b = 0, r0e = a.N, r1b = 0, r1e = 0;
-    if (!t.full_range) {
-        // stencil centres gx0 in [X0 - p, X0 + TX - 1 + p] <=> x in [xlo, xhi)
-        double xlo = ((X0 - p) - 0.5 - 0.5 * a.Ilx) * a.hx, xhi = ((X0 + t.TX - 1 + p) + 0.5 - 0.5 * a.Ilx) * a.hx;
-        int c0 = (int)floor((xlo + 0.5 * t.Lx) / t.cell_w) - 1, c1 = (int)floor((xhi + 0.5 * t.Lx) / t.cell_w) + 1;
-        if (c1 - c0 + 1 >= t.ncx) { c0 = 0; c1 = t.ncx - 1; }
-        if (c0 < 0) {
-            r1b = t.start[(c0 + t.ncx) * t.cells_per_x]; r1e = a.N; c0 = 0;
-        } else if (c1 >= t.ncx) {
-            r1b = 0; r1e = t.start[(c1 - t.ncx + 1) * t.cells_per_x]; c1 = t.ncx - 1;
+    // particle index ranges reaching this tile: the near cells whose (x, y) extent overlaps the
+    // tile's stencil-centre box, one contiguous sorted range per (x column, y run) of cells (all
+    // z), at most LT_MAXR; beyond that whole x slabs (all y)
+    constexpr int LT_MAXR = 64;
+    __shared__ int sRb[LT_MAXR], sRp[LT_MAXR + 1], sNR;
+    if (tid == 0) {
+        int nr = 0, tot = 0;
+        auto add = [&](int b, int e) {
+            if (e > b) { sRb[nr] = b; sRp[nr] = tot; tot += e - b; ++nr; }
+        };
+        if (t.full_range) {
+            add(0, a.N);
+        } else {
+            // stencil centres gx0 in [X0 - p, X0 + TX - 1 + p] <=> x in [xlo, xhi); same in y
+            const double xlo = ((X0 - p) - 0.5 - 0.5 * a.Ilx) * a.hx, xhi = ((X0 + t.TX - 1 + p) + 0.5 - 0.5 * a.Ilx) * a.hx;
+            const double ylo = ((Y0 - p) - 0.5 - 0.5 * a.Ily) * a.hy, yhi = ((Y0 + t.TY - 1 + p) + 0.5 - 0.5 * a.Ily) * a.hy;
+            int c0 = (int)floor((xlo + 0.5 * t.Lx) / t.cell_w) - 1, c1 = (int)floor((xhi + 0.5 * t.Lx) / t.cell_w) + 1;
+            int d0 = (int)floor((ylo + 0.5 * t.Ly) / t.cell_wy) - 1, d1 = (int)floor((yhi + 0.5 * t.Ly) / t.cell_wy) + 1;
+            if (c1 - c0 + 1 >= t.ncx) { c0 = 0; c1 = t.ncx - 1; }
+            const bool ally = d1 - d0 + 1 >= t.ncy;
+            const int nxr = c1 - c0 + 1, nyr = ally ? 1 : (d0 < 0 || d1 >= t.ncy ? 2 : 1);
+            if (nxr * nyr > LT_MAXR - 2 || ally) {
+                // whole x slabs: [c0, c1] split at the periodic seam
+                if (c0 < 0) { add(t.start[(c0 + t.ncx) * t.cells_per_x], a.N); c0 = 0; }
+                if (c1 >= t.ncx) { add(0, t.start[(c1 - t.ncx + 1) * t.cells_per_x]); c1 = t.ncx - 1; }
+                add(t.start[c0 * t.cells_per_x], t.start[(c1 + 1) * t.cells_per_x]);
+            } else {
+                for (int c = c0; c <= c1; ++c) {
+                    const int cc = c < 0 ? c + t.ncx : (c >= t.ncx ? c - t.ncx : c);
+                    const int base = cc * t.ncy;
+                    if (d0 < 0) {
+                        add(t.start[(base + d0 + t.ncy) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
+                        add(t.start[base * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
+                    } else if (d1 >= t.ncy) {
+                        add(t.start[(base + d0) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
+                        add(t.start[base * t.ncz], t.start[(base + d1 - t.ncy + 1) * t.ncz]);
+                    } else {
+                        add(t.start[(base + d0) * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
+                    }
+                }
+            }
         }
-        r0b = t.start[c0 * t.cells_per_x];
-        r0e = t.start[(c1 + 1) * t.cells_per_x];
+        sRp[nr] = tot;
+        sNR = nr;
     }
-    const int n0 = r0e - r0b, ntot = n0 + (r1e - r1b);
+    __syncthreads();
+    const int nr = sNR, ntot = sRp[nr];
     const int per = (ntot + t.nchunk - 1) / t.nchunk;
     const int jb = min(ntot, chunk * per), je = min(ntot, jb + per);
     // my column
@@ -132,36 +165,56 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
 #pragma unroll
     for (int b = 0; b < PCMAX; ++b) acc[b] = 0.0;
     __syncthreads();
+    __shared__ int sCnt[2];
     for (int base = jb; base < je; base += LB) {
-        const int nb = min(LB, je - base);
-        if (tid < nb) {
-            int k = base + tid;
-            int j = k < n0 ? r0b + k : r1b + (k - n0);
-            d4 r = ld_d4(&a.pos[j]);
-            int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
+        const int nbr = min(LB, je - base);
+        // stage only the particles whose stencil meets this tile (ballot compaction, stream order)
+        bool rel = false;
+        d4 r{0.0, 0.0, 0.0, 0.0};
+        int gx0 = 0, gy0 = 0;
+        if (tid < nbr) {
+            const int k = base + tid;
+            int e = 0;
+            while (e + 1 < nr && sRp[e + 1] <= k) ++e;
+            const int j = sRb[e] + (k - sRp[e]);
+            r = ld_d4(&a.pos[j]);
+            gx0 = stencil_g0(r.x, a.hx, a.hpx);
+            gy0 = stencil_g0(r.y, a.hy, a.hpy);
+            // stencil [s, s + P) meets tile [X0, X0 + TX) (mod I) <=> d = (X0 - s) mod I < P or > I - TX
+            int dx = (X0 - (gx0 - p)) % a.Ilx, dy = (Y0 - (gy0 - p)) % a.Ily;
+            dx += dx < 0 ? a.Ilx : 0;
+            dy += dy < 0 ? a.Ily : 0;
+            rel = (dx < P || dx > a.Ilx - t.TX) && (dy < P || dy > a.Ily - t.TY);
+        }
+        unsigned bal = 0;
+        if (tid < LB) {
+            bal = __ballot_sync(0xffffffffu, rel);
+            if ((tid & 31) == 0) sCnt[tid >> 5] = __popc(bal);
+        }
+        __syncthreads();
+        const int nb = sCnt[0] + sCnt[1];
+        if (rel) {
+            const int slot = (tid >= 32 ? sCnt[0] : 0) + __popc(bal & ((1u << (tid & 31)) - 1));
             double wx[P], wy[P];
             long_weights<P, false>(a, r.x, gx0, a.hx, a.halfx, a.invH2Sx, t.gamma_x, wx, nullptr);
             long_weights<P, false>(a, r.y, gy0, a.hy, a.halfy, a.invH2Sy, t.gamma_y, wy, nullptr);
 #pragma unroll
-            for (int u = 0; u < P; ++u) { sW[tid * 2 * P + u] = wx[u]; sW[tid * 2 * P + P + u] = wy[u]; }
-            sQ[tid] = r.w;
-            sG[2 * tid] = gx0 - p;
-            sG[2 * tid + 1] = gy0 - p;
-            double x = r.z * a.two_over_Lz;
+            for (int u = 0; u < P; ++u) { sW[slot * 2 * P + u] = wx[u]; sW[slot * 2 * P + P + u] = wy[u]; }
+            sQ[slot] = r.w;
+            sG[2 * slot] = gx0 - p;
+            sG[2 * slot + 1] = gy0 - p;
+            // T basis: the layer coefficients are T_n(z_j) (S~_n), zero-padded to PCMAX
+            double* L = sL + slot * PCMAX;
+            const double x = r.z * a.two_over_Lz;
             double tm = 1.0, tc = x;
-            sT[tid * PCMAX] = 1.0;
-            if (Pc > 1) sT[tid * PCMAX + 1] = x;
+            L[0] = 1.0;
+            if (Pc > 1) L[1] = x;
             for (int n = 2; n < Pc; ++n) {
-                double tn = 2.0 * x * tc - tm;
-                sT[tid * PCMAX + n] = tn;
+                const double tn = 2.0 * x * tc - tm;
+                L[n] = tn;
                 tm = tc; tc = tn;
             }
-        }
-        __syncthreads();
-        // T-basis: the staged T_n(z_j) are the layer coefficients (S~_n)
-        for (int q = tid; q < nb * PCMAX; q += nthr) {
-            const int j = q / PCMAX, n = q % PCMAX;
-            sL[q] = n < Pc ? sT[j * PCMAX + n] : 0.0;
+            for (int n = Pc; n < PCMAX; ++n) L[n] = 0.0;
         }
         __syncthreads();
         if (own) {
@@ -186,9 +239,16 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
         __syncthreads();
     }
     if (own) {
-        double* o = t.part + (((size_t)tile * t.nchunk + chunk) * (t.TX * t.TY) + tid) * PCMAX;
+        if (t.nchunk == 1) {
+            const size_t G = (size_t)a.Ilx * a.Ily, g = (size_t)cx * a.Ily + cy;
 #pragma unroll
-        for (int b = 0; b < PCMAX; ++b) o[b] = acc[b];
+            for (int b = 0; b < PCMAX; ++b)
+                if (b < Pc) t.grid[b * G + g] = acc[b];
+        } else {
+            double* o = t.part + (((size_t)tile * t.nchunk + chunk) * (t.TX * t.TY) + tid) * PCMAX;
+#pragma unroll
+            for (int b = 0; b < PCMAX; ++b) o[b] = acc[b];
+        }
     }
 }
 

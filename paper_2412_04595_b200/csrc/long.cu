@@ -26,8 +26,11 @@ int long_tile_dispatch(const LongTileArgs& t, int Pl, cudaStream_t st) {
 }
 
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st) {
-    int r = t.a.Pc <= 16 ? long_tile_dispatch<16>(t, Pl, st) : (t.a.Pc <= 32 ? long_tile_dispatch<32>(t, Pl, st) : 1);
+    LongTileArgs tg = t;
+    tg.grid = grid;
+    int r = t.a.Pc <= 16 ? long_tile_dispatch<16>(tg, Pl, st) : (t.a.Pc <= 32 ? long_tile_dispatch<32>(tg, Pl, st) : 1);
     if (r) return r;
+    if (t.nchunk == 1) return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;   // tiles wrote the grid
     int pcmax = t.a.Pc <= 16 ? 16 : 32;
     int n = t.a.Ilx * t.a.Ily * t.a.Pc;
     k_long_reduce<<<(n + 255) / 256, 256, 0, st>>>(t.part, grid, t.a.Ilx, t.a.Ily, t.a.Pc, pcmax, t.TX, t.TY, t.nty,

@@ -418,17 +418,21 @@ int setup(sog_plan* pl) {
         t.full_range = (slab || t.TX + 2 * pl_half + 2 >= p.Ilx) ? 1 : 0;
         int ntile = t.ntx * t.nty;
         t.nchunk = std::max(1, std::min(4 * 148 / ntile + 1, int((p.N + 255) / 256)));
-        if (!t.full_range) t.nchunk = std::max(1, t.nchunk * 3);
+        if (!t.full_range && ntile < 4 * 148) t.nchunk = std::max(1, t.nchunk * 3);   // wide grids: tiles suffice
         t.ncx = pl->geo.ncx;
         t.cells_per_x = pl->geo.ncy * pl->geo.ncz;
         t.cell_w = p.Lx / pl->geo.ncx;
         t.Lx = p.Lx;
+        t.ncy = pl->geo.ncy;
+        t.ncz = pl->geo.ncz;
+        t.cell_wy = p.Ly / pl->geo.ncy;
+        t.Ly = p.Ly;
         auto gam = [&](double h) { double H = (p.Pl - 1) * h / 2.0; return std::exp(-2.0 * p.Sl / (H * H) * h * h); };
         t.gamma_x = gam(p.hlx());
         t.gamma_y = gam(p.hly());
         if (p.window == 1) kb_table(p.Pl, p.Sl, p.nul, pl->kbl);
         int pcmax = p.Pc <= 16 ? 16 : 32;
-        if ((rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
+        if (t.nchunk > 1 && (rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
         if ((rc = dalloc(pl, &pl->lpsiT, (size_t)p.Ilx * p.Ily * 32))) return rc;
         long long n[2] = {p.Ilx, p.Ily};
         size_t ws = 0;

@@ -13,7 +13,8 @@ monovalent particles satisfying the charge neutrality condition"):
     possible; odd N gets a final charge 0.
 Seeds: numpy.random.default_rng(2412_04595 + config_index).
 
-The BASELINE.json configurations are listed in CONFIGS (c1..c5).
+The BASELINE.json configurations are listed in CONFIGS (c1..c5); s1 is the paper's strongly
+confined workload (NEXT #3 evidence).
 """
 from __future__ import annotations
 
@@ -32,6 +33,7 @@ class Config:
     tol: float
     index: int           # seed offset (BASELINE.json configs[index-1])
     note: str = ""
+    scale: str = "volume"  # resizing rule for other N: "volume" (keep density and shape) or "area" (keep Lz)
 
 
 # BASELINE.json "configs" (index 1..5); c2 is swept over tolerances.
@@ -41,6 +43,10 @@ CONFIGS = {
     "c3": Config("c3", 1_000_000, (200.0, 200.0, 25.0), 1e-6, 3, "N=1e6 slab 200x200x25"),
     "c4": Config("c4", 1_000_000, (50.0, 50.0, 400.0), 1e-6, 4, "N=1e6 tall box 50x50x400"),
     "c5": Config("c5", 10_000_000, (215.0, 215.0, 215.0), 1e-6, 5, "N=1e7 cube 215^3"),
+    # not a BASELINE config: the paper's strongly confined workload (Table 5, P:1066, P:1096-1125:
+    # surface density N/(Lx Ly) = 1.1, Lz = 0.3, gamma = Lx/Lz ~ 3200 at N = 1e6), SURVEY 8(f) NEXT #3
+    "s1": Config("s1", 1_000_000, (953.46, 953.46, 0.3), 1e-6, 6,
+                 "N=1e6 strongly confined, surface density 1.1, Lz=0.3 (paper Table 5 shape)", "area"),
 }
 
 
@@ -69,7 +75,12 @@ def config_system(name: str, N: int | None = None, seed_offset: int = 0):
     n = c.N if N is None else N
     L = c.L
     if N is not None and N != c.N:
-        # keep the density and aspect ratio: scale every side by (n/N)^(1/3)
-        f = (n / c.N) ** (1.0 / 3.0)
-        L = tuple(float(v * f) for v in c.L)
+        if c.scale == "area":
+            # keep the surface density and the height: scale Lx, Ly by (n/N)^(1/2)
+            f = (n / c.N) ** 0.5
+            L = (float(c.L[0] * f), float(c.L[1] * f), float(c.L[2]))
+        else:
+            # keep the density and aspect ratio: scale every side by (n/N)^(1/3)
+            f = (n / c.N) ** (1.0 / 3.0)
+            L = tuple(float(v * f) for v in c.L)
     return uniform_system(n, L, SEED_BASE + c.index + seed_offset) + (L,)

@@ -126,6 +126,17 @@ def test_shapes_small(name):
     check_total(op, xyz, q)
 
 
+@pytest.mark.parametrize("window", ["gs", "kb"])
+@pytest.mark.parametrize("tol", [1e-3, 1e-6, 1e-12])
+def test_strongly_confined_paper_workload(window, tol):
+    """The paper's strongly confined workload (Table 5 shape: surface density 1.1, Lz = 0.3; NEXT #3)
+    at N = 3000 (gamma ~ 170): mid solver off (m = -1), wide long grid (tile kernels)."""
+    xyz, q, L = config_system("s1", N=3000)
+    op = make_plan(len(q), *L, tol, window=window)
+    assert op.m == -1 and op.Ilx > 64
+    check_total(op, xyz, q)
+
+
 def test_c4_fp32_tolerance_plan():
     """c4 at its fp32 tolerance 1e-4 (computed in fp64 here; the fp32 path is a NEXT row)."""
     xyz, q, L = config_system("c4", N=4000)
