@@ -86,6 +86,11 @@ typedef struct {
                                window = 1, S and Sl are the KB shapes beta and the support half-width is
                                P h / 2 (R6-KB) */
     int nu, nul;            /* KB polynomial degrees for explicit_params (0: P + 3 / Pl + 3); <= P + 3 */
+    int long_method;        /* 0: Alg. 2, window + 2D FFT per proxy layer (default); 1: Alg. 3 without
+                               FFT (App. B): direct type-1/type-2 Fourier sums over
+                               kx = 2 pi n / Lx, |n| <= Kx, ky = 2 pi n / Ly, 0 <= n <= Ky (DESIGN.md
+                               R8-D), for boxes with few modes (cubic / tall: c2, c4, c5); single-GPU */
+    int Kx, Ky;             /* direct long range mode bounds for explicit_params */
 } sog_plan_opts;
 
 /* Build a plan for N particles in the box (Lx,Ly,Lz) at tolerance tol on the current

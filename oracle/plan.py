@@ -198,6 +198,9 @@ class Plan:
     Sl: float = 0.0
     Pc: int = 0           # Chebyshev proxy layers
     window: str = "gs"    # "gs": Gaussian (Eq. eq::GS); "kb": Kaiser-Bessel, polynomial weights (R6-KB)
+    long_method: str = "fft"   # "fft": Alg. 2 (window + 2D FFT); "direct": Alg. 3 (App. B), R8-D modes
+    Kx: int = 0           # direct: Fourier modes kx = 2 pi n / Lx, |n| <= Kx (R8-D)
+    Ky: int = 0
     nu: int = 0           # KB: degree of the Chebyshev-interpolated window polynomials (mid)
     nul: int = 0          # KB: same for the long-range window
 
@@ -245,6 +248,9 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     window = over.pop("window", "gs")
     if window not in ("gs", "kb"):
         raise ValueError("window must be 'gs' or 'kb'")
+    long_method = over.pop("long_method", "fft")
+    if long_method not in ("fft", "direct"):
+        raise ValueError("long_method must be 'fft' or 'direct'")
     eta = over.pop("eta", ETA)
     rho = N / (Lx * Ly * Lz)
     rc = over.pop("rc", None)
@@ -270,7 +276,7 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
                 m = ell
     m = min(m, M - 1)                                        # keep >= 1 long-range Gaussian
     p = Plan(N=N, Lx=Lx, Ly=Ly, Lz=Lz, tol=tol, b=b, r0=r0, omega=omega, rc=rc,
-             sigma=sigma, M=M, m=m, window=window)
+             sigma=sigma, M=M, m=m, window=window, long_method=long_method)
     eps_w = WIN_C * tol
     if m >= 0:
         sm = s0 * b ** m
@@ -303,6 +309,10 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     p.Ilx = max(friendly_even(math.ceil(Lx / hl)), friendly_even(Pl))
     p.Ily = max(friendly_even(math.ceil(Ly / hl)), friendly_even(Pl))
     p.Pc = choose_cheb(Lz, sl, max(CHEB_C * tol, CHEB_FLOOR))        # R9
+    if long_method == "direct":                                       # R8-D
+        kcut = 2.0 * KAPPA * math.sqrt(math.log(1.0 / tol)) / sl
+        p.Kx = math.ceil(kcut * Lx / (2.0 * math.pi))
+        p.Ky = math.ceil(kcut * Ly / (2.0 * math.pi))
     for k, v in over.items():
         if not hasattr(p, k):
             raise KeyError(k)

@@ -378,9 +378,75 @@ def long_gather(plan: Plan, xyz, Psi: np.ndarray):
     return A * phi, A * grad
 
 
+# --------------------------------------------------- long range without FFT (Alg. 3, App. B)
+def long_modes(plan: Plan):
+    """R8-D mode set: kx = 2 pi n / Lx, n = -Kx..Kx; ky = 2 pi n / Ly, n = 0..Ky (half plane:
+    the field is real, so the ky < 0 modes are the conjugates of ky > 0)."""
+    kx = 2.0 * np.pi * np.arange(-plan.Kx, plan.Kx + 1) / plan.Lx
+    ky = 2.0 * np.pi * np.arange(0, plan.Ky + 1) / plan.Ly
+    return kx, ky
+
+
+def long_kernel_direct(plan: Plan) -> np.ndarray:
+    """K_ab(kdot) = (pi / (Lx Ly)) sum_{l>m} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b), shape
+    (Pc, Pc, 2Kx+1, Ky+1): the 2D Fourier series of the x,y-periodised wide Gaussians (Eq.
+    eq::gridnonfft, P:1243) at the proxies (R9), R10 at kdot = 0; no window, no deconvolution."""
+    w, s = plan.weights()
+    za = 0.5 * plan.Lz * cheb_nodes(plan.Pc)
+    d2 = (za[:, None] - za[None, :]) ** 2
+    kx, ky = long_modes(plan)
+    k2 = kx[:, None] ** 2 + ky[None, :] ** 2
+    K = np.zeros((plan.Pc, plan.Pc) + k2.shape)
+    K0 = np.zeros((plan.Pc, plan.Pc))
+    nonzero = k2 > 0.0
+    for ell in range(plan.m + 1, plan.M + 1):
+        E = np.exp(-d2 / s[ell] ** 2)
+        spec = np.where(nonzero, w[ell] * s[ell] ** 2 * np.exp(-s[ell] ** 2 * k2 / 4.0), 0.0)
+        K += E[:, :, None, None] * spec[None, None]
+        K0 += w[ell] * s[ell] ** 2 * np.expm1(-d2 / s[ell] ** 2)
+    K[:, :, plan.Kx, 0] = K0
+    return math.pi / (plan.Lx * plan.Ly) * K
+
+
+def long_spread_direct(plan: Plan, xyz, q) -> np.ndarray:
+    """Alg. 3 step 1 in the two-sided proxy form (R9): S_b(kdot) = sum_j q_j L_b(z_j)
+    exp(-i kdot . r_j), a type-1 nonuniform DFT per proxy layer; shape (Pc, 2Kx+1, Ky+1)."""
+    kx, ky = long_modes(plan)
+    Lb, _ = long_basis(plan, xyz[:, 2])
+    ex = np.exp(-1j * np.outer(xyz[:, 0], kx))                # (N, nkx)
+    ey = np.exp(-1j * np.outer(xyz[:, 1], ky))                # (N, nky)
+    return np.einsum("jb,jx,jy->bxy", q[:, None] * Lb, ex, ey)
+
+
+def long_solve_direct(plan: Plan, S: np.ndarray) -> np.ndarray:
+    """Alg. 3 step 2: the wide Gaussians' spectra coupled across the proxies."""
+    return np.einsum("abxy,bxy->axy", long_kernel_direct(plan), S)
+
+
+def long_gather_direct(plan: Plan, xyz, Psi: np.ndarray):
+    """Alg. 3 step 3 (Eq. eq::3.13A, P:1247): phi_i = sum_a L_a(z_i) sum_kdot Psi_a(kdot)
+    exp(i kdot . r_i) over the full plane = Re of the half-plane sum with weight 1 (ky = 0) or 2."""
+    kx, ky = long_modes(plan)
+    La, dLa = long_basis(plan, xyz[:, 2])
+    c = np.where(ky > 0, 2.0, 1.0)
+    ex = np.exp(1j * np.outer(xyz[:, 0], kx))
+    ey = np.exp(1j * np.outer(xyz[:, 1], ky)) * c[None, :]
+    E = ex[:, :, None] * ey[:, None, :]                       # (N, nkx, nky)
+    A = np.einsum("jxy,axy->ja", E, Psi)                      # sum over modes per layer
+    Ax = np.einsum("jxy,axy->ja", E * (1j * kx)[None, :, None], Psi)
+    Ay = np.einsum("jxy,axy->ja", E * (1j * ky)[None, None, :], Psi)
+    phi = np.real((La * A).sum(1))
+    grad = np.stack([np.real((La * Ax).sum(1)), np.real((La * Ay).sum(1)), np.real((dLa * A).sum(1))], axis=1)
+    return phi, grad
+
+
 def long_range(plan: Plan, xyz, q, targets=None):
-    """Phi^long (Algorithm 2 with two-sided Chebyshev proxies, R9) at the targets."""
+    """Phi^long (Algorithm 2 with two-sided Chebyshev proxies, R9; or Algorithm 3 without FFT
+    when plan.long_method == "direct") at the targets."""
     tgt = slice(None) if targets is None else np.asarray(targets)
+    if plan.long_method == "direct":
+        Psi = long_solve_direct(plan, long_spread_direct(plan, xyz, q))
+        return long_gather_direct(plan, xyz[tgt], Psi)
     Psi = long_solve(plan, long_spread(plan, xyz, q))
     return long_gather(plan, xyz[tgt], Psi)
 

@@ -226,6 +226,11 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
     for (int P = 2; P < 65; ++P)
         if (cheb_two_sided_error(P, p.Lz, sl) <= std::max(k.cheb_c * p.tol, 5e-14)) { p.Pc = P; break; }
     if (!p.Pc) { err = "Chebyshev order > 64 needed"; return false; }
+    if (p.long_method == 1) {   // R8-D: the narrowest long-range Gaussian's spectrum below tol^(kappa^2)
+        const double kcut = 2.0 * k.kappa * std::sqrt(std::log(1.0 / p.tol)) / sl;
+        p.Kx = int(std::ceil(kcut * p.Lx / (2.0 * kPi)));
+        p.Ky = int(std::ceil(kcut * p.Ly / (2.0 * kPi)));
+    }
     return true;
 }
 
@@ -252,6 +257,9 @@ bool validate_params(const Params& p, std::string& err) {
     if (p.Ilx < p.Pl || p.Ily < p.Pl) return bad("long grid smaller than the window support");
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
     if (p.window != 0 && p.window != 1) return bad("window must be 0 (Gaussian) or 1 (Kaiser-Bessel)");
+    if (p.long_method != 0 && p.long_method != 1) return bad("long_method must be 0 (FFT) or 1 (direct)");
+    if (p.long_method == 1 && (p.Kx < 0 || p.Ky < 0 || p.Kx > 63 || p.Ky > 63))
+        return bad("direct long range: mode bounds Kx, Ky must be in [0, 63]");
     if (p.window == 1) {
         if ((p.m >= 0 && p.P > 17) || p.Pl > 17) return bad("KB window support must be <= 17");
         if (p.m >= 0 && (p.nu < 2 || p.nu > p.P + 3)) return bad("KB mid polynomial degree nu must be in [2, P+3]");
@@ -424,6 +432,55 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
 
 void build_cheb_nodes(int Pc, std::vector<double>& Tn) { Tn = node_T(Pc); }
 
+void build_long_kernel_direct(const Params& p, std::vector<double>& K) {
+    // K_ab(kdot) = pi/(Lx Ly) sum_{l>m} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b), E_l =
+    // exp(-d^2/s_l^2) (expm1 at kdot = 0, R10), then K~ = C^T K C (T basis, as build_long_kernel)
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const int P = p.Pc, nx = 2 * p.Kx + 1, ny = p.Ky + 1;
+    std::vector<double> za(P), Cm;
+    for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
+    build_cheb_matrix(P, Cm);
+    K.assign(size_t(nx) * ny * P * P, 0.0);
+    std::vector<double> Km(size_t(P) * P);
+    for (int ix = 0; ix < nx; ++ix) {
+        const double kx = 2.0 * kPi * (ix - p.Kx) / p.Lx;
+        for (int iy = 0; iy < ny; ++iy) {
+            const double ky = 2.0 * kPi * iy / p.Ly, k2 = kx * kx + ky * ky;
+            for (int a = 0; a < P; ++a)
+                for (int b = 0; b < P; ++b) {
+                    const double d2 = (za[a] - za[b]) * (za[a] - za[b]);
+                    double acc = 0.0;
+                    for (int l = p.m + 1; l <= p.M; ++l) {
+                        const double ss = s[l] * s[l];
+                        if (k2 == 0.0) {
+                            acc += w[l] * ss * std::expm1(-d2 / ss);
+                        } else {
+                            const double g = ss * k2 / 4.0;
+                            if (g > 745.0) continue;
+                            acc += w[l] * ss * std::exp(-g) * std::exp(-d2 / ss);
+                        }
+                    }
+                    Km[a * P + b] = acc * kPi / (p.Lx * p.Ly);
+                }
+            double* Ko = &K[(size_t(ix) * ny + iy) * P * P];
+            std::vector<long double> KC(size_t(P) * P, 0.0L);
+            for (int a = 0; a < P; ++a)
+                for (int n = 0; n < P; ++n) {
+                    long double t = 0.0L;
+                    for (int b = 0; b < P; ++b) t += (long double)Km[a * P + b] * Cm[size_t(b) * P + n];
+                    KC[size_t(a) * P + n] = t;
+                }
+            for (int m = 0; m < P; ++m)
+                for (int n = 0; n < P; ++n) {
+                    long double t = 0.0L;
+                    for (int a = 0; a < P; ++a) t += (long double)Cm[size_t(a) * P + m] * KC[size_t(a) * P + n];
+                    Ko[m * P + n] = double(t);
+                }
+        }
+    }
+}
+
 double kb_hat(double k, double H, double beta) {
     // int_{-H}^{H} I0(beta sqrt(1 - (x/H)^2)) / I0(beta) e^{-ikx} dx
     //   = 2H sinh(sqrt(beta^2 - (kH)^2)) / (I0(beta) sqrt(beta^2 - (kH)^2))   (sin form past kH = beta)
@@ -486,7 +543,8 @@ std::string describe(const Params& p) {
       << "\nIx=" << p.Ix << "\nIy=" << p.Iy << "\nIz=" << p.Iz << "\nIzs=" << p.Izs
       << "\nP=" << p.P << "\nS=" << p.S << "\nIlx=" << p.Ilx << "\nIly=" << p.Ily
       << "\nPl=" << p.Pl << "\nSl=" << p.Sl << "\nPc=" << p.Pc << "\nwindow=" << p.window
-      << "\nnu=" << p.nu << "\nnul=" << p.nul << "\n";
+      << "\nnu=" << p.nu << "\nnul=" << p.nul << "\nlong_method=" << p.long_method << "\nKx=" << p.Kx
+      << "\nKy=" << p.Ky << "\n";
     return o.str();
 }
 

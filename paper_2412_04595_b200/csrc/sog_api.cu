@@ -799,13 +799,18 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
         p.Ix = o->Ix; p.Iy = o->Iy; p.Iz = o->Iz; p.Izs = o->Izs; p.P = o->P; p.S = o->S;
         p.Ilx = o->Ilx; p.Ily = o->Ily; p.Pl = o->Pl; p.Sl = o->Sl; p.Pc = o->Pc;
         p.window = o->window;
+        p.long_method = o->long_method;
+        p.Kx = o->Kx;
+        p.Ky = o->Ky;
         if (p.window == 1) {
             p.nu = p.m >= 0 ? (o->nu > 0 ? o->nu : p.P + knobs.kb_nu_extra) : 0;
             p.nul = o->nul > 0 ? o->nul : p.Pl + knobs.kb_nu_extra;
         }
     } else {
         if (o && o->window != 0 && o->window != 1) return fail(SOG_EINVAL, "window must be 0 or 1");
+        if (o && o->long_method != 0 && o->long_method != 1) return fail(SOG_EINVAL, "long_method must be 0 or 1");
         p.window = o ? o->window : 0;
+        p.long_method = o ? o->long_method : 0;
         if (o && o->rc_factor > 0) knobs.rc_factor = o->rc_factor;
         if (o && o->eta > 0) knobs.eta = o->eta;
         if (!choose_params(p, knobs, err)) return fail(SOG_EINFEASIBLE, err);

@@ -26,6 +26,9 @@ struct Params {
     // window (R6 / R6-KB): 0 = Gaussian (Eq. eq::GS), 1 = Kaiser-Bessel as per-stencil-point
     // polynomials of degree nu (mid) / nul (long); S, Sl hold beta for KB
     int window = 0, nu = 0, nul = 0;
+    // long range: 0 = Alg. 2 (window + 2D FFT), 1 = Alg. 3 without FFT (App. B): direct Fourier
+    // sums over kx = 2 pi n / Lx, |n| <= Kx, ky = 2 pi n / Ly, 0 <= n <= Ky (R8-D)
+    int long_method = 0, Kx = 0, Ky = 0;
     // derived
     double hx() const { return Lx / Ix; }
     double hy() const { return Ly / Iy; }
@@ -74,6 +77,9 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
 // Long-range kernel matrices per half mode (mode = ix*(Ily/2+1)+iy), in the Chebyshev T
 // basis: K~[mode][m][n] = sum_ab C[a][m] K_ab C[b][n], K_ab from R9/R10.
 void build_long_kernel(const Params& p, std::vector<double>& K);
+// R8-D direct long range: K~ = C^T K C per mode, modes ordered (ix = 0..2Kx, iy = 0..Ky), K with
+// pi / (Lx Ly) and no window (App. B, Eq. eq::gridnonfft P:1243)
+void build_long_kernel_direct(const Params& p, std::vector<double>& K);
 // R6-KB: monomial coefficients c[n * P + j] (n = 0..nu) in u = x/h + I/2 - g0 of the degree-nu
 // Chebyshev interpolant of W_KB((j - p - u) h), H = P h / 2 (Remark rmk::PWindow)
 void build_kb_poly(int P, double beta, int nu, std::vector<double>& c);

@@ -35,18 +35,24 @@ class Opts(ctypes.Structure):
                 ("Ilx", ctypes.c_int), ("Ily", ctypes.c_int), ("Pl", ctypes.c_int), ("Sl", ctypes.c_double),
                 ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint),
                 ("precision", ctypes.c_int), ("window", ctypes.c_int), ("nu", ctypes.c_int),
-                ("nul", ctypes.c_int)]
+                ("nul", ctypes.c_int), ("long_method", ctypes.c_int), ("Kx", ctypes.c_int), ("Ky", ctypes.c_int)]
 
 WINDOWS = {"gs": 0, "kb": 1}
+LONG_METHODS = {"fft": 0, "direct": 1}
 
 
-def _set_window(o, window, params):
-    """Window choice: explicit params carry their own (oracle Plan: "gs"/"kb"), else `window`."""
+def _set_window(o, window, params, long_method="fft"):
+    """Window / long-range method: explicit params carry their own (oracle Plan: "gs"/"kb",
+    "fft"/"direct"), else the keyword arguments."""
     w = params.get("window", window) if params is not None else window
     o.window = WINDOWS[w] if isinstance(w, str) else int(w)
+    lm = params.get("long_method", long_method) if params is not None else long_method
+    o.long_method = LONG_METHODS[lm] if isinstance(lm, str) else int(lm)
     if params is not None:
         o.nu = int(params.get("nu", 0))
         o.nul = int(params.get("nul", 0))
+        o.Kx = int(params.get("Kx", 0))
+        o.Ky = int(params.get("Ky", 0))
 
 
 def lib_path() -> str:
@@ -126,7 +132,7 @@ class Plan:
     """
 
     def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
-                 validate=True, timing=False, precision="fp64", window="gs"):
+                 validate=True, timing=False, precision="fp64", window="gs", long_method="fft"):
         self.lib = load_library()
         self.N = int(N)
         self.L = tuple(float(v) for v in L)
@@ -141,7 +147,7 @@ class Plan:
         o.flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
         o.cuda_stream = _stream_handle(stream)
         o.precision = {"fp64": 0, "fp32": 1}[precision]
-        _set_window(o, window, params)
+        _set_window(o, window, params, long_method)
         h = self.lib.sog_plan_create_ex(self.N, *self.L, self.tol, ctypes.byref(o))
         if not h:
             raise SogError(-1, self.lib.sog_last_error().decode())
@@ -266,13 +272,13 @@ def _parse(text):
     return out
 
 
-def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs") -> dict:
+def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method="fft") -> dict:
     """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU)."""
     lib = load_library()
     o = Opts()
     o.rc_factor = float(rc_factor or 0.0)
     o.eta = float(eta or 0.0)
-    _set_window(o, window, None)
+    _set_window(o, window, None, long_method)
     n = lib.sog_plan_choose(int(N), *[float(v) for v in L], float(tol), ctypes.byref(o), None, 0)
     if n < 0:
         raise _err(lib, n)

@@ -41,14 +41,20 @@ CASES += [("tiny", 2, (20.0, 20.0, 20.0), 1e-6), ("confined", 5000, (60.0, 60.0,
           ("tall", 3000, (6.0, 7.0, 90.0), 1e-4), ("dense", 100000, (10.0, 10.0, 10.0), 1e-8)]
 
 
-@pytest.mark.parametrize("window", ["gs", "kb"])
+@pytest.mark.parametrize("window,long_method", [("gs", "fft"), ("kb", "fft"), ("gs", "direct")])
 @pytest.mark.parametrize("name,N,L,tol", CASES)
-def test_plan_rules_match_oracle(name, N, L, tol, window):
-    lib_p = B.choose_params(N, L, tol, window=window)
-    ora = dataclasses.asdict(make_plan(N, *L, tol, window=window))
+def test_plan_rules_match_oracle(name, N, L, tol, window, long_method):
+    ora = dataclasses.asdict(make_plan(N, *L, tol, window=window, long_method=long_method))
+    if long_method == "direct" and max(ora["Kx"], ora["Ky"]) > 63:
+        with pytest.raises(B.SogError):       # too many modes for the direct sums (library bound)
+            B.choose_params(N, L, tol, window=window, long_method=long_method)
+        return
+    lib_p = B.choose_params(N, L, tol, window=window, long_method=long_method)
     for k, v in ora.items():
         if k == "window":
             assert lib_p[k] == B.WINDOWS[v]
+        elif k == "long_method":
+            assert lib_p[k] == B.LONG_METHODS[v]
         elif isinstance(v, int):
             assert lib_p[k] == v, (k, lib_p[k], v)
         else:
