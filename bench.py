@@ -53,6 +53,8 @@ def parse():
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
     ap.add_argument("--window", default="gs", choices=["gs", "kb"],
                     help="mid/long window: Gaussian (Eq. eq::GS) or Kaiser-Bessel polynomials (DESIGN.md R6-KB)")
+    ap.add_argument("--long-method", default="fft", choices=["fft", "direct"],
+                    help="long range: Alg. 2 (window + FFT) or Alg. 3 without FFT (DESIGN.md R8-D)")
     ap.add_argument("--parallelism", default="xslab", choices=["xslab", "replicas"],
                     help="N>1: x-slab decomposition of one system (strong scaling, NCCL) or replicas")
     return ap.parse_args()
@@ -134,7 +136,7 @@ def barrier(ws):
         dist.barrier()
 
 
-def oracle_sample(cfg, tol, target_seconds=15.0, window="gs"):
+def oracle_sample(cfg, tol, target_seconds=15.0, window="gs", long_method="fft"):
     """The oracle as it stands on a bounded sample of the workload: a system of the same
     density and aspect ratio, N chosen so one evaluation takes ~target_seconds."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -144,7 +146,7 @@ def oracle_sample(cfg, tol, target_seconds=15.0, window="gs"):
     n = 2000
     while True:
         xyz, q, L = config_system(cfg, N=n)
-        op = make_plan(n, *L, tol, window=window)
+        op = make_plan(n, *L, tol, window=window, long_method=long_method)
         t0 = time.perf_counter()
         O.evaluate(op, xyz, q)
         dt = time.perf_counter() - t0
@@ -158,11 +160,11 @@ def run_reference(args, ws, rank):
         return
     c = CONFIGS[args.config]
     tol = args.tol or c.tol
-    n, dt0, L = oracle_sample(args.config, tol, window=args.window)
+    n, dt0, L = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
     import oracle.sog as O
     from oracle.plan import make_plan
     xyz, q, L = config_system(args.config, N=n)
-    op = make_plan(n, *L, tol, window=args.window)
+    op = make_plan(n, *L, tol, window=args.window, long_method=args.long_method)
     for _ in range(min(args.warmup, 1)):
         O.evaluate(op, xyz, q)
     t0 = time.perf_counter()
@@ -336,7 +338,7 @@ def main():
     N = len(q)
     stream = torch.cuda.current_stream()
     plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision, eta=args.eta,
-                rc_factor=args.rc_factor, window=args.window)
+                rc_factor=args.rc_factor, window=args.window, long_method=args.long_method)
     xd = torch.from_numpy(xyz).cuda()
     qd = torch.from_numpy(q).cuda()
     phi = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -392,7 +394,7 @@ def main():
                "host_wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n, dt, Ls = oracle_sample(args.config, tol, window=args.window)
+        n, dt, Ls = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
         cpu = {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "oracle",
                "sample": f"one full oracle evaluation of a {args.config}-density system, N={n}, "
                          f"box {Ls[0]:.2f}x{Ls[1]:.2f}x{Ls[2]:.2f}, tol {tol:g}, 1 host thread"}
@@ -405,8 +407,8 @@ def main():
                                f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
                    "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",
                    "l2": "working set (mid grid %.1f GB) >> 126 MB L2; no flush" % (d["Ix"] * d["Iy"] * d["Izs"] * 8 / 1e9),
-                   "window": args.window,
-                   "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc")}},
+                   "window": args.window, "long_method": args.long_method,
+                   "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc", "Kx", "Ky")}},
         "stages_ms": acc,
         "roofline": roof,
         "stage_roofline": per_stage,

@@ -12,6 +12,7 @@ struct MidSortArgs;
 struct MidZArgs;
 struct LongArgs;
 struct LongTileArgs;
+struct DftArgs;
 int launch_stencil_origins(const d4* pos, int N, const MidArgs& a, int has_mid, double lhx, double lhy, double lhpx,
                            double lhpy, int4* g0, cudaStream_t st);
 int launch_mid_sort_keys(const int4* g0, int N, const MidSortArgs& s, int* key, int* count, cudaStream_t st);
@@ -39,6 +40,11 @@ int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double
 int launch_long_gather_bc(const LongArgs& a, const int4* g0, const void* psi, d4* out, bool f32, cudaStream_t st);
 int launch_long_scale(const void* in, void* out, const double* K, int nmode, int Pc, bool f32, cudaStream_t st);
 int launch_long_to_nodes(const double* in, double* out, int G, int Pc, const double* M, cudaStream_t st);
+// long range without FFT (Alg. 3): type-1 sums into S~[n][mode] complex, type-2 sums to the particles
+int launch_long_dft_spread(const LongArgs& a, const DftArgs& d, int nblk, void* part, void* S, bool f32,
+                           cudaStream_t st);
+int launch_long_dft_gather(const LongArgs& a, const DftArgs& d, const void* psi, d4* out, bool f32, cudaStream_t st);
+bool long_dft_ok(const DftArgs& d, int Pc);
 // exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total); temp from scan_temp_bytes
 size_t scan_temp_bytes(int n);
 int launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes, cudaStream_t st);

@@ -22,6 +22,7 @@
 #include "kernels_common.cuh"
 #include "kernels_dist.cuh"
 #include "kernels_long.cuh"
+#include "kernels_dft.cuh"
 #include "kernels_mid.cuh"
 #include "launch.h"
 #include "kernels_near.cuh"
@@ -124,6 +125,8 @@ struct sog_plan {
     double *d_K = nullptr, *d_C = nullptr, *d_Tn = nullptr;
     KBTab kbl{};                                 // R6-KB long-window table (mid: in mz)
     bool long_small = false;        // small long grid: register-tiled spread + broadcast gather
+    DftArgs dft{};                  // long_method = 1 (Alg. 3): mode set
+    double *ldS = nullptr, *ldP = nullptr, *ldpart = nullptr, *d_Kd = nullptr;   // S~, Psi~ [Pc][mode] complex
     int lg_nblk = 0;
     double* lpart2 = nullptr;       // [lg_nblk][PCP][Ilx*Ily] spread partials
     double* ldbg = nullptr;         // debug: T basis -> proxy-node basis
@@ -195,7 +198,8 @@ void free_plan(sog_plan* pl) {
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
-                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp};
+                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp,
+                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -444,6 +448,21 @@ int setup(sog_plan* pl) {
         CKF(cufftMakePlanMany64(pl->linv, 2, n, nullptr, 1, (long long)p.Ilx * (p.Ily / 2 + 1), nullptr, 1,
                                 (long long)p.Ilx * p.Ily, pl->f32 ? CUFFT_C2R : CUFFT_Z2D, p.Pc, &ws));
         pl->bytes += ws;
+        if (p.long_method == 1) {   // Alg. 3: direct sums over the R8-D modes
+            if (slab) return fail(SOG_EINVAL, "the direct long range (long_method 1) is single-GPU only");
+            DftArgs& d = pl->dft;
+            d.Kx = p.Kx; d.Ky = p.Ky; d.nkx = 2 * p.Kx + 1; d.nky = p.Ky + 1; d.nmode = d.nkx * d.nky;
+            const double twopi = 6.283185307179586476925286766559;
+            d.kx1 = twopi / p.Lx; d.ky1 = twopi / p.Ly;
+            if (!long_dft_ok(d, p.Pc)) return fail(SOG_EINVAL, "direct long range: too many modes (use long_method 0)");
+            std::vector<double> Kd;
+            build_long_kernel_direct(p, Kd);
+            const size_t ns = 2 * (size_t)p.Pc * d.nmode;
+            pl->lg_nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (p.N + 255) / 256));
+            if ((rc = upload(pl, &pl->d_Kd, Kd)) || (rc = dalloc(pl, &pl->ldS, ns)) || (rc = dalloc(pl, &pl->ldP, ns)) ||
+                (rc = dalloc(pl, &pl->ldpart, (size_t)pl->lg_nblk * long_small_pcp(p.Pc) * 2 * d.nmode)))
+                return rc;
+        }
     }
     pl->scan_bytes = std::max(scan_temp_bytes(pl->ncell), pl->nkeys ? scan_temp_bytes(pl->nkeys) : size_t(0));
     if ((rc = dalloc(pl, (char**)&pl->scan_tmp, pl->scan_bytes))) return rc;
@@ -633,6 +652,8 @@ int st_long_spread(sog_plan* pl) {
         k_own_mask<<<(pl->Ncur + 255) / 256, 256, 0, st>>>(pl->pos_s, pl->perm, pl->Ncur, pl->Nown, pl->pos_long);
         la.pos = pl->pos_long;
     }
+    if (p.long_method == 1)
+        return lchk(launch_long_dft_spread(la, pl->dft, pl->lg_nblk, pl->ldpart, pl->ldS, pl->f32, st));
     if (pl->long_small) {
         if ((rc = lchk(launch_long_spread_gemm(la, pl->g0, pl->lt.gamma_x, pl->lt.gamma_y, pl->lg_nblk, pl->lpart2,
                                                pl->lgrid, pl->f32, st))))
@@ -653,6 +674,8 @@ int st_long_solve(sog_plan* pl) {
     const Params& p = pl->p;
     cudaStream_t st = pl->stream;
     int rc;
+    if (p.long_method == 1)
+        return lchk(launch_long_scale(pl->ldS, pl->ldP, pl->d_Kd, pl->dft.nmode, p.Pc, pl->f32, st));
     const int nmode = p.Ilx * (p.Ily / 2 + 1);
     if (pl->f32) {
         CKF(cufftExecR2C(pl->lfwd, (float*)pl->lgrid, (cufftComplex*)pl->lspec));
@@ -669,6 +692,8 @@ int st_long_solve(sog_plan* pl) {
 // S12
 int st_long_gather(sog_plan* pl) {
     const Params& p = pl->p;
+    if (p.long_method == 1)
+        return lchk(launch_long_dft_gather(long_args(pl), pl->dft, pl->ldP, pl->o_long, pl->f32, pl->stream));
     if (pl->long_small)
         return lchk(launch_long_gather_bc(long_args(pl), pl->g0, pl->lgrid, pl->o_long, pl->f32, pl->stream));
     if (pl->f32) return fail(SOG_EINVAL, "fp32 mode needs a small long grid (register-tiled path)");
@@ -906,6 +931,7 @@ int sog_debug_stage(sog_plan* pl, int stage, const double* xyz, const double* q,
         need = (size_t)p.Ix * p.Iy * p.Izs;
         src = stage == 1 ? pl->mgrid : pl->mpsi;
     } else if (stage == 3 || stage == 4) {
+        if (p.long_method == 1) return fail(SOG_EINVAL, "stages 3, 4 are the FFT long range's grids (long_method 0)");
         need = (size_t)p.Pc * p.Ilx * p.Ily;
         src = pl->ldbg;                 // converted from the T basis below
     } else {
@@ -971,7 +997,7 @@ int sog_launches_per_eval(const sog_plan* pl) {
     // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
     // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
     // [transpose,] gather, combine  (cuFFT launches are not counted)
-    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->long_small ? 4 : 5) + 1;
+    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 1;
 }
 
 }  // extern "C"
