@@ -42,7 +42,7 @@ namespace sog {
 
 __global__ void k_combine(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
                           const d4* __restrict__ pos, const int* __restrict__ perm, int N, int nown, double selfc,
-                          double* __restrict__ phi, double* __restrict__ force, double* __restrict__ energy) {
+                          double* __restrict__ phi, double* __restrict__ force, double* __restrict__ epart) {
     // phi_i = Phi^N + Phi^mid + Phi^long - q_i sum_l w_l; F_i = -q_i grad phi
     // (x-slab: only the nown own particles are written; halo entries have perm >= nown)
     int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -60,8 +60,31 @@ __global__ void k_combine(const d4* __restrict__ nearo, const d4* __restrict__ m
         }
         e = 0.5 * q * ph;                                     // U = 1/2 sum q phi
     }
+    // per-block partial of U in a fixed order (k_sum_partials adds the blocks: deterministic,
+    // and no single-address atomic stream)
+    __shared__ double se[32];
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(energy, e);
+    if ((threadIdx.x & 31) == 0) se[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += se[w];
+        epart[blockIdx.x] = t;
+    }
+}
+
+// out = sum of part[0..n) in a fixed order (one block)
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double s[1024];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += part[i];
+    s[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = s[0];
 }
 
 __global__ void k_components(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
@@ -127,6 +150,7 @@ struct sog_plan {
     bool long_small = false;        // small long grid: register-tiled spread + broadcast gather
     DftArgs dft{};                  // long_method = 1 (Alg. 3): mode set
     double *ldS = nullptr, *ldP = nullptr, *ldpart = nullptr, *d_Kd = nullptr;   // S~, Psi~ [Pc][mode] complex
+    double* epart = nullptr;        // per-block partial energies of k_combine
     int lg_nblk = 0;
     double* lpart2 = nullptr;       // [lg_nblk][PCP][Ilx*Ily] spread partials
     double* ldbg = nullptr;         // debug: T basis -> proxy-node basis
@@ -199,7 +223,7 @@ void free_plan(sog_plan* pl) {
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
                     pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp,
-                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd};
+                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -260,7 +284,7 @@ int setup(sog_plan* pl) {
         (rc = dalloc(pl, &pl->tmp, N)) || (rc = dalloc(pl, &pl->perm, N)) || (rc = dalloc(pl, &pl->g0, N)) ||
         (rc = dalloc(pl, &pl->count, pl->ncell + 1)) || (rc = dalloc(pl, &pl->start, pl->ncell + 1)) ||
         (rc = dalloc(pl, &pl->cursor, pl->ncell + 1)) || (rc = dalloc(pl, &pl->dflags, 1)) ||
-        (rc = dalloc(pl, &pl->qsums, 4)) || (rc = upload(pl, &pl->d_cF, pl->near.cF)) ||
+        (rc = dalloc(pl, &pl->qsums, 4)) || (rc = dalloc(pl, &pl->epart, ((size_t)N + 255) / 256 + 1)) || (rc = upload(pl, &pl->d_cF, pl->near.cF)) ||
         (rc = upload(pl, &pl->d_cdF, pl->near.cdF)))
         return rc;
     CK(cudaMallocHost((void**)&pl->pinned, 8 * sizeof(double)));
@@ -612,7 +636,7 @@ int st_near(sog_plan* pl) {
         a.cap = 1536;                            // multiple of 128 (packed staging layout)
         a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
         size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
-                    NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;
+                    2 * NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;   // two pending lists per warp
         CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
     } else {
@@ -883,7 +907,8 @@ int sog_eval(sog_plan* pl, const double* xyz, const double* q, double* phi, doub
     if (rc) return rc;
     const int N = int(pl->p.N);
     k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N, N,
-                                                       pl->selfc, phi, force, pl->qsums + 2);
+                                                       pl->selfc, phi, force, pl->epart);
+    k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
     CK(cudaGetLastError());
     mark(pl, 11);
     collect_timings(pl);
@@ -997,7 +1022,7 @@ int sog_launches_per_eval(const sog_plan* pl) {
     // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
     // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
     // [transpose,] gather, combine  (cuFFT launches are not counted)
-    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 1;
+    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 2;
 }
 
 }  // extern "C"
@@ -1309,9 +1334,9 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
         if (!pl->Ncur) continue;
         if ((rc = st_long_gather(pl))) return rc;
         const int N = pl->Ncur;
-        CK(cudaMemsetAsync(pl->qsums + 2, 0, sizeof(double), pl->stream));
         k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N,
-                                                           pl->Nown, pl->selfc, phi[i], force[i], pl->qsums + 2);
+                                                           pl->Nown, pl->selfc, phi[i], force[i], pl->epart);
+        k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
         CK(cudaGetLastError());
     }
     return SOG_OK;
