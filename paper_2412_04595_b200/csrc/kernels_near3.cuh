@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
     // staged sources in 64-wide blocks, candidate q = 64 b + 32 h + l stored as
     //   sxy[b][l] = (x_h0, x_h1, y_h0, y_h1), sz[b][l] = (z_h0, z_h1), sc[b][l] = (code_h0, code_h1)
     // so that one lane tests two candidates with packed fp32x2 arithmetic
-    float4* sxy = reinterpret_cast<float4*>(lists + 2 * NEAR3_WARPS * 160); // [cap/64][32] (after 2 lists per warp)
+    float4* sxy = reinterpret_cast<float4*>(lists + NEAR3_WARPS * 160); // [cap/64][32]
     float2* sz = reinterpret_cast<float2*>(sxy + a.cap / 2);             // [cap/64][32]
     int2* sc = reinterpret_cast<int2*>(sz + a.cap / 2);                  // [cap/64][32]
     const CellGeo& g = a.g;
@@ -125,26 +125,16 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
             for (int q = nsrc + threadIdx.x; q < npad; q += blockDim.x) put(q, 1e18f, 0.f, 0.f, 0);   // sentinels
         }
         __syncthreads();
-        // two targets per warp: every staged candidate pair (one packed fp32x2 load) is pre-tested
-        // against both, so the shared-memory loads and the loop are paid once per two targets;
-        // each target keeps its own pending-pair list and fp64 accumulators
-        for (int ia = t0 + 2 * warp; ia < t1; ia += 2 * NEAR3_WARPS) {
-            const int ib = ia + 1;
-            const bool hasb = ib < t1;
-            const d4 pa = ld_d4(&a.pos[ia]);
-            const d4 pb = hasb ? ld_d4(&a.pos[ib]) : pa;
-            const float xa = (float)(pa.x - ox), ya = (float)(pa.y - oy), za = (float)(pa.z - oz);
-            const float xb = hasb ? (float)(pb.x - ox) : 1e18f, yb = (float)(pb.y - oy), zb = (float)(pb.z - oz);
-            const float2 xa2 = make_float2(xa, xa), ya2 = make_float2(ya, ya), za2 = make_float2(za, za);
-            const float2 xb2 = make_float2(xb, xb), yb2 = make_float2(yb, yb), zb2 = make_float2(zb, zb);
+        for (int it = t0 + warp; it < t1; it += NEAR3_WARPS) {
+            const d4 pi = ld_d4(&a.pos[it]);
+            const float xi = (float)(pi.x - ox), yi = (float)(pi.y - oy), zi = (float)(pi.z - oz);
+            const float2 xi2 = make_float2(xi, xi), yi2 = make_float2(yi, yi), zi2 = make_float2(zi, zi);
             const float2 m1 = make_float2(-1.f, -1.f);
-            int* wla = wl;
-            int* wlb = wl + NEAR3_WARPS * 160;               // second list block (see the host smem size)
-            double phA = 0.0, gxA = 0.0, gyA = 0.0, gzA = 0.0;
-            double phB = 0.0, gxB = 0.0, gyB = 0.0, gzB = 0.0;
-            int npa = 0, npb = 0;
+            double phi = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+            int npend = 0;
             for (int q0 = 0; q0 < npad; q0 += 128) {
-                bool passa[4], passb[4];
+                // fp32 pre-test of 4 x 32 sources, two per packed fp32x2 operation
+                bool pass[4];
                 int code[4];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
@@ -152,63 +142,42 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
                     const float4 xy = sxy[e];
                     const float2 zz = sz[e];
                     const int2 cc = sc[e];
-                    const float2 sx2 = make_float2(xy.x, xy.y), sy2 = make_float2(xy.z, xy.w);
-                    {
-                        const float2 dx = __ffma2_rn(sx2, m1, xa2), dy = __ffma2_rn(sy2, m1, ya2), dz = __ffma2_rn(zz, m1, za2);
-                        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
-                        passa[2 * r] = r2.x < rc2f;
-                        passa[2 * r + 1] = r2.y < rc2f;
-                    }
-                    {
-                        const float2 dx = __ffma2_rn(sx2, m1, xb2), dy = __ffma2_rn(sy2, m1, yb2), dz = __ffma2_rn(zz, m1, zb2);
-                        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
-                        passb[2 * r] = r2.x < rc2f;
-                        passb[2 * r + 1] = r2.y < rc2f;
-                    }
+                    const float2 dx = __ffma2_rn(make_float2(xy.x, xy.y), m1, xi2);
+                    const float2 dy = __ffma2_rn(make_float2(xy.z, xy.w), m1, yi2);
+                    const float2 dz = __ffma2_rn(zz, m1, zi2);
+                    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+                    pass[2 * r] = r2.x < rc2f;
+                    pass[2 * r + 1] = r2.y < rc2f;
                     code[2 * r] = cc.x;
                     code[2 * r + 1] = cc.y;
                 }
-                const unsigned below = (1u << lane) - 1;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const unsigned ma = __ballot_sync(0xffffffffu, passa[r]);
-                    const unsigned mb = __ballot_sync(0xffffffffu, passb[r]);
-                    if (passa[r]) wla[npa + __popc(ma & below)] = code[r];
-                    if (passb[r]) wlb[npb + __popc(mb & below)] = code[r];
-                    npa += __popc(ma);
-                    npb += __popc(mb);
+                    const unsigned m = __ballot_sync(0xffffffffu, pass[r]);
+                    if (pass[r]) wl[npend + __popc(m & ((1u << lane) - 1))] = code[r];
+                    npend += __popc(m);
                 }
                 __syncwarp();
-                while (npa >= 32) {
-                    npa -= 32;
-                    near_pair<D>(tab, a, pa, wla[npa + lane], shift, phA, gxA, gyA, gzA);
-                }
-                while (npb >= 32) {
-                    npb -= 32;
-                    near_pair<D>(tab, a, pb, wlb[npb + lane], shift, phB, gxB, gyB, gzB);
+                while (npend >= 32) {                    // evaluate 32 pending pairs, all lanes busy
+                    npend -= 32;
+                    near_pair<D>(tab, a, pi, wl[npend + lane], shift, phi, gx, gy, gz);
                 }
                 __syncwarp();
             }
-            if (lane < npa) near_pair<D>(tab, a, pa, wla[lane], shift, phA, gxA, gyA, gzA);
-            if (lane < npb) near_pair<D>(tab, a, pb, wlb[lane], shift, phB, gxB, gyB, gzB);
-            // 4-value butterflies; lanes 0..3 hold (phi, gx, gy, gz) of target a, lanes 4..7 of b
+            if (lane < npend) near_pair<D>(tab, a, pi, wl[lane], shift, phi, gx, gy, gz);
+            // 4-value butterfly; lanes 0..3 hold phi, gx, gy, gz
+            const bool b1 = lane & 1;
+            double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;
+            k0v += __shfl_xor_sync(0xffffffffu, b1 ? phi : gx, 1);
+            k1v += __shfl_xor_sync(0xffffffffu, b1 ? gy : gz, 1);
+            const bool b2 = lane & 2;
+            double kk = b2 ? k1v : k0v;
+            kk += __shfl_xor_sync(0xffffffffu, b2 ? k0v : k1v, 2);
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const double phi = t ? phB : phA, gx = t ? gxB : gxA, gy = t ? gyB : gyA, gz = t ? gzB : gzA;
-                const bool b1 = lane & 1;
-                double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;
-                k0v += __shfl_xor_sync(0xffffffffu, b1 ? phi : gx, 1);
-                k1v += __shfl_xor_sync(0xffffffffu, b1 ? gy : gz, 1);
-                const bool b2 = lane & 2;
-                double kk = b2 ? k1v : k0v;
-                kk += __shfl_xor_sync(0xffffffffu, b2 ? k0v : k1v, 2);
-#pragma unroll
-                for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
-                const int it = t ? ib : ia;
-                if (lane < 4 && (t == 0 || hasb)) {
-                    double* o = reinterpret_cast<double*>(&a.out[it]);
-                    o[lane] = sbeg == 0 ? kk : o[lane] + kk;
-                }
+            for (int o = 4; o < 32; o <<= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
+            if (lane < 4) {
+                double* o = reinterpret_cast<double*>(&a.out[it]);
+                o[lane] = sbeg == 0 ? kk : o[lane] + kk;
             }
             __syncwarp();
         }

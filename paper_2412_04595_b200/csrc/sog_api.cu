@@ -636,7 +636,7 @@ int st_near(sog_plan* pl) {
         a.cap = 1536;                            // multiple of 128 (packed staging layout)
         a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
         size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
-                    2 * NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;   // two pending lists per warp
+                    NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;
         CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_near3<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
     } else {
