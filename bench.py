@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--rc-factor", type=float, default=None, help="override rule R2's r_c factor (plan knob)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
+    ap.add_argument("--no-graph", action="store_true", help="launch the kernels one by one (no CUDA graph replay)")
     ap.add_argument("--window", default="gs", choices=["gs", "kb"],
                     help="mid/long window: Gaussian (Eq. eq::GS) or Kaiser-Bessel polynomials (DESIGN.md R6-KB)")
     ap.add_argument("--long-method", default="fft", choices=["fft", "direct"],
@@ -346,7 +347,7 @@ def main():
     # one validated evaluation first (catches bad inputs), then warm-up
     plan.set_flags(validate=True)
     plan.eval(xd, qd, phi, F)
-    plan.set_flags(validate=False)
+    plan.set_flags(validate=False, graph=not args.no_graph)   # the evaluation replayed as one CUDA graph
     for _ in range(max(0, args.warmup - 1)):
         plan.eval(xd, qd, phi, F)
     torch.cuda.synchronize()
@@ -379,6 +380,7 @@ def main():
         hq = torch.from_numpy(q).pin_memory()
         hphi = torch.empty(N, dtype=torch.float64).pin_memory()
         hF = torch.empty(N, 3, dtype=torch.float64).pin_memory()
+        plan.set_flags(validate=False, graph=not args.no_graph)
         plan.eval_host(hx, hq, hphi, hF)
         barrier(ws)
         t0 = time.perf_counter()
@@ -407,7 +409,7 @@ def main():
                                f"{L[0]:g}x{L[1]:g}x{L[2]:g}, periodic x,y / free z, tol {tol:g}",
                    "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",
                    "l2": "working set (mid grid %.1f GB) >> 126 MB L2; no flush" % (d["Ix"] * d["Iy"] * d["Izs"] * 8 / 1e9),
-                   "window": args.window, "long_method": args.long_method,
+                   "window": args.window, "long_method": args.long_method, "cuda_graph": not args.no_graph,
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc", "Kx", "Ky")}},
         "stages_ms": acc,
         "roofline": roof,

@@ -146,6 +146,9 @@ int sog_plan_describe(const sog_plan* p, char* buf, size_t len);
  * [6] mid gather, [7] long spread, [8] long FFT+scale+IFFT, [9] long gather, [10] combine.
  * Returns the number of entries written (<= n). */
 #define SOG_TIMING 2u
+/* Replay the evaluation as one CUDA graph: captured at the first sog_eval and re-captured when the
+ * (xyz, q, phi, force) pointers change; stage timings are not collected in this mode. */
+#define SOG_GRAPH 4u
 int sog_get_timings(const sog_plan* p, double* ms, int n);
 
 int sog_set_flags(sog_plan* p, unsigned flags);

@@ -161,6 +161,10 @@ struct sog_plan {
     double* pinned = nullptr;   // [sum q, sum|q|, energy, flags]
     double last_energy = 0;
     cudaEvent_t ev[16] = {};
+    // SOG_GRAPH: the whole evaluation captured once per (xyz, q, phi, force) pointer tuple, replayed
+    cudaGraphExec_t gexec = nullptr;
+    const void* gkey[4] = {};
+    cudaStream_t gstream = nullptr;         // private capture stream (the legacy stream cannot capture)
     double timings[11] = {};
     size_t bytes = 0;
     // ---- x-slab rank (R > 1); R == 1: the whole periodic box ----
@@ -235,6 +239,8 @@ void free_plan(sog_plan* pl) {
         if (p) cudaFree(p);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    if (pl->gstream) cudaStreamDestroy(pl->gstream);
     delete pl;
 }
 
@@ -901,8 +907,8 @@ sog_plan* sog_plan_create(int64_t N, double Lx, double Ly, double Lz, double tol
 
 void sog_plan_destroy(sog_plan* p) { free_plan(p); }
 
-int sog_eval(sog_plan* pl, const double* xyz, const double* q, double* phi, double* force) {
-    if (!pl || !xyz || !q) return fail(SOG_EINVAL, "null argument");
+namespace {
+int eval_body(sog_plan* pl, const double* xyz, const double* q, double* phi, double* force) {
     int rc = run_pipeline(pl, xyz, q);
     if (rc) return rc;
     const int N = int(pl->p.N);
@@ -911,7 +917,49 @@ int sog_eval(sog_plan* pl, const double* xyz, const double* q, double* phi, doub
     k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
     CK(cudaGetLastError());
     mark(pl, 11);
-    collect_timings(pl);
+    return SOG_OK;
+}
+
+// capture eval_body into a CUDA graph (the launch sequence has no host synchronisation), or
+// reuse the instantiated one when the caller's buffers are the same as last time
+int eval_graph(sog_plan* pl, const double* xyz, const double* q, double* phi, double* force) {
+    const void* key[4] = {xyz, q, phi, force};
+    if (!pl->gexec || std::memcmp(key, pl->gkey, sizeof key) != 0) {
+        if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
+        const unsigned saved = pl->flags;
+        pl->flags &= ~SOG_TIMING;                       // no event nodes in the graph
+        // capture on a private stream (the plan's stream may be the legacy default stream); the
+        // graph is launched on the plan's stream
+        if (!pl->gstream) CK(cudaStreamCreateWithFlags(&pl->gstream, cudaStreamNonBlocking));
+        const cudaStream_t user = pl->stream;
+        CK(cudaStreamSynchronize(user));                // no pending plan work crosses into the capture
+        int rc = set_stream(pl, pl->gstream);
+        if (rc) return rc;
+        CK(cudaStreamBeginCapture(pl->gstream, cudaStreamCaptureModeRelaxed));
+        rc = eval_body(pl, xyz, q, phi, force);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(pl->gstream, &g);
+        pl->flags = saved;
+        const int rs = set_stream(pl, user);
+        if (rs) { if (g) cudaGraphDestroy(g); return rs; }
+        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        if (e != cudaSuccess) return fail(SOG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        const cudaError_t ei = cudaGraphInstantiate(&pl->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) { pl->gexec = nullptr; return fail(SOG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+        std::memcpy(pl->gkey, key, sizeof key);
+    }
+    CK(cudaGraphLaunch(pl->gexec, pl->stream));
+    return SOG_OK;
+}
+}  // namespace
+
+int sog_eval(sog_plan* pl, const double* xyz, const double* q, double* phi, double* force) {
+    if (!pl || !xyz || !q) return fail(SOG_EINVAL, "null argument");
+    const int rc = (pl->flags & SOG_GRAPH) && pl->R <= 1 ? eval_graph(pl, xyz, q, phi, force)
+                                                         : eval_body(pl, xyz, q, phi, force);
+    if (rc) return rc;
+    if (!(pl->flags & SOG_GRAPH)) collect_timings(pl);
     if (!(pl->flags & SOG_NO_VALIDATE)) return check_flags(pl);
     return SOG_OK;
 }

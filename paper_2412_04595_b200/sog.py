@@ -9,6 +9,7 @@ _LIB = None
 
 SOG_NO_VALIDATE = 1
 SOG_TIMING = 2
+SOG_GRAPH = 4
 STATUS = {0: "SOG_OK", -1: "SOG_EINVAL", -2: "SOG_ENONNEUTRAL", -3: "SOG_EZRANGE",
           -4: "SOG_ENONFINITE", -5: "SOG_EINFEASIBLE", -6: "SOG_ECUDA", -7: "SOG_ENCCL", -8: "SOG_ENOMEM"}
 TIMING_NAMES = ["sort", "near", "mid_spread", "mid_fft_fwd", "mid_scale", "mid_fft_inv", "mid_gather",
@@ -179,8 +180,9 @@ class Plan:
         self.lib.sog_plan_describe(self.h, buf, n + 1)
         return _parse(buf.value.decode())
 
-    def set_flags(self, validate=True, timing=False):
-        self._flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
+    def set_flags(self, validate=True, timing=False, graph=False):
+        """graph=True: replay the evaluation as one CUDA graph (SOG_GRAPH; no stage timings)."""
+        self._flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0) | (SOG_GRAPH if graph else 0)
         self._check(self.lib.sog_set_flags(self.h, self._flags))
 
     def set_stream(self, stream):

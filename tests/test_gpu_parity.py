@@ -182,6 +182,30 @@ def test_determinism_and_host_path():
     assert np.array_equal(ph, a[0].cpu().numpy()) and np.array_equal(F, a[1].cpu().numpy())
 
 
+def test_cuda_graph_replay_is_bitwise_identical():
+    """SOG_GRAPH: the captured evaluation gives the same bits as the stream launches, re-captures
+    when the caller's buffers change, and follows new input values in the same buffers."""
+    xyz, q, L = config_system("c2", N=4000)
+    op = make_plan(len(q), *L, 1e-8)
+    pl = gpu_plan(op)
+    x, qq = to_dev(xyz, q)
+    p0, F0 = pl.eval(x, qq)
+    pl.set_flags(validate=True, graph=True)
+    for _ in range(2):
+        p1, F1 = pl.eval(x, qq)                      # new output tensors -> re-capture
+        assert torch.equal(p1, p0) and torch.equal(F1, F0)
+    phi = torch.empty_like(p0); F = torch.empty_like(F0)
+    pl.eval(x, qq, phi, F)
+    pl.eval(x, qq, phi, F)                           # replay
+    assert torch.equal(phi, p0) and torch.equal(F, F0)
+    x.add_(torch.tensor([0.37, -0.11, 0.0], dtype=torch.float64, device="cuda"))
+    pl.eval(x, qq, phi, F)                           # same buffers, new values
+    pl.set_flags(validate=True)
+    p2, F2 = pl.eval(x, qq)
+    assert torch.equal(phi, p2) and torch.equal(F, F2)
+    pl.close()
+
+
 def test_validation_errors():
     from paper_2412_04595_b200 import SogError
     xyz, q = uniform_system(100, (6.0, 6.0, 6.0), 5)
