@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--rc-factor", type=float, default=None, help="override rule R2's r_c factor (plan knob)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
+    ap.add_argument("--optimize", action="store_true", help="plan by R20 (eq::optimiz with B200 costs) instead of R2/R4")
     ap.add_argument("--no-graph", action="store_true", help="launch the kernels one by one (no CUDA graph replay)")
     ap.add_argument("--window", default="gs", choices=["gs", "kb"],
                     help="mid/long window: Gaussian (Eq. eq::GS) or Kaiser-Bessel polynomials (DESIGN.md R6-KB)")
@@ -339,7 +340,7 @@ def main():
     N = len(q)
     stream = torch.cuda.current_stream()
     plan = Plan(N, L, tol, stream=stream, validate=False, precision=args.precision, eta=args.eta,
-                rc_factor=args.rc_factor, window=args.window, long_method=args.long_method)
+                rc_factor=args.rc_factor, window=args.window, long_method=args.long_method, optimize=args.optimize)
     xd = torch.from_numpy(xyz).cuda()
     qd = torch.from_numpy(q).cuda()
     phi = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -410,6 +411,7 @@ def main():
                    "N_per_gpu": N, "tol": tol, "parallelism": f"replicas x{ws} (independent systems)",
                    "l2": "working set (mid grid %.1f GB) >> 126 MB L2; no flush" % (d["Ix"] * d["Iy"] * d["Izs"] * 8 / 1e9),
                    "window": args.window, "long_method": args.long_method, "cuda_graph": not args.no_graph,
+                   "plan_rule": "R20 optimiser" if args.optimize else "R1-R9",
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc", "Kx", "Ky")}},
         "stages_ms": acc,
         "roofline": roof,

@@ -91,6 +91,9 @@ typedef struct {
                                kx = 2 pi n / Lx, |n| <= Kx, ky = 2 pi n / Ly, 0 <= n <= Ky (DESIGN.md
                                R8-D), for boxes with few modes (cubic / tall: c2, c4, c5); single-GPU */
     int Kx, Ky;             /* direct long range mode bounds for explicit_params */
+    int optimize;           /* 1: R20, eq::optimiz with B200-calibrated costs: the
+                               plan of least predicted time over r_c factors {2.75 .. 3.75} x eta
+                               {0.2 .. 0.5} (rc_factor / eta ignored) */
 } sog_plan_opts;
 
 /* Build a plan for N particles in the box (Lx,Ly,Lz) at tolerance tol on the current

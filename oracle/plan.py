@@ -237,9 +237,42 @@ class Plan:
         return d
 
 
+# R20: eq::optimiz with B200-calibrated costs in seconds (c5 stage times, R20):
+# near per pair, mid spread+gather per stencil point, mid FFT+scale per grid point, long
+# spread+gather per (particle x Pl^2 x Pc), long FFT+scale per long grid point and layer
+GPU_COST = {"pair": 1.35e-11, "stencil": 1.39e-12, "grid": 2.6e-11, "long": 4.33e-13, "lgrid": 3.6e-11}
+OPT_RC = (2.75, 3.0, 3.25, 3.5, 3.75)
+OPT_ETA = (0.2, 0.25, 0.3, 0.35, 0.4, 0.5)
+
+
+def plan_cost(p: "Plan") -> float:
+    """R20 predicted evaluation time (s) of a plan: the terms of eq::comp (P:597) weighted by the
+    measured B200 costs; near pairs from the cutoff sphere clipped to the box height."""
+    c = GPU_COST
+    rho = p.N / (p.Lx * p.Ly * p.Lz)
+    vol = min(4.0 / 3.0 * math.pi * p.rc ** 3, math.pi * p.rc ** 2 * p.Lz)
+    t = c["pair"] * p.N * rho * vol
+    if p.m >= 0:
+        t += c["stencil"] * p.N * p.P ** 3 + c["grid"] * p.Ix * p.Iy * p.Izs
+    t += c["long"] * p.N * p.Pl ** 2 * p.Pc + c["lgrid"] * p.Ilx * p.Ily * p.Pc
+    return t
+
+
 def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Plan:
     """Rules R1-R9.  Keyword overrides replace any chosen value
-    (rc_factor, eta, b-row via `row`, or any Plan field)."""
+    (rc_factor, eta, b-row via `row`, or any Plan field).  optimize=True: R20, the plan of least
+    predicted time over r_c factors OPT_RC x range splits OPT_ETA (first minimum in that order)."""
+    if over.pop("optimize", False):
+        best, bc = None, None
+        for f in OPT_RC:
+            for e in OPT_ETA:
+                q = make_plan(N, Lx, Ly, Lz, tol, rc_factor=f, eta=e, **over)
+                if q.Pc > 32 or q.Pl > 25 or (q.m >= 0 and q.P > 25):
+                    continue                       # outside the GPU path's compiled range
+                c = plan_cost(q)
+                if bc is None or c < bc:
+                    best, bc = q, c
+        return best
     if N < 1 or not all(math.isfinite(v) and v > 0 for v in (Lx, Ly, Lz)):
         raise ValueError("invalid N or box")
     row = over.pop("row", None) or select_row(tol)

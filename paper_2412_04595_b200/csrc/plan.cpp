@@ -234,6 +234,39 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
     return true;
 }
 
+double plan_cost(const Params& p) {
+    // seconds: near per pair, mid stencil point, mid grid point, long particle x Pl^2 x Pc, long grid point x layer
+    const double c_pair = 1.35e-11, c_st = 1.39e-12, c_grid = 2.6e-11, c_long = 4.33e-13, c_lgrid = 3.6e-11;
+    const double N = double(p.N), rho = N / (p.Lx * p.Ly * p.Lz);
+    const double vol = std::min(4.0 / 3.0 * kPi * p.rc * p.rc * p.rc, kPi * p.rc * p.rc * p.Lz);
+    double t = c_pair * N * rho * vol;
+    if (p.m >= 0) t += c_st * N * double(p.P) * p.P * p.P + c_grid * double(p.Ix) * p.Iy * p.Izs;
+    t += c_long * N * double(p.Pl) * p.Pl * p.Pc + c_lgrid * double(p.Ilx) * p.Ily * p.Pc;
+    return t;
+}
+
+bool choose_params_opt(Params& p, const RuleKnobs& k, std::string& err) {
+    static const double rcs[] = {2.75, 3.0, 3.25, 3.5, 3.75};
+    static const double etas[] = {0.2, 0.25, 0.3, 0.35, 0.4, 0.5};
+    Params best;
+    double bc = -1.0;
+    for (double f : rcs)
+        for (double e : etas) {
+            Params q = p;
+            RuleKnobs kk = k;
+            kk.rc_factor = f;
+            kk.eta = e;
+            std::string er;
+            if (!choose_params(q, kk, er)) { err = er; continue; }
+            if (q.Pc > 32 || q.Pl > 25 || (q.m >= 0 && q.P > 25)) continue;   // GPU compiled range
+            const double c = plan_cost(q);
+            if (bc < 0.0 || c < bc) { best = q; bc = c; }
+        }
+    if (bc < 0.0) return false;
+    p = best;
+    return true;
+}
+
 bool validate_params(const Params& p, std::string& err) {
     auto bad = [&](const char* m) { err = m; return false; };
     if (p.N < 1 || p.N > (int64_t(1) << 31) - 1) return bad("N out of range [1, 2^31)");

@@ -868,7 +868,11 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
         p.long_method = o ? o->long_method : 0;
         if (o && o->rc_factor > 0) knobs.rc_factor = o->rc_factor;
         if (o && o->eta > 0) knobs.eta = o->eta;
-        if (!choose_params(p, knobs, err)) return fail(SOG_EINFEASIBLE, err);
+        if (o && o->optimize) {
+            if (!choose_params_opt(p, knobs, err)) return fail(SOG_EINFEASIBLE, err);
+        } else if (!choose_params(p, knobs, err)) {
+            return fail(SOG_EINFEASIBLE, err);
+        }
     }
     if (!validate_params(p, err)) return fail(SOG_EINVAL, err);
     return SOG_OK;

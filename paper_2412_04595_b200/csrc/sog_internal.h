@@ -54,6 +54,9 @@ struct RuleKnobs {
 
 // plan.cpp
 bool choose_params(Params& p, const RuleKnobs& k, std::string& err);   // rules R1-R9
+// R20: eq::optimiz with B200-calibrated costs: the least predicted time over r_c factor x eta grids
+bool choose_params_opt(Params& p, const RuleKnobs& k, std::string& err);
+double plan_cost(const Params& p);
 bool validate_params(const Params& p, std::string& err);
 void sog_weights(const Params& p, std::vector<double>& w, std::vector<double>& s);
 double erfcinv_host(double y);

@@ -36,7 +36,8 @@ class Opts(ctypes.Structure):
                 ("Ilx", ctypes.c_int), ("Ily", ctypes.c_int), ("Pl", ctypes.c_int), ("Sl", ctypes.c_double),
                 ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint),
                 ("precision", ctypes.c_int), ("window", ctypes.c_int), ("nu", ctypes.c_int),
-                ("nul", ctypes.c_int), ("long_method", ctypes.c_int), ("Kx", ctypes.c_int), ("Ky", ctypes.c_int)]
+                ("nul", ctypes.c_int), ("long_method", ctypes.c_int), ("Kx", ctypes.c_int), ("Ky", ctypes.c_int),
+                ("optimize", ctypes.c_int)]
 
 WINDOWS = {"gs": 0, "kb": 1}
 LONG_METHODS = {"fft": 0, "direct": 1}
@@ -133,7 +134,7 @@ class Plan:
     """
 
     def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
-                 validate=True, timing=False, precision="fp64", window="gs", long_method="fft"):
+                 validate=True, timing=False, precision="fp64", window="gs", long_method="fft", optimize=False):
         self.lib = load_library()
         self.N = int(N)
         self.L = tuple(float(v) for v in L)
@@ -149,6 +150,7 @@ class Plan:
         o.cuda_stream = _stream_handle(stream)
         o.precision = {"fp64": 0, "fp32": 1}[precision]
         _set_window(o, window, params, long_method)
+        o.optimize = int(bool(optimize))
         h = self.lib.sog_plan_create_ex(self.N, *self.L, self.tol, ctypes.byref(o))
         if not h:
             raise SogError(-1, self.lib.sog_last_error().decode())
@@ -274,13 +276,14 @@ def _parse(text):
     return out
 
 
-def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method="fft") -> dict:
+def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method="fft", optimize=False) -> dict:
     """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU)."""
     lib = load_library()
     o = Opts()
     o.rc_factor = float(rc_factor or 0.0)
     o.eta = float(eta or 0.0)
     _set_window(o, window, None, long_method)
+    o.optimize = int(bool(optimize))
     n = lib.sog_plan_choose(int(N), *[float(v) for v in L], float(tol), ctypes.byref(o), None, 0)
     if n < 0:
         raise _err(lib, n)

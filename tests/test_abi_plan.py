@@ -61,6 +61,20 @@ def test_plan_rules_match_oracle(name, N, L, tol, window, long_method):
             assert abs(lib_p[k] - v) <= 1e-13 * abs(v), (k, lib_p[k], v)
 
 
+@pytest.mark.parametrize("name,N,L,tol", CASES)
+def test_optimised_plan_matches_oracle(name, N, L, tol):
+    """R20 (eq::optimiz with B200 costs): library and oracle pick the same plan."""
+    lib_p = B.choose_params(N, L, tol, optimize=True)
+    ora = dataclasses.asdict(make_plan(N, *L, tol, optimize=True))
+    for k, v in ora.items():
+        if k in ("window", "long_method"):
+            continue
+        if isinstance(v, int):
+            assert lib_p[k] == v, (k, lib_p[k], v)
+        else:
+            assert abs(lib_p[k] - v) <= 1e-13 * abs(v), (k, lib_p[k], v)
+
+
 def test_plan_choose_errors():
     lib = B.load_library()
     o = B.Opts()
