@@ -53,7 +53,7 @@ def parse():
                     help="fp32 mode (BASELINE config c4 at tol 1e-4); the headline is fp64")
     ap.add_argument("--optimize", action="store_true", help="plan by R20 (eq::optimiz with B200 costs) instead of R2/R4")
     ap.add_argument("--no-graph", action="store_true", help="launch the kernels one by one (no CUDA graph replay)")
-    ap.add_argument("--window", default="gs", choices=["gs", "kb"],
+    ap.add_argument("--window", default="gs", choices=["gs", "kb", "es"],
                     help="mid/long window: Gaussian (Eq. eq::GS) or Kaiser-Bessel polynomials (DESIGN.md R6-KB)")
     ap.add_argument("--long-method", default="fft", choices=["fft", "direct"],
                     help="long range: Alg. 2 (window + FFT) or Alg. 3 without FFT (DESIGN.md R8-D)")

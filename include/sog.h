@@ -80,8 +80,9 @@ typedef struct {
     int precision;          /* 0: fp64 (default); 1: fp32 mode (S2-S12 in fp32 storage and
                                arithmetic, positions/outputs fp64 at the boundary; tol >= 1e-5,
                                whole-box plans with small long grids; parity bar 1e-5) */
-    int window;             /* 0: Gaussian window (Eq. eq::GS; default); 1: Kaiser-Bessel window
-                               (Remark rmk::PWindow) evaluated as per-stencil-point polynomials
+    int window;             /* 0: Gaussian window (Eq. eq::GS; default); 1: Kaiser-Bessel window,
+                               2: "exponential of semicircle" (ES) window (R6-ES; transform by
+                               quadrature) (Remark rmk::PWindow) evaluated as per-stencil-point polynomials
                                of degree nu (mid) / nul (long) from Chebyshev interpolation; with
                                window = 1, S and Sl are the KB shapes beta and the support half-width is
                                P h / 2 (R6-KB) */

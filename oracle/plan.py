@@ -112,7 +112,11 @@ def choose_window(s: float, eps_w: float, tol: float, cost_fn):
     return best[1], S, best[2]
 
 
-def choose_window_kb(s: float, eps_w: float, tol: float):
+ES_BETA = 2.3        # R6-ES: exponential-of-semicircle shape beta = ES_BETA * P (cf. beta = 2.5 P)
+ES_NU_EXTRA = 3      # R6-ES: nu = P + 3 as KB (the paper needs 1-2 more for ES; not with H = P h/2)
+
+
+def choose_window_kb(s: float, eps_w: float, tol: float, window: str = "kb"):
     """R6-KB: Kaiser-Bessel window (Remark rmk::PWindow, P:477-480), shape beta = KB_BETA P,
     support P = the smallest odd P >= 5 with 10^(a - b P) <= eps_w, mesh size at the Nyquist
     bound of R5 (the window does not constrain h).  Returns (P, beta, h, nu)."""
@@ -121,6 +125,8 @@ def choose_window_kb(s: float, eps_w: float, tol: float):
     while 10.0 ** (a - b * P) > eps_w:
         P += 2
     h = math.pi * s / (2.0 * KAPPA * math.sqrt(math.log(1.0 / tol)))
+    if window == "es":
+        return P, ES_BETA * P, h, P + ES_NU_EXTRA
     return P, KB_BETA * P, h, P + KB_NU_EXTRA
 
 
@@ -279,8 +285,8 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     b, r0, omega = row[0], row[1], row[2]
     rc_factor = over.pop("rc_factor", RC_FACTOR)
     window = over.pop("window", "gs")
-    if window not in ("gs", "kb"):
-        raise ValueError("window must be 'gs' or 'kb'")
+    if window not in ("gs", "kb", "es"):
+        raise ValueError("window must be 'gs', 'kb' or 'es'")
     long_method = over.pop("long_method", "fft")
     if long_method not in ("fft", "direct"):
         raise ValueError("long_method must be 'fft' or 'direct'")
@@ -318,8 +324,8 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
             pad = max(2.0 * ((P - 1) * h / 2.0 + h), sm * math.sqrt(math.log(PAD_C / tol)))
             return P ** 3 + FFT_COST * (Lx * Ly * (Lz + pad)) / (N * h ** 3)
 
-        if window == "kb":
-            P, S, h, p.nu = choose_window_kb(s0, eps_w, tol)
+        if window in ("kb", "es"):
+            P, S, h, p.nu = choose_window_kb(s0, eps_w, tol, window)
         else:
             P, S, h = choose_window(s0, eps_w, tol, cost_mid)
         p.P, p.S = P, S
@@ -334,8 +340,8 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
     def cost_long(P, h):
         return P ** 2 + LONG_FFT_COST * (Lx * Ly) / (N * h ** 2)
 
-    if window == "kb":
-        Pl, Sl, hl, p.nul = choose_window_kb(sl, eps_w, tol)      # R8 with R6-KB
+    if window in ("kb", "es"):
+        Pl, Sl, hl, p.nul = choose_window_kb(sl, eps_w, tol, window)   # R8 with R6-KB / R6-ES
     else:
         Pl, Sl, hl = choose_window(sl, eps_w, tol, cost_long)      # R8
     p.Pl, p.Sl = Pl, Sl

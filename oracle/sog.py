@@ -149,14 +149,38 @@ def kb_window_hat(k, H: float, beta: float):
     return 2.0 * H * f / scipy.special.i0(beta)
 
 
+def es_window(d, H: float, beta: float):
+    """"Exponential of semicircle" window exp(beta (sqrt(1 - (x/H)^2) - 1)) for |x| <= H, else 0
+    (Remark rmk::PWindow, P:477-480; Barnett et al. 2019)."""
+    d = np.asarray(d, dtype=np.float64)
+    t = np.clip(1.0 - (d / H) ** 2, 0.0, None)
+    return np.where(np.abs(d) <= H, np.exp(beta * (np.sqrt(t) - 1.0)), 0.0)
+
+
+def es_window_hat(k, H: float, beta: float):
+    """Fourier transform of the ES window (no closed form): with x = H sin(theta),
+    H int_{-pi/2}^{pi/2} exp(beta (cos theta - 1)) cos(k H sin theta) cos theta dtheta, by adaptive
+    quadrature (R6-ES)."""
+    from scipy.integrate import quad
+    ks = np.atleast_1d(np.asarray(k, dtype=np.float64))
+    out = np.empty_like(ks)
+    for i, kk in enumerate(ks):
+        f = lambda th: math.exp(beta * (math.cos(th) - 1.0)) * math.cos(kk * H * math.sin(th)) * math.cos(th)
+        out[i] = H * quad(f, -0.5 * math.pi, 0.5 * math.pi, epsabs=1e-17, epsrel=1e-13, limit=400)[0]
+    return out.reshape(np.shape(k)) if np.ndim(k) else out[0]
+
+
+POLY_WINDOWS = {"kb": kb_window, "es": es_window}
+
+
 def window_half_width(window: str, P: int, h: float) -> float:
-    """Support half-width H: (P-1)h/2 for the Gaussian (Eq. eq::GS, P:676); P h/2 for KB
-    (R6-KB: every one of the P stencil points stays inside the support for all particle
-    offsets, so each stencil point's weight is analytic in the offset)."""
-    return (P * h if window == "kb" else (P - 1) * h) / 2.0
+    """Support half-width H: (P-1)h/2 for the Gaussian (Eq. eq::GS, P:676); P h/2 for the
+    polynomial windows KB / ES (R6-KB: every one of the P stencil points stays inside the support
+    for all particle offsets, so each stencil point's weight is analytic in the offset)."""
+    return (P * h if window in POLY_WINDOWS else (P - 1) * h) / 2.0
 
 
-def kb_stencil_polys(P: int, beta: float, nu: int):
+def kb_stencil_polys(P: int, beta: float, nu: int, window: str = "kb"):
     """R6-KB (the paper's polynomial windows, Remark rmk::PWindow P:477-480): for stencil
     point j = 0..P-1 and the particle's offset u = x/h + I/2 - g0 in [-1/2, 1/2), the weight
     W_KB((j - p - u) h) is replaced by its degree-nu interpolant at the nu+1 first-kind
@@ -165,7 +189,7 @@ def kb_stencil_polys(P: int, beta: float, nu: int):
     p = (P - 1) // 2
     C = np.empty((P, nu + 1))
     for j in range(P):
-        C[j] = npcheb.chebinterpolate(lambda t: kb_window((j - p - 0.5 * t), 0.5 * P, beta), nu)
+        C[j] = npcheb.chebinterpolate(lambda t: POLY_WINDOWS[window]((j - p - 0.5 * t), 0.5 * P, beta), nu)
     return C
 
 
@@ -174,6 +198,8 @@ def window_hat(plan: Plan, k, H: float, long: bool = False):
     shape = plan.Sl if long else plan.S
     if plan.window == "kb":
         return kb_window_hat(k, H, shape)
+    if plan.window == "es":
+        return es_window_hat(k, H, shape)
     return gaussian_window_hat(k, H, shape)
 
 
@@ -187,9 +213,9 @@ def stencil(x: np.ndarray, I: int, h: float, P: int, S: float, periodic: bool, w
     H = window_half_width(window, P, h)
     g0 = np.floor(x / h + (I / 2.0 + 0.5)).astype(np.int64)
     g = g0[:, None] + np.arange(-p, p + 1)[None, :]
-    if window == "kb":
+    if window in POLY_WINDOWS:
         u = x / h + I / 2.0 - g0                 # in [-1/2, 1/2)
-        C = kb_stencil_polys(P, S, nu)
+        C = kb_stencil_polys(P, S, nu, window)
         W = np.stack([npcheb.chebval(2.0 * u, C[j]) for j in range(P)], axis=1)
         dW = np.stack([npcheb.chebval(2.0 * u, npcheb.chebder(C[j])) * 2.0 / h for j in range(P)], axis=1)
     else:

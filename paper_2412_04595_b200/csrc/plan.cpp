@@ -67,12 +67,12 @@ bool choose_window(double s, double eps_w, double tol, double kappa, Cost cost, 
 
 // R6-KB: support P = smallest odd >= 5 with 10^(a - b P) <= eps_w, beta = kb_beta P, the mesh at
 // the Nyquist bound (the window does not constrain h), nu = P + kb_nu_extra
-void choose_window_kb(double s, double eps_w, double tol, const RuleKnobs& k, int& Pout, double& beta, double& h,
-                      int& nu) {
+void choose_window_kb(double s, double eps_w, double tol, const RuleKnobs& k, int window, int& Pout, double& beta,
+                      double& h, int& nu) {
     int P = 5;
     while (std::pow(10.0, k.kb_rate_a - k.kb_rate_b * P) > eps_w) P += 2;
     Pout = P;
-    beta = k.kb_beta * P;
+    beta = (window == 2 ? k.es_beta : k.kb_beta) * P;   // R6-ES / R6-KB
     h = kPi * s / (2.0 * k.kappa * std::sqrt(std::log(1.0 / tol)));
     nu = P + k.kb_nu_extra;
 }
@@ -200,8 +200,8 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
             return double(P) * P * P + k.fft_cost * (p.Lx * p.Ly * (p.Lz + pad)) / (N * h * h * h);
         };
         double h;
-        if (p.window == 1)
-            choose_window_kb(s0, eps_w, p.tol, k, p.P, p.S, h, p.nu);
+        if (p.window == 1 || p.window == 2)
+            choose_window_kb(s0, eps_w, p.tol, k, p.window, p.P, p.S, h, p.nu);
         else if (!choose_window(s0, eps_w, p.tol, k.kappa, cost_mid, p.P, p.S, h)) { err = "no mid window"; return false; }
         p.Ix = friendly_even(long(std::ceil(p.Lx / h)));
         p.Iy = friendly_even(long(std::ceil(p.Ly / h)));
@@ -216,8 +216,8 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
         return double(P) * P + k.long_fft_cost * (p.Lx * p.Ly) / (N * h * h);
     };
     double hl;
-    if (p.window == 1)
-        choose_window_kb(sl, eps_w, p.tol, k, p.Pl, p.Sl, hl, p.nul);
+    if (p.window == 1 || p.window == 2)
+        choose_window_kb(sl, eps_w, p.tol, k, p.window, p.Pl, p.Sl, hl, p.nul);
     else if (!choose_window(sl, eps_w, p.tol, k.kappa, cost_long, p.Pl, p.Sl, hl)) { err = "no long window"; return false; }
     p.Ilx = std::max(friendly_even(long(std::ceil(p.Lx / hl))), friendly_even(p.Pl));
     p.Ily = std::max(friendly_even(long(std::ceil(p.Ly / hl))), friendly_even(p.Pl));
@@ -289,11 +289,11 @@ bool validate_params(const Params& p, std::string& err) {
     if (!(p.Sl > 0)) return bad("bad long window shape");
     if (p.Ilx < p.Pl || p.Ily < p.Pl) return bad("long grid smaller than the window support");
     if (p.Pc < 2 || p.Pc > 32) return bad("Pc must be in [2,32]");
-    if (p.window != 0 && p.window != 1) return bad("window must be 0 (Gaussian) or 1 (Kaiser-Bessel)");
+    if (p.window < 0 || p.window > 2) return bad("window must be 0 (Gaussian), 1 (Kaiser-Bessel) or 2 (ES)");
     if (p.long_method != 0 && p.long_method != 1) return bad("long_method must be 0 (FFT) or 1 (direct)");
     if (p.long_method == 1 && (p.Kx < 0 || p.Ky < 0 || p.Kx > 63 || p.Ky > 63))
         return bad("direct long range: mode bounds Kx, Ky must be in [0, 63]");
-    if (p.window == 1) {
+    if (p.window == 1 || p.window == 2) {
         if ((p.m >= 0 && p.P > 17) || p.Pl > 17) return bad("KB window support must be <= 17");
         if (p.m >= 0 && (p.nu < 2 || p.nu > p.P + 3)) return bad("KB mid polynomial degree nu must be in [2, P+3]");
         if (p.nul < 2 || p.nul > p.Pl + 3) return bad("KB long polynomial degree nul must be in [2, Pl+3]");
@@ -382,13 +382,13 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
     auto axis = [&](int I, double Lper, double h, bool half, std::vector<double>& T) {
         int n = half ? I / 2 + 1 : I;
         T.resize(size_t(L) * n);
-        double H = (p.window == 1 ? p.P : p.P - 1) * h / 2.0;
+        double H = (p.window != 0 ? p.P : p.P - 1) * h / 2.0;
         for (int l = 0; l < L; ++l)
             for (int i = 0; i < n; ++i) {
                 int f = (half || i < (I + 1) / 2) ? i : i - I;   // numpy fftfreq ordering
                 double kk = 2.0 * kPi * f / Lper;
-                if (p.window == 1) {   // R6-KB: exp(-k^2 s_l^2/4) / W_KB(k)^2
-                    const double wh = kb_hat(kk, H, p.S);
+                if (p.window != 0) {   // R6-KB / R6-ES: exp(-k^2 s_l^2/4) / W(k)^2
+                    const double wh = poly_window_hat(p.window, kk, H, p.S);
                     T[size_t(l) * n + i] = std::exp(-kk * kk * s[l] * s[l] / 4.0) / (wh * wh);
                     continue;
                 }
@@ -410,7 +410,7 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
     const int P = p.Pc, nx = p.Ilx, ny = p.Ily / 2 + 1;
     std::vector<double> za(P);
     for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
-    const int Pw = p.window == 1 ? p.Pl : p.Pl - 1;   // support width in mesh steps (R6 / R6-KB)
+    const int Pw = p.window != 0 ? p.Pl : p.Pl - 1;   // support width in mesh steps (R6 / R6-KB)
     const double Hx = Pw * p.hlx() / 2.0, Hy = Pw * p.hly() / 2.0;
     K.assign(size_t(nx) * ny * P * P, 0.0);
     std::vector<double> Cm;
@@ -422,9 +422,9 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
             double ky = 2.0 * kPi * iy / p.Ly;
             double k2 = kx * kx + ky * ky;
             // 1 / (W_x W_y)^2
-            double Wx = p.window == 1 ? kb_hat(kx, Hx, p.Sl)
+            double Wx = p.window != 0 ? poly_window_hat(p.window, kx, Hx, p.Sl)
                                       : std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
-            double Wy = p.window == 1 ? kb_hat(ky, Hy, p.Sl)
+            double Wy = p.window != 0 ? poly_window_hat(p.window, ky, Hy, p.Sl)
                                       : std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
             // 1/(Ilx Ily) of the (unnormalised) cuFFT inverse is folded in here (R12)
             double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
@@ -523,7 +523,47 @@ double kb_hat(double k, double H, double beta) {
     return 2.0 * H * f / std::cyl_bessel_i(0.0, beta);
 }
 
-void build_kb_poly(int P, double beta, int nu, std::vector<double>& c) {
+// ES transform H int_{-pi/2}^{pi/2} exp(beta (cos t - 1)) cos(k H sin t) cos t dt (x = H sin t; the
+// integrand is entire in t): 192-point Gauss-Legendre, nodes by Newton on P_n in long double
+double es_hat(double k, double H, double beta) {
+    static std::vector<long double> xs, ws;
+    if (xs.empty()) {
+        const int n = 192;
+        const long double pi = 3.141592653589793238462643383279502884L;
+        xs.resize(n);
+        ws.resize(n);
+        for (int i = 0; i < n; ++i) {
+            long double x = std::cos(pi * (i + 0.75L) / (n + 0.5L)), dp = 0;
+            for (int it = 0; it < 100; ++it) {
+                long double p0 = 1, p1 = x;
+                for (int m = 2; m <= n; ++m) {
+                    const long double p2 = ((2 * m - 1) * x * p1 - (m - 1) * p0) / m;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                dp = n * (x * p1 - p0) / (x * x - 1);
+                const long double dx = p1 / dp;
+                x -= dx;
+                if (std::fabs(dx) < 1e-19L) break;
+            }
+            xs[i] = x;
+            ws[i] = 2.0L / ((1 - x * x) * dp * dp);
+        }
+    }
+    const long double half = 1.5707963267948966192313216916397514L;
+    long double acc = 0;
+    for (size_t i = 0; i < xs.size(); ++i) {
+        const long double t = half * xs[i];
+        acc += ws[i] * std::exp((long double)beta * (std::cos(t) - 1)) * std::cos((long double)k * H * std::sin(t)) * std::cos(t);
+    }
+    return double((long double)H * half * acc);
+}
+
+double poly_window_hat(int window, double k, double H, double beta) {
+    return window == 2 ? es_hat(k, H, beta) : kb_hat(k, H, beta);
+}
+
+void build_kb_poly(int P, double beta, int nu, std::vector<double>& c, int window) {
     // Chebyshev interpolation in t = 2u at the nu+1 first-kind points (discrete orthogonality),
     // then the series sum_n a_n T_n(2u) re-expanded in powers of u, all in long double.
     const int p = (P - 1) / 2, n1 = nu + 1;
@@ -536,7 +576,9 @@ void build_kb_poly(int P, double beta, int nu, std::vector<double>& c) {
             const long double t = std::cos((i + 0.5L) * pi / n1);
             const long double x = (long double)(j - p) - 0.5L * t;      // (x_g - x) / h
             const long double r = 1.0L - (x / half_w) * (x / half_w);
-            f[i] = r < 0 ? 0.0L : std::cyl_bessel_il(0.0L, (long double)beta * std::sqrt(r)) / i0b;
+            f[i] = r < 0 ? 0.0L
+                         : (window == 2 ? std::exp((long double)beta * (std::sqrt(r) - 1.0L))    // ES
+                                        : std::cyl_bessel_il(0.0L, (long double)beta * std::sqrt(r)) / i0b);
         }
         for (int n = 0; n < n1; ++n) {
             long double acc = 0;

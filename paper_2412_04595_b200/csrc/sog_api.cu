@@ -244,7 +244,7 @@ void free_plan(sog_plan* pl) {
     delete pl;
 }
 
-void kb_table(int P, double beta, int nu, KBTab& t);
+void kb_table(int P, double beta, int nu, int window, KBTab& t);
 
 int setup(sog_plan* pl) {
     Params& p = pl->p;
@@ -368,8 +368,8 @@ int setup(sog_plan* pl) {
         if ((rc = upload(pl, &pl->d_A, A)) || (rc = upload(pl, &pl->d_Tx, Tx)) || (rc = upload(pl, &pl->d_Ty, Ty)) ||
             (rc = upload(pl, &pl->d_Tz, Tz)))
             return rc;
-        z.kb = p.window == 1 ? 1 : 0;
-        if (z.kb) kb_table(p.P, p.S, p.nu, z.kt);
+        z.kb = p.window != 0 ? 1 : 0;                  // KB and ES: the polynomial-window kernels
+        if (z.kb) kb_table(p.P, p.S, p.nu, p.window, z.kt);
         size_t ws = 0;
         if (!slab) {
             // z-pruned 3D FFT: 2D (x,y) over the planes the spread writes, 1D along z on zero-padded
@@ -464,7 +464,7 @@ int setup(sog_plan* pl) {
         auto gam = [&](double h) { double H = (p.Pl - 1) * h / 2.0; return std::exp(-2.0 * p.Sl / (H * H) * h * h); };
         t.gamma_x = gam(p.hlx());
         t.gamma_y = gam(p.hly());
-        if (p.window == 1) kb_table(p.Pl, p.Sl, p.nul, pl->kbl);
+        if (p.window != 0) kb_table(p.Pl, p.Sl, p.nul, p.window, pl->kbl);
         int pcmax = p.Pc <= 16 ? 16 : 32;
         if (t.nchunk > 1 && (rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
         if ((rc = dalloc(pl, &pl->lpsiT, (size_t)p.Ilx * p.Ily * 32))) return rc;
@@ -535,9 +535,9 @@ MidArgs mid_args(const sog_plan* pl) {
 }
 
 // R6-KB table: the degree-nu monomial coefficients, zero-padded to degree P + 3 (kernels_common.cuh)
-void kb_table(int P, double beta, int nu, KBTab& t) {
+void kb_table(int P, double beta, int nu, int window, KBTab& t) {
     std::vector<double> c;
-    build_kb_poly(P, beta, nu, c);
+    build_kb_poly(P, beta, nu, c, window);
     for (int i = 0; i < KB_TAB; ++i) t.c[i] = 0.0;
     for (int n = 0; n <= nu; ++n)
         for (int j = 0; j < P; ++j) t.c[n * P + j] = c[size_t(n) * P + j];
@@ -557,7 +557,7 @@ LongArgs long_args(const sog_plan* pl) {
     a.two_over_Lz = 2.0 / p.Lz;
     a.A = a.hx * a.hy;
     a.C = pl->d_C;
-    a.kb = p.window == 1 ? 1 : 0;
+    a.kb = p.window != 0 ? 1 : 0;
     a.kt = pl->kbl;
     return a;
 }
@@ -857,12 +857,12 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
         p.long_method = o->long_method;
         p.Kx = o->Kx;
         p.Ky = o->Ky;
-        if (p.window == 1) {
+        if (p.window != 0) {
             p.nu = p.m >= 0 ? (o->nu > 0 ? o->nu : p.P + knobs.kb_nu_extra) : 0;
             p.nul = o->nul > 0 ? o->nul : p.Pl + knobs.kb_nu_extra;
         }
     } else {
-        if (o && o->window != 0 && o->window != 1) return fail(SOG_EINVAL, "window must be 0 or 1");
+        if (o && (o->window < 0 || o->window > 2)) return fail(SOG_EINVAL, "window must be 0, 1 or 2");
         if (o && o->long_method != 0 && o->long_method != 1) return fail(SOG_EINVAL, "long_method must be 0 or 1");
         p.window = o ? o->window : 0;
         p.long_method = o ? o->long_method : 0;

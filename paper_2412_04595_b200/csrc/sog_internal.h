@@ -23,8 +23,9 @@ struct Params {
     int Ilx = 0, Ily = 0, Pl = 0;
     double Sl = 0;
     int Pc = 0;
-    // window (R6 / R6-KB): 0 = Gaussian (Eq. eq::GS), 1 = Kaiser-Bessel as per-stencil-point
-    // polynomials of degree nu (mid) / nul (long); S, Sl hold beta for KB
+    // window (R6 / R6-KB / R6-ES): 0 = Gaussian (Eq. eq::GS), 1 = Kaiser-Bessel, 2 = exponential of
+    // semicircle, the last two as per-stencil-point polynomials of degree nu (mid) / nul (long); S, Sl
+    // hold beta for KB / ES
     int window = 0, nu = 0, nul = 0;
     // long range: 0 = Alg. 2 (window + 2D FFT), 1 = Alg. 3 without FFT (App. B): direct Fourier
     // sums over kx = 2 pi n / Lx, |n| <= Kx, ky = 2 pi n / Ly, 0 <= n <= Ky (R8-D)
@@ -48,6 +49,7 @@ struct RuleKnobs {
     double fft_cost = 30.0;   // R6 cost model (grid point vs stencil point, B200-measured)
     double long_fft_cost = 30.0;
     double kb_beta = 2.2;     // R6-KB: beta = kb_beta * P
+    double es_beta = 2.3;     // R6-ES: beta = es_beta * P
     int kb_nu_extra = 3;      // R6-KB: nu = P + kb_nu_extra
     double kb_rate_a = 0.4, kb_rate_b = 0.92;   // R6-KB: window error ~ 10^(a - b P)
 };
@@ -85,9 +87,10 @@ void build_long_kernel(const Params& p, std::vector<double>& K);
 void build_long_kernel_direct(const Params& p, std::vector<double>& K);
 // R6-KB: monomial coefficients c[n * P + j] (n = 0..nu) in u = x/h + I/2 - g0 of the degree-nu
 // Chebyshev interpolant of W_KB((j - p - u) h), H = P h / 2 (Remark rmk::PWindow)
-void build_kb_poly(int P, double beta, int nu, std::vector<double>& c);
+void build_kb_poly(int P, double beta, int nu, std::vector<double>& c, int window = 1);   // 1 KB, 2 ES
 // Fourier transform of the KB window of half-width H (sinh / sin branches)
 double kb_hat(double k, double H, double beta);
+double poly_window_hat(int window, double k, double H, double beta);   // KB (1) closed form, ES (2) quadrature
 // Chebyshev -> Lagrange coefficient matrix C[b][n]: L_b(x) = sum_n C[b][n] T_n(x).
 void build_cheb_matrix(int Pc, std::vector<double>& C);
 // Tn[a][m] = T_m(x_a) at the first-kind nodes x_a = cos((a+1/2) pi / Pc).

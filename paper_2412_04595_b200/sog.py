@@ -39,7 +39,7 @@ class Opts(ctypes.Structure):
                 ("nul", ctypes.c_int), ("long_method", ctypes.c_int), ("Kx", ctypes.c_int), ("Ky", ctypes.c_int),
                 ("optimize", ctypes.c_int)]
 
-WINDOWS = {"gs": 0, "kb": 1}
+WINDOWS = {"gs": 0, "kb": 1, "es": 2}
 LONG_METHODS = {"fft": 0, "direct": 1}
 
 

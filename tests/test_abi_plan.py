@@ -41,7 +41,7 @@ CASES += [("tiny", 2, (20.0, 20.0, 20.0), 1e-6), ("confined", 5000, (60.0, 60.0,
           ("tall", 3000, (6.0, 7.0, 90.0), 1e-4), ("dense", 100000, (10.0, 10.0, 10.0), 1e-8)]
 
 
-@pytest.mark.parametrize("window,long_method", [("gs", "fft"), ("kb", "fft"), ("gs", "direct")])
+@pytest.mark.parametrize("window,long_method", [("gs", "fft"), ("kb", "fft"), ("es", "fft"), ("gs", "direct")])
 @pytest.mark.parametrize("name,N,L,tol", CASES)
 def test_plan_rules_match_oracle(name, N, L, tol, window, long_method):
     ora = dataclasses.asdict(make_plan(N, *L, tol, window=window, long_method=long_method))

@@ -118,3 +118,29 @@ def test_kb_library_rules_vs_ewald():
     phi = phi.cpu().numpy()[t]
     assert np.max(np.abs(phi - ref)) / np.max(np.abs(ref)) < 1e-6
     assert rel(F.cpu().numpy()[t], -q[t, None] * g) < 1e-5
+
+
+# ------------------------------------------------------------------ ES window (R6-ES), same kernels
+def test_es_c1_components_and_total():
+    xyz, q, L = config_system("c1")
+    check_total(make_plan(len(q), *L, 1e-6, window="es"), xyz, q)
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-12])
+def test_es_c2_tolerance_sweep_small(tol):
+    xyz, q, L = config_system("c2", N=3000)
+    check_total(make_plan(len(q), *L, tol, window="es"), xyz, q)
+
+
+def test_es_c5_small_and_fp32():
+    xyz, q, L = config_system("c5", N=5000)
+    check_total(make_plan(len(q), *L, 1e-6, window="es"), xyz, q)
+    xyz, q, L = config_system("c4", N=4000)
+    op = make_plan(len(q), *L, 1e-4, window="es")
+    pl = gpu_plan(op, precision="fp32")
+    x, qq = to_dev(xyz, q)
+    phi, F = pl.eval(x, qq)
+    torch.cuda.synchronize()
+    phi_o, F_o = O.evaluate(op, xyz, q)
+    pl.close()
+    assert rel(phi.cpu().numpy(), phi_o) <= TOL_FP32 and rel(F.cpu().numpy(), F_o) <= TOL_FP32

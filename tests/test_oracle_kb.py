@@ -116,3 +116,53 @@ def test_kb_total_vs_ewald2d(name, N, tol):
     Fref = -q[t, None] * g
     assert np.max(np.abs(phi - ref)) / np.max(np.abs(ref)) < tol
     assert np.linalg.norm(F - Fref) / np.linalg.norm(Fref) < 10 * tol
+
+
+# ------------------------------------------------------------------ ES window (R6-ES)
+def _es(x, H, beta):
+    return math.exp(beta * (math.sqrt(1.0 - (x / H) ** 2) - 1.0)) if abs(x) <= H else 0.0
+
+
+@pytest.mark.parametrize("H,beta", [(2.5, 11.5), (4.5, 20.7), (7.5, 34.5)])
+def test_es_window_fourier_transform(H, beta):
+    """The oracle's ES transform (quadrature in theta, x = H sin theta) equals the direct x-integral
+    of the window written out independently."""
+    for kH in (0.0, 0.5, 2.0, 0.5 * math.pi * 2 * H, 1.3 * beta):
+        k = kH / H
+        ref = quad(lambda x: _es(x, H, beta) * math.cos(k * x), -H, H, limit=800, epsabs=1e-15, epsrel=1e-12)[0]
+        scale = quad(lambda x: _es(x, H, beta), -H, H, limit=800)[0]
+        assert abs(sog.es_window_hat(k, H, beta) - ref) < 1e-10 * scale
+
+
+def test_es_polynomials_interpolate_the_window():
+    for Pw, nu, acc in ((7, 10, 1e-6), (11, 14, 1e-9), (15, 18, 1e-12)):
+        beta = 2.3 * Pw
+        p = (Pw - 1) // 2
+        C = sog.kb_stencil_polys(Pw, beta, nu, "es")
+        tt = np.linspace(-1, 1, 101)
+        for j in range(Pw):
+            exact = np.array([_es(j - p - 0.5 * t, 0.5 * Pw, beta) for t in tt])
+            assert np.max(np.abs(npcheb.chebval(tt, C[j]) - exact)) < acc
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-12])
+def test_es_mid_long_converge_to_exact(tol):
+    xyz, q, L = config_system("c1", N=300)
+    t = np.arange(12)
+    p = P.make_plan(len(q), *L, tol, window="es")
+    assert p.S == pytest.approx(2.3 * p.P)
+    x = sog.canonicalize(xyz, p)
+    for spec, exact in ((sog.mid_range, sog_exact.mid_exact), (sog.long_range, sog_exact.long_exact)):
+        sp, ex = spec(p, x, q, t), exact(p, x, q, t)
+        assert np.max(np.abs(sp[0] - ex[0])) < 10 * tol
+        assert np.max(np.abs(sp[1] - ex[1])) < 100 * tol
+
+
+def test_es_total_vs_ewald2d():
+    xyz, q, L = config_system("c1", N=1000)
+    t = np.arange(24)
+    p = P.make_plan(len(q), *L, 1e-6, window="es")
+    phi, F = sog.evaluate(p, xyz, q, targets=t)
+    ref, g = ewald2d.ewald2d(xyz, q, L, targets=t)
+    assert np.max(np.abs(phi - ref)) / np.max(np.abs(ref)) < 1e-6
+    assert np.linalg.norm(F + q[t, None] * g) / np.linalg.norm(q[t, None] * g) < 1e-5
