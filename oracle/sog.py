@@ -161,7 +161,9 @@ def es_window_hat(k, H: float, beta: float):
     """Fourier transform of the ES window (no closed form): with x = H sin(theta),
     H int_{-pi/2}^{pi/2} exp(beta (cos theta - 1)) cos(k H sin theta) cos theta dtheta, by adaptive
     quadrature (R6-ES)."""
-    from scipy.integrate import quad
+    import warnings
+    from scipy.integrate import IntegrationWarning, quad
+    warnings.simplefilter("ignore", IntegrationWarning)    # round-off notices near 1e-16 relative
     ks = np.atleast_1d(np.asarray(k, dtype=np.float64))
     out = np.empty_like(ks)
     for i, kk in enumerate(ks):
