@@ -304,6 +304,38 @@ def test_full_size_c5_properties():
     assert np.linalg.norm(F0.sum(0)) <= 1e-6 * np.abs(F0).max() * math.sqrt(len(q))
 
 
+@pytest.mark.parametrize("window", ["gs", "kb"])
+def test_full_size_s1_properties(window):
+    """The confined workload s1 (N=1e6, Lz = 0.3, mid off, 3840^2 long grid) in the bench
+    configuration: the near component at sampled targets vs the oracle, exact invariance under a
+    shift by one period in x and y, z-reflection symmetry, linearity in q and sum F ~ 0."""
+    xyz, q, L = config_system("s1")
+    op = make_plan(len(q), *L, 1e-6, window=window)
+    assert op.m == -1
+    pl = gpu_plan(op)
+    xd, qd = to_dev(xyz, q)
+    phi, F = pl.eval(xd, qd)
+    comp = pl.components(xd, qd)
+    t = np.random.default_rng(6).choice(len(q), 64, replace=False)
+    x = O.canonicalize(xyz, op)
+    pn, gn = O.near_field(op, x, q, targets=t)
+    c = comp[0].cpu().numpy()[t]
+    assert rel(c[:, 0], pn) <= TOL_FP64 and rel(c[:, 1:], gn) <= TOL_FP64
+    phi0, F0 = phi.cpu().numpy(), F.cpu().numpy()
+    s = xyz.copy(); s[:, 0] -= L[0]; s[:, 1] += L[1]
+    p2, _ = pl.eval(*to_dev(s, q))
+    # exact up to the rounding of the wrapped coordinates (ulp(L/2) = 1.1e-13 at L = 953)
+    assert rel(p2.cpu().numpy(), phi0) <= 5e-12
+    r = xyz.copy(); r[:, 2] *= -1
+    p3, F3 = pl.eval(*to_dev(r, q))
+    assert rel(p3.cpu().numpy(), phi0) <= 1e-12
+    assert rel(F3.cpu().numpy()[:, 2], -F0[:, 2]) <= 1e-11
+    p4, _ = pl.eval(xd, 0.5 * qd)
+    assert rel(p4.cpu().numpy(), 0.5 * phi0) <= 1e-14
+    assert np.linalg.norm(F0.sum(0)) <= 1e-6 * np.abs(F0).max() * math.sqrt(len(q))
+    pl.close()
+
+
 TOL_FP32 = 1e-5      # north_star: <= 1e-5 relative L2 vs the fp64 oracle in fp32 mode
 
 
