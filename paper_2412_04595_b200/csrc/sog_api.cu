@@ -165,6 +165,10 @@ struct sog_plan {
     cudaGraphExec_t gexec = nullptr;
     const void* gkey[4] = {};
     cudaStream_t gstream = nullptr;         // private capture stream (the legacy stream cannot capture)
+    // near field on a side stream, concurrent with the mid / long chain (ALU-bound pair kernel next
+    // to the HBM-bound FFT steps); joined before the combine
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double timings[11] = {};
     size_t bytes = 0;
     // ---- x-slab rank (R > 1); R == 1: the whole periodic box ----
@@ -241,6 +245,9 @@ void free_plan(sog_plan* pl) {
         if (e) cudaEventDestroy(e);
     if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
     if (pl->gstream) cudaStreamDestroy(pl->gstream);
+    if (pl->side) cudaStreamDestroy(pl->side);
+    if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
+    if (pl->ev_join) cudaEventDestroy(pl->ev_join);
     delete pl;
 }
 
@@ -508,6 +515,17 @@ int setup(sog_plan* pl) {
         CK(cudaMallocHost((void**)&pl->pin_i, 8 * sizeof(int)));
     }
     for (auto& e : pl->ev) CK(cudaEventCreate(&e));
+    if (!slab) {   // SOG_NEAR_STREAM=off|low|high (default low): near-field side stream and its priority
+        const char* env = std::getenv("SOG_NEAR_STREAM");
+        const std::string mode = env ? env : "low";
+        if (mode != "off") {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&pl->side, cudaStreamNonBlocking, mode == "high" ? hi : lo));
+            CK(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
+        }
+    }
     return SOG_OK;
 }
 
@@ -740,7 +758,20 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
     int rc;
     if ((rc = st_sort(pl, xyz, q, int(p.N)))) return rc;
     mark(pl, 1);
-    if (!stop_stage && (rc = st_near(pl))) return rc;
+    // near field: on the side stream, concurrent with the mid / long chain (not when per-stage
+    // timings are collected: they need the stages in sequence)
+    const bool overlap = !stop_stage && pl->side && !(pl->flags & SOG_TIMING);
+    if (overlap) {
+        CK(cudaEventRecord(pl->ev_fork, st));
+        CK(cudaStreamWaitEvent(pl->side, pl->ev_fork, 0));
+        pl->stream = pl->side;
+        rc = st_near(pl);
+        pl->stream = st;
+        if (rc) return rc;
+        CK(cudaEventRecord(pl->ev_join, pl->side));
+    } else if (!stop_stage && (rc = st_near(pl))) {
+        return rc;
+    }
     mark(pl, 2);
     // S3-S7 mid range
     if (pl->has_mid && (stop_stage == 0 || stop_stage == 1 || stop_stage == 2)) {
@@ -791,6 +822,7 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         if (stop_stage == 4) return SOG_OK;
         if ((rc = st_long_gather(pl))) return rc;
     }
+    if (overlap) CK(cudaStreamWaitEvent(st, pl->ev_join, 0));
     mark(pl, 10);
     return SOG_OK;
 }
