@@ -39,6 +39,7 @@ struct CellGeo {
     double sx, sy, sz;      // cells per unit length (nc / L)
     double x0;              // x of the first cell edge (-Lx/2 for the whole box)
     int px;                 // 1: x periodic (whole box), 0: x-slab (no x images)
+    int nzr;                // z neighbour reach in cells: cell height >= r_c / nzr (near field)
 };
 
 // One axis of a window stencil on a uniform grid x_g = (g - I/2) h (R6):

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_near(NearArgs a) {
         for (int iy = 0; iy < a.noffy; ++iy) {
             int ny = cy + a.oy[iy];
             ny = ny < 0 ? ny + g.ncy : (ny >= g.ncy ? ny - g.ncy : ny);
-            int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
+            int z0 = max(0, cz - g.nzr), z1 = min(g.ncz - 1, cz + g.nzr);
             int c0 = (nx * g.ncy + ny) * g.ncz;
             int j0 = a.start[c0 + z0], j1 = a.start[c0 + z1 + 1];   // z-adjacent cells are contiguous
             for (int j = j0; j < j1; ++j) {

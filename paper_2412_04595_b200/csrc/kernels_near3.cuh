@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
                                 uy < 0 ? -g.Ly : (uy >= g.ncy ? g.Ly : 0.0));
     }
     const double ox = g.x0 + cx / g.sx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
-    const int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
+    const int z0 = max(0, cz - g.nzr), z1 = min(g.ncz - 1, cz + g.nzr);
     int* wl = lists + warp * 160;
     int ns_total = 0;
     for (int k = 0; k < 9; ++k) {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3f(Near3Args a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = (float)a.cF[t];
     const double ox = g.x0 + cx / g.sx, oy = cy / g.sy - 0.5 * g.Ly, oz = cz / g.sz - 0.5 * g.Lz;
-    const int z0 = max(0, cz - 1), z1 = min(g.ncz - 1, cz + 1);
+    const int z0 = max(0, cz - g.nzr), z1 = min(g.ncz - 1, cz + g.nzr);
     int* wl = lists + warp * 160;
     int ns_total = 0;
     for (int k = 0; k < 9; ++k) {
