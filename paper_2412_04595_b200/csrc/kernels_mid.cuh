@@ -482,6 +482,19 @@ __device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
 __device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
 }
+// shared-memory load from a 32-bit shared address (one 3-input add per address, no re-materialised
+// products)
+__device__ __forceinline__ double lds_t(unsigned a, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_t(unsigned a, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -509,14 +522,16 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
     const int cb = a.c_lo + blockIdx.y * a.cps;
     const int ce = min(cb + a.cps, a.c_hi + 1);
     // this lane's stencil columns (a, b), row-major over P x P
-    int coff[NR], ca[NR], cbb[NR];
+    int ca[NR], cbb[NR];
+    unsigned coffS[NR];                                  // column byte offsets in a plane window
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int idx = lane + 32 * r;
         ca[r] = idx < P * P ? idx / P : 0;
         cbb[r] = idx < P * P ? idx - ca[r] * P : 0;
-        coff[r] = ca[r] * WYP + cbb[r];
+        coffS[r] = unsigned(ca[r] * WYP + cbb[r]) * unsigned(sizeof(T));
     }
+    const unsigned ringS = smem_u32(ring);
     // issue async copies of planes [p0, p1) of the window into their ring slots
     auto load_planes = [&](int p0, int p1) {
         constexpr int NPL = WX * WY;
@@ -613,22 +628,26 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                     wz[i] = wsc[2 * P + i];
                     dwz[i] = KB ? wsc[5 * P + i] : az2 * (d0z + T(i) * hzT) * wz[i];
                 }
-                int pb[P];                               // ring plane offsets of the P stencil planes
+                // shared byte addresses of the particle's window origin in its P stencil planes
+                unsigned pbS[P];
                 {
                     int zs = hd.z;
+                    const unsigned o0 = ringS + unsigned(hd.x * WYP + hd.y) * unsigned(sizeof(T));
 #pragma unroll
-                    for (int i = 0; i < P; ++i) { pb[i] = zs * PL; zs = zs + 1 == DR ? 0 : zs + 1; }
+                    for (int i = 0; i < P; ++i) {
+                        pbS[i] = o0 + unsigned(zs * PL) * unsigned(sizeof(T));
+                        zs = zs + 1 == DR ? 0 : zs + 1;
+                    }
                 }
-                const T* base = ring + hd.x * WYP + hd.y;
                 T phi = 0, gx = 0, gy = 0, gz = 0;
 #pragma unroll
                 for (int rr = 0; rr < NR; ++rr) {
                     if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
-                    const T* col = base + coff[rr];
+                    const unsigned cS = coffS[rr];
                     T t0 = 0, t1 = 0;
 #pragma unroll
                     for (int kz = 0; kz < P; ++kz) {
-                        const T v = col[pb[kz]];
+                        const T v = lds_t(pbS[kz] + cS, T(0));
                         t0 = fma(wz[kz], v, t0);
                         t1 = fma(dwz[kz], v, t1);
                     }
