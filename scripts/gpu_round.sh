@@ -10,7 +10,8 @@ fi
 timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?
 tail -1 gpurun_out/bench_full.log
 for v in "--window kb" "--long-method direct" "--config c4" "--config c4 --precision fp32 --tol 1e-4" "--config c4 --long-method direct" \
-         "--config c2 --tol 1e-4" "--config c2 --tol 1e-8" "--config c2 --tol 1e-12" "--config c3" "--config s1" "--config s1 --window kb"; do
+         "--config c2 --tol 1e-4" "--config c2 --tol 1e-8" "--config c2 --tol 1e-12" "--config c3" "--config s1" "--config s1 --window kb" "--window es" \
+         "--config t2" "--config t4" "--config t4 --window kb" "--config c5 --optimize"; do
   tag=$(echo "$v" | tr -d ' -' | tr '.' '_')
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline $v > gpurun_out/bench_var_$tag.log 2>&1; echo "bench $v = $?"
 done

@@ -47,6 +47,10 @@ CONFIGS = {
     # surface density N/(Lx Ly) = 1.1, Lz = 0.3, gamma = Lx/Lz ~ 3200 at N = 1e6), SURVEY 8(f) NEXT #3
     "s1": Config("s1", 1_000_000, (953.46, 953.46, 0.3), 1e-6, 6,
                  "N=1e6 strongly confined, surface density 1.1, Lz=0.3 (paper Table 5 shape)", "area"),
+    # paper-table workloads for context (not BASELINE configs): Table 2's N=1e6 cube at density
+    # 0.125 and Table 4's high-density cube N=1e5 in 10^3 at 1e-12
+    "t2": Config("t2", 1_000_000, (200.0, 200.0, 200.0), 1e-6, 7, "N=1e6 cube 200^3 (paper Table 2 row)"),
+    "t4": Config("t4", 100_000, (10.0, 10.0, 10.0), 1e-12, 8, "N=1e5 cube 10^3, density 100 (paper Table 4)"),
 }
 
 
