@@ -94,6 +94,52 @@ struct LongTileArgs {
 
 constexpr int LB = 64;       // particles per staged batch
 
+// particle index ranges reaching the tile at (X0, Y0): the near cells whose (x, y) extent overlaps
+// the tile's stencil-centre box, one contiguous sorted range per (x column, y run) of cells (all z),
+// at most LT_MAXR; beyond that whole x slabs (all y).  One thread; returns the range count.
+constexpr int LT_MAXR = 64;
+__device__ __forceinline__ int tile_ranges(const LongTileArgs& t, int X0, int Y0, int p, int* sRb, int* sRp) {
+    const LongArgs& a = t.a;
+    int nr = 0, tot = 0;
+    auto add = [&](int b, int e) {
+        if (e > b) { sRb[nr] = b; sRp[nr] = tot; tot += e - b; ++nr; }
+    };
+    if (t.full_range) {
+        add(0, a.N);
+    } else {
+        // stencil centres gx0 in [X0 - p, X0 + TX - 1 + p] <=> x in [xlo, xhi); same in y
+        const double xlo = ((X0 - p) - 0.5 - 0.5 * a.Ilx) * a.hx, xhi = ((X0 + t.TX - 1 + p) + 0.5 - 0.5 * a.Ilx) * a.hx;
+        const double ylo = ((Y0 - p) - 0.5 - 0.5 * a.Ily) * a.hy, yhi = ((Y0 + t.TY - 1 + p) + 0.5 - 0.5 * a.Ily) * a.hy;
+        int c0 = (int)floor((xlo + 0.5 * t.Lx) / t.cell_w) - 1, c1 = (int)floor((xhi + 0.5 * t.Lx) / t.cell_w) + 1;
+        const int d0 = (int)floor((ylo + 0.5 * t.Ly) / t.cell_wy) - 1, d1 = (int)floor((yhi + 0.5 * t.Ly) / t.cell_wy) + 1;
+        if (c1 - c0 + 1 >= t.ncx) { c0 = 0; c1 = t.ncx - 1; }
+        const bool ally = d1 - d0 + 1 >= t.ncy;
+        const int nxr = c1 - c0 + 1, nyr = ally ? 1 : (d0 < 0 || d1 >= t.ncy ? 2 : 1);
+        if (nxr * nyr > LT_MAXR - 2 || ally) {
+            // whole x slabs: [c0, c1] split at the periodic seam
+            if (c0 < 0) { add(t.start[(c0 + t.ncx) * t.cells_per_x], a.N); c0 = 0; }
+            if (c1 >= t.ncx) { add(0, t.start[(c1 - t.ncx + 1) * t.cells_per_x]); c1 = t.ncx - 1; }
+            add(t.start[c0 * t.cells_per_x], t.start[(c1 + 1) * t.cells_per_x]);
+        } else {
+            for (int c = c0; c <= c1; ++c) {
+                const int cc = c < 0 ? c + t.ncx : (c >= t.ncx ? c - t.ncx : c);
+                const int base = cc * t.ncy;
+                if (d0 < 0) {
+                    add(t.start[(base + d0 + t.ncy) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
+                    add(t.start[base * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
+                } else if (d1 >= t.ncy) {
+                    add(t.start[(base + d0) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
+                    add(t.start[base * t.ncz], t.start[(base + d1 - t.ncy + 1) * t.ncz]);
+                } else {
+                    add(t.start[(base + d0) * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
+                }
+            }
+        }
+    }
+    sRp[nr] = tot;
+    return nr;
+}
+
 template <int P, int PCMAX>
 __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
     extern __shared__ double sm[];
@@ -109,51 +155,8 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
     const int tile = blockIdx.y, chunk = blockIdx.x;
     const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    // particle index ranges reaching this tile: the near cells whose (x, y) extent overlaps the
-    // tile's stencil-centre box, one contiguous sorted range per (x column, y run) of cells (all
-    // z), at most LT_MAXR; beyond that whole x slabs (all y)
-    constexpr int LT_MAXR = 64;
     __shared__ int sRb[LT_MAXR], sRp[LT_MAXR + 1], sNR;
-    if (tid == 0) {
-        int nr = 0, tot = 0;
-        auto add = [&](int b, int e) {
-            if (e > b) { sRb[nr] = b; sRp[nr] = tot; tot += e - b; ++nr; }
-        };
-        if (t.full_range) {
-            add(0, a.N);
-        } else {
-            // stencil centres gx0 in [X0 - p, X0 + TX - 1 + p] <=> x in [xlo, xhi); same in y
-            const double xlo = ((X0 - p) - 0.5 - 0.5 * a.Ilx) * a.hx, xhi = ((X0 + t.TX - 1 + p) + 0.5 - 0.5 * a.Ilx) * a.hx;
-            const double ylo = ((Y0 - p) - 0.5 - 0.5 * a.Ily) * a.hy, yhi = ((Y0 + t.TY - 1 + p) + 0.5 - 0.5 * a.Ily) * a.hy;
-            int c0 = (int)floor((xlo + 0.5 * t.Lx) / t.cell_w) - 1, c1 = (int)floor((xhi + 0.5 * t.Lx) / t.cell_w) + 1;
-            int d0 = (int)floor((ylo + 0.5 * t.Ly) / t.cell_wy) - 1, d1 = (int)floor((yhi + 0.5 * t.Ly) / t.cell_wy) + 1;
-            if (c1 - c0 + 1 >= t.ncx) { c0 = 0; c1 = t.ncx - 1; }
-            const bool ally = d1 - d0 + 1 >= t.ncy;
-            const int nxr = c1 - c0 + 1, nyr = ally ? 1 : (d0 < 0 || d1 >= t.ncy ? 2 : 1);
-            if (nxr * nyr > LT_MAXR - 2 || ally) {
-                // whole x slabs: [c0, c1] split at the periodic seam
-                if (c0 < 0) { add(t.start[(c0 + t.ncx) * t.cells_per_x], a.N); c0 = 0; }
-                if (c1 >= t.ncx) { add(0, t.start[(c1 - t.ncx + 1) * t.cells_per_x]); c1 = t.ncx - 1; }
-                add(t.start[c0 * t.cells_per_x], t.start[(c1 + 1) * t.cells_per_x]);
-            } else {
-                for (int c = c0; c <= c1; ++c) {
-                    const int cc = c < 0 ? c + t.ncx : (c >= t.ncx ? c - t.ncx : c);
-                    const int base = cc * t.ncy;
-                    if (d0 < 0) {
-                        add(t.start[(base + d0 + t.ncy) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
-                        add(t.start[base * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
-                    } else if (d1 >= t.ncy) {
-                        add(t.start[(base + d0) * t.ncz], t.start[(base + t.ncy) * t.ncz]);
-                        add(t.start[base * t.ncz], t.start[(base + d1 - t.ncy + 1) * t.ncz]);
-                    } else {
-                        add(t.start[(base + d0) * t.ncz], t.start[(base + d1 + 1) * t.ncz]);
-                    }
-                }
-            }
-        }
-        sRp[nr] = tot;
-        sNR = nr;
-    }
+    if (tid == 0) sNR = tile_ranges(t, X0, Y0, p, sRb, sRp);
     __syncthreads();
     const int nr = sNR, ntot = sRp[nr];
     const int per = (ntot + t.nchunk - 1) / t.nchunk;
@@ -508,6 +511,155 @@ __global__ void k_long_sum(const T* __restrict__ part, T* __restrict__ grid, int
     double s = 0.0;
     for (int b = 0; b < nblk; ++b) s += p[(size_t)b * PCP * G];
     grid[idx] = T(s);
+}
+
+// S8 v3 for wide long grids: the register-tiled product of k_long_spread_gemm restricted to one
+// TX x TY column tile.  The tile's candidates are its near-cell runs (tile_ranges), staged 64 at a
+// time as rows [Rx (TX) | Ry (TYP) | T_n (PCP)] holding only the tile's columns (zeros elsewhere)
+// plus a relevance flag (rows whose stencil misses the tile are skipped, uniformly per block);
+// thread = (1 cx, 4 cy, 6 layers) register accumulators.  Tiles own their columns: one chunk per
+// tile writes the grid directly, several write partials summed in a fixed order.
+template <int PCP>
+__global__ void __launch_bounds__(256, 2) k_long_spread_tgemm(LongTileArgs t) {
+    constexpr int NLG = PCP / LG_LT;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    __shared__ unsigned char sRel[2][LG_KB];
+    __shared__ int sRb[LT_MAXR], sRp[LT_MAXR + 1], sNR;
+    const LongArgs& a = t.a;
+    const int P = a.Pl, p = (P - 1) / 2;
+    const int tile = blockIdx.y, chunk = blockIdx.x;
+    const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
+    const int tid = threadIdx.x;
+    const int TYP = (t.TY + 3) & ~3, TYG = TYP / 4, RW = ((t.TX + TYP + PCP) + 1) & ~1;
+    const int lg = tid % NLG, cg = tid / NLG;
+    const int cx = cg / TYG, cy0 = 4 * (cg % TYG);
+    const bool own = cx < t.TX;
+    if (tid == 0) sNR = tile_ranges(t, X0, Y0, p, sRb, sRp);
+    __syncthreads();
+    const int nr = sNR, ntot = sRp[nr];
+    const int per = (ntot + t.nchunk - 1) / t.nchunk;
+    const int jb = min(ntot, chunk * per), je = min(ntot, jb + per);
+    double acc[4][LG_LT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int l = 0; l < LG_LT; ++l) acc[i][l] = 0.0;
+    // staging: (particle, role) work items, role 0 -> Rx row, 1 -> Ry row, 2 -> T row + flag
+    auto stage = [&](int base, int buf) {
+        const int nb = min(LG_KB, je - base);
+        for (int w = tid; w < 3 * nb; w += blockDim.x) {
+            const int k = w / 3, role = w - 3 * k;
+            const int kk = base + k;
+            int e = 0;
+            while (e + 1 < nr && sRp[e + 1] <= kk) ++e;
+            const int j = sRb[e] + (kk - sRp[e]);
+            const d4 r = ld_d4(&a.pos[j]);
+            double* row = sm + ((size_t)buf * LG_KB + k) * RW;
+            if (role == 2) {
+                double* tt = row + t.TX + TYP;
+                const double x = r.z * a.two_over_Lz;
+                double tm = 1.0, tc = x;
+                tt[0] = 1.0;
+                if (PCP > 1) tt[1] = x;
+                for (int n = 2; n < PCP; ++n) {
+                    const double tn = 2.0 * x * tc - tm;
+                    tt[n] = tn;
+                    tm = tc; tc = tn;
+                }
+                const int gx0 = stencil_g0(r.x, a.hx, a.hpx), gy0 = stencil_g0(r.y, a.hy, a.hpy);
+                int dx = (X0 - (gx0 - p)) % a.Ilx, dy = (Y0 - (gy0 - p)) % a.Ily;
+                dx += dx < 0 ? a.Ilx : 0;
+                dy += dy < 0 ? a.Ily : 0;
+                sRel[buf][k] = (dx < P || dx > a.Ilx - t.TX) && (dy < P || dy > a.Ily - t.TY);
+            } else {
+                const bool isx = role == 0;
+                const int I = isx ? a.Ilx : a.Ily, T0 = isx ? X0 : Y0, TW = isx ? t.TX : TYP;
+                const int TV = isx ? t.TX : t.TY;           // valid columns of the row
+                const double xc = isx ? r.x : r.y, hh = isx ? a.hx : a.hy, hf = isx ? a.halfx : a.halfy;
+                double* rw = isx ? row : row + t.TX;
+                for (int c = 0; c < TW; ++c) rw[c] = 0.0;
+                const int g0 = stencil_g0(xc, hh, isx ? a.hpx : a.hpy), s0 = g0 - p;
+                const double qw = isx ? r.w : 1.0;
+                int c = (s0 - T0) % I;
+                c += c < 0 ? I : 0;
+                auto put = [&](int, double w, double) {
+                    if (c < TV) rw[c] = qw * w;
+                    c = c + 1 == I ? 0 : c + 1;
+                };
+                if (a.kb) {
+                    kb_emit_rt<false>(P, kb_offset(xc, hh, hf, g0), a.kt, put);
+                } else {
+                    const double ih = isx ? a.invH2Sx : a.invH2Sy, gam = isx ? t.gamma_x : t.gamma_y;
+                    const double d0 = ((double)s0 - hf) * hh - xc;
+                    double w = exp(-ih * d0 * d0), q = exp(-ih * hh * (2.0 * d0 + hh));
+                    for (int u = 0; u < P; ++u) {
+                        put(u, w, 0.0);
+                        w *= q; q *= gam;
+                    }
+                }
+            }
+        }
+    };
+    if (jb < je) stage(jb, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int base = jb; base < je; base += LG_KB, buf ^= 1) {
+        if (base + LG_KB < je) stage(base + LG_KB, buf ^ 1);
+        const int nb = min(LG_KB, je - base);
+        if (own) {
+            const double* rows = sm + (size_t)buf * LG_KB * RW;
+            for (int k = 0; k < nb; ++k) {
+                if (!sRel[buf][k]) continue;                   // uniform across the block
+                const double* row = rows + (size_t)k * RW;
+                const double rx = row[cx];
+                const double2 y01 = *reinterpret_cast<const double2*>(row + t.TX + cy0);
+                const double2 y23 = *reinterpret_cast<const double2*>(row + t.TX + cy0 + 2);
+                double tl[LG_LT];
+#pragma unroll
+                for (int l = 0; l < LG_LT; l += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(row + t.TX + TYP + lg * LG_LT + l);
+                    tl[l] = v.x; tl[l + 1] = v.y;
+                }
+                const double av[4] = {rx * y01.x, rx * y01.y, rx * y23.x, rx * y23.y};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int l = 0; l < LG_LT; ++l) acc[i][l] = fma(av[i], tl[l], acc[i][l]);
+            }
+        }
+        __syncthreads();
+    }
+    if (own) {
+        const size_t G = (size_t)a.Ilx * a.Ily;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int cy = cy0 + i, gx = X0 + cx, gy = Y0 + cy;
+            if (cy >= t.TY || gx >= a.Ilx || gy >= a.Ily) continue;
+#pragma unroll
+            for (int l = 0; l < LG_LT; ++l) {
+                const int n = lg * LG_LT + l;
+                if (n >= a.Pc) continue;
+                if (t.nchunk == 1)
+                    t.grid[n * G + (size_t)gx * a.Ily + gy] = acc[i][l];
+                else
+                    t.part[(((size_t)tile * t.nchunk + chunk) * PCP + n) * (t.TX * t.TY) + cx * t.TY + cy] = acc[i][l];
+            }
+        }
+    }
+}
+
+// grid[n][g] = sum over the chunks of a tile (fixed order) of k_long_spread_tgemm's partials
+static __global__ void k_long_treduce(const double* __restrict__ part, double* __restrict__ grid, int Ilx, int Ily,
+                                      int Pc, int PCP, int TX, int TY, int nty, int nchunk) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= Ilx * Ily * Pc) return;
+    const int n = idx / (Ilx * Ily), g = idx % (Ilx * Ily);
+    const int gx = g / Ily, gy = g % Ily;
+    const int tile = (gx / TX) * nty + gy / TY, col = (gx % TX) * TY + gy % TY;
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += part[(((size_t)tile * nchunk + c) * PCP + n) * (TX * TY) + col];
+    grid[idx] = s;
 }
 
 // S12 for small long grids: one thread per particle, the whole T-basis field Psi~ in shared

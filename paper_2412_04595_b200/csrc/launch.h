@@ -33,6 +33,8 @@ int launch_long_gather2(const LongArgs& a, int Pl, const double* psi, double* ps
                         cudaStream_t st);
 int long_pcmax(int Pc);
 int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStream_t st);
+// register-tiled spread per column tile (k_long_spread_tgemm); 1 = unsupported shape (use the tile kernel)
+int launch_long_spread_tgemm(const LongTileArgs& t, double* grid, cudaStream_t st);
 bool long_small_ok(int Ilx, int Ily, int Pc);
 int long_small_pcp(int Pc);
 int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, void* part, void* grid,

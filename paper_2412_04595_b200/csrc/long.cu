@@ -38,6 +38,38 @@ int launch_long_spread_tile(const LongTileArgs& t, int Pl, double* grid, cudaStr
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
+template <int PCP>
+int tgemm_go(const LongTileArgs& t, double* grid, cudaStream_t st) {
+    const int TYP = (t.TY + 3) & ~3;
+    const int nthr = ((t.TX * (TYP / 4) * (PCP / LG_LT) + 31) / 32) * 32;
+    if (nthr > 256) return 1;
+    const int RW = ((t.TX + TYP + PCP) + 1) & ~1;
+    const size_t sh = sizeof(double) * 2 * LG_KB * RW;
+    if (cudaFuncSetAttribute(k_long_spread_tgemm<PCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+        cudaSuccess)
+        return 2;
+    LongTileArgs tg = t;
+    tg.grid = grid;
+    k_long_spread_tgemm<PCP><<<dim3(t.nchunk, t.ntx * t.nty), nthr, sh, st>>>(tg);
+    if (t.nchunk > 1) {
+        const int n = t.a.Ilx * t.a.Ily * t.a.Pc;
+        k_long_treduce<<<(n + 255) / 256, 256, 0, st>>>(t.part, grid, t.a.Ilx, t.a.Ily, t.a.Pc, PCP, t.TX, t.TY, t.nty,
+                                                       t.nchunk);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_long_spread_tgemm(const LongTileArgs& t, double* grid, cudaStream_t st) {
+    switch (long_small_pcp(t.a.Pc)) {
+        case 6: return tgemm_go<6>(t, grid, st);
+        case 12: return tgemm_go<12>(t, grid, st);
+        case 18: return tgemm_go<18>(t, grid, st);
+        case 24: return tgemm_go<24>(t, grid, st);
+        case 30: return tgemm_go<30>(t, grid, st);
+    }
+    return 1;
+}
+
 #define SOG_PCMAX(M) M(8) M(12) M(16) M(20) M(24) M(28) M(32)
 
 int long_pcmax(int Pc) {

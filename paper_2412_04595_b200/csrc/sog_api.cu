@@ -458,7 +458,7 @@ int setup(sog_plan* pl) {
         // S8 tiling: one tile = whole grid when it fits one CTA, else 16x16 column tiles
         LongTileArgs& t = pl->lt;
         if (p.Ilx * p.Ily <= 256) { t.TX = p.Ilx; t.TY = p.Ily; }
-        else { t.TX = std::min(16, p.Ilx); t.TY = std::min(16, p.Ily); }
+        else { t.TX = std::min(long_small_pcp(p.Pc) > 24 ? 8 : 16, p.Ilx); t.TY = std::min(16, p.Ily); }   // tgemm: <= 256 threads
         t.ntx = (p.Ilx + t.TX - 1) / t.TX;
         t.nty = (p.Ily + t.TY - 1) / t.TY;
         const int pl_half = (p.Pl - 1) / 2;
@@ -478,7 +478,7 @@ int setup(sog_plan* pl) {
         t.gamma_x = gam(p.hlx());
         t.gamma_y = gam(p.hly());
         if (p.window != 0) kb_table(p.Pl, p.Sl, p.nul, p.window, pl->kbl);
-        int pcmax = p.Pc <= 16 ? 16 : 32;
+        int pcmax = std::max(p.Pc <= 16 ? 16 : 32, long_small_pcp(p.Pc));   // tile kernel / tgemm partials
         if (t.nchunk > 1 && (rc = dalloc(pl, &pl->lpart, (size_t)ntile * t.nchunk * t.TX * t.TY * pcmax))) return rc;
         if ((rc = dalloc(pl, &pl->lpsiT, (size_t)p.Ilx * p.Ily * 32))) return rc;
         long long n[2] = {p.Ilx, p.Ily};
@@ -718,7 +718,14 @@ int st_long_spread(sog_plan* pl) {
         t.a = la;
         t.start = pl->start;
         t.part = pl->lpart;
-        if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
+        // wide grids: the register-tiled product per column tile; the per-column tile kernel when
+        // the thread tile does not fit (Pc > 24)
+        const int r = launch_long_spread_tgemm(t, pl->lgrid, st);
+        if (r == 1) {
+            if ((rc = lchk(launch_long_spread_tile(t, p.Pl, pl->lgrid, st)))) return rc;
+        } else if ((rc = lchk(r))) {
+            return rc;
+        }
     }
     return SOG_OK;
 }
