@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k_long_spread_tile(LongTileArgs t) {
     const int Pc = a.Pc;
     const int tile = blockIdx.y, chunk = blockIdx.x;
     const int X0 = (tile / t.nty) * t.TX, Y0 = (tile % t.nty) * t.TY;
-    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tid = threadIdx.x;
     __shared__ int sRb[LT_MAXR], sRp[LT_MAXR + 1], sNR;
     if (tid == 0) sNR = tile_ranges(t, X0, Y0, p, sRb, sRp);
     __syncthreads();
