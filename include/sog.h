@@ -175,6 +175,11 @@ int sog_launches_per_eval(const sog_plan* p);
  * --------------------------------------------------------------------------------------- */
 typedef struct sog_dist sog_dist;
 
+/* One-process check of the library's NCCL plumbing (libnccl.so.2 resolved at run time): a 1-rank
+ * communicator on the current device, grouped send/recv to itself and an all-reduce; SOG_OK or
+ * SOG_ENCCL with the reason in sog_last_error(). */
+int sog_nccl_selftest(void);
+
 /* 128 bytes of ncclUniqueId for sog_dist_create (call on one rank, broadcast to the others,
  * e.g. with torch.distributed).  SOG_ENCCL if libnccl.so.2 cannot be loaded. */
 int sog_nccl_unique_id(void* id128);

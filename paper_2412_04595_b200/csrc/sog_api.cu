@@ -1461,6 +1461,41 @@ int dist_plan_setup(sog_plan* pl, int rank, int R, int64_t nown_max) {
 
 extern "C" {
 
+// One-process check of the NCCL plumbing (run-time symbol binding and call conventions) on the
+// current device: a 1-rank communicator, grouped send/recv to itself and an all-reduce.
+int sog_nccl_selftest(void) {
+    if (!nccl().ok) return fail(SOG_ENCCL, "libnccl.so.2 not available");
+    const NcclApi& api = nccl();
+    ncclUniqueId id;
+    NCK(api.GetUniqueId(&id));
+    ncclComm_t comm;
+    NCK(api.CommInitRank(&comm, 1, id, 0));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t n = 1 << 16;
+    double *a = nullptr, *b = nullptr;
+    CK(cudaMalloc(&a, n * sizeof(double)));
+    CK(cudaMalloc(&b, n * sizeof(double)));
+    std::vector<double> h(n), g(n);
+    for (size_t i = 0; i < n; ++i) h[i] = 0.5 * double(i) - 7.0;
+    CK(cudaMemcpy(a, h.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemset(b, 0, n * sizeof(double)));
+    NCK(api.GroupStart());
+    NCK(api.Send(a, n * sizeof(double), ncclUint8, 0, comm, st));
+    NCK(api.Recv(b, n * sizeof(double), ncclUint8, 0, comm, st));
+    NCK(api.GroupEnd());
+    NCK(api.AllReduce(b, b, n, ncclFloat64, ncclSum, comm, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(g.data(), b, n * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(a);
+    cudaFree(b);
+    cudaStreamDestroy(st);
+    api.CommDestroy(comm);
+    for (size_t i = 0; i < n; ++i)
+        if (g[i] != h[i]) return fail(SOG_ENCCL, "NCCL self-test: wrong data");
+    return SOG_OK;
+}
+
 int sog_nccl_unique_id(void* id128) {
     if (!id128) return fail(SOG_EINVAL, "null argument");
     if (!nccl().ok) return fail(SOG_ENCCL, "libnccl.so.2 not available");

@@ -17,7 +17,7 @@ TIMING_NAMES = ["sort", "near", "mid_spread", "mid_fft_fwd", "mid_scale", "mid_f
 EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval", "sog_eval_host", "sog_eval_components",
            "sog_debug_stage", "sog_last_energy", "sog_plan_destroy", "sog_last_error", "sog_plan_describe",
            "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval",
-           "sog_nccl_unique_id", "sog_dist_create", "sog_dist_create_loopback", "sog_dist_eval",
+           "sog_nccl_selftest", "sog_nccl_unique_id", "sog_dist_create", "sog_dist_create_loopback", "sog_dist_eval",
            "sog_dist_local_ranks", "sog_dist_describe", "sog_dist_destroy"]
 
 

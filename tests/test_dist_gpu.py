@@ -98,6 +98,18 @@ def test_loopback_empty_ranks():
     assert rel(phi, p1) <= 1e-13 and rel(F, F1) <= 1e-13, (rel(phi, p1), rel(F, F1))
 
 
+def test_nccl_plumbing_selftest():
+    """The library's run-time-bound NCCL calls (communicator, grouped send/recv, all-reduce) on one
+    GPU: the multi-GPU x-slab path uses exactly these calls."""
+    from paper_2412_04595_b200 import load_library
+    import ctypes
+    lib = load_library()
+    lib.sog_nccl_selftest.restype = ctypes.c_int
+    torch.cuda.init()
+    rc = lib.sog_nccl_selftest()
+    assert rc == 0, lib.sog_last_error().decode()
+
+
 def test_particle_outside_its_slab_is_rejected():
     from paper_2412_04595_b200 import DistPlan, SogError
     xyz, q, L, op, params = slab_plan("c5", 4000, 2)
