@@ -100,7 +100,8 @@ __global__ void k_scatter(const int* __restrict__ cell, int N, int* __restrict__
 // the sorted SoA and the permutation.  Cells are z-major inside an (x,y) column, so every
 // column is z-sorted (the near-field z windows rely on it); the order is deterministic.
 __global__ void k_cellsort(const int* __restrict__ start, int ncell, const int* __restrict__ tmp,
-                           const d4* __restrict__ pos, d4* __restrict__ pos_s, int* __restrict__ perm) {
+                           const d4* __restrict__ pos, d4* __restrict__ pos_s, int* __restrict__ perm,
+                           int* __restrict__ iperm) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= ncell) return;
@@ -119,6 +120,7 @@ __global__ void k_cellsort(const int* __restrict__ start, int ncell, const int* 
             rank = e;   // pathological clustering: arrival order (z windows fall back to full columns)
         }
         perm[s + rank] = my;
+        iperm[my] = s + rank;                  // inverse: caller / local index -> sorted index
         st_d4(&pos_s[s + rank], ld_d4(&pos[my]));
     }
 }

@@ -5,7 +5,7 @@
 //   S2 k_near3 (warp per target; k_near for tiny boxes)        (near field + nothing else)
 //   S3-S7 k_mid_spread_z -> cuFFT D2Z -> k_mid_scale -> cuFFT Z2D -> k_mid_gather_z
 //   S8-S12 k_long_spread -> cuFFT D2Z (batched 2D) -> k_long_scale -> Z2D -> k_long_gather
-//   S13 k_combine                                               (self term, forces, unpermute, U)
+//   S13 k_combine_g + k_sum_partials                            (self term, forces, unpermute, U)
 // cuFFT supplies only the butterflies.  All other steps are the kernels in kernels_*.cuh.
 #include <cuda_runtime.h>
 #include <cufft.h>
@@ -40,28 +40,26 @@ int fail(int code, const std::string& msg) {
 
 namespace sog {
 
-__global__ void k_combine(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
-                          const d4* __restrict__ pos, const int* __restrict__ perm, int N, int nown, double selfc,
-                          double* __restrict__ phi, double* __restrict__ force, double* __restrict__ epart) {
-    // phi_i = Phi^N + Phi^mid + Phi^long - q_i sum_l w_l; F_i = -q_i grad phi
-    // (x-slab: only the nown own particles are written; halo entries have perm >= nown)
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
+// S13 in gather form: thread = caller (local) index i < nown, reading its sorted slot k = iperm[i]
+// (full 32-byte sectors) and writing phi / force in caller order (coalesced stores)
+__global__ void k_combine_g(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
+                            const d4* __restrict__ pos, const int* __restrict__ iperm, int nown, double selfc,
+                            double* __restrict__ phi, double* __restrict__ force, double* __restrict__ epart) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0;
-    if (k < N && perm[k] < nown) {
-        d4 a = ld_d4(&nearo[k]), b = ld_d4(&mido[k]), c = ld_d4(&longo[k]);
-        double q = ld_d4(&pos[k]).w;
-        double ph = a.x + b.x + c.x - q * selfc;
-        int i = perm[k];
+    if (i < nown) {
+        const int k = iperm[i];
+        const d4 a = ld_d4(&nearo[k]), b = ld_d4(&mido[k]), c = ld_d4(&longo[k]);
+        const double q = ld_d4(&pos[k]).w;
+        const double ph = a.x + b.x + c.x - q * selfc;
         if (phi) phi[i] = ph;
-        if (force) {
+        if (force) {                                       // F = -q grad phi
             force[3 * (size_t)i] = -q * (a.y + b.y + c.y);
             force[3 * (size_t)i + 1] = -q * (a.z + b.z + c.z);
             force[3 * (size_t)i + 2] = -q * (a.w + b.w + c.w);
         }
-        e = 0.5 * q * ph;                                     // U = 1/2 sum q phi
+        e = 0.5 * q * ph;                                  // U = 1/2 sum q phi
     }
-    // per-block partial of U in a fixed order (k_sum_partials adds the blocks: deterministic,
-    // and no single-address atomic stream)
     __shared__ double se[32];
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
     if ((threadIdx.x & 31) == 0) se[threadIdx.x >> 5] = e;
@@ -118,6 +116,7 @@ struct sog_plan {
     // workspace
     d4 *pos = nullptr, *pos_s = nullptr, *o_near = nullptr, *o_mid = nullptr, *o_long = nullptr;
     int *cell = nullptr, *tmp = nullptr, *perm = nullptr, *count = nullptr, *start = nullptr, *cursor = nullptr;
+    int* iperm = nullptr;                   // inverse permutation (caller / local index -> sorted)
     int4* g0 = nullptr;             // stencil origins per sorted particle (mid x,y,z; long packed)
     unsigned* dflags = nullptr;
     double* qsums = nullptr;   // [0] sum q, [1] sum |q|, [2] energy
@@ -150,7 +149,7 @@ struct sog_plan {
     bool long_small = false;        // small long grid: register-tiled spread + broadcast gather
     DftArgs dft{};                  // long_method = 1 (Alg. 3): mode set
     double *ldS = nullptr, *ldP = nullptr, *ldpart = nullptr, *d_Kd = nullptr;   // S~, Psi~ [Pc][mode] complex
-    double* epart = nullptr;        // per-block partial energies of k_combine
+    double* epart = nullptr;        // per-block partial energies of k_combine_g
     int lg_nblk = 0;
     double* lpart2 = nullptr;       // [lg_nblk][PCP][Ilx*Ily] spread partials
     double* ldbg = nullptr;         // debug: T basis -> proxy-node basis
@@ -224,7 +223,7 @@ int upload(sog_plan* pl, T** ptr, const std::vector<T>& v) {
 
 void free_plan(sog_plan* pl) {
     if (!pl) return;
-    void* ptrs[] = {pl->g0, pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm,
+    void* ptrs[] = {pl->g0, pl->pos, pl->pos_s, pl->o_near, pl->o_mid, pl->o_long, pl->cell, pl->tmp, pl->perm, pl->iperm,
                     pl->count, pl->start, pl->cursor, pl->dflags, pl->qsums, pl->d_cF, pl->d_cdF, pl->mgrid,
                     pl->mspec, pl->d_A, pl->d_Tx, pl->d_Ty, pl->d_Tz, pl->lgrid, pl->lspec, pl->lspec2,
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
@@ -300,7 +299,7 @@ int setup(sog_plan* pl) {
     int rc;
     if ((rc = dalloc(pl, &pl->pos, N)) || (rc = dalloc(pl, &pl->pos_s, N)) || (rc = dalloc(pl, &pl->o_near, N)) ||
         (rc = dalloc(pl, &pl->o_mid, N)) || (rc = dalloc(pl, &pl->o_long, N)) || (rc = dalloc(pl, &pl->cell, N)) ||
-        (rc = dalloc(pl, &pl->tmp, N)) || (rc = dalloc(pl, &pl->perm, N)) || (rc = dalloc(pl, &pl->g0, N)) ||
+        (rc = dalloc(pl, &pl->tmp, N)) || (rc = dalloc(pl, &pl->perm, N)) || (rc = dalloc(pl, &pl->iperm, N)) || (rc = dalloc(pl, &pl->g0, N)) ||
         (rc = dalloc(pl, &pl->count, pl->ncell + 1)) || (rc = dalloc(pl, &pl->start, pl->ncell + 1)) ||
         (rc = dalloc(pl, &pl->cursor, pl->ncell + 1)) || (rc = dalloc(pl, &pl->dflags, 1)) ||
         (rc = dalloc(pl, &pl->qsums, 4)) || (rc = dalloc(pl, &pl->epart, ((size_t)N + 255) / 256 + 1)) || (rc = upload(pl, &pl->d_cF, pl->near.cF)) ||
@@ -616,7 +615,8 @@ int st_sort(sog_plan* pl, const double* xyz, const double* q, int N) {
     if ((rc = lchk(launch_exclusive_scan(pl->count, pl->start, pl->ncell, pl->scan_tmp, pl->scan_bytes, st)))) return rc;
     CK(cudaMemcpyAsync(pl->cursor, pl->start, sizeof(int) * pl->ncell, cudaMemcpyDeviceToDevice, st));
     k_scatter<<<nb, 256, 0, st>>>(pl->cell, N, pl->cursor, pl->tmp);
-    k_cellsort<<<(pl->ncell * 32 + 255) / 256, 256, 0, st>>>(pl->start, pl->ncell, pl->tmp, pl->pos, pl->pos_s, pl->perm);
+    k_cellsort<<<(pl->ncell * 32 + 255) / 256, 256, 0, st>>>(pl->start, pl->ncell, pl->tmp, pl->pos, pl->pos_s, pl->perm,
+                                                            pl->iperm);
     {
         MidArgs ma{};
         if (pl->has_mid) ma = mid_args(pl);
@@ -961,8 +961,8 @@ int eval_body(sog_plan* pl, const double* xyz, const double* q, double* phi, dou
     int rc = run_pipeline(pl, xyz, q);
     if (rc) return rc;
     const int N = int(pl->p.N);
-    k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N, N,
-                                                       pl->selfc, phi, force, pl->epart);
+    k_combine_g<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->iperm, N,
+                                                         pl->selfc, phi, force, pl->epart);
     k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
     CK(cudaGetLastError());
     mark(pl, 11);
@@ -1430,10 +1430,10 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
         if ((rc = st_long_solve(pl))) return rc;
         if (!pl->Ncur) continue;
         if ((rc = st_long_gather(pl))) return rc;
-        const int N = pl->Ncur;
-        k_combine<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->perm, N,
-                                                           pl->Nown, pl->selfc, phi[i], force[i], pl->epart);
-        k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
+        k_combine_g<<<std::max(1, (pl->Nown + 255) / 256), 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s,
+                                                                    pl->iperm, pl->Nown, pl->selfc, phi[i], force[i],
+                                                                    pl->epart);
+        k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, std::max(1, (pl->Nown + 255) / 256), pl->qsums + 2);
         CK(cudaGetLastError());
     }
     return SOG_OK;
