@@ -12,7 +12,7 @@ A = Lx Ly, for target i (target-subsampled: cost O(N (images + modes)) each):
   self:       -2 alpha q_i / sqrt(pi)
 
 and the analytic gradient of each term.  Pinned by alpha-independence and by
-the alpha -> infinity quasi-2D limits (tests/test_oracle_ewald.py).
+the alpha -> infinity quasi-2D limits (tests/test_oracle_pins.py::test_ewald2d_*).
 """
 from __future__ import annotations
 

@@ -2,7 +2,7 @@
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  The CUDA library has its
 own, independent implementation of the same rules (paper_2412_04595_b200/csrc/
-plan.cpp); tests/test_plan_parity.py compares the two.
+plan.cpp); tests/test_abi_plan.py::test_plan_rules_match_oracle compares the two.
 
 The paper gives the ingredients (section 4.3) with
 unit-prefactor O(.) estimates; the concrete rules are the readings R1-R9 of

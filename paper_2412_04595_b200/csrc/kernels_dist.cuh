@@ -14,21 +14,60 @@
 namespace sog {
 
 // own particles: d4 copy, halo flags (bit 0: within H of the left edge, bit 1: of the right
-// edge), validation of slab membership (x in [xlo, xhi) after the canonical wrap)
+// edge) and the rank's input status, summed into st[] (block-reduced, then one atomic per block):
+//   st[0] particles outside the rank's x slab (after the canonical wrap, R14)
+//   st[1] non-finite position or charge, st[2] z outside [-Lz/2, Lz/2] (S1 rules)
+//   st[4] sum q, st[5] sum |q| over the finite charges (neutrality)
+// Particles that fail a check are parked at the slab centre with their (finite) charge so every
+// later kernel stays in bounds; the evaluation is rejected on every rank after the agreement.
 static __global__ void k_slab_flags(const double* __restrict__ xyz, const double* __restrict__ q, int n, double Lx,
-                                    double xlo, double xhi, double H, d4* __restrict__ own, int* __restrict__ fl,
-                                    int* __restrict__ fr, unsigned* __restrict__ bad) {
+                                    double Lz, double xlo, double xhi, double H, d4* __restrict__ own,
+                                    int* __restrict__ fl, int* __restrict__ fr, double* __restrict__ st) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double x = xyz[3 * (size_t)i];
-    const double halfL = 0.5 * Lx;
-    const double f = floor(__ddiv_rn(__dadd_rn(x, halfL), Lx));      // canonical wrap (R14)
-    x = __dsub_rn(x, __dmul_rn(Lx, f));
-    if (x >= halfL) x = __dsub_rn(x, Lx);
-    own[i] = d4{x, xyz[3 * (size_t)i + 1], xyz[3 * (size_t)i + 2], q[i]};
-    if (!(x >= xlo && x < xhi)) atomicOr(bad, 1u);
-    fl[i] = x < xlo + H ? 1 : 0;
-    fr[i] = x >= xhi - H ? 1 : 0;
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (i < n) {
+        double x = xyz[3 * (size_t)i];
+        const double y = xyz[3 * (size_t)i + 1], z = xyz[3 * (size_t)i + 2], qi = q[i];
+        const bool fin = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(qi);
+        const double halfL = 0.5 * Lx;
+        if (fin) {
+            const double f = floor(__ddiv_rn(__dadd_rn(x, halfL), Lx));      // canonical wrap (R14)
+            x = __dsub_rn(x, __dmul_rn(Lx, f));
+            if (x >= halfL) x = __dsub_rn(x, Lx);
+        }
+        const bool inslab = fin && x >= xlo && x < xhi;
+        const bool zok = fin && fabs(z) <= 0.5 * Lz;
+        v[0] = fin && !inslab ? 1.0 : 0.0;
+        v[1] = fin ? 0.0 : 1.0;
+        v[2] = fin && !zok ? 1.0 : 0.0;
+        v[3] = isfinite(qi) ? qi : 0.0;
+        v[4] = isfinite(qi) ? fabs(qi) : 0.0;
+        const bool ok = inslab && zok;
+        const double xm = 0.5 * (xlo + xhi);
+        own[i] = ok ? d4{x, y, z, qi} : d4{xm, 0.0, 0.0, v[3]};
+        fl[i] = ok && x < xlo + H ? 1 : 0;
+        fr[i] = ok && x >= xhi - H ? 1 : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    __shared__ double red[5][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0)
+        for (int k = 0; k < 5; ++k) red[k][wid] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += red[threadIdx.x][w];
+        const int slot = threadIdx.x < 3 ? threadIdx.x : threadIdx.x + 1;
+        if (t != 0.0) atomicAdd(&st[slot], t);
+    }
+}
+
+// st[3] += halo sends over capacity (the select cannot overflow: its buffers hold every own
+// particle) + a host-side capacity violation
+static __global__ void k_halo_status(const int* __restrict__ nsel, int cap, int host_err, double* __restrict__ st) {
+    st[3] += double((nsel[0] > cap) + (nsel[1] > cap) + host_err);
 }
 
 static __global__ void k_shift_x(d4* __restrict__ p, const int* __restrict__ n, double dx) {

@@ -183,7 +183,9 @@ struct sog_plan {
     double *hsb = nullptr, *hrb = nullptr;             // Psi halo planes [2][Izs][HP][Iy]
     d4 *own = nullptr, *hsend = nullptr, *hrecv = nullptr, *pos_long = nullptr;
     int *fl = nullptr, *fr = nullptr, *nsel = nullptr;
-    unsigned* dbad = nullptr;
+    double* dstat = nullptr;                // [8] input status summed over ranks (k_slab_flags)
+    double* pin_d = nullptr;                // pinned copy of dstat after the agreement
+    int nown_cap = 0;                       // own-particle capacity
     double *lxyz = nullptr, *lq = nullptr;
     void* sel_tmp = nullptr;
     size_t sel_bytes = 0;
@@ -229,12 +231,13 @@ void free_plan(sog_plan* pl) {
                     pl->d_K, pl->d_C, pl->lpart, pl->lpsiT, pl->h_xyz, pl->h_q, pl->h_phi, pl->h_force,
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
-                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dbad, pl->lxyz, pl->lq, pl->sel_tmp,
+                    pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dstat, pl->lxyz, pl->lq, pl->sel_tmp,
                     pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
     if (pl->pin_i) cudaFreeHost(pl->pin_i);
+    if (pl->pin_d) cudaFreeHost(pl->pin_d);
     for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
                           pl->mzfft})
         if (h) cufftDestroy(h);
@@ -510,14 +513,18 @@ int setup(sog_plan* pl) {
     if ((rc = dalloc(pl, (char**)&pl->scan_tmp, pl->scan_bytes))) return rc;
     if (slab) {   // particle halos
         const int nown = pl->Ncap - 2 * pl->halo_cap;
+        pl->nown_cap = nown;
         pl->sel_bytes = select_temp_bytes(nown);
-        if ((rc = dalloc(pl, &pl->own, nown)) || (rc = dalloc(pl, &pl->hsend, 2 * pl->halo_cap)) ||
+        // the halo selects write into [left | right] halves of nown entries each, so clustered
+        // input cannot overflow them; sends over halo_cap are rejected on every rank
+        if ((rc = dalloc(pl, &pl->own, nown)) || (rc = dalloc(pl, &pl->hsend, 2 * (size_t)nown)) ||
             (rc = dalloc(pl, &pl->hrecv, 2 * pl->halo_cap)) || (rc = dalloc(pl, &pl->pos_long, N)) ||
             (rc = dalloc(pl, &pl->fl, nown)) || (rc = dalloc(pl, &pl->fr, nown)) || (rc = dalloc(pl, &pl->nsel, 4)) ||
-            (rc = dalloc(pl, &pl->dbad, 1)) || (rc = dalloc(pl, &pl->lxyz, 3 * (size_t)N)) ||
+            (rc = dalloc(pl, &pl->dstat, 8)) || (rc = dalloc(pl, &pl->lxyz, 3 * (size_t)N)) ||
             (rc = dalloc(pl, &pl->lq, N)) || (rc = dalloc(pl, (char**)&pl->sel_tmp, pl->sel_bytes)))
             return rc;
         CK(cudaMallocHost((void**)&pl->pin_i, 8 * sizeof(int)));
+        CK(cudaMallocHost((void**)&pl->pin_d, 8 * sizeof(double)));
     }
     for (auto& e : pl->ev) CK(cudaEventCreate(&e));
     if (!slab) {   // SOG_NEAR_STREAM=off|low|high (default low): near-field side stream and its priority
@@ -1268,49 +1275,72 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
     int rc;
     auto left = [&](int r) { return (r + R - 1) % R; };
     auto right = [&](int r) { return (r + 1) % R; };
-    // ---- particle halos: select, exchange counts, exchange particles ----
+    // ---- particle halos: select, agree on the input status, exchange counts, exchange particles ----
+    // No rank returns before the agreement: a rank-local error (capacity, slab membership, invalid
+    // input) is summed into every rank's status, so all ranks reject the evaluation together
+    // instead of leaving the others blocked in a collective.
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
         const Params& p = pl->p;
-        const int n = int(nown[i]);
-        if (n < 0 || n > pl->Ncap - 2 * pl->halo_cap) return fail(SOG_EINVAL, "own particle count exceeds the plan capacity");
+        const int64_t n64 = nown[i];
+        const int host_err = (n64 < 0 || n64 > pl->nown_cap) ? 1 : 0;
+        const int n = host_err ? 0 : int(n64);
         pl->Nown = n;
         cudaStream_t st = pl->stream;
-        CK(cudaMemsetAsync(pl->dbad, 0, sizeof(unsigned), st));
+        CK(cudaMemsetAsync(pl->dstat, 0, 8 * sizeof(double), st));
         CK(cudaMemsetAsync(pl->nsel, 0, 4 * sizeof(int), st));
         if (n > 0) {
-            k_slab_flags<<<(n + 255) / 256, 256, 0, st>>>(xyz[i], q[i], n, p.Lx, pl->xs0, pl->xs1, pl->Hh, pl->own, pl->fl,
-                                                         pl->fr, pl->dbad);
+            k_slab_flags<<<(n + 255) / 256, 256, 0, st>>>(xyz[i], q[i], n, p.Lx, p.Lz, pl->xs0, pl->xs1, pl->Hh, pl->own,
+                                                         pl->fl, pl->fr, pl->dstat);
             if ((rc = lchk(launch_select_flagged(pl->own, pl->fl, pl->hsend, pl->nsel, n, pl->sel_tmp, pl->sel_bytes, st))) ||
-                (rc = lchk(launch_select_flagged(pl->own, pl->fr, pl->hsend + pl->halo_cap, pl->nsel + 1, n, pl->sel_tmp,
+                (rc = lchk(launch_select_flagged(pl->own, pl->fr, pl->hsend + pl->nown_cap, pl->nsel + 1, n, pl->sel_tmp,
                                                  pl->sel_bytes, st))))
                 return rc;
             // across the periodic seam the halo copies carry the image shift of the receiver's frame
             if (pl->rank == 0)
                 k_shift_x<<<(pl->halo_cap + 255) / 256, 256, 0, st>>>(pl->hsend, pl->nsel, p.Lx);
             if (pl->rank == R - 1)
-                k_shift_x<<<(pl->halo_cap + 255) / 256, 256, 0, st>>>(pl->hsend + pl->halo_cap, pl->nsel + 1, -p.Lx);
+                k_shift_x<<<(pl->halo_cap + 255) / 256, 256, 0, st>>>(pl->hsend + pl->nown_cap, pl->nsel + 1, -p.Lx);
         }
+        k_halo_status<<<1, 1, 0, st>>>(pl->nsel, pl->halo_cap, host_err, pl->dstat);
         CK(cudaGetLastError());
         const int r = pl->rank;
         ex[i].send = {{left(r), pl->nsel, sizeof(int)}, {right(r), pl->nsel + 1, sizeof(int)}};
         ex[i].recv = {{right(r), pl->nsel + 2, sizeof(int)}, {left(r), pl->nsel + 3, sizeof(int)}};
     }
+    if (d->loopback) {
+        for (int i = 1; i < L; ++i)
+            k_sum_into<<<1, 8, 0, d->stream>>>(d->pl[0]->dstat, d->pl[i]->dstat, 8);
+        for (int i = 1; i < L; ++i)
+            CK(cudaMemcpyAsync(d->pl[i]->dstat, d->pl[0]->dstat, 8 * sizeof(double), cudaMemcpyDeviceToDevice, d->stream));
+    } else {
+        NCK(nccl().AllReduce(d->pl[0]->dstat, d->pl[0]->dstat, 8, ncclFloat64, ncclSum, d->comm, d->stream));
+    }
     if ((rc = run_exchange(d, ex))) return rc;
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
         CK(cudaMemcpyAsync(pl->pin_i, pl->nsel, 4 * sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
-        CK(cudaMemcpyAsync(pl->pin_i + 4, pl->dbad, sizeof(unsigned), cudaMemcpyDeviceToHost, pl->stream));
+        CK(cudaMemcpyAsync(pl->pin_d, pl->dstat, 8 * sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
     }
     CK(cudaStreamSynchronize(d->stream));
+    {
+        // identical on every rank (summed status)
+        const double* sd = d->pl[0]->pin_d;
+        if (sd[3] > 0) return fail(SOG_EINVAL, "x-slab capacity exceeded (own count or halo of clustered input) on some rank");
+        if (sd[0] > 0) return fail(SOG_EINVAL, "own particle outside its rank's x slab");
+        if (!(d->pl[0]->flags & SOG_NO_VALIDATE)) {
+            if (sd[1] > 0) return fail(SOG_ENONFINITE, "non-finite position or charge");
+            if (sd[2] > 0) return fail(SOG_EZRANGE, "z outside [-Lz/2, Lz/2]");
+            if (std::fabs(sd[4]) > 1e-12 * sd[5]) return fail(SOG_ENONNEUTRAL, "system not charge neutral");
+        } else if (sd[1] > 0 || sd[2] > 0) {
+            return fail(SOG_EINVAL, "invalid particle (non-finite or z out of range)");
+        }
+    }
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
         const int* c = pl->pin_i;
-        if (c[4]) return fail(SOG_EINVAL, "own particle outside the rank's x slab");
-        for (int k = 0; k < 4; ++k)
-            if (c[k] > pl->halo_cap) return fail(SOG_EINVAL, "x-slab halo exceeds its capacity (clustered input)");
         const int r = pl->rank;
-        ex[i].send = {{left(r), pl->hsend, sizeof(d4) * c[0]}, {right(r), pl->hsend + pl->halo_cap, sizeof(d4) * c[1]}};
+        ex[i].send = {{left(r), pl->hsend, sizeof(d4) * c[0]}, {right(r), pl->hsend + pl->nown_cap, sizeof(d4) * c[1]}};
         ex[i].recv = {{right(r), pl->hrecv + pl->halo_cap, sizeof(d4) * c[2]}, {left(r), pl->hrecv, sizeof(d4) * c[3]}};
     }
     if ((rc = run_exchange(d, ex))) return rc;

@@ -226,6 +226,9 @@ class Plan:
             phi = torch.empty(self.N, dtype=torch.float64, device=xyz.device)
         if force is None and want_force:
             force = torch.empty(self.N, 3, dtype=torch.float64, device=xyz.device)
+        _check_out(phi, (self.N,), xyz.device, "phi")
+        if force is not None:
+            _check_out(force, (self.N, 3), xyz.device, "force")
         self._check(self.lib.sog_eval(self.h, xyz.data_ptr(), q.data_ptr(), phi.data_ptr(),
                                       force.data_ptr() if force is not None else None))
         return phi, force
@@ -233,11 +236,17 @@ class Plan:
     def eval_host(self, xyz, q, phi=None, force=None):
         """Host-buffer path (sog_eval_host): numpy or (pinned) CPU torch arrays in, host arrays out."""
         import numpy as np
-        xyz_p, q_p, keep = _host_ptr(xyz), _host_ptr(q), []
+        for a, shape, name in ((xyz, (self.N, 3), "xyz"), (q, (self.N,), "q")):
+            if tuple(a.shape) != shape:
+                raise ValueError(f"{name} must have shape {shape}")
+        xyz_p, q_p = _host_ptr(xyz), _host_ptr(q)
         if phi is None:
             phi = np.empty(self.N, dtype=np.float64)
         if force is None:
             force = np.empty((self.N, 3), dtype=np.float64)
+        for a, shape, name in ((phi, (self.N,), "phi"), (force, (self.N, 3), "force")):
+            if tuple(a.shape) != shape:
+                raise ValueError(f"{name} must have shape {shape}")
         self._check(self.lib.sog_eval_host(self.h, xyz_p, q_p, _host_ptr(phi), _host_ptr(force)))
         return phi, force
 
@@ -292,6 +301,21 @@ def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method=
     return _parse(buf.value.decode())
 
 
+def _check_out(t, shape, device, name):
+    """Caller-supplied output tensors: the library writes 8 bytes x prod(shape) through the pointer."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.device != device:
+        raise ValueError(f"{name} must be a CUDA tensor on {device}")
+    if t.dtype != torch.float64 or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float64 tensor of shape {tuple(shape)}")
+
+
+def _check_in(x, shape, name):
+    import torch
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64 or tuple(x.shape) != tuple(shape):
+        raise ValueError(f"{name} must be a float64 CUDA tensor of shape {tuple(shape)}")
+
+
 def _stream_handle(stream):
     if stream is None:
         return None
@@ -336,7 +360,9 @@ class DistPlan:
     """
 
     def __init__(self, N_total, n_own_max, L, tol, R, rank=0, nccl_id=None, loopback=False, params=None,
-                 stream=None, window="gs"):
+                 stream=None, window="gs", validate=True):
+        """validate=False skips the invalid-input checks (non-finite, z range, neutrality); slab
+        membership and capacities are always checked, identically on every rank."""
         self.lib = load_library()
         self.L = tuple(float(v) for v in L)
         self.R = int(R)
@@ -345,7 +371,7 @@ class DistPlan:
             o.explicit_params = 1
             for k in PLAN_FIELDS:
                 setattr(o, k, type(getattr(o, k))(params[k]))
-        o.flags = SOG_NO_VALIDATE
+        o.flags = 0 if validate else SOG_NO_VALIDATE
         o.cuda_stream = _stream_handle(stream)
         _set_window(o, window, params)
         if loopback:
@@ -393,10 +419,22 @@ class DistPlan:
             raise ValueError(f"expected {self.nlocal} per-rank inputs")
         xs = [x.contiguous() for x in xs]
         qs = [v.contiguous() for v in qs]
+        for x, v in zip(xs, qs):
+            if v.dim() != 1:
+                raise ValueError("q must be one-dimensional")
+            _check_in(v, (len(v),), "q")
+            _check_in(x, (len(v), 3), "xyz")
+            if x.device != v.device:
+                raise ValueError("xyz and q of a rank must be on the same device")
         phis = [torch.empty(len(v), dtype=torch.float64, device=v.device) for v in qs] if phi is None else (
             [phi] if single else list(phi))
         fs = [torch.empty(len(v), 3, dtype=torch.float64, device=v.device) for v in qs] if force is None else (
             [force] if single else list(force))
+        if len(phis) != self.nlocal or len(fs) != self.nlocal:
+            raise ValueError(f"expected {self.nlocal} per-rank outputs")
+        for v, ph, f in zip(qs, phis, fs):
+            _check_out(ph, (len(v),), v.device, "phi")
+            _check_out(f, (len(v), 3), v.device, "force")
         n = (ctypes.c_int64 * self.nlocal)(*[len(v) for v in qs])
         P = ctypes.c_void_p * self.nlocal
         rc = self.lib.sog_dist_eval(self.h, n, P(*[x.data_ptr() for x in xs]), P(*[v.data_ptr() for v in qs]),

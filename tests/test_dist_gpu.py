@@ -121,3 +121,87 @@ def test_particle_outside_its_slab_is_rejected():
     with pytest.raises(SogError):       # all particles handed to rank 0
         dp.eval([x, empty_x], [qq, empty_q])
     dp.close()
+
+
+def test_clustered_halo_is_rejected_without_overflow():
+    """Every own particle of rank 0 sits within the halo width of its right edge, with a capacity
+    far above the halo capacity: the selects must not write past their buffers, every rank must
+    return the same error, and the plan must still evaluate a valid input afterwards."""
+    from paper_2412_04595_b200 import DistPlan, SogError, slab_owner
+    xyz, q, L, op, params = slab_plan("c5", 6000, 2)
+    R = 2
+    owner = slab_owner(xyz[:, 0], L[0], R)
+    idx = [np.nonzero(owner == r)[0] for r in range(R)]
+    nmax = 4 * max(len(i) for i in idx)
+    dp = DistPlan(len(q), nmax, L, op.tol, R, loopback=True, params=params)
+    cap = dp.describe()["halo_capacity"]
+    assert cap < nmax
+    n = min(nmax, 3 * cap)                       # > cap particles in rank 0's right halo strip
+    rng = np.random.default_rng(5)
+    c = np.empty((n, 3))
+    c[:, 0] = -1e-3 * rng.random(n) - 1e-9       # just left of the slab edge x = 0
+    c[:, 1] = (rng.random(n) - 0.5) * L[1]
+    c[:, 2] = (rng.random(n) - 0.5) * L[2]
+    cq = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    if n % 2:
+        cq[-1] = 0.0
+    xs = [torch.from_numpy(c).cuda(), torch.from_numpy(np.ascontiguousarray(xyz[idx[1]])).cuda()]
+    qs = [torch.from_numpy(cq).cuda(), torch.from_numpy(np.ascontiguousarray(q[idx[1]])).cuda()]
+    with pytest.raises(SogError) as e:
+        dp.eval(xs, qs)
+    assert "capacity" in str(e.value)
+    torch.cuda.synchronize()                     # no fault
+    xs = [torch.from_numpy(np.ascontiguousarray(xyz[i])).cuda() for i in idx]
+    qs = [torch.from_numpy(np.ascontiguousarray(q[i])).cuda() for i in idx]
+    phis, _ = dp.eval(xs, qs)
+    assert all(torch.isfinite(p).all() for p in phis)
+    dp.close()
+
+
+def test_dist_validation_errors():
+    """The x-slab path rejects invalid input as sog_eval does (non-finite, z range, non-neutral),
+    with the status summed over ranks (a rank's own particles need not be neutral)."""
+    from paper_2412_04595_b200 import DistPlan, SogError, slab_owner
+    xyz, q, L, op, params = slab_plan("c5", 4000, 2)
+    owner = slab_owner(xyz[:, 0], L[0], 2)
+    idx = [np.nonzero(owner == r)[0] for r in range(2)]
+    dp = DistPlan(len(q), max(len(i) for i in idx), L, op.tol, 2, loopback=True, params=params)
+
+    def run(x, qq):
+        return dp.eval([torch.from_numpy(np.ascontiguousarray(x[i])).cuda() for i in idx],
+                       [torch.from_numpy(np.ascontiguousarray(qq[i])).cuda() for i in idx])
+
+    run(xyz, q)
+    for mod, code in (("z", -3), ("nan", -4), ("q", -2)):
+        x, qq = xyz.copy(), q.copy()
+        j = idx[1][3]
+        if mod == "z":
+            x[j, 2] = 0.51 * L[2]
+        elif mod == "nan":
+            x[j, 1] = np.nan
+        else:
+            qq[j] += 0.25
+        with pytest.raises(SogError) as e:
+            run(x, qq)
+        assert e.value.code == code, (mod, e.value.code)
+    phis, _ = run(xyz, q)
+    assert all(torch.isfinite(p).all() for p in phis)
+    dp.close()
+
+
+def test_output_tensor_validation():
+    """Caller-supplied outputs of the wrong dtype, shape or device are refused before any write."""
+    from paper_2412_04595_b200 import Plan
+    xyz, q, L = config_system("c1", N=500)
+    op = make_plan(len(q), *L, 1e-6)
+    pl = Plan(len(q), L, 1e-6)
+    x, qq = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
+    good_phi = torch.empty(len(q), dtype=torch.float64, device="cuda")
+    good_F = torch.empty(len(q), 3, dtype=torch.float64, device="cuda")
+    for phi, F in ((good_phi.float(), good_F), (good_phi[:-1], good_F), (good_phi, good_F[:-1]),
+                   (good_phi, good_F.cpu()), (good_phi, good_F.t().contiguous().t())):
+        with pytest.raises(ValueError):
+            pl.eval(x, qq, phi, F)
+    pl.eval(x, qq, good_phi, good_F)
+    assert torch.isfinite(good_phi).all()
+    pl.close()
