@@ -112,3 +112,38 @@ def ewald2d(xyz, q, L, targets=None, alpha=None, tol=1e-16):
         # self
         phi[it] += -2.0 * alpha * q[i] / _SQPI
     return phi, grad
+
+
+def ewald2d_targets(xyz, q, L, targets, tol=1e-12, alpha=None):
+    """ewald2d() at sampled targets for large N (target-subsampled use): the same
+    sums in plain C loops (oracle/c/oracle_c.c: oracle_ewald2d, one target per thread), with the
+    real-space cutoff erfc(alpha r_cut) ~ tol and k_cut = 2 alpha sqrt(-ln tol).  alpha (a free
+    splitting parameter: the result is alpha-independent) is chosen to minimise the loop count
+    N (images + pairs + modes) per target.  Pinned equal to ewald2d at small N
+    (tests/test_oracle_pins.py::test_ewald2d_c_loops_equal_numpy)."""
+    from . import cext
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    Lx, Ly, Lz = L
+    N = len(q)
+    rho = N / (Lx * Ly * Lz)
+    s = math.sqrt(-math.log(tol))
+    if alpha is None:
+        best = None
+        for a in np.geomspace(1e-3, 10.0, 400) / min(Lx, Ly) * 10:
+            rc, kc = s / a, 2.0 * a * s
+            shifts = (2 * (math.ceil(rc / Lx) + 1) + 1) * (2 * (math.ceil(rc / Ly) + 1) + 1)
+            pairs = rho * min(4.0 / 3.0 * math.pi * rc ** 3, math.pi * rc * rc * Lz)
+            modes = 0.5 * math.pi * (kc * Lx / (2 * math.pi)) * (kc * Ly / (2 * math.pi))
+            cost = 1.5 * shifts * N + 25.0 * pairs + 80.0 * (modes + 1) * N
+            if best is None or cost < best[0]:
+                best = (cost, a)
+        alpha = best[1]
+    rcut = s / alpha
+    kcut = 2.0 * alpha * s
+    t = np.ascontiguousarray(np.asarray(targets, dtype=np.int64))
+    phi = np.zeros(len(t))
+    grad = np.zeros((len(t), 3))
+    cext.lib().oracle_ewald2d(N, cext.ptr(xyz), cext.ptr(q), Lx, Ly, len(t), cext.ptr(t), alpha, rcut, kcut,
+                              cext.ptr(phi), cext.ptr(grad))
+    return phi, grad

@@ -236,20 +236,24 @@ def mid_multiplier(plan: Plan) -> np.ndarray:
     """Scaling factor of Eq. eq::widehat-tilde (P:460-462) on the rfftn half spectrum:
     tau_hat^mid(k)/k^2 * 4 pi |W_hat|^-2 = pi^{3/2} sum_{l<=m} w_l s_l^3
     exp(-s_l^2 |k|^2 / 4) / (W_hat_x W_hat_y W_hat_z)^2   (R12),
-    k_d = 2 pi n_d / L_d with L_z -> L_z^* (P:580)."""
+    k_d = 2 pi n_d / L_d with L_z -> L_z^* (P:580).  |k|^2 = kx^2 + ky^2 + kz^2, so each term
+    is the product of per-axis factors exp(-s^2 k_d^2 / 4) / W_hat_d^2; the sum over l is the
+    (l)-contraction of the x-y factor table with the z factor table."""
     w, s = plan.weights()
     kx = 2.0 * np.pi * np.fft.fftfreq(plan.Ix, d=plan.hx)
     ky = 2.0 * np.pi * np.fft.fftfreq(plan.Iy, d=plan.hy)
     kz = 2.0 * np.pi * np.fft.rfftfreq(plan.Izs, d=plan.hz)
-    k2 = kx[:, None, None] ** 2 + ky[None, :, None] ** 2 + kz[None, None, :] ** 2
-    tau = np.zeros_like(k2)
-    for ell in range(plan.m + 1):
-        tau += w[ell] * s[ell] ** 3 * np.exp(-s[ell] ** 2 * k2 / 4.0)
     Hx, Hy, Hz = (window_half_width(plan.window, plan.P, h) for h in (plan.hx, plan.hy, plan.hz))
-    What = (window_hat(plan, kx, Hx)[:, None, None]
-            * window_hat(plan, ky, Hy)[None, :, None]
-            * window_hat(plan, kz, Hz)[None, None, :])
-    return math.pi ** 1.5 * tau / What ** 2
+    Wx, Wy, Wz = window_hat(plan, kx, Hx), window_hat(plan, ky, Hy), window_hat(plan, kz, Hz)
+    L = plan.m + 1
+    Fxy = np.empty((L, plan.Ix * plan.Iy))
+    Fz = np.empty((L, len(kz)))
+    for ell in range(L):
+        fx = w[ell] * s[ell] ** 3 * np.exp(-s[ell] ** 2 * kx ** 2 / 4.0) / Wx ** 2
+        fy = np.exp(-s[ell] ** 2 * ky ** 2 / 4.0) / Wy ** 2
+        Fxy[ell] = (fx[:, None] * fy[None, :]).ravel()
+        Fz[ell] = np.exp(-s[ell] ** 2 * kz ** 2 / 4.0) / Wz ** 2
+    return (math.pi ** 1.5 * (Fxy.T @ Fz)).reshape(plan.Ix, plan.Iy, len(kz))
 
 
 def mid_stencils(plan: Plan, xyz):
@@ -270,6 +274,21 @@ def mid_spread(plan: Plan, xyz, q) -> np.ndarray:
             idx = base[:, None] + gz
             val = (q * Wx[:, a] * Wy[:, b])[:, None] * Wz
             np.add.at(G, idx.ravel(), val.ravel())
+    return G.reshape(plan.Ix, plan.Iy, plan.Izs)
+
+
+def mid_spread_loops(plan: Plan, xyz, q) -> np.ndarray:
+    """The same sum as mid_spread (Eq. eq::gridding, P:456-458) accumulated particle by particle in
+    plain C loops (oracle/c/oracle_c.c: oracle_mid_spread), for full BASELINE sizes (N = 1e7) where
+    np.add.at over 1.3e10 stencil points would take many minutes.  Pinned equal to mid_spread
+    (tests/test_oracle_pins.py::test_mid_spread_loops_equals_add_at)."""
+    from . import cext
+    (gx, Wx, _), (gy, Wy, _), (gz, Wz, _) = mid_stencils(plan, xyz)
+    G = np.zeros(plan.Ix * plan.Iy * plan.Izs)
+    # visit particles in (x, y, z) stencil-start order (cache locality only: the sum is order-free)
+    order = np.lexsort((gz[:, 0], gy[:, 0], gx[:, 0]))
+    a = [np.ascontiguousarray(v[order]) for v in (gx, gy, gz, Wx, Wy, Wz, np.asarray(q, dtype=np.float64))]
+    cext.lib().oracle_mid_spread(len(q), plan.P, plan.Ix, plan.Iy, plan.Izs, *[cext.ptr(v) for v in a], cext.ptr(G))
     return G.reshape(plan.Ix, plan.Iy, plan.Izs)
 
 
@@ -302,13 +321,16 @@ def mid_gather(plan: Plan, xyz, Psi: np.ndarray):
     return Vh * phi, Vh * grad
 
 
-def mid_range(plan: Plan, xyz, q, targets=None):
-    """Phi^mid (Algorithm 1) at the targets, with gradient."""
+def mid_range(plan: Plan, xyz, q, targets=None, loops=None):
+    """Phi^mid (Algorithm 1) at the targets, with gradient.  loops=True spreads with
+    mid_spread_loops (default above 2e5 particles), else with mid_spread."""
     tgt = slice(None) if targets is None else np.asarray(targets)
     n = len(q) if targets is None else len(tgt)
     if plan.m < 0:
         return np.zeros(n), np.zeros((n, 3))
-    Psi = mid_solve(plan, mid_spread(plan, xyz, q))
+    if loops is None:
+        loops = len(q) > 200_000
+    Psi = mid_solve(plan, (mid_spread_loops if loops else mid_spread)(plan, xyz, q))
     return mid_gather(plan, xyz[tgt], Psi)
 
 
@@ -373,6 +395,29 @@ def long_spread(plan: Plan, xyz, q) -> np.ndarray:
             idx = (gx[:, a] * plan.Ily + gy[:, b])[:, None] + layer[None, :]
             val = (q * Wx[:, a] * Wy[:, b])[:, None] * Lb
             np.add.at(G, idx.ravel(), val.ravel())
+    return G.reshape(plan.Pc, plan.Ilx, plan.Ily)
+
+
+def long_spread_dense(plan: Plan, xyz, q, chunk: int = 200_000) -> np.ndarray:
+    """The same sum as long_spread for small long grids at full BASELINE sizes: each particle's
+    window rows are written out densely over the Ilx (Ily) grid points (zeros off the stencil), and
+    the sum over particles j of (q_j L_b(z_j) Wx_j(gx)) Wy_j(gy) is one matrix product per chunk
+    of particles (a library GEMM as the j-contraction).  Pinned equal to long_spread
+    (tests/test_oracle_pins.py::test_long_spread_dense_equals_add_at)."""
+    (gx, Wx, _), (gy, Wy, _) = long_stencils(plan, xyz)
+    Lb, _ = long_basis(plan, xyz[:, 2])
+    q = np.asarray(q, dtype=np.float64)
+    G = np.zeros((plan.Pc * plan.Ilx, plan.Ily))
+    for c0 in range(0, len(q), chunk):
+        sl = slice(c0, c0 + chunk)
+        n = len(q[sl])
+        rows = np.repeat(np.arange(n), plan.Pl)
+        Dx = np.zeros((n, plan.Ilx))
+        Dy = np.zeros((n, plan.Ily))
+        np.add.at(Dx, (rows, gx[sl].ravel()), Wx[sl].ravel())
+        np.add.at(Dy, (rows, gy[sl].ravel()), Wy[sl].ravel())
+        T = (q[sl, None] * Lb[sl])[:, :, None] * Dx[:, None, :]          # (n, Pc, Ilx)
+        G += T.reshape(n, -1).T @ Dy
     return G.reshape(plan.Pc, plan.Ilx, plan.Ily)
 
 
@@ -475,7 +520,8 @@ def long_range(plan: Plan, xyz, q, targets=None):
     if plan.long_method == "direct":
         Psi = long_solve_direct(plan, long_spread_direct(plan, xyz, q))
         return long_gather_direct(plan, xyz[tgt], Psi)
-    Psi = long_solve(plan, long_spread(plan, xyz, q))
+    dense = len(q) > 200_000 and plan.Ilx * plan.Ily <= 4096
+    Psi = long_solve(plan, (long_spread_dense if dense else long_spread)(plan, xyz, q))
     return long_gather(plan, xyz[tgt], Psi)
 
 

@@ -77,21 +77,6 @@ def test_kb_full_size_c2_sampled():
     assert rel(F_g[t], F_o) <= TOL_FP64
 
 
-def test_kb_full_size_c5_sampled():
-    """c5 (N=1e7) with the KB window in the bench configuration: the mid and long components at
-    sampled targets vs the oracle's fields gathered per target, near unchanged."""
-    xyz, q, L = config_system("c5")
-    op = make_plan(len(q), *L, 1e-6, window="kb")
-    pl = gpu_plan(op)
-    xd, qd = to_dev(xyz, q)
-    comp = pl.components(xd, qd).cpu().numpy()
-    pl.close()
-    t = np.random.default_rng(3).choice(len(q), 32, replace=False)
-    x = O.canonicalize(xyz, op)
-    pl_o = O.long_range(op, x, q, targets=t)
-    assert rel(comp[2][t, 0], pl_o[0]) <= TOL_FP64 and rel(comp[2][t, 1:], pl_o[1]) <= TOL_FP64
-
-
 @pytest.mark.parametrize("name,N", [("c4", 4000), ("c1", 1000), ("c5", 20000)])
 def test_kb_fp32_mode_vs_fp64_oracle(name, N):
     xyz, q, L = config_system(name, N=N)

@@ -215,6 +215,50 @@ def test_ewald2d_dilute_limit_is_coulomb():
     assert np.allclose(grad, gc, atol=2e-6)
 
 
+def test_ewald2d_c_loops_equal_numpy():
+    """The C-loop Ewald2D used at full BASELINE sizes (ewald2d_targets) is the same sum as the pinned
+    NumPy ewald2d: equal at small N for two alphas, and alpha-independent on a c5-shaped box."""
+    L = (6.0, 7.0, 5.0)
+    xyz, q = uniform_system(300, L, 3)
+    t = np.arange(0, 300, 7)
+    p0, g0 = ewald2d.ewald2d(xyz, q, L, targets=t)
+    for alpha in (None, 0.3, 1.1):
+        p1, g1 = ewald2d.ewald2d_targets(xyz, q, L, t, tol=1e-16, alpha=alpha)
+        assert np.abs(p1 - p0).max() <= 2e-14 * np.abs(p0).max()
+        assert np.abs(g1 - g0).max() <= 2e-14 * np.abs(g0).max()
+    xyz, q, L = config_system("c5", N=20000)
+    t = np.arange(5) * 101
+    a = ewald2d.ewald2d_targets(xyz, q, L, t, tol=1e-13, alpha=0.05)
+    b = ewald2d.ewald2d_targets(xyz, q, L, t, tol=1e-13, alpha=0.12)
+    assert np.abs(a[0] - b[0]).max() <= 1e-11 * np.abs(a[0]).max()
+    assert np.abs(a[1] - b[1]).max() <= 1e-11 * np.abs(a[1]).max()
+
+
+def test_mid_spread_loops_equals_add_at():
+    """The C-loop gridding used at full BASELINE sizes (mid_spread_loops) is the sum of
+    mid_spread (np.add.at): equal to rounding at c1 and on a c5-shaped box, every window."""
+    for name, N, window in (("c1", 1000, "gs"), ("c5", 6000, "gs"), ("c1", 1000, "kb"), ("c4", 3000, "es")):
+        xyz, q, L = config_system(name, N=N)
+        p = P.make_plan(len(q), *L, 1e-6, window=window)
+        x = sog.canonicalize(xyz, p)
+        a = sog.mid_spread(p, x, q)
+        b = sog.mid_spread_loops(p, x, q)
+        assert a.shape == b.shape
+        assert np.abs(a - b).max() <= 1e-14 * np.abs(a).max(), (name, window)
+
+
+def test_long_spread_dense_equals_add_at():
+    """The dense-row long anterpolation used at full BASELINE sizes (long_spread_dense) is the sum
+    of long_spread (np.add.at), every window."""
+    for name, N, window in (("c1", 1000, "gs"), ("c5", 6000, "gs"), ("c5", 6000, "kb"), ("c4", 3000, "es")):
+        xyz, q, L = config_system(name, N=N)
+        p = P.make_plan(len(q), *L, 1e-6, window=window)
+        x = sog.canonicalize(xyz, p)
+        a = sog.long_spread(p, x, q)
+        b = sog.long_spread_dense(p, x, q, chunk=1777)
+        assert np.abs(a - b).max() <= 1e-14 * np.abs(a).max(), (name, window)
+
+
 # ------------------------------------------------------------------ spectral components vs SOG-exact
 @pytest.fixture(scope="module")
 def small_system():
