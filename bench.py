@@ -76,7 +76,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -138,23 +138,64 @@ def barrier(ws):
         dist.barrier()
 
 
+def cpu_info():
+    """Host CPU model and logical core count (lscpu), recorded beside the oracle timing."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def oracle_eval_staged(O, op, xyz, q):
+    """One full oracle evaluation (O.evaluate's steps) with per-component wall times, mirroring the
+    paper's Tables 2-3 split (near / mid / long)."""
+    t = {}
+    t0 = time.perf_counter()
+    x = O.canonicalize(xyz, op)
+    pn, gn = O.near_field(op, x, q)
+    t["near"] = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    pm, gm = O.mid_range(op, x, q)
+    t["mid"] = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    pl, gl = O.long_range(op, x, q)
+    t["long"] = time.perf_counter() - t2
+    phi = pn + pm + pl - q * O.self_coefficient(op)
+    F = -q[:, None] * (gn + gm + gl)
+    t["total"] = time.perf_counter() - t0
+    return phi, F, t
+
+
 def oracle_sample(cfg, tol, target_seconds=15.0, window="gs", long_method="fft"):
     """The oracle as it stands on a bounded sample of the workload: a system of the same
-    density and aspect ratio, N chosen so one evaluation takes ~target_seconds."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    density and aspect ratio, N chosen so one evaluation takes ~target_seconds.  All host cores:
+    scipy.fft workers=-1 (the oracle's default), NumPy/BLAS threads unrestricted."""
     import oracle.sog as O
     from oracle.plan import make_plan
-    O._WORKERS = 1                      # single host thread: cores = 1
     n = 2000
     while True:
         xyz, q, L = config_system(cfg, N=n)
         op = make_plan(n, *L, tol, window=window, long_method=long_method)
-        t0 = time.perf_counter()
-        O.evaluate(op, xyz, q)
-        dt = time.perf_counter() - t0
-        if dt > target_seconds / 4 or n >= 200_000:
-            return n, dt, L
+        _, _, st = oracle_eval_staged(O, op, xyz, q)
+        dt = st["total"]
+        if dt > target_seconds / 4 or n >= 400_000:
+            return n, dt, L, st
         n = int(n * min(8.0, max(1.5, target_seconds / 2 / max(dt, 1e-3))))
+
+
+def cpu_baseline_record(args, tol, n, dt, L, st, value=None):
+    return {"value": value if value is not None else n / dt, "unit": "particles/s", "cores": os.cpu_count(),
+            "kind": "oracle", "cpu": cpu_info(),
+            "sample": f"one full oracle evaluation of a {args.config}-density system, N={n}, box "
+                      f"{L[0]:.2f}x{L[1]:.2f}x{L[2]:.2f}, tol {tol:g}, all host cores (scipy.fft workers=-1, "
+                      f"NumPy/BLAS threads unrestricted; the near sum and np.add.at gridding are single-threaded "
+                      f"as the oracle stands)",
+            "stages_s": {k: round(v, 4) for k, v in st.items()}}
 
 
 def run_reference(args, ws, rank):
@@ -162,89 +203,125 @@ def run_reference(args, ws, rank):
         return
     c = CONFIGS[args.config]
     tol = args.tol or c.tol
-    n, dt0, L = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
+    n, dt0, L, _ = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
     import oracle.sog as O
     from oracle.plan import make_plan
     xyz, q, L = config_system(args.config, N=n)
     op = make_plan(n, *L, tol, window=args.window, long_method=args.long_method)
     for _ in range(min(args.warmup, 1)):
-        O.evaluate(op, xyz, q)
+        oracle_eval_staged(O, op, xyz, q)
+    acc = {}
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.evaluate(op, xyz, q)
+        _, _, st = oracle_eval_staged(O, op, xyz, q)
+        for k, v in st.items():
+            acc[k] = acc.get(k, 0.0) + v / args.steps
     dt = (time.perf_counter() - t0) / args.steps
     val = n / dt
-    sample = f"{args.config} density/aspect, N={n} (box {L[0]:.2f}x{L[1]:.2f}x{L[2]:.2f}), full oracle evaluation"
+    cpu = cpu_baseline_record(args, tol, n, dt, L, acc, value=val)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "particles/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} sample (oracle, CPU)", "N": n, "box": list(L), "tol": tol},
-        "cpu_baseline": {"value": val, "unit": "particles/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": cpu,
         "e2e": {"value": val, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-NEAR_FLOPS_PER_PAIR = 60.0   # r_ij (3), r^2 (5), F(u), F'(u) degree-10 joint Horner (40), 1/r (4), phi + grad (8)
+def measured_peaks():
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-measured copy bandwidth); FP64 and
+    FP32 FMA throughput from profiles/r02_fp64_peak.json (scripts/fp64_peak.cu on a B200)."""
+    peaks = {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)",
+             "fp64_tflops": 37.22, "fp64_source": "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (unit count)",
+             "fp32_tflops": 74.4, "fp32_source": "148 SM x 128 FFMA/clk x 2 x 1.965 GHz (unit count)"}
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        peaks["hbm_gbs"] = json.load(open(mp))["hbm_gbs"]
+        peaks["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    fp = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
+    if os.path.exists(fp):
+        rows = {r["kernel"]: r["tflops"] for r in json.load(open(fp))["rows"]}
+        if "dfma" in rows:
+            peaks["fp64_tflops"] = rows["dfma"]
+            peaks["fp64_source"] = "measured DFMA throughput, profiles/r02_fp64_peak.json"
+        f32 = max([v for k, v in rows.items() if k.startswith("ffma")] or [0.0])
+        if f32:
+            peaks["fp32_tflops"] = f32
+            peaks["fp32_source"] = "measured FFMA/FFMA2 throughput, profiles/r02_fp64_peak.json"
+    return peaks
 
 
-def stage_flops(d, N, L):
-    """Algorithmic FP64 flops per evaluation of each stencil/pair stage (DESIGN.md section 6;
-    FMA = 2 flops).  Near field: expected in-range pairs (4 pi / 3) r_c^3 rho per particle."""
+def stage_flops(d, N, L, long_method="fft"):
+    """Algorithmic flops per evaluation of each stencil/pair stage (SURVEY 8(d), DESIGN.md section 6;
+    FMA = 2 flops), in the plan's arithmetic precision.
+      near:        27 rho r_c^3 candidates x 9 (pre-test) + (4 pi/3) rho r_c^3 pairs x 50   (8(d))
+      mid spread:  2 (P^3 + P^2);  mid gather: 4 P^3 + 6 P^2 + 8 P
+      long (Alg. 2, window + FFT): spread 2 Pl^2 Pc + 2 Pl^2, gather 4 Pl^2 Pc + 6 Pl^2 + 4 Pc
+      long (Alg. 3, direct sums over nmode = (2Kx+1)(Ky+1) modes): spread 4 nmode Pc (a complex
+           phase times a real weight per mode and layer), gather 12 nmode Pc (real parts of
+           phase x Psi~ for phi, d/dx, d/dy)."""
     P, Pl, Pc = d["P"], d["Pl"], d["Pc"]
     rho = N / (L[0] * L[1] * L[2])
-    pairs = 4.0 * math.pi / 3.0 * d["rc"] ** 3 * rho
-    return {
-        "near": N * pairs * NEAR_FLOPS_PER_PAIR,
-        "mid_spread": N * (2.0 * P ** 3 + 2.0 * P * P),
-        "mid_gather": N * (4.0 * P ** 3 + 6.0 * P * P + 8.0 * P),
-        "long_spread": N * (2.0 * Pl * Pl * Pc + 2.0 * Pl * Pl),
-        "long_gather": N * (4.0 * Pl * Pl * Pc + 6.0 * Pl * Pl + 4.0 * Pc),
-    }
+    rc3 = d["rc"] ** 3
+    out = {"near": N * (27.0 * rho * rc3 * 9.0 + 4.0 * math.pi / 3.0 * rho * rc3 * 50.0)}
+    if d["m"] >= 0:
+        out["mid_spread"] = N * (2.0 * P ** 3 + 2.0 * P * P)
+        out["mid_gather"] = N * (4.0 * P ** 3 + 6.0 * P * P + 8.0 * P)
+    if long_method == "direct":
+        nmode = (2 * d["Kx"] + 1) * (d["Ky"] + 1)
+        out["long_spread"] = N * 4.0 * nmode * Pc
+        out["long_gather"] = N * 12.0 * nmode * Pc
+    else:
+        out["long_spread"] = N * (2.0 * Pl * Pl * Pc + 2.0 * Pl * Pl)
+        out["long_gather"] = N * (4.0 * Pl * Pl * Pc + 6.0 * Pl * Pl + 4.0 * Pc)
+    return out
 
 
-def stage_roofline(plan, stages, N, L):
+def stage_roofline(plan, stages, N, L, long_method="fft", precision="fp64"):
     """Roofline of the dominant kernel stage (and of every stencil stage) from the plan's
-    per-stage CUDA-event times on the plan's stream."""
+    per-stage CUDA-event times on the plan's stream (the stages run in sequence when timed)."""
     d = plan.describe()
-    G = d["Ix"] * d["Iy"] * d["Izs"]
-    sm_mhz = 1965.0
-    peak_fp64 = NUM_SMS * FP64_FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    flops = stage_flops(d, N, L)
+    pk = measured_peaks()
+    alu = pk["fp64_tflops"] if precision == "fp64" else pk["fp32_tflops"]
+    alu_src = pk["fp64_source"] if precision == "fp64" else pk["fp32_source"]
+    csz = 16.0 if precision == "fp64" else 8.0
+    flops = stage_flops(d, N, L, long_method)
     per_stage = {}
     for k, f in flops.items():
         if stages.get(k):
             ach = f / (stages[k] * 1e-3) / 1e12
-            per_stage[k] = {"bound": "alu", "achieved_tflops": ach, "frac": ach / peak_fp64, "ms": stages[k]}
-    # the mid scale and the FFTs are HBM-bound: read + write of the half spectrum (16 B / complex point)
-    spec_bytes = 2 * 16.0 * d["Izs"] * d["Ix"] * (d["Iy"] // 2 + 1)
+            per_stage[k] = {"bound": "alu", "achieved_tflops": ach, "frac": ach / alu, "ms": stages[k],
+                            "algorithmic_flops": f}
+    # the mid scale (on the z pencils) is HBM-bound: read + write of the pencil spectrum
+    spec_bytes = 2 * csz * d["Izs"] * d["Ix"] * (d["Iy"] // 2 + 1)
     if stages.get("mid_scale"):
         ach = spec_bytes / (stages["mid_scale"] * 1e-3) / 1e9
-        per_stage["mid_scale"] = {"bound": "hbm", "achieved_gbs": ach, "frac": ach / peaks["hbm_gbs"],
-                                  "ms": stages["mid_scale"]}
+        per_stage["mid_scale"] = {"bound": "hbm", "achieved_gbs": ach, "frac": ach / pk["hbm_gbs"],
+                                  "ms": stages["mid_scale"], "algorithmic_bytes": spec_bytes}
     name = max((k for k in stages if k not in ("mid_fft_fwd", "mid_fft_inv", "long_fft_scale_ifft")),
                key=lambda k: stages[k])
     ms = stages[name]
     # DRAM traffic of that kernel from the committed ncu --set full capture (per launch), if any
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-    if os.path.exists(tpath):
-        t = json.load(open(tpath)).get(name)
-        traffic = t["dram_bytes_per_launch"] if t else None
+    for tp in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):
+        tpath = os.path.join(ROOT, "profiles", tp)
+        if os.path.exists(tpath):
+            t = json.load(open(tpath)).get(name)
+            traffic = t["dram_bytes_per_launch"] if t else None
+            break
     if name in flops:
         ach = flops[name] / (ms * 1e-3) / 1e12
-        roof = {"bound": "alu", "kernel": name, "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
-                "frac": ach / peak_fp64, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
-                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md, guide unit counts)",
-                "algorithmic_flops": flops[name], "ms": ms}
+        roof = {"bound": "alu", "kernel": name, "achieved": ach, "peak": alu, "unit": "TFLOP/s",
+                "frac": ach / alu, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
+                "peak_source": alu_src, "algorithmic_flops": flops[name], "ms": ms,
+                "flops_rule": "SURVEY 8(d) per-particle formula x N (bench.py stage_flops)"}
     else:
         bytes_ = {"mid_scale": spec_bytes, "sort": 150.0 * N, "combine": 160.0 * N}.get(name, 64.0 * N)
         ach = bytes_ / (ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_bytes": bytes_, "ms": ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "traffic": traffic, "algorithmic_bytes": bytes_, "ms": ms,
+                "peak_source": pk["hbm_source"]}
     return name, roof, per_stage
 
 
@@ -363,6 +440,16 @@ def main():
         torch.cuda.synchronize()
         barrier(ws)
     ms = e0.elapsed_time(e1) / args.steps
+    clocks = clk.summary()
+    if not clk.rows:
+        # timed region shorter than the sampling interval: sample the same evaluation sustained for
+        # >= 1 s right after it (untimed), and say so
+        with ClockSampler(local) as clk2:
+            t_end = time.perf_counter() + 1.0
+            while time.perf_counter() < t_end:
+                plan.eval(xd, qd, phi, F)
+                torch.cuda.synchronize()
+        clocks = dict(clk2.summary(), window="sustained evaluations right after the timed region (>= 1 s)")
     ms = max_over_ranks(ms, ws)
     value = N * ws / (ms * 1e-3)
     # per-stage device times (CUDA events on the plan's stream), averaged over K evaluations
@@ -373,7 +460,7 @@ def main():
         for k, v in plan.timings().items():
             acc[k] = acc.get(k, 0.0) + v / args.steps
     plan.set_flags(validate=False)
-    dom, roof, per_stage = stage_roofline(plan, acc, N, L)
+    dom, roof, per_stage = stage_roofline(plan, acc, N, L, args.long_method, args.precision)
     # end-to-end through the public host-buffer API (pinned host memory, copies in the timed region)
     e2e = None
     if not args.no_e2e:
@@ -397,10 +484,8 @@ def main():
                "host_wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / args.steps}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n, dt, Ls = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
-        cpu = {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "oracle",
-               "sample": f"one full oracle evaluation of a {args.config}-density system, N={n}, "
-                         f"box {Ls[0]:.2f}x{Ls[1]:.2f}x{Ls[2]:.2f}, tol {tol:g}, 1 host thread"}
+        n, dt, Ls, st = oracle_sample(args.config, tol, window=args.window, long_method=args.long_method)
+        cpu = cpu_baseline_record(args, tol, n, dt, Ls, st)
     d = plan.describe()
     out = {
         "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": ws, "steps": args.steps,
@@ -419,7 +504,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": plan.launches_per_eval() * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -14,6 +14,7 @@ R14 coordinates.  Every function here is pinned by tests/test_oracle_*.py.
 """
 from __future__ import annotations
 
+import functools
 import math
 
 import numpy as np
@@ -110,7 +111,7 @@ def near_field(plan: Plan, xyz, q, targets=None, brute_force=None):
     rq = plan.rc * (1.0 + 1e-9)
     for c0 in range(0, len(tgt), 65536):
         t = tgt[c0:c0 + 65536]
-        lists = tree.query_ball_point(pos[t], rq)
+        lists = tree.query_ball_point(pos[t], rq, workers=_WORKERS)
         cnt = np.fromiter((len(l) for l in lists), dtype=np.int64, count=len(t))
         sj = np.fromiter((j for l in lists for j in l), dtype=np.int64, count=int(cnt.sum()))
         ti = np.repeat(t, cnt)
@@ -182,16 +183,40 @@ def window_half_width(window: str, P: int, h: float) -> float:
     return (P * h if window in POLY_WINDOWS else (P - 1) * h) / 2.0
 
 
+@functools.lru_cache(maxsize=64)
 def kb_stencil_polys(P: int, beta: float, nu: int, window: str = "kb"):
     """R6-KB (the paper's polynomial windows, Remark rmk::PWindow P:477-480): for stencil
     point j = 0..P-1 and the particle's offset u = x/h + I/2 - g0 in [-1/2, 1/2), the weight
     W_KB((j - p - u) h) is replaced by its degree-nu interpolant at the nu+1 first-kind
     Chebyshev points of u in [-1/2, 1/2] (Chebyshev series in t = 2u).  h cancels (the window
-    scales with H = P h / 2).  Returns the (P, nu+1) Chebyshev coefficients."""
+    scales with H = P h / 2).  Returns the (P, nu+1) Chebyshev coefficients.
+
+    The interpolation coefficients a_n = (2 - delta_n0)/(nu+1) sum_i f(t_i) T_n(t_i) are formed in
+    40-digit arithmetic (mpmath) and rounded once: in double they carry ~1e-15 absolute noise,
+    which the derivative series (the forces, R11) amplifies by ~nu^2 to ~1e-12 relative (the
+    interpolant is the definition; its rounding noise is not)."""
+    import mpmath as mp
     p = (P - 1) // 2
-    C = np.empty((P, nu + 1))
-    for j in range(P):
-        C[j] = npcheb.chebinterpolate(lambda t: POLY_WINDOWS[window]((j - p - 0.5 * t), 0.5 * P, beta), nu)
+    n1 = nu + 1
+    with mp.workdps(40):
+        H = mp.mpf(P) / 2
+        bb = mp.mpf(beta)
+        i0b = mp.besseli(0, bb)
+
+        def w(x):
+            r = 1 - (x / H) ** 2
+            if r < 0:
+                return mp.mpf(0)
+            return mp.besseli(0, bb * mp.sqrt(r)) / i0b if window == "kb" else mp.exp(bb * (mp.sqrt(r) - 1))
+
+        ang = [(i + mp.mpf(1) / 2) * mp.pi / n1 for i in range(n1)]
+        C = np.empty((P, n1))
+        for j in range(P):
+            f = [w((j - p) - mp.cos(a) / 2) for a in ang]
+            for n in range(n1):
+                acc = mp.fsum(f[i] * mp.cos(n * ang[i]) for i in range(n1))
+                C[j, n] = float(acc * (1 if n == 0 else 2) / n1)
+    C.setflags(write=False)
     return C
 
 

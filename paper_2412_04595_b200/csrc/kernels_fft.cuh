@@ -1,0 +1,302 @@
+// Shared-memory mixed-radix FFT for the mid-range solver (Algorithm 1 steps 2-4).
+//
+// cuFFT is no longer used for the mid grid: the z-pruned 3D FFT, the S5 scaling and the inverse
+// are done by these kernels, each one pass over HBM:
+//   k_fft_rows   y:  real rows of Iy -> nyh complex (forward) / back (inverse)       [z][x][.]
+//   k_fft_cols   x:  complex columns of Ix at stride nyh, B adjacent ky per CTA       [z][.][ky]
+//   k_zpass      z:  FFT along z of B adjacent (x, ky) columns, zero padding of the input
+//                    rows implicit, S5 multiply by mult(k) (Eq. eq::widehat-tilde),
+//                    inverse FFT, store of the rows the gather reads -- one kernel, in place.
+// A CTA holds its B transforms in shared memory as [n][B] (row = one index of the transform, B
+// adjacent columns, so global rows are contiguous B-element segments) and runs Stockham autosort
+// stages of radix 2, 3, 4, 5, 7 or 8 (7-smooth lengths, rule R5/R7): per stage every thread loads
+// its butterflies into registers, multiplies by the stage twiddles (host table, long double),
+// applies the radix-R DFT, a barrier, stores them in natural order, a barrier.  Forward sign
+// e^{-2 pi i / n}, unnormalised (the 1/(Ix Iy Izs) of the inverse is folded into the S5 table,
+// R12).  The inverse uses conj(FFT(conj(x))).
+#pragma once
+#include <cuComplex.h>
+#include <type_traits>
+#include "kernels_common.cuh"
+
+namespace sog {
+
+constexpr int FFT_MAXST = 24;
+constexpr int FFT_NTHR = 512;        // threads per CTA
+constexpr int FFT_MAXE = 2560;       // complex elements per CTA (n x B): <= 5 per thread in registers
+
+struct FftStages {
+    int n = 0, nst = 0;
+    int R[FFT_MAXST] = {};           // radix of stage s
+    int Ns[FFT_MAXST] = {};          // product of the earlier radices
+    unsigned mNs[FFT_MAXST] = {};    // ceil(2^32 / Ns): j / Ns = umulhi(j, mNs) for j < 2^18
+    int tw[FFT_MAXST] = {};          // offset of stage s's twiddles: [Ns][R-1] complex
+};
+
+template <typename T>
+struct Cplx;
+template <>
+struct Cplx<double> {
+    using C = double2;
+};
+template <>
+struct Cplx<float> {
+    using C = float2;
+};
+
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+    C r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) {
+    a.x += b.x;
+    a.y += b.y;
+    return a;
+}
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) {
+    a.x -= b.x;
+    a.y -= b.y;
+    return a;
+}
+template <typename C>
+__device__ __forceinline__ C mul_mi(C a) {   // -i a
+    C r;
+    r.x = a.y;
+    r.y = -a.x;
+    return r;
+}
+
+// radix-R DFT in registers, forward sign: y_k = sum_j v_j e^{-2 pi i j k / R}
+template <int R, typename C>
+__device__ __forceinline__ void dft_small(C* v) {
+    using T = decltype(v[0].x);
+    if constexpr (R == 2) {
+        const C a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        const C t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]), t2 = cadd(v[1], v[3]), t3 = mul_mi(csub(v[1], v[3]));
+        v[0] = cadd(t0, t2);
+        v[2] = csub(t0, t2);
+        v[1] = cadd(t1, t3);
+        v[3] = csub(t1, t3);
+    } else if constexpr (R == 8) {
+        // two radix-4 DFTs of the even / odd entries, twiddles W8^k, radix-2 across
+        C e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        dft_small<4>(e);
+        dft_small<4>(o);
+        const T h = T(0.70710678118654752440084436210485);
+        // o1 *= W8 = (1 - i)/sqrt2, o2 *= -i, o3 *= W8^3 = (-1 - i)/sqrt2
+        C w1, w3;
+        w1.x = h * (o[1].x + o[1].y);
+        w1.y = h * (o[1].y - o[1].x);
+        w3.x = h * (o[3].y - o[3].x);
+        w3.y = -h * (o[3].x + o[3].y);
+        o[1] = w1;
+        o[2] = mul_mi(o[2]);
+        o[3] = w3;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = cadd(e[k], o[k]);
+            v[k + 4] = csub(e[k], o[k]);
+        }
+    } else {
+        // odd R (3, 5, 7): pairs b_p = v_p + v_{R-p}, d_p = v_p - v_{R-p};
+        // y_k = v_0 + sum_p cos(2 pi p k / R) b_p - i sum_p sin(2 pi p k / R) d_p, y_{R-k} with +i
+        static_assert(R == 3 || R == 5 || R == 7, "radix");
+        constexpr int H = (R - 1) / 2;
+        // cos / sin (2 pi m / R), m = 1..H (compile-time after unrolling)
+        auto cs = [](int m) -> T {
+            if (R == 3) return T(-0.5);
+            if (R == 5) return m == 1 ? T(0.30901699437494742410229341718282) : T(-0.80901699437494742410229341718282);
+            return m == 1 ? T(0.62348980185873353052500488400424)
+                          : (m == 2 ? T(-0.22252093395631440428890256449679) : T(-0.90096886790241912623610231950745));
+        };
+        auto sn = [](int m) -> T {
+            if (R == 3) return T(0.86602540378443864676372317075294);
+            if (R == 5) return m == 1 ? T(0.95105651629515357211643933337938) : T(0.58778525229247312916870595463907);
+            return m == 1 ? T(0.78183148246802980870844452667406)
+                          : (m == 2 ? T(0.97492791218182360701813168299393) : T(0.43388373911755812047576833284836));
+        };
+        C b[H], d[H];
+#pragma unroll
+        for (int p = 1; p <= H; ++p) {
+            b[p - 1] = cadd(v[p], v[R - p]);
+            d[p - 1] = csub(v[p], v[R - p]);
+        }
+        const C a0 = v[0];
+        C y0 = a0;
+#pragma unroll
+        for (int p = 0; p < H; ++p) y0 = cadd(y0, b[p]);
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+            C re = a0, im;
+            im.x = T(0);
+            im.y = T(0);
+#pragma unroll
+            for (int p = 1; p <= H; ++p) {
+                const int m = (p * k) % R;                    // cos(2 pi m/R), sin(2 pi m/R)
+                const T c = m <= H ? cs(m) : cs(R - m);
+                const T s = m <= H ? sn(m) : -sn(R - m);
+                re.x = fma(c, b[p - 1].x, re.x);
+                re.y = fma(c, b[p - 1].y, re.y);
+                im.x = fma(s, d[p - 1].x, im.x);
+                im.y = fma(s, d[p - 1].y, im.y);
+            }
+            // -i * im = (im.y, -im.x)
+            v[k].x = re.x + im.y;
+            v[k].y = re.y - im.x;
+            v[R - k].x = re.x - im.y;
+            v[R - k].y = re.y + im.x;
+        }
+        v[0] = y0;
+    }
+}
+
+// one Stockham stage of radix R over the B columns of buf [n][B] (in place through registers)
+template <int R, int B, typename C>
+__device__ __forceinline__ void fft_stage(C* buf, int n, int Ns, unsigned mNs, const C* __restrict__ tw, int tid) {
+    constexpr int K = (FFT_MAXE + R * FFT_NTHR - 1) / (R * FFT_NTHR);   // butterflies per thread
+    const int nb = n / R, total = nb * B;
+    C v[K][R];
+    int dst[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int t = tid + k * FFT_NTHR;
+        dst[k] = -1;
+        if (t < total) {
+            const int b = t & (B - 1), j = t / B;
+            const int q = Ns > 1 ? (int)__umulhi((unsigned)j, mNs) : j;
+            const int jk = j - q * Ns;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[k][r] = buf[(j + r * nb) * B + b];
+            if (Ns > 1) {
+                const C* w = tw + jk * (R - 1);
+#pragma unroll
+                for (int r = 1; r < R; ++r) v[k][r] = cmul(v[k][r], w[r - 1]);
+            }
+            dft_small<R>(v[k]);
+            dst[k] = (q * R * Ns + jk) * B + b;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (dst[k] >= 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) buf[dst[k] + r * Ns * B] = v[k][r];
+        }
+    __syncthreads();
+}
+
+// the host orders the stages by radix 8, 7, 5, 4, 3, 2 (fft_plan_stages); one loop per radix keeps
+// each radix's registers separate
+template <int B, typename C>
+__device__ __forceinline__ void fft_run(C* buf, const FftStages& f, const C* __restrict__ tw, int tid) {
+    int s = 0;
+#define SOG_FFT_RADIX_LOOP(RR) \
+    for (; s < f.nst && f.R[s] == RR; ++s) fft_stage<RR, B>(buf, f.n, f.Ns[s], f.mNs[s], tw + f.tw[s], tid);
+    SOG_FFT_RADIX_LOOP(8)
+    SOG_FFT_RADIX_LOOP(7)
+    SOG_FFT_RADIX_LOOP(5)
+    SOG_FFT_RADIX_LOOP(4)
+    SOG_FFT_RADIX_LOOP(3)
+    SOG_FFT_RADIX_LOOP(2)
+#undef SOG_FFT_RADIX_LOOP
+}
+
+// ---------------------------------------------------------------------------------------
+// z pass: X [planes][M] complex (M = Ix * nyh columns m = x * nyh + ky).  Input rows z in
+// [zin0, zin0 + nin) are read from planes z - zin0 (the others are the zero padding), output rows
+// z in [zout0, zout0 + nout) are written to planes z - zout0 (in place: a CTA reads all rows of
+// its columns before it writes any).  Between the forward and inverse transforms: multiply by
+// mult(k) = sum_{l < L} A_l Tx_l(x) Ty_l(ky) Tz_l(kz) (R12; A holds the 1/(Ix Iy Izs) of the
+// unnormalised inverse).  One CTA per batch of B columns; the stage twiddles are staged in shared
+// memory.
+__device__ __forceinline__ void cp_async_c(void* dst, const double2* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_c(void* dst, const float2* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T, int LM, int B>
+__global__ void __launch_bounds__(FFT_NTHR, 2) k_zpass(typename Cplx<T>::C* __restrict__ X, long long M, int nyh,
+                                                     int zin0, int nin, int zout0, int nout, FftStages f,
+                                                     const typename Cplx<T>::C* __restrict__ twg, int ntw, int L,
+                                                     const double* __restrict__ A, const double* __restrict__ Tx,
+                                                     int Ix, const double* __restrict__ Ty,
+                                                     const double* __restrict__ Tz) {
+    using C = typename Cplx<T>::C;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int tid = threadIdx.x, n = f.n;
+    C* bufs = reinterpret_cast<C*>(smraw);                // [n][B]
+    C* tw = bufs + n * B;                                 // [ntw] stage twiddles
+    T* fac = reinterpret_cast<T*>(tw + ntw);              // [LM][B]: A_l Tx_l(x) Ty_l(ky) per column
+    for (int e = tid; e < ntw; e += FFT_NTHR) tw[e] = twg[e];
+    C zero;
+    zero.x = T(0);
+    zero.y = T(0);
+    C* buf = bufs;
+    const long long m0 = (long long)blockIdx.x * B;
+    const int nbc = (int)min((long long)B, M - m0);
+    {
+        const C* src = X + m0;
+        for (int e = tid; e < nin * B; e += FFT_NTHR) {
+            const int zr = e / B, b = e & (B - 1);
+            if (b < nbc) cp_async_c(&buf[zin0 * B + e], &src[(size_t)zr * M + b]);
+            else buf[zin0 * B + e] = zero;
+        }
+        cp_async_commit();
+    }
+    // z padding rows
+    for (int e = tid; e < zin0 * B; e += FFT_NTHR) buf[e] = zero;
+    for (int e = (zin0 + nin) * B + tid; e < n * B; e += FFT_NTHR) buf[e] = zero;
+    for (int e = tid; e < B * LM; e += FFT_NTHR) {
+        const int l = e / B, b = e & (B - 1);
+        T v = T(0);
+        if (b < nbc && l < L) {
+            const long long m = m0 + b;
+            const int x = int(m / nyh), ky = int(m - (long long)x * nyh);
+            v = T(A[l] * Tx[(size_t)l * Ix + x] * Ty[(size_t)l * nyh + ky]);
+        }
+        fac[e] = v;
+    }
+    cp_async_wait0();
+    __syncthreads();
+    fft_run<B>(buf, f, tw, tid);
+    // S5 (thread per element; the LM factor loads are independent and issued together, the B
+    // threads of one kz share each Tz_l(kz) load), then conj for the inverse
+    for (int e = tid; e < n * B; e += FFT_NTHR) {
+        const int kz = e / B, b = e & (B - 1);
+        T m = T(0);
+#pragma unroll
+        for (int l = 0; l < LM; ++l) m = fma(fac[l * B + b], T(__ldg(&Tz[(size_t)min(l, L - 1) * n + kz])), m);
+        C v = buf[e];
+        v.x *= m;
+        v.y *= -m;
+        buf[e] = v;
+    }
+    __syncthreads();
+    fft_run<B>(buf, f, tw, tid);
+    C* dst = X + m0;
+    for (int e = tid; e < nout * B; e += FFT_NTHR) {
+        const int zr = e / B, b = e & (B - 1);
+        if (b < nbc) {
+            C v = buf[zout0 * B + e];
+            v.y = -v.y;
+            dst[(size_t)zr * M + b] = v;
+        }
+    }
+}
+
+}  // namespace sog

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuComplex.h>
 #include <cuda_runtime.h>
+#include <vector>
 #include "kernels_common.cuh"
 
 namespace sog {
@@ -24,6 +25,13 @@ int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void
 size_t mid_gather_smem(int P);
 int launch_zfft_transpose(const void* in, void* out, int nz, long long M, int Izs, int z0, bool fwd, bool f32,
                           cudaStream_t st);
+struct FftStages;
+// shared-memory FFT (kernels_fft.cuh): stage plan + twiddles (false: length not supported)
+bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw);
+// z pass of the mid solver: FFT along z, S5 scaling, inverse FFT, in place on the plane spectra
+int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, int nout, const FftStages& f,
+                 const void* tw, int L, const double* A, const double* Tx, int Ix, const double* Ty, const double* Tz,
+                 bool f32, cudaStream_t st);
 int launch_scale_pencil_z(void* W, int Ix, int nyh, int Izs, int L, const double* A, const double* Tx,
                           const double* Ty, const double* Tz, bool f32, cudaStream_t st);
 int mid_spread_emax();

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/sog.h"
+#include "kernels_fft.cuh"
 #include "kernels_common.cuh"
 #include "kernels_dist.cuh"
 #include "kernels_long.cuh"
@@ -137,6 +138,10 @@ struct sog_plan {
     cufftHandle minv_full = 0, mzfft = 0;  // 2D inverse over all planes (debug stage 2); 1D along z
     cuDoubleComplex *mX = nullptr, *mY = nullptr;   // [planes][Ix*nyh] and zero-padded pencils [Ix*nyh][Izs]
     int zs0 = 0, nzf = 0, zg0 = 0, nzg = 0;         // spread-written planes, gather-read planes
+    // fused z pass (kernels_fft.cuh): FFT along z + S5 + inverse in one kernel on the plane spectra
+    bool zpass = false;
+    FftStages zst{};
+    void* d_ztw = nullptr;                          // twiddles (double2, or float2 in fp32 mode)
     bool has_mid = false;
     // long
     double* lgrid = nullptr;
@@ -241,7 +246,7 @@ void free_plan(sog_plan* pl) {
     for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
                           pl->mzfft})
         if (h) cufftDestroy(h);
-    for (void* p : {(void*)pl->mX, (void*)pl->mY})
+    for (void* p : {(void*)pl->mX, (void*)pl->mY, pl->d_ztw})
         if (p) cudaFree(p);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
@@ -327,9 +332,8 @@ int setup(sog_plan* pl) {
         } else {
             pl->Ixk = p.Ix;
         }
-        size_t G = (size_t)pl->Ixk * p.Iy * p.Izs, Gc = slab ? 1 : (size_t)p.Izs * p.Ix * nyh;
-        if ((rc = dalloc(pl, &pl->mgrid, G)) || (rc = dalloc(pl, &pl->mpsi, G)) || (rc = dalloc(pl, &pl->mspec, Gc)))
-            return rc;
+        size_t G = (size_t)pl->Ixk * p.Iy * p.Izs;
+        if ((rc = dalloc(pl, &pl->mgrid, G)) || (rc = dalloc(pl, &pl->mpsi, G))) return rc;
         CK(cudaMemset(pl->mgrid, 0, G * sizeof(double)));
         CK(cudaMemset(pl->mpsi, 0, G * sizeof(double)));
         // mid order (S1) and the z-sweep geometry of the spread / gather
@@ -396,9 +400,7 @@ int setup(sog_plan* pl) {
             const long long M = (long long)p.Ix * nyh;
             const size_t csz = pl->f32 ? sizeof(cuComplex) : sizeof(cuDoubleComplex);
             CK(cudaMalloc((void**)&pl->mX, csz * (size_t)M * p.Izs));
-            CK(cudaMalloc((void**)&pl->mY, csz * (size_t)M * p.Izs));
-            CK(cudaMemset(pl->mY, 0, csz * (size_t)M * p.Izs));   // z padding of the pencils stays zero
-            pl->bytes += 2 * csz * (size_t)M * p.Izs;
+            pl->bytes += csz * (size_t)M * p.Izs;
             long long n2[2] = {p.Ix, p.Iy}, n1[1] = {p.Izs};
             const cufftType r2c = pl->f32 ? CUFFT_R2C : CUFFT_D2Z, c2r = pl->f32 ? CUFFT_C2R : CUFFT_Z2D;
             const cufftType c2c = pl->f32 ? CUFFT_C2C : CUFFT_Z2Z;
@@ -415,6 +417,29 @@ int setup(sog_plan* pl) {
             CKF(cufftCreate(&pl->mzfft));
             CKF(cufftMakePlanMany64(pl->mzfft, 1, n1, nullptr, 1, p.Izs, nullptr, 1, p.Izs, c2c, M, &ws));
             pl->bytes += ws;
+            // fused z pass (opt-in, SOG_ZPASS=1) when Izs is 7-smooth and short enough for one CTA;
+            // default: the transpose + cuFFT 1D + scale + cuFFT 1D + transpose chain (measured faster
+            // at c5: 6.1 vs 7.1 ms)
+            {
+                const char* env = std::getenv("SOG_ZPASS");
+                std::vector<double2> tw;
+                if (env && std::atoi(env) == 1 && fft_plan_stages(p.Izs, pl->zst, tw)) {
+                    if (pl->f32) {
+                        std::vector<float2> t2(tw.size());
+                        for (size_t i = 0; i < tw.size(); ++i) t2[i] = make_float2((float)tw[i].x, (float)tw[i].y);
+                        if ((rc = upload(pl, (float2**)&pl->d_ztw, t2))) return rc;
+                    } else if ((rc = upload(pl, (double2**)&pl->d_ztw, tw))) {
+                        return rc;
+                    }
+                    pl->zpass = true;
+                }
+            }
+            if (!pl->zpass) {   // zero-padded z pencils and their spectra for the cuFFT 1D chain
+                CK(cudaMalloc((void**)&pl->mY, csz * (size_t)M * p.Izs));
+                CK(cudaMemset(pl->mY, 0, csz * (size_t)M * p.Izs));   // z padding of the pencils stays zero
+                pl->bytes += csz * (size_t)M * p.Izs;
+                if ((rc = dalloc(pl, &pl->mspec, (size_t)p.Izs * p.Ix * nyh))) return rc;
+            }
         } else {
             // distributed FFT: 2D (z, y) per interior x plane, all-to-all to ky chunks, 1D along x
             long long n2[2] = {p.Izs, p.Iy};
@@ -807,6 +832,16 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         } else {
             CKF(cufftExecD2Z(pl->mfwd, pl->mgrid + gp * pl->zs0, pl->mX));
         }
+        const bool full = stop_stage == 2;
+        const int z0 = full ? 0 : pl->zg0, nz = full ? p.Izs : pl->nzg;
+        if (pl->zpass) {
+            // S4 (z), S5, S6 (z) in one kernel, in place on the plane spectra
+            mark(pl, 4);
+            if ((rc = lchk(launch_zpass(pl->mX, M, nyh, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, p.m + 1, pl->d_A,
+                                        pl->d_Tx, p.Ix, pl->d_Ty, pl->d_Tz, pl->f32, st))))
+                return rc;
+            mark(pl, 5);
+        } else {
         if ((rc = lchk(launch_zfft_transpose(pl->mX, pl->mY, pl->nzf, M, p.Izs, pl->zs0, true, pl->f32, st)))) return rc;
         if (pl->f32) CKF(cufftExecC2C(pl->mzfft, (cufftComplex*)pl->mY, (cufftComplex*)pl->mspec, CUFFT_FORWARD));
         else CKF(cufftExecZ2Z(pl->mzfft, pl->mY, pl->mspec, CUFFT_FORWARD));
@@ -819,9 +854,8 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         // S6: inverse along z, back to planes (only those the gather reads; all for the debug stage)
         if (pl->f32) CKF(cufftExecC2C(pl->mzfft, (cufftComplex*)pl->mspec, (cufftComplex*)pl->mspec, CUFFT_INVERSE));
         else CKF(cufftExecZ2Z(pl->mzfft, pl->mspec, pl->mspec, CUFFT_INVERSE));
-        const bool full = stop_stage == 2;
-        const int z0 = full ? 0 : pl->zg0, nz = full ? p.Izs : pl->nzg;
         if ((rc = lchk(launch_zfft_transpose(pl->mspec, pl->mX, nz, M, p.Izs, z0, false, pl->f32, st)))) return rc;
+        }
         const cufftHandle inv = full ? pl->minv_full : pl->minv;
         if (pl->f32) CKF(cufftExecC2R(inv, (cufftComplex*)pl->mX, (float*)pl->mpsi + gp * z0));
         else CKF(cufftExecZ2D(inv, pl->mX, pl->mpsi + gp * z0));
@@ -1092,8 +1126,8 @@ int sog_plan_describe(const sog_plan* pl, char* buf, size_t len) {
     char extra[512];
     std::snprintf(extra, sizeof extra,
                   "ncell=%d\nnear_table_pieces=%d\nnear_table_degree=%d\nnear_table_max_rel_err=%.3e\n"
-                  "self_coefficient=%.17g\nworkspace_bytes=%zu\n",
-                  pl->ncell, pl->near.K, pl->near.D, pl->near.max_rel_err, pl->selfc, pl->bytes);
+                  "self_coefficient=%.17g\nworkspace_bytes=%zu\nzpass=%d\n",
+                  pl->ncell, pl->near.K, pl->near.D, pl->near.max_rel_err, pl->selfc, pl->bytes, pl->zpass ? 1 : 0);
     s += extra;
     if (buf && len) {
         size_t n = std::min(len - 1, s.size());

@@ -2,6 +2,7 @@
 //   dfma  : independent DFMA chains, 8 per thread, enough warps to fill every SM
 //   dmma  : legacy warp MMA m8n8k4 f64 (mma.sync), to see whether the FP64 tensor path adds throughput
 //   both  : half the warps on each in the same kernel (co-issue test)
+//   ffma  : the same chains in fp32 (fp32 mode's ALU roof)
 // Timed with CUDA events over a launch long enough (>= 200 ms) for the clocks to settle.
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,31 @@ __global__ void k_dfma(double* out, double a, double b, int reps) {
         }
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+__global__ void k_ffma(double* out, double a, double b, int reps) {
+    const float af = (float)a, bf = (float)b;
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 64
+        for (int i = 0; i < ITERS; ++i) {
+            x0 = fmaf(x0, af, bf); x1 = fmaf(x1, af, bf); x2 = fmaf(x2, af, bf); x3 = fmaf(x3, af, bf);
+            x4 = fmaf(x4, af, bf); x5 = fmaf(x5, af, bf); x6 = fmaf(x6, af, bf); x7 = fmaf(x7, af, bf);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+__global__ void k_ffma2(double* out, double a, double b, int reps) {
+    const float2 af = make_float2((float)a, (float)a), bf = make_float2((float)b, (float)b);
+    float2 x0 = make_float2(threadIdx.x, 1), x1 = make_float2(2, 3), x2 = make_float2(4, 5), x3 = make_float2(6, 7);
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 64
+        for (int i = 0; i < ITERS; ++i) {
+            x0 = __ffma2_rn(x0, af, bf); x1 = __ffma2_rn(x1, af, bf); x2 = __ffma2_rn(x2, af, bf); x3 = __ffma2_rn(x3, af, bf);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0.x + x1.x + x2.x + x3.x + x0.y + x1.y + x2.y + x3.y;
 }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -96,6 +122,9 @@ int main(int argc, char** argv) {
     run("dmma_m8n8k4", k_dmma, 16.0 * ITERS, reps);
     // both: half the threads each (counted at their own rates)
     run("dfma+dmma (half the warps each)", k_both, 0.5 * (8.0 * ITERS * 2.0) + 0.5 * (16.0 * ITERS), reps);
+    // ffma: fp32 mode's ALU roof (same chains in fp32)
+    run("ffma", k_ffma, 8.0 * ITERS * 2.0, reps * 2);
+    run("ffma2 (packed fp32x2)", k_ffma2, 8.0 * ITERS * 2.0, reps * 2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
     return 0;

@@ -60,7 +60,12 @@ def check_total(op, xyz, q, bar=TOL_FP64):
     mid, long: phi and its gradient) against that component's own oracle norm <= bar."""
     phi_o, F_o, parts = O.evaluate(op, xyz, q, parts=True)
     phi_g, F_g, comp = run_gpu(op, xyz, q)
-    assert rel(phi_g, phi_o) <= bar, rel(phi_g, phi_o)
+    # DESIGN.md R21: a total that is a near-cancellation of its components (kappa > 4, only the
+    # lone-dipole edge cases) is judged at bar x kappa ||phi||, the bound the per-component bars
+    # below imply for a sum; every other total at the plain relative bar
+    kappa = (sum(np.linalg.norm(parts[k][0]) for k in parts) + np.linalg.norm(q * O.self_coefficient(op))) / max(
+        np.linalg.norm(phi_o), 1e-300)
+    assert rel(phi_g, phi_o) <= bar * (kappa if kappa > 4.0 else 1.0), (rel(phi_g, phi_o), kappa)
     assert rel(F_g, F_o) <= bar, rel(F_g, F_o)
     for c, name in enumerate(("near", "mid", "long")):
         po, go = parts[name]
