@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libsog.so")
-SOURCES = ["sog_api.cu", "mid.cu", "long.cu", "dft.cu", "fft.cu", "scan.cu", "plan.cpp"]
+SOURCES = ["sog_api.cu", "mid.cu", "long.cu", "dft.cu", "fft.cu", "near.cu", "scan.cu", "plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = (["-DSOG_ASSERTS"] if os.environ.get("SOG_ASSERTS") else []) + ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

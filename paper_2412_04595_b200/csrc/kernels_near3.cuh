@@ -25,23 +25,54 @@ struct Near3Args {
 
 constexpr int NEAR3_WARPS = 4;
 
+// F(u), dF/du from the piecewise table (R16) in shared memory
 template <int D>
-__device__ __forceinline__ void near_pair(const double* tab, const Near3Args& a, const d4& pi, int code,
+struct NearTab {
+    const double* tab;
+    int K;
+    double du, inv_du;
+    __device__ __forceinline__ void operator()(double u, double& F, double& dF) const {
+        const int kk = min(K - 1, (int)(u * inv_du));
+        const double d = u - (kk + 0.5) * du;
+        const double* cf = tab + kk * (D + 1);
+        F = cf[D];
+        dF = 0.0;
+#pragma unroll
+        for (int n = D - 1; n >= 0; --n) {
+            dF = fma(dF, d, F);
+            F = fma(F, d, cf[n]);
+        }
+    }
+};
+
+// F(u), dF/du from one polynomial in t = u inv_h - 1 (R16-G): the same coefficients for every lane
+template <int D>
+struct NearPolyArg {
+    double c[D + 1];
+    double inv_h;
+    __device__ __forceinline__ void operator()(double u, double& F, double& dF) const {
+        const double t = fma(u, inv_h, -1.0);
+        F = c[D];
+        double g = 0.0;
+#pragma unroll
+        for (int n = D - 1; n >= 0; --n) {
+            g = fma(g, t, F);
+            F = fma(F, t, c[n]);
+        }
+        dF = g * inv_h;
+    }
+};
+
+template <class KF>
+__device__ __forceinline__ void near_pair(const KF& kf, const Near3Args& a, const d4& pi, int code,
                                           const double2* shift, double& phi, double& gx, double& gy, double& gz) {
     const d4 s = ld_d4(&a.pos[code >> 4]);
     const double2 sh = shift[code & 15];
     const double dx = pi.x - (s.x + sh.x), dy = pi.y - (s.y + sh.y), dz = pi.z - s.z;
     const double u = fma(dx, dx, fma(dy, dy, dz * dz));
     if (!(u < a.rc2 && u > 0.0)) return;        // exact fp64 decision (the fp32 test is a superset)
-    const int kk = min(a.K - 1, (int)(u * a.inv_du));
-    const double d = u - (kk + 0.5) * a.du;
-    const double* cf = tab + kk * (D + 1);
-    double F = cf[D], dF = 0.0;
-#pragma unroll
-    for (int n = D - 1; n >= 0; --n) {
-        dF = fma(dF, d, F);
-        F = fma(F, d, cf[n]);
-    }
+    double F, dF;
+    kf(u, F, dF);
     const double rinv = rsqrt(u);
     phi = fma(s.w, rinv - F, phi);
     const double cc = s.w * (-rinv * rinv * rinv - 2.0 * dF);
@@ -50,11 +81,11 @@ __device__ __forceinline__ void near_pair(const double* tab, const Near3Args& a,
     gz = fma(cc, dz, gz);
 }
 
-template <int D>
-__global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
+template <int D, int PD = 0>
+__global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a, NearPolyArg<PD == 0 ? 1 : PD> poly = {}) {
     extern __shared__ double sm[];
-    double* tab = sm;                                                   // [K*(D+1)]
-    double2* shift = reinterpret_cast<double2*>(sm + ((a.K * (D + 1) + 1) & ~1));   // [9]
+    double* tab = sm;                                                   // [K*(D+1)] (PD == 0)
+    double2* shift = reinterpret_cast<double2*>(sm + (PD == 0 ? ((a.K * (D + 1) + 1) & ~1) : 0));   // [9]
     int* lists = reinterpret_cast<int*>(shift + 10);                    // [warps][160]
     // staged sources in 64-wide blocks, candidate q = 64 b + 32 h + l stored as
     //   sxy[b][l] = (x_h0, x_h1, y_h0, y_h1), sz[b][l] = (z_h0, z_h1), sc[b][l] = (code_h0, code_h1)
@@ -68,7 +99,8 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
     const int t0 = a.start[c], t1 = a.start[c + 1];
     if (t0 == t1) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = a.cF[t];
+    if (PD == 0)
+        for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = a.cF[t];
     if (threadIdx.x < 9) {
         const int k = threadIdx.x, ux = cx + k / 3 - 1, uy = cy + k % 3 - 1;
         shift[k] = make_double2(!g.px ? 0.0 : (ux < 0 ? -g.Lx : (ux >= g.ncx ? g.Lx : 0.0)),
@@ -160,11 +192,15 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a) {
                 __syncwarp();
                 while (npend >= 32) {                    // evaluate 32 pending pairs, all lanes busy
                     npend -= 32;
-                    near_pair<D>(tab, a, pi, wl[npend + lane], shift, phi, gx, gy, gz);
+                    if constexpr (PD == 0) near_pair(NearTab<D>{tab, a.K, a.du, a.inv_du}, a, pi, wl[npend + lane], shift, phi, gx, gy, gz);
+                    else near_pair(poly, a, pi, wl[npend + lane], shift, phi, gx, gy, gz);
                 }
                 __syncwarp();
             }
-            if (lane < npend) near_pair<D>(tab, a, pi, wl[lane], shift, phi, gx, gy, gz);
+            if (lane < npend) {
+                if constexpr (PD == 0) near_pair(NearTab<D>{tab, a.K, a.du, a.inv_du}, a, pi, wl[lane], shift, phi, gx, gy, gz);
+                else near_pair(poly, a, pi, wl[lane], shift, phi, gx, gy, gz);
+            }
             // 4-value butterfly; lanes 0..3 hold phi, gx, gy, gz
             const bool b1 = lane & 1;
             double k0v = b1 ? gx : phi, k1v = b1 ? gz : gy;

@@ -26,6 +26,13 @@ size_t mid_gather_smem(int P);
 int launch_zfft_transpose(const void* in, void* out, int nz, long long M, int Izs, int z0, bool fwd, bool f32,
                           cudaStream_t st);
 struct FftStages;
+struct Near4Args;
+struct Near3Args;
+struct NearPoly;
+int launch_near3p(const Near3Args& a, const NearPoly& p, int ncell, cudaStream_t st);
+// target-stationary near field (kernels_near4.cuh): 1 = unsupported degree / warps
+int launch_near4(const Near4Args& a, const NearPoly& p, int nw, cudaStream_t st);
+size_t near4_smem(int cap, int nw);
 // shared-memory FFT (kernels_fft.cuh): stage plan + twiddles (false: length not supported)
 bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw);
 // z pass of the mid solver: FFT along z, S5 scaling, inverse FFT, in place on the plane spectra

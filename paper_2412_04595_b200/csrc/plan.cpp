@@ -305,6 +305,87 @@ bool validate_params(const Params& p, std::string& err) {
     return true;
 }
 
+// R16-G (k_near4): ONE polynomial for F(u) on [0, r_c^2], so every lane evaluates the same
+// coefficients (kernel-parameter / constant-bank operands, no table lookups).  The degree-D
+// Chebyshev interpolant of F in t = 2u/r_c^2 - 1 (long double, D + 1 first-kind nodes) is
+// re-expanded in powers of t (long double) and rounded once; F and dF/dt come from one joint
+// Horner.  The monomial form keeps sum |c_n| = F(0) (an alternating series for a sum of decaying
+// exponentials), so Horner loses nothing.  D = the smallest supported degree whose F and F'
+// errors on a dense sample are <= 1e-15 of F(0) and of max |F'| (validated, long double).
+bool build_near_poly(const Params& p, NearPoly& t) {
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const long double umax = (long double)p.rc * p.rc, h = umax / 2;
+    auto Fl = [&](long double u, long double* dF) {
+        long double F = 0, d = 0;
+        for (int l = 0; l <= p.M; ++l) {
+            const long double a = 1.0L / ((long double)s[l] * s[l]);
+            const long double e = (long double)w[l] * expl(-u * a);
+            F += e;
+            d -= e * a;
+        }
+        if (dF) *dF = d;
+        return F;
+    };
+    long double dF0 = 0;
+    const long double F0 = Fl(0, &dF0);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int D : {16, 20, 24, 28, 32, 40, 48, 56}) {
+        if (D > NEAR_POLY_DMAX) break;
+        const int n1 = D + 1;
+        std::vector<long double> f(n1), a(n1), mono(n1 + 1, 0.0L), Tm(n1 + 1), Tc(n1 + 1), Tn(n1 + 1);
+        for (int i = 0; i < n1; ++i) f[i] = Fl(h * (1.0L + cosl((i + 0.5L) * pi / n1)), nullptr);
+        for (int n = 0; n < n1; ++n) {
+            long double acc = 0;
+            for (int i = 0; i < n1; ++i) acc += f[i] * cosl(n * (i + 0.5L) * pi / n1);
+            a[n] = acc * (n == 0 ? 1.0L : 2.0L) / n1;
+        }
+        std::fill(Tm.begin(), Tm.end(), 0.0L);
+        std::fill(Tc.begin(), Tc.end(), 0.0L);
+        Tm[0] = 1.0L;
+        Tc[1] = 1.0L;
+        mono[0] += a[0];
+        mono[1] += a[1];
+        for (int n = 2; n < n1; ++n) {
+            for (int e = 0; e <= n1; ++e) Tn[e] = (e > 0 ? 2.0L * Tc[e - 1] : 0.0L) - Tm[e];
+            for (int e = 0; e <= n1; ++e) mono[e] += a[n] * Tn[e];
+            Tm.swap(Tc);
+            Tc.swap(Tn);
+        }
+        NearPoly q;
+        q.D = D;
+        q.inv_h = double(1.0L / h);
+        long double cond = 0;
+        for (int n = 0; n <= D; ++n) {
+            q.c[n] = double(mono[n]);
+            cond += fabsl(mono[n]);
+        }
+        // validation in the arithmetic the kernel uses (double Horner) against the long-double sum
+        double eF = 0, edF = 0, mdF = 0;
+        for (int i = 0; i <= 4000; ++i) {
+            const double u = double(umax) * i / 4000.0;
+            const double tt = u * q.inv_h - 1.0;
+            double F = q.c[D], dF = 0;
+            for (int n = D - 1; n >= 0; --n) {
+                dF = dF * tt + F;
+                F = F * tt + q.c[n];
+            }
+            long double dFe = 0;
+            const long double Fe = Fl(u, &dFe);
+            eF = std::max(eF, double(fabsl((long double)F - Fe)));
+            edF = std::max(edF, double(fabsl((long double)(dF * q.inv_h) - dFe)));
+            mdF = std::max(mdF, double(fabsl(dFe)));
+        }
+        q.err_F = eF / double(F0);
+        q.err_dF = edF / mdF;
+        if (q.err_F <= 1e-15 && q.err_dF <= 1e-15 && cond <= 2.0L * F0) {
+            t = q;
+            return true;
+        }
+    }
+    return false;
+}
+
 bool build_near_table(const Params& p, NearTable& t, std::string& err) {
     // F(u) = sum_l w_l exp(-u/s_l^2) (Eq. eq::SOGField) as piecewise Taylor polynomials
     // in u = r^2 on [0, r_c^2]; pieces narrow enough that du/(2 s_0^2) <= 1/4 (R16).

@@ -28,6 +28,7 @@
 #include "launch.h"
 #include "kernels_near.cuh"
 #include "kernels_near3.cuh"
+#include "kernels_near4.cuh"
 #include "kernels_sort.cuh"
 #include "sog_internal.h"
 
@@ -110,6 +111,10 @@ struct sog_plan {
     int ncell = 0;
     int offx[3] = {0, 0, 0}, noffx = 0, offy[3] = {0, 0, 0}, noffy = 0;
     NearTable near;
+    NearPoly npoly;                 // R16-G single polynomial (k_near4), when near4 is set
+    bool near4 = false;
+    int near_mode = 5;              // SOG_NEAR: 3 (table, k_near3), 4 (k_near4), 5 (k_near3 + polynomial: default)
+    int n4_kc = 1, n4_nw = 1, n4_cap = 0;
     double selfc = 0;
     cudaStream_t stream = nullptr;
     unsigned flags = 0;
@@ -304,6 +309,22 @@ int setup(sog_plan* pl) {
     offs(g.ncy, pl->offy, pl->noffy);
     std::string err;
     if (!build_near_table(p, pl->near, err)) return fail(SOG_EINVAL, err);
+    // target-stationary near field (k_near4) when the single polynomial validates and the cell grid
+    // has >= 3 cells per periodic axis (SOG_NEAR=3: the warp-per-target k_near3 instead)
+    {
+        const char* env = std::getenv("SOG_NEAR");
+        pl->near_mode = env ? std::atoi(env) : 5;
+        if (pl->near_mode != 3 && !pl->f32 && g.ncx >= 3 && g.ncy >= 3 && build_near_poly(p, pl->npoly)) {
+            const double m = std::max(1.0, double(pl->Ncap) / pl->ncell);       // mean particles per cell
+            pl->n4_kc = std::max(1, std::min(g.ncz, int(140.0 / m)));
+            pl->n4_nw = std::max(1, std::min(N4_MAXW, int(std::ceil(pl->n4_kc * m / 32.0))));
+            const double expect = 3.0 * 3.0 * (pl->n4_kc + 2 * g.nzr) * m;       // staged records
+            const int capmax = std::min(65535, int((227 * 1024 - sizeof(unsigned short) * (size_t)pl->n4_nw * N4_Q * 32) / 44));
+            // expectation + 4 sigma (uniform input; rare overflows run in pieces)
+            pl->n4_cap = std::max(256, std::min(capmax, int(expect + 4.0 * std::sqrt(expect) + 64)) & ~3);
+            pl->near4 = true;
+        }
+    }
     int rc;
     if ((rc = dalloc(pl, &pl->pos, N)) || (rc = dalloc(pl, &pl->pos_s, N)) || (rc = dalloc(pl, &pl->o_near, N)) ||
         (rc = dalloc(pl, &pl->o_mid, N)) || (rc = dalloc(pl, &pl->o_long, N)) || (rc = dalloc(pl, &pl->cell, N)) ||
@@ -676,6 +697,7 @@ int st_near(sog_plan* pl) {
     const Params& p = pl->p;
     const int N = pl->Ncur;
     cudaStream_t st = pl->stream;
+    int rc;
     if (N == 0) return SOG_OK;
     const int D = pl->near.D;
     if (D != NEAR_D) return fail(SOG_EINVAL, "near table degree");
@@ -690,6 +712,24 @@ int st_near(sog_plan* pl) {
                     sizeof(float4) * a.cap;
         CK(cudaFuncSetAttribute(k_near3f<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_near3f<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+    } else if (pl->near4 && pl->near_mode == 5) {   // k_near3 with the single polynomial (R16-G)
+        Near3Args a;
+        a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
+        a.K = pl->near.K; a.du = pl->near.du; a.inv_du = pl->near.inv_du; a.rc2 = p.rc * p.rc;
+        a.g = pl->geo;
+        a.cap = 1536;
+        a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+        if ((rc = lchk(launch_near3p(a, pl->npoly, pl->ncell, st)))) return rc;
+    } else if (pl->near4) {   // k_near4: target-stationary, one polynomial (R16-G)
+        Near4Args a;
+        a.pos = pl->pos_s; a.start = pl->start; a.out = pl->o_near;
+        a.g = pl->geo;
+        a.rc2 = p.rc * p.rc;
+        a.rc2f = (float)(a.rc2 * (1.0 + 1e-6)) + 1e-4f;
+        a.rcz = (float)(p.rc * (1.0 + 1e-6)) + 1e-4f;
+        a.kc = pl->n4_kc;
+        a.cap = pl->n4_cap;
+        if ((rc = lchk(launch_near4(a, pl->npoly, pl->n4_nw, st)))) return rc;
     } else if (pl->geo.ncx >= 3 && pl->geo.ncy >= 3 && N < (1 << 27)) {   // k_near3: warp per target
         Near3Args a;
         a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
@@ -1123,11 +1163,13 @@ int sog_last_energy(sog_plan* pl, double* U) {
 int sog_plan_describe(const sog_plan* pl, char* buf, size_t len) {
     if (!pl) return fail(SOG_EINVAL, "null plan");
     std::string s = describe(pl->p);
-    char extra[512];
+    char extra[1024];
     std::snprintf(extra, sizeof extra,
                   "ncell=%d\nnear_table_pieces=%d\nnear_table_degree=%d\nnear_table_max_rel_err=%.3e\n"
-                  "self_coefficient=%.17g\nworkspace_bytes=%zu\nzpass=%d\n",
-                  pl->ncell, pl->near.K, pl->near.D, pl->near.max_rel_err, pl->selfc, pl->bytes, pl->zpass ? 1 : 0);
+                  "self_coefficient=%.17g\nworkspace_bytes=%zu\nzpass=%d\nnear_kernel=%d\nnear_poly_degree=%d\n"
+                  "near_poly_err_F=%.3e\nnear_poly_err_dF=%.3e\n",
+                  pl->ncell, pl->near.K, pl->near.D, pl->near.max_rel_err, pl->selfc, pl->bytes, pl->zpass ? 1 : 0,
+                  pl->near4 ? pl->near_mode : 3, pl->npoly.D, pl->npoly.err_F, pl->npoly.err_dF);
     s += extra;
     if (buf && len) {
         size_t n = std::min(len - 1, s.size());

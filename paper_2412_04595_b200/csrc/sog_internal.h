@@ -74,6 +74,16 @@ struct NearTable {
     double max_rel_err = 0;    // validated at plan time against the direct sum
 };
 bool build_near_table(const Params& p, NearTable& t, std::string& err);
+// R16-G: one polynomial of degree D <= NEAR_POLY_DMAX in t = 2u/r_c^2 - 1 for F(u) on [0, r_c^2]
+// (monomial coefficients c[0..D]); false when no supported degree meets the 1e-15 validation
+constexpr int NEAR_POLY_DMAX = 56;
+struct NearPoly {
+    int D = 0;
+    double inv_h = 0;            // dt/du
+    double c[NEAR_POLY_DMAX + 1] = {};
+    double err_F = 0, err_dF = 0;
+};
+bool build_near_poly(const Params& p, NearPoly& t);
 
 // Mid-range scaling tables: mult(k) = sum_{l<=m} A_l Tx[l][ix] Ty[l][iy] Tz[l][iz] (R12);
 // Ty covers the half axis iy < Iy/2+1, Tx and Tz the full axes (fftfreq order).
