@@ -483,19 +483,62 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
     axis(p.Izs, p.Lzs(), p.hz(), false, Tz);
 }
 
+// K_ab(kdot) accumulated in long double: pi sum_{l>m} w_l s_l^2 exp(-s_l^2 k^2/4) E_l(z_a - z_b) without the
+// window / normalisation factors (R9, R10).  The T-basis transform K~ = C^T K C below concentrates the
+// smooth K into low orders; double rounding of K_ab would leave ~1e-15 absolute noise in every K~
+// entry, which the gather's T'_n (~n^2) amplifies in the forces, so the whole chain is long double
+// and K~ is rounded once.
+static const long double kPiL = 3.141592653589793238462643383279502884L;
+static long double long_kab(const Params& p, const std::vector<double>& w, const std::vector<double>& s,
+                            long double za, long double zb, double k2) {
+    const long double d2 = (za - zb) * (za - zb);
+    long double acc = 0.0L;
+    for (int l = p.m + 1; l <= p.M; ++l) {
+        const long double ss = (long double)s[l] * s[l];
+        if (k2 == 0.0) {
+            acc += (long double)w[l] * ss * expm1l(-d2 / ss);
+        } else {
+            const long double g = ss * k2 / 4.0L;
+            if (g > 11000.0L) continue;
+            acc += (long double)w[l] * ss * expl(-g - d2 / ss);
+        }
+    }
+    return acc;
+}
+static void cheb_matrix_l(int P, std::vector<long double>& C) {   // L_b(x) = sum_n C[b][n] T_n(x)
+    C.resize(size_t(P) * P);
+    for (int b = 0; b < P; ++b)
+        for (int n = 0; n < P; ++n)
+            C[size_t(b) * P + n] = (n == 0 ? 1.0L : 2.0L * cosl(n * (b + 0.5L) * kPiL / P)) / P;
+}
+static void cheb_transform(int P, const std::vector<long double>& Kl, const std::vector<long double>& C, double* out) {
+    std::vector<long double> KC(size_t(P) * P, 0.0L);
+    for (int a = 0; a < P; ++a)
+        for (int n = 0; n < P; ++n) {
+            long double t = 0.0L;
+            for (int b = 0; b < P; ++b) t += Kl[size_t(a) * P + b] * C[size_t(b) * P + n];
+            KC[size_t(a) * P + n] = t;
+        }
+    for (int m = 0; m < P; ++m)
+        for (int n = 0; n < P; ++n) {
+            long double t = 0.0L;
+            for (int a = 0; a < P; ++a) t += C[size_t(a) * P + m] * KC[size_t(a) * P + n];
+            out[size_t(m) * P + n] = double(t);
+        }
+}
+
 void build_long_kernel(const Params& p, std::vector<double>& K) {
     // K_ab(kdot) = pi sum_{l=m+1}^{M} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b) / (W_x W_y)^2,
     // E_l(d) = exp(-d^2/s_l^2) for kdot != 0 and expm1(-d^2/s_l^2) at kdot = 0 (R10).
     std::vector<double> w, s;
     sog_weights(p, w, s);
     const int P = p.Pc, nx = p.Ilx, ny = p.Ily / 2 + 1;
-    std::vector<double> za(P);
-    for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
     const int Pw = p.window != 0 ? p.Pl : p.Pl - 1;   // support width in mesh steps (R6 / R6-KB)
     const double Hx = Pw * p.hlx() / 2.0, Hy = Pw * p.hly() / 2.0;
     K.assign(size_t(nx) * ny * P * P, 0.0);
-    std::vector<double> Cm;
-    build_cheb_matrix(P, Cm);
+    std::vector<long double> Cl, zal(P), Kl(size_t(P) * P);
+    cheb_matrix_l(P, Cl);
+    for (int a = 0; a < P; ++a) zal[a] = 0.5L * p.Lz * cosl((a + 0.5L) * kPiL / P);
     for (int ix = 0; ix < nx; ++ix) {
         int fx = ix < (nx + 1) / 2 ? ix : ix - nx;
         double kx = 2.0 * kPi * fx / p.Lx;
@@ -509,37 +552,10 @@ void build_long_kernel(const Params& p, std::vector<double>& K) {
                                       : std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
             // 1/(Ilx Ily) of the (unnormalised) cuFFT inverse is folded in here (R12)
             double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
-            double* Km = &K[(size_t(ix) * ny + iy) * P * P];
+            double* Ko = &K[(size_t(ix) * ny + iy) * P * P];
             for (int a = 0; a < P; ++a)
-                for (int b = 0; b < P; ++b) {
-                    double d2 = (za[a] - za[b]) * (za[a] - za[b]);
-                    double acc = 0.0;
-                    for (int l = p.m + 1; l <= p.M; ++l) {
-                        double ss = s[l] * s[l];
-                        if (k2 == 0.0) {
-                            acc += w[l] * ss * std::expm1(-d2 / ss);
-                        } else {
-                            double g = ss * k2 / 4.0;
-                            if (g > 745.0) continue;
-                            acc += w[l] * ss * std::exp(-g) * std::exp(-d2 / ss);
-                        }
-                    }
-                    Km[a * P + b] = acc * dec;
-                }
-            // T basis (kernels_long.cuh): K~ = C^T K C with L_b(x) = sum_n C[b][n] T_n(x)
-            std::vector<long double> KC(size_t(P) * P, 0.0L);
-            for (int a = 0; a < P; ++a)
-                for (int n = 0; n < P; ++n) {
-                    long double t = 0.0L;
-                    for (int b = 0; b < P; ++b) t += (long double)Km[a * P + b] * Cm[size_t(b) * P + n];
-                    KC[size_t(a) * P + n] = t;
-                }
-            for (int m = 0; m < P; ++m)
-                for (int n = 0; n < P; ++n) {
-                    long double t = 0.0L;
-                    for (int a = 0; a < P; ++a) t += (long double)Cm[size_t(a) * P + m] * KC[size_t(a) * P + n];
-                    Km[m * P + n] = double(t);
-                }
+                for (int b = 0; b < P; ++b) Kl[a * P + b] = long_kab(p, w, s, zal[a], zal[b], k2) * (long double)dec;
+            cheb_transform(P, Kl, Cl, Ko);
         }
     }
 }
@@ -552,48 +568,22 @@ void build_long_kernel_direct(const Params& p, std::vector<double>& K) {
     std::vector<double> w, s;
     sog_weights(p, w, s);
     const int P = p.Pc, nx = 2 * p.Kx + 1, ny = p.Ky + 1;
-    std::vector<double> za(P), Cm;
-    for (int a = 0; a < P; ++a) za[a] = 0.5 * p.Lz * std::cos((a + 0.5) * kPi / P);
-    build_cheb_matrix(P, Cm);
+    std::vector<long double> Cl, zal(P), Kl(size_t(P) * P);
+    cheb_matrix_l(P, Cl);
+    for (int a = 0; a < P; ++a) zal[a] = 0.5L * p.Lz * cosl((a + 0.5L) * kPiL / P);
     K.assign(size_t(nx) * ny * P * P, 0.0);
-    std::vector<double> Km(size_t(P) * P);
     for (int ix = 0; ix < nx; ++ix) {
         const double kx = 2.0 * kPi * (ix - p.Kx) / p.Lx;
         for (int iy = 0; iy < ny; ++iy) {
             const double ky = 2.0 * kPi * iy / p.Ly, k2 = kx * kx + ky * ky;
             for (int a = 0; a < P; ++a)
-                for (int b = 0; b < P; ++b) {
-                    const double d2 = (za[a] - za[b]) * (za[a] - za[b]);
-                    double acc = 0.0;
-                    for (int l = p.m + 1; l <= p.M; ++l) {
-                        const double ss = s[l] * s[l];
-                        if (k2 == 0.0) {
-                            acc += w[l] * ss * std::expm1(-d2 / ss);
-                        } else {
-                            const double g = ss * k2 / 4.0;
-                            if (g > 745.0) continue;
-                            acc += w[l] * ss * std::exp(-g) * std::exp(-d2 / ss);
-                        }
-                    }
-                    Km[a * P + b] = acc * kPi / (p.Lx * p.Ly);
-                }
-            double* Ko = &K[(size_t(ix) * ny + iy) * P * P];
-            std::vector<long double> KC(size_t(P) * P, 0.0L);
-            for (int a = 0; a < P; ++a)
-                for (int n = 0; n < P; ++n) {
-                    long double t = 0.0L;
-                    for (int b = 0; b < P; ++b) t += (long double)Km[a * P + b] * Cm[size_t(b) * P + n];
-                    KC[size_t(a) * P + n] = t;
-                }
-            for (int m = 0; m < P; ++m)
-                for (int n = 0; n < P; ++n) {
-                    long double t = 0.0L;
-                    for (int a = 0; a < P; ++a) t += (long double)Cm[size_t(a) * P + m] * KC[size_t(a) * P + n];
-                    Ko[m * P + n] = double(t);
-                }
+                for (int b = 0; b < P; ++b)
+                    Kl[a * P + b] = long_kab(p, w, s, zal[a], zal[b], k2) * (kPiL / ((long double)p.Lx * p.Ly));
+            cheb_transform(P, Kl, Cl, &K[(size_t(ix) * ny + iy) * P * P]);
         }
     }
 }
+
 
 double kb_hat(double k, double H, double beta) {
     // int_{-H}^{H} I0(beta sqrt(1 - (x/H)^2)) / I0(beta) e^{-ikx} dx
