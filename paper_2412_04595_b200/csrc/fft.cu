@@ -8,14 +8,14 @@
 namespace sog {
 
 // radices (largest first): 8, 7, 5, 4, 3, 2; false when n is not 7-smooth or too long
-bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw) {
+bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw, int E) {
     f = FftStages();
     f.n = n;
     if (n < 1 || n > FFT_MAXE) return false;
     std::vector<int> rs;
     int m = n;
     for (int r : {8, 7, 5, 4, 3, 2})
-        while (m % r == 0) {
+        while (m % r == 0 && (E == 0 || E % r == 0)) {
             rs.push_back(r);
             m /= r;
         }
@@ -86,6 +86,43 @@ int zpass_l(void* X, long long M, int nyh, int zin0, int nin, int zout0, int nou
     if (L <= 48) return zpass_b<T, 48>(X, M, nyh, zin0, nin, zout0, nout, f, tw, L, A, Tx, Ix, Ty, Tz, st);
     if (L <= 64) return zpass_b<T, 64>(X, M, nyh, zin0, nin, zout0, nout, f, tw, L, A, Tx, Ix, Ty, Tz, st);
     return 1;
+}
+
+// register-resident z pass: E elements per thread, every radix of the plan divides E
+template <typename T, int E, int B>
+int zpass_r_go(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+               const void* mult, cudaStream_t st) {
+    using C = typename Cplx<T>::C;
+    const int Tc = f.n / E;
+    if (f.n % E || B * Tc > 512) return 1;
+    for (int s = 0; s < f.nst; ++s)
+        if (E % f.R[s]) return 1;
+    const size_t sh = sizeof(C) * (size_t)f.n * B;
+    if (cudaFuncSetAttribute(k_zpass_r<T, E, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+        return 2;
+    k_zpass_r<T, E, B><<<(unsigned)((M + B - 1) / B), B * Tc, sh, st>>>((C*)X, M, zin0, nin, zout0, nout, f,
+                                                                     (const C*)tw, (const T*)mult);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_zpass_r(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+                   const void* mult, bool f32, int E, int B, cudaStream_t st) {
+#define SOG_ZR(EE, BB)                                                                                          \
+    if (E == EE && B == BB)                                                                                     \
+        return f32 ? zpass_r_go<float, EE, BB>(X, M, zin0, nin, zout0, nout, f, tw, mult, st)                   \
+                   : zpass_r_go<double, EE, BB>(X, M, zin0, nin, zout0, nout, f, tw, mult, st);
+    SOG_ZR(10, 2) SOG_ZR(10, 4) SOG_ZR(8, 2) SOG_ZR(8, 4) SOG_ZR(12, 2) SOG_ZR(12, 4) SOG_ZR(16, 2) SOG_ZR(16, 4)
+#undef SOG_ZR
+    return 1;
+}
+
+int build_mult_table(void* out, long long M, int nyh, int Izs, int L, const double* A, const double* Tx, int Ix,
+                     const double* Ty, const double* Tz, bool f32, void* tmp, cudaStream_t st) {
+    const long long n = M * Izs;
+    double* d = f32 ? (double*)tmp : (double*)out;
+    k_mult_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d, M, nyh, Izs, L, A, Tx, Ix, Ty, Tz);
+    if (f32) k_mult_table_f<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((float*)out, d, n);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
 int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, int nout, const FftStages& f,

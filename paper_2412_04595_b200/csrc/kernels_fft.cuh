@@ -300,3 +300,142 @@ __global__ void __launch_bounds__(FFT_NTHR, 2) k_zpass(typename Cplx<T>::C* __re
 }
 
 }  // namespace sog
+
+namespace sog {
+
+// ---------------------------------------------------------------------------------------
+// Register-resident z pass (k_zpass_r).  Thread (b, tau) of a CTA owns the E elements
+// x[tau + Tc k], k < E (Tc = n / E) of column b for the whole transform.  A Stockham stage of radix
+// R (R | E) is E / R butterflies on the thread's own registers (butterfly j = tau + Tc u reads
+// x[j + r n/R] = register u + r E/R); its outputs go to shared memory in natural order and the next
+// stage reads its E registers back (one exchange per stage, two barriers).  After the last
+// forward stage the outputs a thread holds are again x[tau + Tc k] (Ns R = n), so the S5 multiply
+// and the first inverse stage need no exchange, and the inverse's last stage stores its registers
+// straight to the output rows.  The twiddles come from the host table through L1 (__ldg).
+template <int R, int E, int B, typename C>
+__device__ __forceinline__ void zr_stage(C (&x)[E], C* buf, int tau, int Tc, int b, int Ns, unsigned mNs,
+                                         const C* __restrict__ tw, bool last) {
+    constexpr int U = E / R;
+    static_assert(E % R == 0, "radix must divide the elements per thread");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        C v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = x[u + r * U];
+        const int j = tau + Tc * u;
+        const int q = Ns > 1 ? (int)__umulhi((unsigned)j, mNs) : j;
+        const int jk = j - q * Ns;
+        if (Ns > 1) {
+            const C* w = tw + jk * (R - 1);
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&w[r - 1]));
+        }
+        dft_small<R>(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[u + r * U] = v[r];
+    }
+    if (last) return;                       // outputs already at tau + Tc k (see above)
+    __syncthreads();                        // the previous exchange's reads are done
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = tau + Tc * u;
+        const int q = Ns > 1 ? (int)__umulhi((unsigned)j, mNs) : j;
+        const int jk = j - q * Ns;
+        const int dst = q * R * Ns + jk;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[(dst + r * Ns) * B + b] = x[u + r * U];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = buf[(tau + Tc * k) * B + b];
+}
+
+template <int E, int B, typename C>
+__device__ __forceinline__ void zr_fft(C (&x)[E], C* buf, int tau, int Tc, int b, const FftStages& f,
+                                       const C* __restrict__ tw) {
+    int s = 0;
+#define SOG_ZR_LOOP(RR)                                                                                         \
+    if constexpr (E % RR == 0)                                                                                  \
+        for (; s < f.nst && f.R[s] == RR; ++s)                                                                  \
+            zr_stage<RR, E, B>(x, buf, tau, Tc, b, f.Ns[s], f.mNs[s], tw + f.tw[s], s == f.nst - 1);
+    SOG_ZR_LOOP(8)
+    SOG_ZR_LOOP(7)
+    SOG_ZR_LOOP(5)
+    SOG_ZR_LOOP(4)
+    SOG_ZR_LOOP(3)
+    SOG_ZR_LOOP(2)
+#undef SOG_ZR_LOOP
+}
+
+template <typename T, int E, int B>
+__global__ void __launch_bounds__(512) k_zpass_r(typename Cplx<T>::C* __restrict__ X, long long M, int zin0, int nin,
+                                                 int zout0, int nout, FftStages f,
+                                                 const typename Cplx<T>::C* __restrict__ tw,
+                                                 const T* __restrict__ mult) {
+    using C = typename Cplx<T>::C;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* buf = reinterpret_cast<C*>(smraw);                 // [n][B] exchange buffer
+    const int n = f.n, Tc = n / E;
+    const int t = threadIdx.x, b = t & (B - 1), tau = t / B;   // blockDim.x == B * Tc
+    const long long m0 = (long long)blockIdx.x * B;
+    const bool col = m0 + b < M;
+    const size_t stride = (size_t)Tc * M;                 // rows tau + Tc k, k = 0, 1, ...
+    C x[E];
+    {
+        const C* src = X + (size_t)tau * M + m0 + b - (size_t)zin0 * M;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int z = tau + Tc * k;
+            C v;
+            v.x = T(0);
+            v.y = T(0);
+            if (col && z >= zin0 && z < zin0 + nin) v = src[k * stride];
+            x[k] = v;
+        }
+    }
+    zr_fft<E, B>(x, buf, tau, Tc, b, f, tw);
+    // S5 on the registers: mult [kz][m] (plan-time table, R12), conj for the inverse transform
+    {
+        const T* mrow = mult + (size_t)tau * M + m0 + b;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const T m = col ? __ldg(&mrow[k * stride]) : T(0);
+            x[k].x *= m;
+            x[k].y *= -m;
+        }
+    }
+    zr_fft<E, B>(x, buf, tau, Tc, b, f, tw);
+    if (col) {
+        C* dst = X + (size_t)tau * M + m0 + b - (size_t)zout0 * M;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int z = tau + Tc * k;
+            if (z >= zout0 && z < zout0 + nout) {
+                C v = x[k];
+                v.y = -v.y;
+                dst[k * stride] = v;
+            }
+        }
+    }
+}
+
+// S5 multiplier table mult[kz][m] = sum_{l < L} A_l Tx_l(x) Ty_l(ky) Tz_l(kz), m = x nyh + ky (R12),
+// written once at plan time for the register-resident z pass
+static __global__ void k_mult_table(double* __restrict__ out, long long M, int nyh, int Izs, int L, const double* __restrict__ A,
+                             const double* __restrict__ Tx, int Ix, const double* __restrict__ Ty,
+                             const double* __restrict__ Tz) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M * Izs) return;
+    const int kz = int(e / M);
+    const long long m = e - (long long)kz * M;
+    const int x = int(m / nyh), ky = int(m - (long long)x * nyh);
+    double v = 0.0;
+    for (int l = 0; l < L; ++l) v = fma(A[l] * Tx[(size_t)l * Ix + x], Ty[(size_t)l * nyh + ky] * Tz[(size_t)l * Izs + kz], v);
+    out[e] = v;
+}
+static __global__ void k_mult_table_f(float* __restrict__ out, const double* __restrict__ in, long long n) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) out[e] = (float)in[e];
+}
+
+}  // namespace sog

@@ -15,6 +15,7 @@
 #pragma once
 #include <cuComplex.h>
 #include <type_traits>
+#include <utility>
 #include "kernels_common.cuh"
 
 namespace sog {
@@ -466,10 +467,10 @@ struct GRing {
     static constexpr int D = MZ_ZC + P - 1;                       // planes a chunk reads
     static constexpr int DR = D + MZ_ZC;                          // ring: + the next chunk's planes (prefetch)
     static constexpr int AL = 16 / int(sizeof(T));
-    // [Wx Wy Wz | d0x d0y d0z] (Gaussian: W' from W and d0) or [Wx Wy Wz | W'x W'y W'z] (KB), then hdr
-    static constexpr int HOFF = (((KB ? 6 * P : 3 * P + 3) + AL - 1) / AL) * AL;
+    // [Wx Wy Wz | W'x W'y W'z] (dW/dx of the particle, R11), then the int4 header
+    static constexpr int HOFF = ((6 * P + AL - 1) / AL) * AL;
     static constexpr int WSZ = HOFF + AL;                         // per-particle weight scratch
-    static constexpr int WB = 4;                                  // particles per warp batch
+    static constexpr int WB = 2;                                  // particles per warp batch
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
     static constexpr size_t BYTES = sizeof(T) * (size_t(DR) * PL + 8 * WB * WSZ);
     static constexpr bool FITS = BYTES <= 227 * 1024;
@@ -493,6 +494,28 @@ __device__ __forceinline__ float lds_t(unsigned a, float) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
     return v;
+}
+
+// shared-memory load at a compile-time byte offset from a 32-bit shared address (one LDS with an
+// immediate offset, no address add)
+template <int OFF>
+__device__ __forceinline__ double lds_off(unsigned a, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ float lds_off(unsigned a, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+// t0 += wz[kz] Psi[kz], t1 += dwz[kz] Psi[kz] over kz = 0..P-1 at plane stride PLB bytes
+template <int PLB, typename T, int... KZ>
+__device__ __forceinline__ void zcontract(unsigned a, const T* wz, const T* dwz, T& t0, T& t1,
+                                          std::integer_sequence<int, KZ...>) {
+    ((t0 = fma(wz[KZ], lds_off<KZ * PLB>(a, T(0)), t0),
+      t1 = fma(dwz[KZ], lds_off<KZ * PLB>(a, T(0)), t1)), ...);
 }
 
 __device__ __forceinline__ void cp_async_wait_all() {
@@ -596,16 +619,19 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                         o[3 * P + i] = T(dw[i] * ih);          // dW/dx = dW/du / h
                     }
                 } else {
+                    // Gaussian recurrence; W' = 2 a (x_g - x) W (R11), stored with W so the gather
+                    // loop reads it instead of every lane recomputing it
                     const double d0 = ((double)sa - hf) * hh - x;
                     double w = exp(-aa * d0 * d0);
                     double q = exp(-aa * hh * (2.0 * d0 + hh));
+                    const double a2 = 2.0 * aa;
 #pragma unroll
                     for (int i = 0; i < P; ++i) {
                         o[i] = T(w);
+                        o[3 * P + i] = T(a2 * (d0 + i * hh) * w);
                         w *= q;
                         q *= gg;
                     }
-                    wsb[pp * G::WSZ + 3 * P + axl] = T(d0);   // for W' = 2 a (d0 + i h) W
                 }
                 if (axl == 0) {
                     int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + G::HOFF);
@@ -616,49 +642,60 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                 }
             }
             __syncwarp();
-            const T ax2 = T(2.0 * a.invH2Sx), ay2 = T(2.0 * a.invH2Sy), az2 = T(2.0 * a.invH2Sz);
-            const T hxT = T(a.hx), hyT = T(a.hy), hzT = T(a.hz);
             for (int pp = 0; pp < nb; ++pp) {
                 const T* wsc = wsb + pp * G::WSZ;
                 const int4 hd = *reinterpret_cast<const int4*>(wsc + G::HOFF);
-                const T d0x = wsc[3 * P], d0y = wsc[3 * P + 1], d0z = wsc[3 * P + 2];
                 T wz[P], dwz[P];
 #pragma unroll
                 for (int i = 0; i < P; ++i) {
                     wz[i] = wsc[2 * P + i];
-                    dwz[i] = KB ? wsc[5 * P + i] : az2 * (d0z + T(i) * hzT) * wz[i];
+                    dwz[i] = wsc[5 * P + i];
                 }
-                // shared byte addresses of the particle's window origin in its P stencil planes
-                unsigned pbS[P];
-                {
-                    int zs = hd.z;
-                    const unsigned o0 = ringS + unsigned(hd.x * WYP + hd.y) * unsigned(sizeof(T));
-#pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        pbS[i] = o0 + unsigned(zs * PL) * unsigned(sizeof(T));
-                        zs = zs + 1 == DR ? 0 : zs + 1;
-                    }
-                }
+                const unsigned o0 = ringS + unsigned(hd.x * WYP + hd.y) * unsigned(sizeof(T));
                 T phi = 0, gx = 0, gy = 0, gz = 0;
-#pragma unroll
-                for (int rr = 0; rr < NR; ++rr) {
-                    if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
-                    const unsigned cS = coffS[rr];
-                    T t0 = 0, t1 = 0;
-#pragma unroll
-                    for (int kz = 0; kz < P; ++kz) {
-                        const T v = lds_t(pbS[kz] + cS, T(0));
-                        t0 = fma(wz[kz], v, t0);
-                        t1 = fma(dwz[kz], v, t1);
-                    }
+                // contraction of one stencil column (z first), then the separable x / y weights
+                auto column = [&](int rr, const T t0, const T t1) {
                     const T wx = wsc[ca[rr]], wy = wsc[P + cbb[rr]];
-                    const T dwx = KB ? wsc[3 * P + ca[rr]] : ax2 * (d0x + T(ca[rr]) * hxT) * wx;
-                    const T dwy = KB ? wsc[4 * P + cbb[rr]] : ay2 * (d0y + T(cbb[rr]) * hyT) * wy;
+                    const T dwx = wsc[3 * P + ca[rr]], dwy = wsc[4 * P + cbb[rr]];
                     const T wxy = wx * wy;
                     phi = fma(wxy, t0, phi);
                     gz = fma(wxy, t1, gz);
                     gx = fma(dwx * wy, t0, gx);
                     gy = fma(wx * dwy, t0, gy);
+                };
+                if (hd.z + P <= DR) {
+                    // the particle's P planes are consecutive ring slots: immediate plane offsets
+                    const unsigned zb = o0 + unsigned(hd.z * PL) * unsigned(sizeof(T));
+#pragma unroll
+                    for (int rr = 0; rr < NR; ++rr) {
+                        if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                        T t0 = 0, t1 = 0;
+                        zcontract<PL * int(sizeof(T))>(zb + coffS[rr], wz, dwz, t0, t1,
+                                                       std::make_integer_sequence<int, P>{});
+                        column(rr, t0, t1);
+                    }
+                } else {
+                    // shared byte addresses of the particle's window origin in its P (wrapped) planes
+                    unsigned pbS[P];
+                    int zs = hd.z;
+#pragma unroll
+                    for (int i = 0; i < P; ++i) {
+                        pbS[i] = o0 + unsigned(zs * PL) * unsigned(sizeof(T));
+                        zs = zs + 1 == DR ? 0 : zs + 1;
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < NR; ++rr) {
+                        if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                        const unsigned cS = coffS[rr];
+                        T t0 = 0, t1 = 0;
+#pragma unroll
+                        for (int kz = 0; kz < P; ++kz) {
+                            const T v = lds_t(pbS[kz] + cS, T(0));
+                            t0 = fma(wz[kz], v, t0);
+                            t1 = fma(dwz[kz], v, t1);
+                        }
+                        column(rr, t0, t1);
+                    }
                 }
                 // 4-value butterfly (fp64): after two levels each lane carries one value
                 const bool b1 = lane & 1;

@@ -34,11 +34,17 @@ int launch_near3p(const Near3Args& a, const NearPoly& p, int ncell, cudaStream_t
 int launch_near4(const Near4Args& a, const NearPoly& p, int nw, cudaStream_t st);
 size_t near4_smem(int cap, int nw);
 // shared-memory FFT (kernels_fft.cuh): stage plan + twiddles (false: length not supported)
-bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw);
+// E > 0: radices restricted to divisors of E (register-resident z pass)
+bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw, int E = 0);
 // z pass of the mid solver: FFT along z, S5 scaling, inverse FFT, in place on the plane spectra
 int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, int nout, const FftStages& f,
                  const void* tw, int L, const double* A, const double* Tx, int Ix, const double* Ty, const double* Tz,
                  bool f32, cudaStream_t st);
+int launch_zpass_r(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+                   const void* mult, bool f32, int E, int B, cudaStream_t st);
+// S5 multiplier table [Izs][M] (fp64, or fp32 through the fp64 scratch tmp)
+int build_mult_table(void* out, long long M, int nyh, int Izs, int L, const double* A, const double* Tx, int Ix,
+                     const double* Ty, const double* Tz, bool f32, void* tmp, cudaStream_t st);
 int launch_scale_pencil_z(void* W, int Ix, int nyh, int Izs, int L, const double* A, const double* Tx,
                           const double* Ty, const double* Tz, bool f32, cudaStream_t st);
 int mid_spread_emax();

@@ -3,7 +3,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <sstream>
+#include <thread>
 
 #include "sog_internal.h"
 
@@ -489,22 +491,6 @@ void build_mid_tables(const Params& p, std::vector<double>& A, std::vector<doubl
 // entry, which the gather's T'_n (~n^2) amplifies in the forces, so the whole chain is long double
 // and K~ is rounded once.
 static const long double kPiL = 3.141592653589793238462643383279502884L;
-static long double long_kab(const Params& p, const std::vector<double>& w, const std::vector<double>& s,
-                            long double za, long double zb, double k2) {
-    const long double d2 = (za - zb) * (za - zb);
-    long double acc = 0.0L;
-    for (int l = p.m + 1; l <= p.M; ++l) {
-        const long double ss = (long double)s[l] * s[l];
-        if (k2 == 0.0) {
-            acc += (long double)w[l] * ss * expm1l(-d2 / ss);
-        } else {
-            const long double g = ss * k2 / 4.0L;
-            if (g > 11000.0L) continue;
-            acc += (long double)w[l] * ss * expl(-g - d2 / ss);
-        }
-    }
-    return acc;
-}
 static void cheb_matrix_l(int P, std::vector<long double>& C) {   // L_b(x) = sum_n C[b][n] T_n(x)
     C.resize(size_t(P) * P);
     for (int b = 0; b < P; ++b)
@@ -527,35 +513,94 @@ static void cheb_transform(int P, const std::vector<long double>& Kl, const std:
         }
 }
 
+// Gaussian part of K~ (T basis, no window / normalisation factor) for every distinct |kdot|^2 of the
+// mode set: K depends on kdot only through |kdot|^2 (E_l(d) is k-independent), so wide grids (the
+// confined s1: 3840 x 1921 modes, ~1.4e6 distinct |k|^2) are built once per value, on all host threads.
+static void long_kernel_unique(const Params& p, const std::vector<long double>& k2u, std::vector<double>& Ku) {
+    std::vector<double> w, s;
+    sog_weights(p, w, s);
+    const int P = p.Pc, L = p.M - p.m;
+    std::vector<long double> Cl, zal(P), E(size_t(L) * P * P), E0(size_t(L) * P * P);
+    cheb_matrix_l(P, Cl);
+    for (int a = 0; a < P; ++a) zal[a] = 0.5L * p.Lz * cosl((a + 0.5L) * kPiL / P);
+    for (int l = 0; l < L; ++l) {
+        const long double ss = (long double)s[p.m + 1 + l] * s[p.m + 1 + l];
+        for (int a = 0; a < P; ++a)
+            for (int b = 0; b < P; ++b) {
+                const long double d2 = (zal[a] - zal[b]) * (zal[a] - zal[b]);
+                E[(size_t(l) * P + a) * P + b] = expl(-d2 / ss);
+                E0[(size_t(l) * P + a) * P + b] = expm1l(-d2 / ss);            // R10 at kdot = 0
+            }
+    }
+    Ku.assign(k2u.size() * P * P, 0.0);
+    const size_t nu = k2u.size();
+    unsigned nth = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    if (nu < 64) nth = 1;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nth; ++t)
+        th.emplace_back([&, t]() {
+            std::vector<long double> Kl(size_t(P) * P);
+            for (size_t u = t; u < nu; u += nth) {
+                const long double k2 = k2u[u];
+                std::fill(Kl.begin(), Kl.end(), 0.0L);
+                for (int l = 0; l < L; ++l) {
+                    const long double ss = (long double)s[p.m + 1 + l] * s[p.m + 1 + l];
+                    const long double g = ss * k2 / 4.0L;
+                    // s_l grows with l: once exp(-g) < 1e-323 every later term rounds to 0 in the double K~
+                    if (k2 != 0.0L && g > 745.0L) break;
+                    const long double f = (long double)w[p.m + 1 + l] * ss * (k2 == 0.0L ? 1.0L : expl(-g));
+                    const long double* El = (k2 == 0.0L ? E0.data() : E.data()) + size_t(l) * P * P;
+                    for (int ab = 0; ab < P * P; ++ab) Kl[ab] += f * El[ab];
+                }
+                cheb_transform(P, Kl, Cl, &Ku[u * P * P]);
+            }
+        });
+    for (auto& x : th) x.join();
+}
+
 void build_long_kernel(const Params& p, std::vector<double>& K) {
     // K_ab(kdot) = pi sum_{l=m+1}^{M} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b) / (W_x W_y)^2,
     // E_l(d) = exp(-d^2/s_l^2) for kdot != 0 and expm1(-d^2/s_l^2) at kdot = 0 (R10).
-    std::vector<double> w, s;
-    sog_weights(p, w, s);
     const int P = p.Pc, nx = p.Ilx, ny = p.Ily / 2 + 1;
     const int Pw = p.window != 0 ? p.Pl : p.Pl - 1;   // support width in mesh steps (R6 / R6-KB)
     const double Hx = Pw * p.hlx() / 2.0, Hy = Pw * p.hly() / 2.0;
-    K.assign(size_t(nx) * ny * P * P, 0.0);
-    std::vector<long double> Cl, zal(P), Kl(size_t(P) * P);
-    cheb_matrix_l(P, Cl);
-    for (int a = 0; a < P; ++a) zal[a] = 0.5L * p.Lz * cosl((a + 0.5L) * kPiL / P);
+    // distinct |kdot|^2 (integer key (fx^2, fy^2) scaled by the box; one key per value when Lx == Ly)
+    const bool sq = p.Lx == p.Ly;
+    std::map<std::pair<long long, long long>, size_t> key;
+    std::vector<long double> k2u;
+    std::vector<size_t> mode_u(size_t(nx) * ny);
     for (int ix = 0; ix < nx; ++ix) {
-        int fx = ix < (nx + 1) / 2 ? ix : ix - nx;
-        double kx = 2.0 * kPi * fx / p.Lx;
+        const long long fx = ix < (nx + 1) / 2 ? ix : ix - nx;
         for (int iy = 0; iy < ny; ++iy) {
-            double ky = 2.0 * kPi * iy / p.Ly;
-            double k2 = kx * kx + ky * ky;
+            const long long a2 = fx * fx, b2 = (long long)iy * iy;
+            const std::pair<long long, long long> kk = sq ? std::make_pair(a2 + b2, 0LL) : std::make_pair(a2, b2);
+            auto it = key.find(kk);
+            if (it == key.end()) {
+                it = key.emplace(kk, k2u.size()).first;
+                const long double kx = 2.0L * kPiL * fx / p.Lx, ky = 2.0L * kPiL * iy / p.Ly;
+                k2u.push_back(kx * kx + ky * ky);
+            }
+            mode_u[size_t(ix) * ny + iy] = it->second;
+        }
+    }
+    std::vector<double> Ku;
+    long_kernel_unique(p, k2u, Ku);
+    K.assign(size_t(nx) * ny * P * P, 0.0);
+    for (int ix = 0; ix < nx; ++ix) {
+        const int fx = ix < (nx + 1) / 2 ? ix : ix - nx;
+        const double kx = 2.0 * kPi * fx / p.Lx;
+        for (int iy = 0; iy < ny; ++iy) {
+            const double ky = 2.0 * kPi * iy / p.Ly;
             // 1 / (W_x W_y)^2
             double Wx = p.window != 0 ? poly_window_hat(p.window, kx, Hx, p.Sl)
                                       : std::sqrt(kPi / p.Sl) * Hx * std::exp(-kx * kx * Hx * Hx / (4.0 * p.Sl));
             double Wy = p.window != 0 ? poly_window_hat(p.window, ky, Hy, p.Sl)
                                       : std::sqrt(kPi / p.Sl) * Hy * std::exp(-ky * ky * Hy * Hy / (4.0 * p.Sl));
-            // 1/(Ilx Ily) of the (unnormalised) cuFFT inverse is folded in here (R12)
-            double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
-            double* Ko = &K[(size_t(ix) * ny + iy) * P * P];
-            for (int a = 0; a < P; ++a)
-                for (int b = 0; b < P; ++b) Kl[a * P + b] = long_kab(p, w, s, zal[a], zal[b], k2) * (long double)dec;
-            cheb_transform(P, Kl, Cl, Ko);
+            // pi and the 1/(Ilx Ily) of the (unnormalised) cuFFT inverse are folded in here (R12)
+            const double dec = kPi / (Wx * Wx * Wy * Wy) / (double(p.Ilx) * p.Ily);
+            const double* src = &Ku[mode_u[size_t(ix) * ny + iy] * P * P];
+            double* dst = &K[(size_t(ix) * ny + iy) * P * P];
+            for (int e = 0; e < P * P; ++e) dst[e] = src[e] * dec;
         }
     }
 }
@@ -565,23 +610,18 @@ void build_cheb_nodes(int Pc, std::vector<double>& Tn) { Tn = node_T(Pc); }
 void build_long_kernel_direct(const Params& p, std::vector<double>& K) {
     // K_ab(kdot) = pi/(Lx Ly) sum_{l>m} w_l s_l^2 exp(-s_l^2 |kdot|^2/4) E_l(z_a - z_b), E_l =
     // exp(-d^2/s_l^2) (expm1 at kdot = 0, R10), then K~ = C^T K C (T basis, as build_long_kernel)
-    std::vector<double> w, s;
-    sog_weights(p, w, s);
     const int P = p.Pc, nx = 2 * p.Kx + 1, ny = p.Ky + 1;
-    std::vector<long double> Cl, zal(P), Kl(size_t(P) * P);
-    cheb_matrix_l(P, Cl);
-    for (int a = 0; a < P; ++a) zal[a] = 0.5L * p.Lz * cosl((a + 0.5L) * kPiL / P);
-    K.assign(size_t(nx) * ny * P * P, 0.0);
-    for (int ix = 0; ix < nx; ++ix) {
-        const double kx = 2.0 * kPi * (ix - p.Kx) / p.Lx;
+    std::vector<long double> k2u;
+    for (int ix = 0; ix < nx; ++ix)
         for (int iy = 0; iy < ny; ++iy) {
-            const double ky = 2.0 * kPi * iy / p.Ly, k2 = kx * kx + ky * ky;
-            for (int a = 0; a < P; ++a)
-                for (int b = 0; b < P; ++b)
-                    Kl[a * P + b] = long_kab(p, w, s, zal[a], zal[b], k2) * (kPiL / ((long double)p.Lx * p.Ly));
-            cheb_transform(P, Kl, Cl, &K[(size_t(ix) * ny + iy) * P * P]);
+            const long double kx = 2.0L * kPiL * (ix - p.Kx) / p.Lx, ky = 2.0L * kPiL * iy / p.Ly;
+            k2u.push_back(kx * kx + ky * ky);
         }
-    }
+    std::vector<double> Ku;
+    long_kernel_unique(p, k2u, Ku);
+    K.assign(Ku.size(), 0.0);
+    const double f = kPi / (p.Lx * p.Ly);
+    for (size_t e = 0; e < Ku.size(); ++e) K[e] = Ku[e] * f;
 }
 
 

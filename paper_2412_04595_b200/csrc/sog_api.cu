@@ -145,8 +145,10 @@ struct sog_plan {
     int zs0 = 0, nzf = 0, zg0 = 0, nzg = 0;         // spread-written planes, gather-read planes
     // fused z pass (kernels_fft.cuh): FFT along z + S5 + inverse in one kernel on the plane spectra
     bool zpass = false;
+    int zr_E = 0, zr_B = 0;                         // register-resident variant (SOG_ZPASS=2)
     FftStages zst{};
     void* d_ztw = nullptr;                          // twiddles (double2, or float2 in fp32 mode)
+    void* d_mult = nullptr;                         // S5 table [Izs][Ix nyh] (register-resident z pass)
     bool has_mid = false;
     // long
     double* lgrid = nullptr;
@@ -251,7 +253,7 @@ void free_plan(sog_plan* pl) {
     for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
                           pl->mzfft})
         if (h) cufftDestroy(h);
-    for (void* p : {(void*)pl->mX, (void*)pl->mY, pl->d_ztw})
+    for (void* p : {(void*)pl->mX, (void*)pl->mY, pl->d_ztw, pl->d_mult})
         if (p) cudaFree(p);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
@@ -438,13 +440,29 @@ int setup(sog_plan* pl) {
             CKF(cufftCreate(&pl->mzfft));
             CKF(cufftMakePlanMany64(pl->mzfft, 1, n1, nullptr, 1, p.Izs, nullptr, 1, p.Izs, c2c, M, &ws));
             pl->bytes += ws;
-            // fused z pass (opt-in, SOG_ZPASS=1) when Izs is 7-smooth and short enough for one CTA;
-            // default: the transpose + cuFFT 1D + scale + cuFFT 1D + transpose chain (measured faster
-            // at c5: 6.1 vs 7.1 ms)
+            // fused z pass (FFT along z + S5 + inverse FFT in one kernel, in place on the plane spectra):
+            // SOG_ZPASS=2 (default) the register-resident kernel when a radix set dividing E = 8..16
+            // covers Izs (c5: 5.35 ms vs 6.1 ms for the chain), 1 the shared-memory-stage kernel, 0 (or
+            // an unsupported Izs) the transpose + cuFFT 1D + scale + cuFFT 1D + transpose chain
             {
                 const char* env = std::getenv("SOG_ZPASS");
+                const int mode = env ? std::atoi(env) : 2;
                 std::vector<double2> tw;
-                if (env && std::atoi(env) == 1 && fft_plan_stages(p.Izs, pl->zst, tw)) {
+                bool ok = false;
+                if (mode == 2) {   // register-resident: E elements per thread, radices dividing E
+                    for (int E : {10, 8, 12, 16}) {
+                        if (p.Izs % E || p.Izs / E > 256) continue;
+                        if (fft_plan_stages(p.Izs, pl->zst, tw, E)) {
+                            pl->zr_E = E;
+                            { const char* eb = std::getenv("SOG_ZPASS_B"); pl->zr_B = eb ? std::atoi(eb) : 2; }
+                            ok = true;
+                            break;
+                        }
+                    }
+                } else if (mode == 1) {
+                    ok = fft_plan_stages(p.Izs, pl->zst, tw);
+                }
+                if (ok) {
                     if (pl->f32) {
                         std::vector<float2> t2(tw.size());
                         for (size_t i = 0; i < tw.size(); ++i) t2[i] = make_float2((float)tw[i].x, (float)tw[i].y);
@@ -454,6 +472,18 @@ int setup(sog_plan* pl) {
                     }
                     pl->zpass = true;
                 }
+            }
+            if (pl->zpass && pl->zr_E) {   // S5 table for the register-resident z pass
+                const size_t n = (size_t)M * p.Izs;
+                CK(cudaMalloc(&pl->d_mult, n * (pl->f32 ? sizeof(float) : sizeof(double))));
+                pl->bytes += n * (pl->f32 ? sizeof(float) : sizeof(double));
+                double* tmp = nullptr;
+                if (pl->f32) CK(cudaMalloc((void**)&tmp, n * sizeof(double)));
+                const int r = build_mult_table(pl->d_mult, M, nyh, p.Izs, p.m + 1, pl->d_A, pl->d_Tx, p.Ix, pl->d_Ty,
+                                               pl->d_Tz, pl->f32, tmp, nullptr);
+                CK(cudaDeviceSynchronize());
+                if (tmp) cudaFree(tmp);
+                if (r) return fail(SOG_ECUDA, "S5 multiplier table");
             }
             if (!pl->zpass) {   // zero-padded z pencils and their spectra for the cuFFT 1D chain
                 CK(cudaMalloc((void**)&pl->mY, csz * (size_t)M * p.Izs));
@@ -877,9 +907,14 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         if (pl->zpass) {
             // S4 (z), S5, S6 (z) in one kernel, in place on the plane spectra
             mark(pl, 4);
-            if ((rc = lchk(launch_zpass(pl->mX, M, nyh, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, p.m + 1, pl->d_A,
-                                        pl->d_Tx, p.Ix, pl->d_Ty, pl->d_Tz, pl->f32, st))))
+            if (pl->zr_E) {
+                if ((rc = lchk(launch_zpass_r(pl->mX, M, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, pl->d_mult,
+                                              pl->f32, pl->zr_E, pl->zr_B, st))))
+                    return rc;
+            } else if ((rc = lchk(launch_zpass(pl->mX, M, nyh, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, p.m + 1,
+                                               pl->d_A, pl->d_Tx, p.Ix, pl->d_Ty, pl->d_Tz, pl->f32, st)))) {
                 return rc;
+            }
             mark(pl, 5);
         } else {
         if ((rc = lchk(launch_zfft_transpose(pl->mX, pl->mY, pl->nzf, M, p.Izs, pl->zs0, true, pl->f32, st)))) return rc;
