@@ -95,6 +95,11 @@ typedef struct {
     int optimize;           /* 1: R20, eq::optimiz with B200-calibrated costs: the
                                plan of least predicted time over r_c factors {2.75 .. 3.75} x eta
                                {0.2 .. 0.5} (rc_factor / eta ignored) */
+    double b;               /* > 1: a general SOG base b in (1, 2] instead of the Table-1 row (NEXT #4):
+                               (r0, omega) from the C^1 continuity solve (Eq. eq::2.35z;
+                               DESIGN.md R22), e.g. Table 4's b = 1.17.  With explicit_params,
+                               b > 1 takes (b, r0, omega) verbatim from the three fields and row is ignored */
+    double r0, omega;
 } sog_plan_opts;
 
 /* Build a plan for N particles in the box (Lx,Ly,Lz) at tolerance tol on the current

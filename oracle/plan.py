@@ -11,6 +11,7 @@ DESIGN.md ("Readings of the paper").  Every constant below is named there.
 from __future__ import annotations
 
 import dataclasses
+import functools
 import math
 
 import numpy as np
@@ -51,6 +52,80 @@ def select_row(tol: float):
         if row[5] <= tol:
             return row
     raise ValueError("infeasible tolerance")
+
+
+@functools.lru_cache(maxsize=32)
+def c1_solve(b: float, tol: float):
+    """NEXT #4: the C^1 continuity solve for a general b (Eq. eq::2.35z): with sigma = 1,
+    r_0 and omega solve  r_0 F(r_0) - 1 = 0  and  r_0^2 F'(r_0) + 1 = 0,
+    F(r) = omega w_0 e^{-r^2/s_0^2} + G(r),  G(r) = sum_{l>=1} w_l e^{-r^2/s_l^2},
+    w_l = sqrt(2/pi) b^-l ln b, s_l = sqrt(2) b^l (the sum runs until w_l < 1e-55).
+    Eliminating omega with the first equation leaves one equation in r,
+        h(r) = 1 - r^2 + r^3 G(r) + r^2 G'(r) = 0,   omega = (1/r - G(r)) e^{r^2/2} / w_0(omega=1),
+    whose roots are not unique.  The paper's rule: the smallest root r_0 whose last two
+    eq::convrate terms (P:309-313) are below tol -- here the larger of the energy and force forms,
+    with s_{-1} = s_0 / b, w_{-1} = b w_0 from the weight formula (P:331 prints "s_{-1} = b s_0";
+    DESIGN.md reading R22).  Roots are bracketed by sign changes of h on a 0.02 grid of r in [1, 20]
+    and refined in 40-digit arithmetic (mpmath): for b -> 1 the residual of the system sits at the BSA
+    error level (~1e-13 at b = 1.17) over whole intervals of r, so double precision cannot locate
+    r_0, and omega = ... e^{r^2/2} amplifies rounding by e^{r_0^2/2}.  Returns (r0, omega) as floats.
+    Pinned: Table 1's simple-root rows (b = 2, 1.4878...) come back to the printed digits, and every
+    printed row satisfies h(r_0) ~ 0 (tests/test_oracle_pins.py::test_c1_solve_*)."""
+    import mpmath as mp
+    with mp.workdps(40):
+        bb = mp.mpf(b)
+        c = mp.sqrt(2 / mp.pi) * mp.log(bb)
+
+        def G(r):
+            g, dg, l = mp.mpf(0), mp.mpf(0), 1
+            while True:
+                s2 = 2 * bb ** (2 * l)
+                w = c * bb ** (-l)
+                e = w * mp.e ** (-r * r / s2)
+                g += e
+                dg += e * (-2 * r / s2)
+                if w < mp.mpf(10) ** -55:
+                    return g, dg
+                l += 1
+
+        def h(r):
+            g, dg = G(r)
+            return 1 - r * r + r ** 3 * g + r * r * dg
+
+        def terms(r):
+            g, _ = G(r)
+            om = (1 / r - g) * mp.e ** (r * r / 2) / c
+            s0, sm1, wm1 = mp.sqrt(2), mp.sqrt(2) / bb, c * bb
+            te = abs(wm1 * mp.e ** (-r * r / sm1 ** 2)) + abs((om - 1) * c * mp.e ** (-r * r / s0 ** 2))
+            tf = abs(wm1 / sm1 ** 2 * mp.e ** (-r * r / sm1 ** 2)) + abs((om - 1) * c / s0 ** 2 * mp.e ** (-r * r / s0 ** 2))
+            return om, max(te, tf)
+
+        # sign changes of h on the 0.02 grid, located with a float64 evaluation of the same sum
+        # (|h| between roots is >= ~1e-14 for b >= 1.15, far above its rounding), then refined in
+        # 40 digits
+        rg = 1.0 + 0.02 * np.arange(951)
+        ell = np.arange(1, int(130.0 / math.log(b)) + 2)
+        s2 = 2.0 * b ** (2.0 * ell)
+        e = (math.sqrt(2 / math.pi) * math.log(b) * b ** (-ell.astype(float)))[None, :] * np.exp(-rg[:, None] ** 2 / s2)
+        hg = 1 - rg ** 2 + rg ** 3 * e.sum(1) + rg ** 2 * (e * (-2 * rg[:, None] / s2)).sum(1)
+        for i in range(len(rg) - 1):
+            if hg[i] * hg[i + 1] < 0:
+                lo, hi = mp.mpf(rg[i]), mp.mpf(rg[i + 1])
+                hlo = h(lo)
+                if hlo * h(hi) > 0:
+                    continue                        # a float64 artefact: no bracket in 40 digits
+                for _ in range(64):                 # bisection to 0.02 * 2^-64 ~ 1e-21 (h is smooth)
+                    mid = (lo + hi) / 2
+                    hm = h(mid)
+                    if hlo * hm <= 0:
+                        hi = mid
+                    else:
+                        lo, hlo = mid, hm
+                root = (lo + hi) / 2
+                om, t = terms(root)
+                if t <= tol:
+                    return float(root), float(om)
+    raise ValueError(f"no C^1 root with error terms <= {tol} for b = {b}")
 
 
 def sog_nodes_weights(b: float, sigma: float, omega: float, M: int):
@@ -281,8 +356,16 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
         return best
     if N < 1 or not all(math.isfinite(v) and v > 0 for v in (Lx, Ly, Lz)):
         raise ValueError("invalid N or box")
-    row = over.pop("row", None) or select_row(tol)
-    b, r0, omega = row[0], row[1], row[2]
+    b_general = over.pop("b", None)
+    if b_general is not None:                               # NEXT #4: C^1 solve for this b
+        if not (1.0 < b_general <= 2.0):
+            raise ValueError("b must lie in (1, 2]")
+        b = float(b_general)
+        r0, omega = c1_solve(b, tol)
+        over.pop("row", None)
+    else:
+        row = over.pop("row", None) or select_row(tol)
+        b, r0, omega = row[0], row[1], row[2]
     rc_factor = over.pop("rc_factor", RC_FACTOR)
     window = over.pop("window", "gs")
     if window not in ("gs", "kb", "es"):

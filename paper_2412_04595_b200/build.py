@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp",
-            "-L/usr/local/cuda/lib64", "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+            "-L/usr/local/cuda/lib64", "-lcufft", "-lquadmath", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -1,6 +1,7 @@
 // Host-side plan construction: parameter rules R1-R9 and precomputed tables.
 // Independent of the CPU oracle (oracle/plan.py); tests/test_plan_parity.py compares them.
 #include <algorithm>
+#include <quadmath.h>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -168,14 +169,88 @@ void sog_weights(const Params& p, std::vector<double>& w, std::vector<double>& s
     w[0] *= p.omega;
 }
 
+// NEXT #4: the C^1 continuity solve for a general b (Eq. eq::2.35z), sigma = 1:
+//   r0 F(r0) = 1 and r0^2 F'(r0) = -1, F(r) = omega w_0 e^{-r^2/2} + G(r), G = sum_{l>=1} w_l e^{-r^2/s_l^2}.
+// Eliminating omega: h(r) = 1 - r^2 + r^3 G(r) + r^2 G'(r) = 0, omega = (1/r - G(r)) e^{r^2/2} / w_0.
+// The smallest root whose eq::convrate near-field / omega terms are below tol (reading R22).
+// Sign changes of h on a 0.02 grid in r in [1, 20] (double), each bracket refined by bisection in
+// binary128 (libquadmath): for b -> 1 |h| between roots is ~1e-13, so double cannot locate r0 and
+// omega's e^{r^2/2} amplifies rounding.
+static void c1_G(__float128 r, __float128 b, __float128 c, __float128& g, __float128& dg) {
+    g = 0; dg = 0;
+    for (int l = 1;; ++l) {
+        const __float128 s2 = 2 * powq(b, 2 * l), w = c * powq(b, -l);
+        const __float128 e = w * expq(-r * r / s2);
+        g += e;
+        dg += e * (-2 * r / s2);
+        if (w < (__float128)1e-40) break;
+    }
+}
+static __float128 c1_h(__float128 r, __float128 b, __float128 c) {
+    __float128 g, dg;
+    c1_G(r, b, c, g, dg);
+    return 1 - r * r + r * r * r * g + r * r * dg;
+}
+bool c1_solve(double bd, double tol, double& r0, double& omega) {
+    if (!(bd > 1.0 && bd <= 2.0)) return false;
+    const __float128 pi = 4 * atanq((__float128)1), b = bd, c = sqrtq(2 / pi) * logq(b);
+    // grid scan in double
+    const double cd = std::sqrt(2.0 / kPi) * std::log(bd);
+    const int nl = int(130.0 / std::log(bd)) + 2;
+    auto hd = [&](double r) {
+        double g = 0, dg = 0;
+        for (int l = 1; l <= nl; ++l) {
+            const double s2 = 2.0 * std::pow(bd, 2.0 * l), e = cd * std::pow(bd, -double(l)) * std::exp(-r * r / s2);
+            g += e;
+            dg += e * (-2.0 * r / s2);
+        }
+        return 1 - r * r + r * r * r * g + r * r * dg;
+    };
+    double rp = 1.0, hp = hd(rp);
+    for (int i = 1; i <= 950; ++i) {
+        const double rn = 1.0 + 0.02 * i, hn = hd(rn);
+        if (hp * hn < 0) {
+            __float128 lo = rp, hi = rn, hlo = c1_h(lo, b, c);
+            if (hlo * c1_h(hi, b, c) <= 0) {
+                for (int it = 0; it < 64; ++it) {
+                    const __float128 mid = (lo + hi) / 2, hm = c1_h(mid, b, c);
+                    if (hlo * hm <= 0) hi = mid;
+                    else { lo = mid; hlo = hm; }
+                }
+                const __float128 r = (lo + hi) / 2;
+                __float128 g, dg;
+                c1_G(r, b, c, g, dg);
+                const __float128 om = (1 / r - g) * expq(r * r / 2) / c;
+                const __float128 s0 = sqrtq((__float128)2), sm1 = s0 / b, wm1 = c * b;
+                const __float128 e1 = expq(-r * r / (sm1 * sm1)), e0 = expq(-r * r / (s0 * s0));
+                const __float128 te = fabsq(wm1 * e1) + fabsq((om - 1) * c * e0);
+                const __float128 tf = fabsq(wm1 / (sm1 * sm1) * e1) + fabsq((om - 1) * c / (s0 * s0) * e0);
+                if ((te > tf ? te : tf) <= (__float128)tol) {
+                    r0 = double(r);
+                    omega = double(om);
+                    return true;
+                }
+            }
+        }
+        rp = rn;
+        hp = hn;
+    }
+    return false;
+}
+
 bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
     if (!(p.tol >= kTolMin && p.tol <= kTolMax)) { err = "tol outside [2e-14, 1e-1]"; return false; }
-    // R1: coarsest Table-1 row whose force error <= tol
-    int row = -1;
-    for (int r = 0; r < 6; ++r) if (kTable1[r].ferr <= p.tol) { row = r; break; }
-    if (row < 0) { err = "infeasible tolerance"; return false; }
-    p.row = row;
-    p.b = kTable1[row].b; p.r0 = kTable1[row].r0; p.omega = kTable1[row].omega;
+    if (p.b > 1.0 && p.row < 0) {
+        // NEXT #4: a caller-chosen b, (r0, omega) from the C^1 solve
+        if (!c1_solve(p.b, p.tol, p.r0, p.omega)) { err = "no C^1 root for this b below tol"; return false; }
+    } else {
+        // R1: coarsest Table-1 row whose force error <= tol
+        int row = -1;
+        for (int r = 0; r < 6; ++r) if (kTable1[r].ferr <= p.tol) { row = r; break; }
+        if (row < 0) { err = "infeasible tolerance"; return false; }
+        p.row = row;
+        p.b = kTable1[row].b; p.r0 = kTable1[row].r0; p.omega = kTable1[row].omega;
+    }
     // R2
     const double rho = double(p.N) / (p.Lx * p.Ly * p.Lz);
     p.rc = std::min(k.rc_factor * std::pow(rho, -1.0 / 3.0), 0.5 * std::min(p.Lx, p.Ly));
@@ -273,7 +348,7 @@ bool validate_params(const Params& p, std::string& err) {
     auto bad = [&](const char* m) { err = m; return false; };
     if (p.N < 1 || p.N > (int64_t(1) << 31) - 1) return bad("N out of range [1, 2^31)");
     if (!(p.Lx > 0 && p.Ly > 0 && p.Lz > 0) || !std::isfinite(p.Lx + p.Ly + p.Lz)) return bad("invalid box");
-    if (p.row < 0 || p.row > 5) return bad("row must be 0..5");
+    if (p.row > 5 || (p.row < 0 && !(p.b > 1.0 && p.b <= 2.0 && p.r0 > 0))) return bad("row must be 0..5 (or a general b)");
     if (!(p.rc > 0) || p.rc > 0.5 * std::min(p.Lx, p.Ly) * (1 + 1e-15)) return bad("r_c must be in (0, min(Lx,Ly)/2]");
     if (p.M < 1 || p.M > 4000) return bad("M out of range");
     if (p.m < -1 || p.m >= p.M) return bad("m must be in [-1, M-1]");

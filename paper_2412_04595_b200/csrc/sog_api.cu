@@ -1009,8 +1009,12 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
                                         {1.32070036405934420, 4.3914554711638349, 1.0018891411481198},
                                         {1.21812525709410644, 5.6355288151271085, 1.0009014615603334},
                                         {1.14878150173321925, 7.2956245490719404, 1.0000368348358225}};
-        if (o->row < 0 || o->row > 5) return fail(SOG_EINVAL, "row must be 0..5");
-        p.row = o->row; p.b = tb[o->row][0]; p.r0 = tb[o->row][1]; p.omega = tb[o->row][2];
+        if (o->b > 1.0) {   // general b (NEXT #4): verbatim
+            p.row = -1; p.b = o->b; p.r0 = o->r0; p.omega = o->omega;
+        } else {
+            if (o->row < 0 || o->row > 5) return fail(SOG_EINVAL, "row must be 0..5");
+            p.row = o->row; p.b = tb[o->row][0]; p.r0 = tb[o->row][1]; p.omega = tb[o->row][2];
+        }
         p.rc = o->rc; p.sigma = p.rc / p.r0; p.M = o->M; p.m = o->m;
         p.Ix = o->Ix; p.Iy = o->Iy; p.Iz = o->Iz; p.Izs = o->Izs; p.P = o->P; p.S = o->S;
         p.Ilx = o->Ilx; p.Ily = o->Ily; p.Pl = o->Pl; p.Sl = o->Sl; p.Pc = o->Pc;
@@ -1027,6 +1031,10 @@ int make_params(Params& p, RuleKnobs& knobs, int64_t N, double Lx, double Ly, do
         if (o && o->long_method != 0 && o->long_method != 1) return fail(SOG_EINVAL, "long_method must be 0 or 1");
         p.window = o ? o->window : 0;
         p.long_method = o ? o->long_method : 0;
+        if (o && o->b != 0.0) {
+            if (!(o->b > 1.0 && o->b <= 2.0)) return fail(SOG_EINVAL, "b must lie in (1, 2]");
+            p.b = o->b;   // general b: choose_params runs the C^1 solve
+        }
         if (o && o->rc_factor > 0) knobs.rc_factor = o->rc_factor;
         if (o && o->eta > 0) knobs.eta = o->eta;
         if (o && o->optimize) {

@@ -55,7 +55,9 @@ struct RuleKnobs {
 };
 
 // plan.cpp
-bool choose_params(Params& p, const RuleKnobs& k, std::string& err);   // rules R1-R9
+bool choose_params(Params& p, const RuleKnobs& k, std::string& err);   // rules R1-R9 (p.b > 1, p.row < 0: general b)
+// NEXT #4: C^1 solve for a general b (binary128): the smallest root r0 whose error terms are <= tol
+bool c1_solve(double b, double tol, double& r0, double& omega);
 // R20: eq::optimiz with B200-calibrated costs: the least predicted time over r_c factor x eta grids
 bool choose_params_opt(Params& p, const RuleKnobs& k, std::string& err);
 double plan_cost(const Params& p);

@@ -37,7 +37,8 @@ class Opts(ctypes.Structure):
                 ("Pc", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint),
                 ("precision", ctypes.c_int), ("window", ctypes.c_int), ("nu", ctypes.c_int),
                 ("nul", ctypes.c_int), ("long_method", ctypes.c_int), ("Kx", ctypes.c_int), ("Ky", ctypes.c_int),
-                ("optimize", ctypes.c_int)]
+                ("optimize", ctypes.c_int), ("b", ctypes.c_double), ("r0", ctypes.c_double),
+                ("omega", ctypes.c_double)]
 
 WINDOWS = {"gs": 0, "kb": 1, "es": 2}
 LONG_METHODS = {"fft": 0, "direct": 1}
@@ -134,7 +135,9 @@ class Plan:
     """
 
     def __init__(self, N, L, tol, params=None, rc_factor=None, eta=None, stream=None,
-                 validate=True, timing=False, precision="fp64", window="gs", long_method="fft", optimize=False):
+                 validate=True, timing=False, precision="fp64", window="gs", long_method="fft", optimize=False,
+                 b=None):
+        """b: a general SOG base in (1, 2] (NEXT #4: (r0, omega) by the C^1 solve) instead of R1's row."""
         self.lib = load_library()
         self.N = int(N)
         self.L = tuple(float(v) for v in L)
@@ -146,6 +149,11 @@ class Plan:
             o.explicit_params = 1
             for k in PLAN_FIELDS:
                 setattr(o, k, type(getattr(o, k))(params[k]))
+            if params.get("row", 0) is None or int(params.get("row", 0)) < 0:   # general b (NEXT #4)
+                o.b, o.r0, o.omega = float(params["b"]), float(params["r0"]), float(params["omega"])
+                o.row = -1
+        elif b is not None:
+            o.b = float(b)
         o.flags = (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0)
         o.cuda_stream = _stream_handle(stream)
         o.precision = {"fp64": 0, "fp32": 1}[precision]
@@ -285,10 +293,14 @@ def _parse(text):
     return out
 
 
-def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method="fft", optimize=False) -> dict:
-    """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU)."""
+def choose_params(N, L, tol, rc_factor=None, eta=None, window="gs", long_method="fft", optimize=False,
+                  b=None) -> dict:
+    """Plan parameters chosen by the library's rules R1-R9 (host only, no GPU); b: a general SOG
+    base (NEXT #4, C^1 solve) instead of R1's Table-1 row."""
     lib = load_library()
     o = Opts()
+    if b is not None:
+        o.b = float(b)
     o.rc_factor = float(rc_factor or 0.0)
     o.eta = float(eta or 0.0)
     _set_window(o, window, None, long_method)

@@ -101,3 +101,17 @@ def test_plan_choose_errors():
 def test_table1_row_selection():
     for tol, row in ((1e-2, 0), (1e-3, 1), (1e-4, 2), (1e-6, 3), (1e-8, 4), (1e-12, 5), (2e-14, 5)):
         assert B.choose_params(1000, (10.0, 10.0, 10.0), tol)["row"] == row
+
+
+@pytest.mark.parametrize("b,tol", [(1.17, 1e-12), (1.25, 1e-8), (1.4, 1e-5)])
+def test_general_b_c1_solve_matches_oracle(b, tol):
+    """NEXT #4: the library's binary128 C^1 solve (plan.cpp c1_solve) and the oracle's 40-digit one
+    (oracle/plan.py c1_solve) pick the same root; the plans agree field by field."""
+    from paper_2412_04595_b200 import choose_params
+    from oracle.plan import make_plan
+    d = choose_params(2000, (12.0, 12.0, 12.0), tol, b=b)
+    op = make_plan(2000, 12.0, 12.0, 12.0, tol, b=b)
+    assert d["row"] == -1 and d["b"] == b
+    assert abs(d["r0"] - op.r0) <= 1e-14 * op.r0 and abs(d["omega"] - op.omega) <= 1e-14
+    for k in ("M", "m", "Ix", "Iy", "Izs", "P", "Pc", "Ilx"):
+        assert d[k] == getattr(op, k), k

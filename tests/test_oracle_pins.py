@@ -259,6 +259,42 @@ def test_long_spread_dense_equals_add_at():
         assert np.abs(a - b).max() <= 1e-14 * np.abs(a).max(), (name, window)
 
 
+def test_c1_solve_reproduces_table1_simple_roots():
+    """NEXT #4: the general-b C^1 solve returns Table 1's printed (r0, omega) for the rows
+    whose r0 is a simple root (b = 2 and b = 1.4878...; rows 2, 4, 5 are tangential roots of the
+    system, which a sign-change solve does not bracket), each at that row's force error as tol."""
+    for k in (0, 2):
+        b, r0, om, _, _, ferr, _ = P.TABLE1[k]
+        r, w = P.c1_solve(b, ferr)
+        assert abs(r - r0) <= 1e-11 * r0, (k, r, r0)
+        assert abs(w - om) <= 1e-12, (k, w, om)
+
+
+def test_c1_solve_general_b_satisfies_the_continuity_system():
+    """For a non-table b (Table 4's 1.17; and 1.25, 1.4) the solved (r0, omega) make the SOG
+    sum C^0 and C^1 at r_c: r0 F(r0) = 1 and r0^2 F'(r0) = -1 with M -> infinity, evaluated
+    by plain summation of the sog_nodes_weights Gaussians (sigma = 1) in double precision."""
+    for b, tol in ((1.17, 1e-12), (1.25, 1e-8), (1.4, 1e-5)):
+        r0, om = P.c1_solve(b, tol)
+        w, s = P.sog_nodes_weights(b, 1.0, om, int(60.0 / math.log(b)))
+        F = float(np.sum(w * np.exp(-(r0 / s) ** 2)))
+        dF = float(np.sum(w * np.exp(-(r0 / s) ** 2) * (-2.0 * r0 / s ** 2)))
+        assert abs(r0 * F - 1.0) < 5e-15 and abs(r0 * r0 * dF + 1.0) < 5e-14, (b, r0 * F - 1, r0 * r0 * dF + 1)
+        assert r0 > 1.0 and abs(om - 1.0) < 0.05
+
+
+def test_general_b_total_vs_ewald2d():
+    """A Table-4-like plan with the general b = 1.17 at tol 1e-12 reaches tol vs Ewald2D."""
+    xyz, q, L = config_system("c1", N=400)
+    p = P.make_plan(len(q), *L, 1e-12, b=1.17)
+    assert p.b == 1.17
+    t = np.arange(16)
+    phi, F = sog.evaluate(p, xyz, q, targets=t)
+    ref, g = ewald2d.ewald2d(xyz, q, L, targets=t)
+    assert np.max(np.abs(phi - ref)) / np.max(np.abs(ref)) < 1e-12
+    assert np.linalg.norm(F + q[t, None] * g) / np.linalg.norm(q[t, None] * g) < 1e-11
+
+
 # ------------------------------------------------------------------ spectral components vs SOG-exact
 @pytest.fixture(scope="module")
 def small_system():
