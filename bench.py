@@ -356,6 +356,29 @@ def run_xslab(args, ws, rank, local):
         torch.cuda.synchronize()
         barrier(ws)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    clocks = clk.summary()
+    # per-phase device times of this rank (separate, synchronising evaluations with SOG_TIMING);
+    # the collective phases include waiting for the slowest peer
+    plan.set_flags(validate=False, timing=True)
+    acc = {}
+    for _ in range(args.steps):
+        plan.eval(xd, qd, phi, F)
+        for k, v in plan.timings().items():
+            acc[k] = acc.get(k, 0.0) + v / args.steps
+    plan.set_flags(validate=False)
+    phases = {k: max_over_ranks(v, ws) for k, v in acc.items()}
+    d0 = plan.describe()
+    rho = N / (L[0] * L[1] * L[2])
+    near_flops = len(mine) * (27.0 * rho * d0["rc"] ** 3 * 9.0 + 4.0 * math.pi / 3.0 * rho * d0["rc"] ** 3 * 50.0)
+    pk = measured_peaks()
+    near_ms = acc.get("near", 0.0)
+    roof = None
+    if near_ms > 0:
+        ach = near_flops / (near_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": "near (own targets, rank 0)" if rank == 0 else "near", "achieved": ach,
+                "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": ach / pk["fp64_tflops"], "traffic": None,
+                "peak_source": pk["fp64_source"], "algorithmic_flops": near_flops, "ms": near_ms,
+                "flops_rule": "SURVEY 8(d) per-particle formula x own particles of the rank"}
     # end to end: pinned host -> device copies of this rank's particles and results back
     hx = torch.from_numpy(np.ascontiguousarray(xyz[mine])).pin_memory()
     hq = torch.from_numpy(np.ascontiguousarray(q[mine])).pin_memory()
@@ -386,13 +409,17 @@ def run_xslab(args, ws, rank, local):
                    "window": args.window,
                    "plan": {k: d[k] for k in ("M", "m", "rc", "Ix", "Iy", "Izs", "P", "Ilx", "Ily", "Pl", "Pc",
                                               "slab_planes", "halo")}},
-        "roofline": None,
+        "stages_ms": phases,
+        "collectives_ms": {k: phases.get(k) for k in ("halo", "a2a_fwd", "a2a_bwd", "psi_halo", "long_allreduce")},
+        "roofline": roof,
         "cpu_baseline": None,
         "e2e": {"value": N / (e2e_ms * 1e-3), "unit": "particles/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(32 * N), "d2h_bytes_per_step": int(32 * N)},
         "gpu_launches": None,
-        "clocks": clk.summary(),
+        "clocks": clocks,
+        "a2a_bytes_per_rank_per_transpose": int(16 * d0["Izs"] * (d0["Ix"] // ws) * (d0["Iy"] // 2 + 1) * (ws - 1) / ws),
     }
+    # cpu_baseline: reported at N = 1 only (the oracle on the host cores, see main())
     if rank == 0:
         print(json.dumps(out), flush=True)
     plan.close()

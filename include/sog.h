@@ -207,6 +207,15 @@ int sog_dist_eval(sog_dist* d, const int64_t* n_own, const double* const* xyz, c
                   double* const* phi, double* const* force);
 
 int sog_dist_local_ranks(const sog_dist* d);
+/* SOG_NO_VALIDATE / SOG_TIMING for every local rank.  With SOG_TIMING each evaluation synchronises at
+ * its end and records per-phase device times of local rank 0 (CUDA events on the ranks' stream; the
+ * collective phases include waiting for the slowest peer):
+ *   [0] particle halos (select, status agreement, exchanges), [1] sort, [2] mid spread + 2D FFTs + pack,
+ *   [3] all-to-all forward, [4] x FFT + S5 + pack, [5] all-to-all back, [6] inverse 2D FFTs + plane
+ *   pack, [7] Psi halo planes, [8] mid gather + long spread, [9] long-grid all-reduce,
+ *   [10] long solve + gather + combine, [11] near field (own targets, on the side stream). */
+int sog_dist_set_flags(sog_dist* d, unsigned flags);
+int sog_dist_get_timings(const sog_dist* d, double* ms, int n);   /* writes min(n, 12) values, returns it */
 int sog_dist_describe(const sog_dist* d, char* buf, size_t len);   /* plan + slab key=value lines */
 void sog_dist_destroy(sog_dist* d);                                 /* NULL-safe */
 

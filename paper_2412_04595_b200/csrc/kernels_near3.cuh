@@ -21,7 +21,17 @@ struct Near3Args {
     CellGeo g;
     int cap;                // staged-source capacity (shared memory)
     float rc2f;             // conservative fp32 pre-test threshold
+    const int* perm = nullptr;   // x-slab ranks: sorted -> local index; targets are own particles only
+    int nown = 0;                //   (local index < nown), halo particles are sources only
 };
+
+// x-slab ranks: does cell [t0, t1) hold an own particle (else the CTA has no target)
+__device__ __forceinline__ bool near_has_target(const Near3Args& a, int t0, int t1) {
+    if (!a.perm) return true;
+    int own = 0;
+    for (int it = t0 + (int)threadIdx.x; it < t1; it += blockDim.x) own |= a.perm[it] < a.nown;
+    return __syncthreads_or(own) != 0;
+}
 
 constexpr int NEAR3_WARPS = 4;
 
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a, NearPol
     const int c = blockIdx.x;
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
     const int t0 = a.start[c], t1 = a.start[c + 1];
-    if (t0 == t1) return;
+    if (t0 == t1 || !near_has_target(a, t0, t1)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (PD == 0)
         for (int t = threadIdx.x; t < a.K * (D + 1); t += blockDim.x) tab[t] = a.cF[t];
@@ -158,6 +168,7 @@ __global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a, NearPol
         }
         __syncthreads();
         for (int it = t0 + warp; it < t1; it += NEAR3_WARPS) {
+            if (a.perm && a.perm[it] >= a.nown) continue;      // halo particle: a source only
             const d4 pi = ld_d4(&a.pos[it]);
             const float xi = (float)(pi.x - ox), yi = (float)(pi.y - oy), zi = (float)(pi.z - oz);
             const float2 xi2 = make_float2(xi, xi), yi2 = make_float2(yi, yi), zi2 = make_float2(zi, zi);

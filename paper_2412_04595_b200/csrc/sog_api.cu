@@ -316,6 +316,7 @@ int setup(sog_plan* pl) {
     {
         const char* env = std::getenv("SOG_NEAR");
         pl->near_mode = env ? std::atoi(env) : 5;
+        if (slab && pl->near_mode == 4) pl->near_mode = 5;       // k_near4 has no own-target filter
         if (pl->near_mode != 3 && !pl->f32 && g.ncx >= 3 && g.ncy >= 3 && build_near_poly(p, pl->npoly)) {
             const double m = std::max(1.0, double(pl->Ncap) / pl->ncell);       // mean particles per cell
             pl->n4_kc = std::max(1, std::min(g.ncz, int(140.0 / m)));
@@ -603,7 +604,7 @@ int setup(sog_plan* pl) {
         CK(cudaMallocHost((void**)&pl->pin_d, 8 * sizeof(double)));
     }
     for (auto& e : pl->ev) CK(cudaEventCreate(&e));
-    if (!slab) {   // SOG_NEAR_STREAM=off|low|high (default low): near-field side stream and its priority
+    {   // SOG_NEAR_STREAM=off|low|high (default low): near-field side stream and its priority
         const char* env = std::getenv("SOG_NEAR_STREAM");
         const std::string mode = env ? env : "low";
         if (mode != "off") {
@@ -749,6 +750,7 @@ int st_near(sog_plan* pl) {
         a.g = pl->geo;
         a.cap = 1536;
         a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+        if (pl->R > 1) { a.perm = pl->perm; a.nown = pl->Nown; }   // x-slab: own targets only
         if ((rc = lchk(launch_near3p(a, pl->npoly, pl->ncell, st)))) return rc;
     } else if (pl->near4) {   // k_near4: target-stationary, one polynomial (R16-G)
         Near4Args a;
@@ -767,6 +769,7 @@ int st_near(sog_plan* pl) {
         a.g = pl->geo;
         a.cap = 1536;                            // multiple of 128 (packed staging layout)
         a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+        if (pl->R > 1) { a.perm = pl->perm; a.nown = pl->Nown; }   // x-slab: own targets only
         size_t sh = sizeof(double) * ((pl->near.K * (D + 1) + 1) & ~1) + 10 * sizeof(double2) +
                     NEAR3_WARPS * 160 * sizeof(int) + 16 * a.cap;
         CK(cudaFuncSetAttribute(k_near3<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
@@ -1314,6 +1317,10 @@ struct sog_dist {
     std::vector<sog_plan*> pl;           // loopback: all R ranks; NCCL: this process's rank
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
+    // SOG_TIMING: phase boundaries on the ranks' stream + the near field on plan 0's side stream
+    bool timing = false;
+    cudaEvent_t ev[12] = {}, nev[2] = {};
+    double ms[12] = {};
 };
 
 namespace {
@@ -1381,6 +1388,10 @@ int dbg_sync(sog_dist* d, const char* what) {
     return SOG_OK;
 }
 
+void dmark(sog_dist* d, int k) {
+    if (d->timing) cudaEventRecord(d->ev[k], d->stream);
+}
+
 int kyc_of(const sog_plan* pl, int s) {
     const int nyh = pl->p.Iy / 2 + 1;
     return std::max(0, std::min(pl->kc, nyh - s * pl->kc));
@@ -1394,6 +1405,7 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
     int rc;
     auto left = [&](int r) { return (r + R - 1) % R; };
     auto right = [&](int r) { return (r + 1) % R; };
+    dmark(d, 0);
     // ---- particle halos: select, agree on the input status, exchange counts, exchange particles ----
     // No rank returns before the agreement: a rank-local error (capacity, slab membership, invalid
     // input) is summed into every rank's status, so all ranks reject the evaluation together
@@ -1463,6 +1475,7 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
         ex[i].recv = {{right(r), pl->hrecv + pl->halo_cap, sizeof(d4) * c[2]}, {left(r), pl->hrecv, sizeof(d4) * c[3]}};
     }
     if ((rc = run_exchange(d, ex))) return rc;
+    dmark(d, 1);
     // ---- local particles: near field, mid spread, 2D FFTs, pack for the all-to-all ----
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
@@ -1472,9 +1485,24 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
         if (nloc > 0)
             k_slab_local<<<(nloc + 255) / 256, 256, 0, st>>>(pl->own, pl->Nown, pl->hrecv, nl, pl->hrecv + pl->halo_cap, nr,
                                                             pl->lxyz, pl->lq);
-        if ((rc = st_sort(pl, pl->lxyz, pl->lq, nloc)) || (rc = dbg_sync(d, "slab sort")) || (rc = st_near(pl)) ||
-            (rc = dbg_sync(d, "slab near")))
+        if ((rc = st_sort(pl, pl->lxyz, pl->lq, nloc)) || (rc = dbg_sync(d, "slab sort"))) return rc;
+        // near field (own targets only) on the rank's side stream: it runs under the pencil
+        // all-to-alls and the mid / long chain below; joined before the combine
+        if (i == 0) dmark(d, 2);
+        if (pl->side) {
+            CK(cudaEventRecord(pl->ev_fork, st));
+            CK(cudaStreamWaitEvent(pl->side, pl->ev_fork, 0));
+            if (d->timing && i == 0) cudaEventRecord(d->nev[0], pl->side);
+            pl->stream = pl->side;
+            rc = st_near(pl);
+            pl->stream = st;
+            if (rc) return rc;
+            if (d->timing && i == 0) cudaEventRecord(d->nev[1], pl->side);
+            CK(cudaEventRecord(pl->ev_join, pl->side));
+        } else if ((rc = st_near(pl))) {
             return rc;
+        }
+        if ((rc = dbg_sync(d, "slab near"))) return rc;
         if (!pl->has_mid) continue;
         if ((rc = st_mid_spread(pl)) || (rc = dbg_sync(d, "slab spread"))) return rc;
         CKF(cufftExecD2Z(pl->f2f, pl->mgrid + (size_t)pl->XO * p.Iy, pl->spec2));
@@ -1492,8 +1520,10 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
         }
     }
     const bool has_mid = d->pl[0]->has_mid;
+    dmark(d, 3);
     if (has_mid) {
         if ((rc = run_exchange(d, ex))) return rc;
+        dmark(d, 4);
         // ---- x pencils: 1D FFT along x, S5 scaling, inverse, pack back ----
         for (int i = 0; i < L; ++i) {
             sog_plan* pl = d->pl[i];
@@ -1521,7 +1551,9 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
                 ex[i].recv.push_back({s, pl->rbuf + s * pl->blk, sizeof(cuDoubleComplex) * p.Izs * pl->Ixr * kyc_of(pl, s)});
             }
         }
+        dmark(d, 5);
         if ((rc = run_exchange(d, ex))) return rc;
+        dmark(d, 6);
         // ---- inverse 2D FFTs into the interior planes of Psi; edge planes for the neighbours ----
         for (int i = 0; i < L; ++i) {
             sog_plan* pl = d->pl[i];
@@ -1542,8 +1574,10 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
             ex[i].send = {{left(r), pl->hsb, sizeof(double) * hp}, {right(r), pl->hsb + hp, sizeof(double) * hp}};
             ex[i].recv = {{right(r), pl->hrb + hp, sizeof(double) * hp}, {left(r), pl->hrb, sizeof(double) * hp}};
         }
+        dmark(d, 7);
         if ((rc = run_exchange(d, ex))) return rc;
     }
+    dmark(d, 8);
     // ---- halo planes in, mid gather, long spread of the own particles ----
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
@@ -1569,14 +1603,17 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
     }
     {
         const Params& p = d->pl[0]->p;
+        dmark(d, 9);
         if ((rc = dbg_sync(d, "long spread")) || (rc = run_allreduce(d, (size_t)p.Pc * p.Ilx * p.Ily)) ||
             (rc = dbg_sync(d, "long allreduce")))
             return rc;
+        dmark(d, 10);
     }
     // ---- long solve (redundant per rank: small grid), long gather, combine ----
     for (int i = 0; i < L; ++i) {
         sog_plan* pl = d->pl[i];
         if ((rc = st_long_solve(pl))) return rc;
+        if (pl->side) CK(cudaStreamWaitEvent(pl->stream, pl->ev_join, 0));
         if (!pl->Ncur) continue;
         if ((rc = st_long_gather(pl))) return rc;
         k_combine_g<<<std::max(1, (pl->Nown + 255) / 256), 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s,
@@ -1584,6 +1621,24 @@ int dist_eval(sog_dist* d, const int64_t* nown, const double* const* xyz, const 
                                                                     pl->epart);
         k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, std::max(1, (pl->Nown + 255) / 256), pl->qsums + 2);
         CK(cudaGetLastError());
+    }
+    if (d->timing) {
+        dmark(d, 11);
+        CK(cudaStreamSynchronize(d->stream));
+        // [0] halos, [1] sort, [2] spread + 2D FFT + pack, [3] all-to-all fwd, [4] x FFT + S5 + pack,
+        // [5] all-to-all bwd, [6] inverse 2D FFT + plane pack, [7] Psi halo planes, [8] gather + long
+        // spread, [9] long all-reduce, [10] long solve + gather + combine, [11] near field (side stream)
+        const int pr[11][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}, {8, 9}, {9, 10}, {10, 11}};
+        for (int k = 0; k < 11; ++k) {
+            float ms = 0;
+            if (!has_mid && k >= 3 && k <= 7) { d->ms[k] = 0; continue; }
+            if (cudaEventElapsedTime(&ms, d->ev[pr[k][0]], d->ev[pr[k][1]]) != cudaSuccess) ms = 0;
+            d->ms[k] = ms;
+        }
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, d->nev[0], d->nev[1]) != cudaSuccess) ms = 0;
+        d->ms[11] = ms;
+        cudaGetLastError();
     }
     return SOG_OK;
 }
@@ -1713,6 +1768,25 @@ int sog_dist_eval(sog_dist* d, const int64_t* n_own, const double* const* xyz, c
 
 int sog_dist_local_ranks(const sog_dist* d) { return d ? int(d->pl.size()) : fail(SOG_EINVAL, "null"); }
 
+int sog_dist_set_flags(sog_dist* d, unsigned flags) {
+    if (!d) return fail(SOG_EINVAL, "null");
+    for (sog_plan* pl : d->pl) pl->flags = flags & ~SOG_TIMING;   // the plans' own stage events stay off
+    const bool t = (flags & SOG_TIMING) != 0;
+    if (t && !d->ev[0]) {
+        for (auto& e : d->ev) CK(cudaEventCreate(&e));
+        for (auto& e : d->nev) CK(cudaEventCreate(&e));
+    }
+    d->timing = t;
+    return SOG_OK;
+}
+
+int sog_dist_get_timings(const sog_dist* d, double* ms, int n) {
+    if (!d || !ms) return fail(SOG_EINVAL, "null argument");
+    const int k = std::min(n, 12);
+    for (int i = 0; i < k; ++i) ms[i] = d->ms[i];
+    return k;
+}
+
 int sog_dist_describe(const sog_dist* d, char* buf, size_t len) {
     if (!d || d->pl.empty()) return fail(SOG_EINVAL, "null");
     const sog_plan* pl = d->pl[0];
@@ -1731,6 +1805,10 @@ int sog_dist_describe(const sog_dist* d, char* buf, size_t len) {
 
 void sog_dist_destroy(sog_dist* d) {
     if (!d) return;
+    for (auto& e : d->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : d->nev)
+        if (e) cudaEventDestroy(e);
     if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
     for (sog_plan* pl : d->pl) free_plan(pl);
     delete d;

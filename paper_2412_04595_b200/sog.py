@@ -18,7 +18,8 @@ EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval
            "sog_debug_stage", "sog_last_energy", "sog_plan_destroy", "sog_last_error", "sog_plan_describe",
            "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval",
            "sog_nccl_selftest", "sog_nccl_unique_id", "sog_dist_create", "sog_dist_create_loopback", "sog_dist_eval",
-           "sog_dist_local_ranks", "sog_dist_describe", "sog_dist_destroy"]
+           "sog_dist_local_ranks", "sog_dist_describe", "sog_dist_destroy", "sog_dist_set_flags",
+           "sog_dist_get_timings"]
 
 
 class SogError(RuntimeError):
@@ -116,6 +117,10 @@ def load_library():
     lib.sog_dist_describe.argtypes = [P, ctypes.c_char_p, S]
     lib.sog_dist_destroy.restype = None
     lib.sog_dist_destroy.argtypes = [P]
+    lib.sog_dist_set_flags.restype = I
+    lib.sog_dist_set_flags.argtypes = [P, U]
+    lib.sog_dist_get_timings.restype = I
+    lib.sog_dist_get_timings.argtypes = [P, ctypes.POINTER(D), I]
     _LIB = lib
     return lib
 
@@ -415,6 +420,19 @@ class DistPlan:
         obj = [cls.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return cls(N_total, n_own_max, L, tol, R, rank=rank, nccl_id=obj[0], **kw)
+
+    DIST_TIMING_NAMES = ("halo", "sort", "mid_spread_fft2d", "a2a_fwd", "xfft_scale", "a2a_bwd", "fft2d_inv",
+                         "psi_halo", "gather_long_spread", "long_allreduce", "long_rest", "near")
+
+    def set_flags(self, validate=True, timing=False):
+        rc = self.lib.sog_dist_set_flags(self.h, (0 if validate else SOG_NO_VALIDATE) | (SOG_TIMING if timing else 0))
+        if rc:
+            raise _err(self.lib, rc)
+
+    def timings(self) -> dict:
+        arr = (ctypes.c_double * 12)()
+        n = self.lib.sog_dist_get_timings(self.h, arr, 12)
+        return {self.DIST_TIMING_NAMES[i]: arr[i] for i in range(n)}
 
     def describe(self) -> dict:
         n = self.lib.sog_dist_describe(self.h, None, 0)

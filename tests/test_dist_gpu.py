@@ -205,3 +205,22 @@ def test_output_tensor_validation():
     pl.eval(x, qq, good_phi, good_F)
     assert torch.isfinite(good_phi).all()
     pl.close()
+
+
+def test_dist_phase_timings_and_own_targets():
+    """SOG_TIMING on the x-slab path: per-phase device times of local rank 0 (the near field runs on
+    the side stream with own targets only); results unchanged by the timing mode."""
+    from paper_2412_04595_b200 import DistPlan, slab_owner
+    xyz, q, L, op, params = slab_plan("c5", 20000, 2)
+    owner = slab_owner(xyz[:, 0], L[0], 2)
+    idx = [np.nonzero(owner == r)[0] for r in range(2)]
+    dp = DistPlan(len(q), max(len(i) for i in idx), L, op.tol, 2, loopback=True, params=params)
+    xs = [torch.from_numpy(np.ascontiguousarray(xyz[i])).cuda() for i in idx]
+    qs = [torch.from_numpy(np.ascontiguousarray(q[i])).cuda() for i in idx]
+    p0, _ = dp.eval(xs, qs)
+    dp.set_flags(validate=True, timing=True)
+    p1, _ = dp.eval(xs, qs)
+    t = dp.timings()
+    assert len(t) == 12 and t["near"] > 0 and t["a2a_fwd"] > 0 and t["long_allreduce"] >= 0
+    assert all(torch.equal(a, b) for a, b in zip(p0, p1))
+    dp.close()
