@@ -1,5 +1,5 @@
 """Per-launch DRAM traffic of the stage kernels from an ncu --set full report, as the JSON bench.py
-reads (profiles/r01_ncu_traffic.json).  Usage: python scripts/ncu_traffic.py rep.ncu-rep out.json tag"""
+reads (profiles/r0N_ncu_traffic.json).  Usage: python scripts/ncu_traffic.py rep.ncu-rep out.json tag"""
 import csv
 import io
 import json
@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 STAGES = {"near": "k_near3<", "mid_spread": "k_mid_spread_z<", "mid_gather": "k_mid_gather_z<",
-          "long_spread": "k_long_spread_gemm<", "long_gather": "k_long_gather_bc<", "mid_scale": "k_scale_pencil_z<"}
+          "long_spread": "k_long_spread_gemm<", "long_gather": "k_long_gather_bc<", "mid_scale": "k_zpass_r<"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TUNIT = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
