@@ -145,4 +145,14 @@ __device__ __forceinline__ int wrap(int g, int I) {
     return g < 0 ? g + I : g;
 }
 
+// c += a b on the FP64 tensor path: mma.sync m8n8k4 f64 (DMMA).  Fragments (lane l, gid = l / 4,
+// tig = l % 4): a = A[gid][tig] (8 x 4, row), b = B[tig][gid] (4 x 8, col), c = C[gid][2 tig + {0, 1}].
+// 256 FMAs per warp instruction on the same FP64 pipe as DFMA (profiles/r02_fp64_peak.json), with
+// two register operands per lane instead of one shared-memory operand per FMA.
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
 }  // namespace sog

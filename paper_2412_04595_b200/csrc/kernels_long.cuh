@@ -501,6 +501,134 @@ __global__ void __launch_bounds__(256, 2) k_long_spread_gemm(LongArgs a, const i
     }
 }
 
+// S8 on the FP64 tensor path (small long grids, fp64): the anterpolation of a CTA's particle range
+// is the product C[n][g] = sum_j T_n(z_j) B_j[g], B_j[g] = q_j Wx_j(cx) Wy_j(cy) (g = cx Ily + cy,
+// dense over the Ilx x Ily grid, zero off the stencil) -- a GEMM with K = particles, done with
+// mma.sync m8n8k4 f64 (DMMA: the same FP64 pipe as DFMA, 256 FMAs per warp instruction, operands
+// straight from registers).  Warp w owns all MT n-tiles (8 layers each) x NTW column tiles (8 columns
+// each); per k-step of 4 particles a thread loads one A value per n-tile (T row) and forms one B value
+// per column tile from the staged q Wx and Wy rows.  Rows [T (8 MT) | q Wx (Ilx) | Wy (Ily)] of LS_KB
+// particles are staged (double-buffered) while the previous batch is multiplied.  Partials
+// [block][n][g] as k_long_spread_gemm writes them (summed in a fixed order by k_long_sum).
+constexpr int LS_KB = 32;
+
+template <int MT, int NTW>
+__global__ void __launch_bounds__(384) k_long_spread_mma(LongArgs a, const int4* __restrict__ g0, double gamma_x,
+                                                         double gamma_y, int per, int PCP, double* __restrict__ part) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int TW = 8 * MT, RW = (TW + a.Ilx + a.Ily + 1) & ~1;
+    const int G = a.Ilx * a.Ily, NT = (G + 7) / 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
+    const int P = a.Pl;
+    // this thread's B columns (one per column tile): staged row offsets of Wx(cx), Wy(cy)
+    int offx[NTW], offy[NTW];
+    bool colv[NTW];
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) {
+        const int col = 8 * (warp * NTW + t) + gid;
+        colv[t] = col < G;
+        const int cx = colv[t] ? col / a.Ily : 0, cy = colv[t] ? col - cx * a.Ily : 0;
+        offx[t] = TW + cx;
+        offy[t] = TW + a.Ilx + cy;
+    }
+    double c[MT][NTW][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) c[m][t][0] = c[m][t][1] = 0.0;
+    // stage particles [base, base + LS_KB): thread = (particle, role T / X / Y)
+    auto stage = [&](int base, int buf) {
+        for (int e = tid; e < 3 * LS_KB; e += blockDim.x) {
+            const int t = e / 3, role = e - 3 * t;
+            double* row = sm + ((size_t)buf * LS_KB + t) * RW;
+            const int j = base + t;
+            if (role == 0) {
+                if (j >= j1) {
+                    for (int n = 0; n < TW; ++n) row[n] = 0.0;
+                    continue;
+                }
+                const double x = a.pos[j].z * a.two_over_Lz;
+                double tm = 1.0, tc = x;
+                row[0] = 1.0;
+                for (int n = 1; n < TW; ++n) {
+                    row[n] = n < a.Pc ? tc : 0.0;
+                    const double tn = 2.0 * x * tc - tm;
+                    tm = tc;
+                    tc = tn;
+                }
+            } else {
+                const bool X = role == 1;
+                double* r = row + TW + (X ? 0 : a.Ilx);
+                const int Il = X ? a.Ilx : a.Ily;
+                for (int cc = 0; cc < Il; ++cc) r[cc] = 0.0;
+                if (j >= j1) continue;
+                const d4 pj = ld_d4(&a.pos[j]);
+                const unsigned ow = (unsigned)g0[j].w;
+                const int s0 = (int)(X ? (ow & 0xffffu) : (ow >> 16)) - 32768 - (P - 1) / 2;
+                int cc = s0 < 0 ? s0 + Il : s0;
+                const double xx = X ? pj.x : pj.y, hh = X ? a.hx : a.hy, hf = X ? a.halfx : a.halfy;
+                const double sc = X ? pj.w : 1.0;
+                if (a.kb) {
+                    auto put = [&](int u, double w, double) {
+                        const int c2 = cc + u;
+                        r[c2 >= Il ? c2 - Il : c2] = sc * w;
+                    };
+                    kb_emit_rt<false>(P, kb_offset(xx, hh, hf, s0 + (P - 1) / 2), a.kt, put);
+                } else {
+                    const double al = X ? a.invH2Sx : a.invH2Sy, gm = X ? gamma_x : gamma_y;
+                    const double d0 = ((double)s0 - hf) * hh - xx;
+                    double w = exp(-al * d0 * d0), q = exp(-al * hh * (2.0 * d0 + hh));
+                    for (int u = 0; u < P; ++u) {
+                        r[cc] = sc * w;
+                        w *= q;
+                        q *= gm;
+                        cc = cc + 1 == Il ? 0 : cc + 1;
+                    }
+                }
+            }
+        }
+    };
+    if (j0 < j1) stage(j0, 0);
+    __syncthreads();
+    const bool active = warp * NTW < NT;
+    int buf = 0;
+    for (int base = j0; base < j1; base += LS_KB, buf ^= 1) {
+        if (base + LS_KB < j1) stage(base + LS_KB, buf ^ 1);   // next batch while this one multiplies
+        if (active) {
+            const double* rows = sm + (size_t)buf * LS_KB * RW;
+#pragma unroll 2
+            for (int kk = 0; kk < LS_KB / 4; ++kk) {
+                const double* rw = rows + (size_t)(4 * kk + tig) * RW;   // particle of this thread's k slot
+                double av[MT], bv[NTW];
+#pragma unroll
+                for (int m = 0; m < MT; ++m) av[m] = rw[8 * m + gid];
+#pragma unroll
+                for (int t = 0; t < NTW; ++t) bv[t] = colv[t] ? rw[offx[t]] * rw[offy[t]] : 0.0;
+#pragma unroll
+                for (int m = 0; m < MT; ++m)
+#pragma unroll
+                    for (int t = 0; t < NTW; ++t) dmma_884(c[m][t], av[m], bv[t]);
+            }
+        }
+        __syncthreads();
+    }
+    if (active) {
+        double* o = part + (size_t)blockIdx.x * PCP * G;
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int t = 0; t < NTW; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = 8 * m + gid, col = 8 * (warp * NTW + t) + 2 * tig + h;
+                    if (n < a.Pc && col < G) o[(size_t)n * G + col] = c[m][t][h];
+                }
+    }
+}
+
 // grid[n][g] = sum over blocks (fixed order) of part[block][n][g], n < Pc
 template <typename T>
 __global__ void k_long_sum(const T* __restrict__ part, T* __restrict__ grid, int G, int Pc, int PCP,

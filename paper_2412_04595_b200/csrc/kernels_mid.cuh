@@ -132,18 +132,27 @@ struct MidZArgs {
 // base inside the NACC-slot z window, zeros elsewhere (even length)] [hdr int4: dx, dy, -,
 // chunk].  dx, dy are the stencil start relative to the tile origin: signed in [-(P-1),
 // MZ_TX) when the window does not wrap onto itself, else mod I.
-template <int P, typename T = double>
+//
+// MMA variant (fp64, k_mid_spread_zm, NP producer warps): the Wz slots form a ring of S = 8 NTZ planes,
+// plane g stored at slot g mod S (S >= NACC, so the planes live in one chunk's window never collide).
+template <int P, typename T = double, int NP = 0>
 struct SRec {
+    static constexpr bool M = NP > 0;
     static constexpr int AL = 16 / int(sizeof(T));         // elements per 16 bytes
     static constexpr int NACC = MZ_ZC + P - 1;             // register window per lane (z planes)
-    static constexpr int NZP = (NACC + 1) & ~1;            // padded Wz slots
-    static constexpr int WX = 0, WY = P, WZ = ((2 * P + AL - 1) / AL) * AL;
+    static constexpr int NTZ = (NACC + 7) / 8;             // MMA: z n-tiles of 8 planes
+    static constexpr int S = 8 * NTZ;                      // MMA: ring slots
+    static constexpr int NZP = M ? S : (NACC + 1) & ~1;    // padded Wz slots
+    // MMA: q Wx sits between XPAD zeros on each side (a 4-row patch reads 4 consecutive slots from
+    // its first row's offset, in [-3, P - 1], without bounds selects)
+    static constexpr int XPAD = M ? 3 : 0;
+    static constexpr int WX = XPAD, WY = P + 2 * XPAD, WZ = ((WY + P + AL - 1) / AL) * AL;
     static constexpr int HDR = ((WZ + NZP + AL - 1) / AL) * AL;   // int4 header, 16-byte aligned
     static constexpr int SIZE = HDR + AL;
-    static constexpr int B = 64;                           // particles per staged batch
-    static constexpr int K = SIZE * int(sizeof(T)) <= 48 * 8 ? 4 : 2;   // batch buffers in flight
+    static constexpr int NPROD = M ? NP : 2;               // producer warps (32 particles each)
+    static constexpr int B = 32 * NPROD;                   // particles per staged batch
+    static constexpr int K = M ? (NPROD <= 2 ? 4 : 2) : SIZE * int(sizeof(T)) <= 48 * 8 ? 4 : 2;   // batch buffers in flight
     static constexpr int EMAX = 1024;                      // (chunk, home tile) ranges per CTA
-    static constexpr int NPROD = 2;                        // producer warps (32 particles each)
     static constexpr int NTHR = 32 * (8 + NPROD);
     static constexpr int MINB = P <= 15 || sizeof(T) == 4 ? 2 : 1;   // CTAs per SM (register budget)
     static constexpr size_t BYTES = sizeof(T) * K * B * SIZE + sizeof(int) * (2 * EMAX + 1);
@@ -189,16 +198,26 @@ __device__ __forceinline__ void spread_flush(T (&acc)[SRec<P, T>::NACC], int c, 
 // masks) into K batch buffers; 8 consumer warps (one 4 x 8 column patch each) accumulate
 // their patch's particles.  full/empty mbarriers let consumer warps drift up to K batches
 // apart, so the per-batch imbalance between patches averages out.
-template <int P, typename T = double, bool KB = false>
-__global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spread_z(MidZArgs a, T* __restrict__ grid) {
-    using R = SRec<P, T>;
+//
+// M = true (fp64): the consumer warp's accumulation is a sequence of DMMA products.  For a group
+// of 4 same-chunk particles (k = particle), the patch update is, per x row m of the patch,
+//   C_m[y][s] += sum_k A_m[y][k] B[k][s],  A_m[y][k] = q Wx_k(x_m) Wy_k(y),  B[k][s] = Wz_k(plane of slot s)
+// (Eq. eq::gridding as a rank-4 update), y = the 8 patch columns of the row, s = the NTZ x 8 ring
+// slots: 4 NTZ mma.sync per group, the operands one Wy, four Wx and NTZ Wz loads per lane.  A
+// chunk's 4 planes (slots 4 (c mod S/4) + 0..3) are written and cleared when the sweep leaves it.
+template <int P, typename T, bool KB, int NP>
+__device__ __forceinline__ void mid_spread_body(const MidZArgs& a, T* __restrict__ grid) {
+    using R = SRec<P, T, NP>;
+    constexpr bool M = R::M;
     using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
     constexpr int p = (P - 1) / 2, NACC = R::NACC, B = R::B, K = R::K, EMAX = R::EMAX;
     extern __shared__ __align__(16) unsigned char smraw[];
     T* sRec = reinterpret_cast<T*>(smraw);      // [K][B][SIZE], then sPre[EMAX+1], sBeg[EMAX]
     int* sPre = reinterpret_cast<int*>(sRec + K * B * R::SIZE);
     int* sBeg = sPre + EMAX + 1;
-    __shared__ unsigned short sList[8][B];
+    __shared__ unsigned short sList[M ? 1 : 8][M ? 1 : B];
+    // MMA: per-warp particle list, (dx + 512 | (dy + 512) << 10 | record << 20, chunk)
+    __shared__ int2 sEnt[M ? 8 : 1][M ? B : 1];
     __shared__ unsigned char sMask[K][B];
     __shared__ unsigned long long barFull[K], barEmpty[K];
     __shared__ int sHx[8], sHy[8], sNh[2];
@@ -337,13 +356,21 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                     if (((mx >> (w & 3)) & 1) && ((my >> (w >> 2)) & 1)) mask |= 1u << w;
                 *reinterpret_cast<int4*>(rec + R::HDR) = make_int4(dx, dy, 0, c);
                 if (mask) {
-                    const int o = in.w - c * MZ_ZC;      // z offset of the stencil in the window
+                    // z offset of the stencil in the window (MMA: ring slot of its first plane)
+                    const int o = M ? ((in.w % R::S) + R::S) % R::S : in.w - c * MZ_ZC;
+                    auto zslot = [&](int i) {
+                        int t = o + i;
+                        if constexpr (M) t -= t >= R::S ? R::S : 0;
+                        return t;
+                    };
                     if constexpr (KB) {
                         // one axis at a time (P live weights, no spills at wide supports)
                         double w[P];
                         kb_weights<P, false>(kb_offset(r.x, a.hx, a.halfx, in.y + p), a.kt, w, nullptr);
 #pragma unroll
                         for (int i = 0; i < P; ++i) rec[R::WX + i] = T(r.w * w[i]);
+#pragma unroll
+                        for (int i = 0; i < R::XPAD; ++i) rec[i] = rec[R::WX + P + i] = T(0);
                         kb_weights<P, false>(kb_offset(r.y, a.hy, a.halfy, in.z + p), a.kt, w, nullptr);
 #pragma unroll
                         for (int i = 0; i < P; ++i) rec[R::WY + i] = T(w[i]);
@@ -351,7 +378,7 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                         for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
                         kb_weights<P, false>(kb_offset(r.z, a.hz, a.halfz, in.w + p), a.kt, w, nullptr);
 #pragma unroll
-                        for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(w[i]);
+                        for (int i = 0; i < P; ++i) rec[R::WZ + zslot(i)] = T(w[i]);
                     } else {
                         double wx[P], wy[P], wz[P];
                         window_weights_rec<P, false>(r.x, in.y + p, a.hx, a.halfx, a.invH2Sx, a.gamma_x, wx, nullptr);
@@ -363,9 +390,11 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
                             rec[R::WY + i] = T(wy[i]);
                         }
 #pragma unroll
+                        for (int i = 0; i < R::XPAD; ++i) rec[i] = rec[R::WX + P + i] = T(0);
+#pragma unroll
                         for (int i = 0; i < R::NZP; ++i) rec[R::WZ + i] = T(0);
 #pragma unroll
-                        for (int i = 0; i < P; ++i) rec[R::WZ + o + i] = T(wz[i]);
+                        for (int i = 0; i < P; ++i) rec[R::WZ + zslot(i)] = T(wz[i]);
                     }
                 }
             }
@@ -375,6 +404,119 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
         return;
     }
 
+    if constexpr (M) {
+        // ---------------- consumers (DMMA): warp = one 4 x 8 column patch ----------------
+        constexpr int NTZ = R::NTZ, NG = R::S / 4;
+        const int gid = lane >> 2, tig = lane & 3;
+        const int lx0 = 4 * (warp & 3), ly = 8 * (warp >> 2) + gid, cy = Y0 + ly;
+        double C[4][NTZ][2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int t = 0; t < NTZ; ++t) C[m][t][0] = C[m][t][1] = 0.0;
+        // leave chunk c: its planes sit in n-tile g / 2, lanes tig / 2 == g % 2 (g = c mod NG)
+        auto flush = [&](int c) {
+            const int g = c % NG, nt = g >> 1;
+            const bool mine = (tig >> 1) == (g & 1);
+            const bool wr = mine && c >= cb && cy < a.Iy;
+            const int pl0 = MZ_ZC * c + 2 * (tig & 1);
+#pragma unroll
+            for (int t = 0; t < NTZ; ++t) {
+                if (t != nt) continue;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int cx = X0 + lx0 + m;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (wr && cx < a.Ixk && pl0 + h < a.Izs)
+                            grid[((size_t)(pl0 + h) * a.Ixk + cx) * a.Iy + cy] = C[m][t][h];
+                        if (mine) C[m][t][h] = 0.0;
+                    }
+                }
+            }
+        };
+        int cur = cs;
+        for (int bi = 0; bi < nbat; ++bi) {
+            const int buf = bi % K;
+            mbar_wait(&barFull[buf], (bi / K) & 1);
+            const int nb = min(B, total - bi * B);
+            const T* base = sRec + buf * B * R::SIZE;
+            // this warp's particles in stream order
+            int nmy = 0;
+#pragma unroll
+            for (int s0 = 0; s0 < B; s0 += 32) {
+                const int s = s0 + lane;
+                const bool mine = s < nb && ((sMask[buf][s] >> warp) & 1);
+                const unsigned bm = __ballot_sync(0xffffffffu, mine);
+                if (mine) {
+                    const int4 h = *reinterpret_cast<const int4*>(base + s * R::SIZE + R::HDR);
+                    SOG_ASSERT(h.x > -512 && h.x < 512 && h.y > -512 && h.y < 512);
+                    sEnt[warp][nmy + __popc(bm & ((1u << lane) - 1))] =
+                        make_int2((h.x + 512) | ((h.y + 512) << 10) | (s << 20), h.w);
+                }
+                nmy += __popc(bm);
+            }
+            __syncwarp();
+            // groups of <= 4 same-chunk particles (k = particle)
+            const int last = max(nmy - 1, 0);
+            // operands of the group starting at gi (entry e of lane tig, chunk gc of its first)
+            auto prep = [&](int gi, const int2& e, int gc, double (&am)[4], double (&bz)[NTZ]) {
+                const bool valid = gi + tig < nmy && e.y == gc;   // same-chunk prefix of the group
+                const int nval = __popc(__ballot_sync(0xffffffffu, valid) & 0xfu);
+                const int dx = (e.x & 1023) - 512, dy = ((e.x >> 10) & 1023) - 512;
+                const T* rec = base + (e.x >> 20) * R::SIZE;
+                const int v = smally ? wrapc(ly - dy, a.Iy) : ly - dy;
+                const double wy = rec[R::WY + min((unsigned)v, P - 1u)];
+                const double cy0 = valid && (unsigned)v < (unsigned)P ? wy : 0.0;
+                if (!smallx) {
+                    // rows lx0 .. lx0 + 3 meet the stencil (the patch is touched): u0 in [-3, P - 1]
+                    SOG_ASSERT(lx0 - dx >= -R::XPAD && lx0 - dx <= P - 1);
+                    const T* wxr = rec + R::WX + (lx0 - dx);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) am[m] = wxr[m] * cy0;
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int u = wrapc(lx0 + m - dx, a.Ix);
+                        const double wx = rec[R::WX + min((unsigned)u, P - 1u)];
+                        am[m] = (unsigned)u < (unsigned)P ? wx * cy0 : 0.0;
+                    }
+                }
+                // invalid lanes have a zero A column, so their (finite) Wz row adds nothing
+#pragma unroll
+                for (int t = 0; t < NTZ; ++t) bz[t] = rec[R::WZ + 8 * t + gid];
+                return nval;
+            };
+            auto mma = [&](const double (&am)[4], const double (&bz)[NTZ]) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+#pragma unroll
+                    for (int t = 0; t < NTZ; ++t) dmma_884(C[m][t], am[m], bz[t]);
+            };
+            // (software-pipelining the next group's loads under this group's products measured
+            // slower: the extra registers cost occupancy)
+            int i = 0;
+            while (i < nmy) {                            // warp-uniform
+                const int2 e = sEnt[warp][min(i + tig, last)];
+                const int c0 = sEnt[warp][i].y;
+                double am[4], bz[NTZ];
+                const int nval = prep(i, e, c0, am, bz);
+                while (cur < c0) {                       // entering a later chunk
+                    flush(cur);
+                    ++cur;
+                }
+                mma(am, bz);
+                i += nval;
+            }
+            __syncwarp();
+            mbar_arrive(&barEmpty[buf]);
+        }
+        while (cur < ce) {
+            flush(cur);
+            ++cur;
+        }
+        return;
+    }
     // ---------------- consumers: warp = one 4 x 8 column patch ----------------
     const int lx = 4 * (warp & 3) + (lane >> 3), ly = 8 * (warp >> 2) + (lane & 7);
     const int cx = X0 + lx, cy = Y0 + ly;
@@ -450,6 +592,19 @@ __global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spre
         spread_flush<P, T>(acc, cur, cb, colok, cx, cy, a, grid);
         ++cur;
     }
+}
+
+template <int P, typename T = double, bool KB = false>
+__global__ void __launch_bounds__(SRec<P, T>::NTHR, SRec<P, T>::MINB) k_mid_spread_z(MidZArgs a, T* __restrict__ grid) {
+    mid_spread_body<P, T, KB, 0>(a, grid);
+}
+// DMMA variant, NP producer warps: 2 CTAs of 8 + NP warps per SM; the register file is split over
+// the 4 SM sub-partitions (16384 registers each), so the budget is set for ceil(2 (8 + NP) / 4) warps
+// per sub-partition
+constexpr int spread_mma_regs(int np) { return 16384 / ((2 * (8 + np) + 3) / 4) / 32 / 8 * 8; }
+template <int P, bool KB, int NP>
+__global__ void __maxnreg__(spread_mma_regs(NP)) k_mid_spread_zm(MidZArgs a, double* __restrict__ grid) {
+    mid_spread_body<P, double, KB, NP>(a, grid);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -1,4 +1,6 @@
 // Long-range stencil kernels (Algorithm 2, two-sided proxies) and their launchers.
+#include <algorithm>
+#include <cstdlib>
 #include "kernels_long.cuh"
 #include "launch.h"
 
@@ -156,8 +158,40 @@ int spread_gemm_t(const LongArgs& a, const int4* g0, double gx, double gy, int n
     return 1;
 }
 
+template <int MT>
+int spread_mma_go(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, double* part, double* grid,
+                  cudaStream_t st) {
+    constexpr int NTW = 3;
+    const int G = a.Ilx * a.Ily, NT = (G + 7) / 8, nw = (NT + NTW - 1) / NTW;
+    if (nw * 32 > 384) return 1;
+    const int per = (a.N + nblk - 1) / nblk;
+    const int RW = (8 * MT + a.Ilx + a.Ily + 1) & ~1;
+    const size_t sh = sizeof(double) * 2 * LS_KB * RW;
+    if (cudaFuncSetAttribute(k_long_spread_mma<MT, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
+        cudaSuccess)
+        return 2;
+    const int PCP = long_small_pcp(a.Pc);
+    k_long_spread_mma<MT, NTW><<<nblk, std::max(nw * 32, 96), sh, st>>>(a, g0, gx, gy, per, PCP, part);
+    k_long_sum<double><<<(G * a.Pc + 255) / 256, 256, 0, st>>>(part, grid, G, a.Pc, PCP, nblk);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
 int launch_long_spread_gemm(const LongArgs& a, const int4* g0, double gx, double gy, int nblk, void* part, void* grid,
                             bool f32, cudaStream_t st) {
+    // fp64 opt-in (SOG_LONG_MMA=1): the DMMA product; measured slower than the register-tiled DFMA
+    // kernel at c5 (6.3 vs 3.9 ms), so off by default
+    static const bool mma = std::getenv("SOG_LONG_MMA") && std::atoi(std::getenv("SOG_LONG_MMA")) == 1;
+    if (!f32 && mma) {
+        int r = 1;
+        switch ((a.Pc + 7) / 8) {
+            case 1: r = spread_mma_go<1>(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st); break;
+            case 2: r = spread_mma_go<2>(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st); break;
+            case 3: r = spread_mma_go<3>(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st); break;
+            case 4: r = spread_mma_go<4>(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st); break;
+            default: break;
+        }
+        if (r != 1) return r;
+    }
     return f32 ? spread_gemm_t(a, g0, gx, gy, nblk, (float*)part, (float*)grid, st)
                : spread_gemm_t(a, g0, gx, gy, nblk, (double*)part, (double*)grid, st);
 }

@@ -1,5 +1,6 @@
 // Mid-range stencil kernels (Algorithm 1) and their launchers.
 #include "kernels_mid.cuh"
+#include <cstdlib>
 #include "launch.h"
 
 namespace sog {
@@ -31,16 +32,49 @@ constexpr bool kb_compiled() { return sizeof(T) == 8 ? P <= 17 : P <= 11; }
 
 template <int P, typename T, bool KB>
 int spread_go_w(const MidZArgs& a, int nseg, T* grid, cudaStream_t st) {
-    const size_t sh = SRec<P, T>::BYTES;
+    using R = SRec<P, T>;
+    const size_t sh = R::BYTES;
     if (cudaFuncSetAttribute(k_mid_spread_z<P, T, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
         cudaSuccess)
         return 2;
-    k_mid_spread_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), SRec<P, T>::NTHR, sh, st>>>(a, grid);
+    k_mid_spread_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), R::NTHR, sh, st>>>(a, grid);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int P, bool KB, int NP>
+int spread_go_m(const MidZArgs& a, int nseg, double* grid, cudaStream_t st) {
+    using R = SRec<P, double, NP>;
+    const size_t sh = R::BYTES;
+    auto k = k_mid_spread_zm<P, KB, NP>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess ||
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+        return 2;
+    k<<<dim3(a.ntout * a.nty, nseg), R::NTHR, sh, st>>>(a, grid);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+// fp64 accumulates on the FP64 tensor path (DMMA) with 4 producer warps unless SOG_SPREAD_MMA=0
+// (the DFMA consumer); SOG_SPREAD_MMA = 2 or 3 selects 2 or 3 producer warps at P = 11 (GS window).
+// c5: DFMA 7.87 ms, DMMA with 2 / 3 / 4 producer warps 5.56 / 5.45 / 5.13 ms.
+static int spread_mma() {
+    static const int v = std::getenv("SOG_SPREAD_MMA") ? std::atoi(std::getenv("SOG_SPREAD_MMA")) : 1;
+    return v;
 }
 
 template <int P, typename T>
 int spread_go(const MidZArgs& a, int nseg, T* grid, cudaStream_t st) {
+    if constexpr (sizeof(T) == 8) {
+        const int v = spread_mma();
+        if constexpr (P == 11) {
+            if (!a.kb && v == 2) return spread_go_m<P, false, 2>(a, nseg, grid, st);
+            if (!a.kb && v == 3) return spread_go_m<P, false, 3>(a, nseg, grid, st);
+        }
+        if (v != 0) {
+            if (!a.kb) return spread_go_m<P, false, 4>(a, nseg, grid, st);
+            if constexpr (kb_compiled<P, T>()) return spread_go_m<P, true, 4>(a, nseg, grid, st);
+            return 1;
+        }
+    }
     if (!a.kb) return spread_go_w<P, T, false>(a, nseg, grid, st);
     if constexpr (kb_compiled<P, T>()) return spread_go_w<P, T, true>(a, nseg, grid, st);
     return 1;

@@ -1,0 +1,7 @@
+# mid spread DMMA check: parity + c5 bench with and without it
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kb.py tests/test_dist_gpu.py -q -x -k "not full_size" 2>&1 | tail -4
+for v in 1 0; do
+SOG_SPREAD_MMA=$v python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_sm$v.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/bench_sm$v.log').read().strip().splitlines()[-1]);print('MMA=$v', d['ms_per_step'], {k:round(v,2) for k,v in d['stages_ms'].items()})" || tail -5 gpurun_out/bench_sm$v.log
+done

@@ -6,7 +6,7 @@ import json
 import subprocess
 import sys
 
-STAGES = {"near": "k_near3<", "mid_spread": "k_mid_spread_z<", "mid_gather": "k_mid_gather_z<",
+STAGES = {"near": "k_near3<", "mid_spread": "k_mid_spread_z", "mid_gather": "k_mid_gather_z<",
           "long_spread": "k_long_spread_gemm<", "long_gather": "k_long_gather_bc<", "mid_scale": "k_zpass_r<"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TUNIT = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
