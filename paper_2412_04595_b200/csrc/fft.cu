@@ -132,4 +132,86 @@ int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, in
                : zpass_l<double>(X, M, nyh, zin0, nin, zout0, nout, f, tw, L, A, Tx, Ix, Ty, Tz, st);
 }
 
+// ---------------------------------------------------------------------------------------
+// plane FFTs (rows r2c / c2r along y, complex along x): E elements per thread, BR rows or B columns
+// per CTA; 1 = configuration not supported (the caller keeps the library transform)
+template <typename T, int E, int BR>
+int rows_go(bool inv, const void* in, void* out, long long nrows, int nyh, const FftStages& f, const void* tw,
+            const void* wpost, cudaStream_t st) {
+    using C = typename Cplx<T>::C;
+    const int Tc = f.n / E;
+    if (f.n % E || BR * Tc > (E >= 16 ? 256 : 512) || nyh != f.n + 1) return 1;
+    for (int s = 0; s < f.nst; ++s)
+        if (E % f.R[s]) return 1;
+    const int ntw = f.tw[f.nst - 1] + f.Ns[f.nst - 1] * (f.R[f.nst - 1] - 1);
+    const size_t sh = sizeof(C) * ((size_t)(f.n + 1) * BR + ntw);
+    if (sh > 227 * 1024) return 1;
+    const unsigned grid = (unsigned)((nrows + BR - 1) / BR);
+    if (!inv) {
+        if (cudaFuncSetAttribute(k_rows_r2c<T, E, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+            return 2;
+        k_rows_r2c<T, E, BR><<<grid, BR * Tc, sh, st>>>((const T*)in, (C*)out, nrows, nyh, f, (const C*)tw,
+                                                         (const C*)wpost);
+    } else {
+        if (cudaFuncSetAttribute(k_rows_c2r<T, E, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+            return 2;
+        k_rows_c2r<T, E, BR><<<grid, BR * Tc, sh, st>>>((const C*)in, (T*)out, nrows, nyh, f, (const C*)tw,
+                                                         (const C*)wpost);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <typename T, int E, int B>
+int xfft_go(bool inv, void* X, long long planes, int Ix, int nyh, const FftStages& f, const void* tw, cudaStream_t st) {
+    using C = typename Cplx<T>::C;
+    const int Tc = Ix / E;
+    if (f.n != Ix || Ix % E || B * Tc > (E >= 16 ? 256 : 512)) return 1;
+    for (int s = 0; s < f.nst; ++s)
+        if (E % f.R[s]) return 1;
+    const int ntw = f.tw[f.nst - 1] + f.Ns[f.nst - 1] * (f.R[f.nst - 1] - 1);
+    const size_t sh = sizeof(C) * ((size_t)Ix * B + ntw);
+    if (sh > 227 * 1024) return 1;
+    const int nbk = (nyh + B - 1) / B;
+    const long long nblk = planes * nbk;
+    if (nblk > 0x7fffffffLL) return 1;
+    auto k = inv ? k_xfft<T, E, B, true> : k_xfft<T, E, B, false>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess) return 2;
+    k<<<(unsigned)nblk, B * Tc, sh, st>>>((C*)X, Ix, nyh, nbk, f, (const C*)tw);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+#define SOG_PF_CASES(M_) M_(20, 2) M_(8, 4) M_(8, 8) M_(8, 16) M_(10, 4) M_(10, 8) M_(10, 16) M_(16, 4) M_(16, 8) M_(16, 16) \
+    M_(20, 4) M_(20, 8) M_(20, 16)
+
+int launch_rows_fft(bool inv, const void* in, void* out, long long nrows, int nyh, const FftStages& f, const void* tw,
+                    const void* wpost, bool f32, int E, int BR, cudaStream_t st) {
+#define C_(EE, BB)                                                                                  \
+    if (E == EE && BR == BB)                                                                        \
+        return f32 ? rows_go<float, EE, BB>(inv, in, out, nrows, nyh, f, tw, wpost, st)             \
+                   : rows_go<double, EE, BB>(inv, in, out, nrows, nyh, f, tw, wpost, st);
+    SOG_PF_CASES(C_)
+#undef C_
+    return 1;
+}
+
+int launch_xfft(bool inv, void* X, long long planes, int Ix, int nyh, const FftStages& f, const void* tw, bool f32,
+                int E, int B, cudaStream_t st) {
+#define C_(EE, BB)                                                                                  \
+    if (E == EE && B == BB)                                                                         \
+        return f32 ? xfft_go<float, EE, BB>(inv, X, planes, Ix, nyh, f, tw, st)                      \
+                   : xfft_go<double, EE, BB>(inv, X, planes, Ix, nyh, f, tw, st);
+    SOG_PF_CASES(C_)
+#undef C_
+    return 1;
+}
+
+bool plane_fft_supported(int n, int E, int B) {
+    if (n % E || (n / E) * B > (E >= 16 ? 256 : 512) || sizeof(double2) * (size_t)(n + 1) * (B + 1) > 227 * 1024) return false;
+    bool ok = false;
+#define C_(EE, BB) ok = ok || (E == EE && B == BB);
+    SOG_PF_CASES(C_)
+#undef C_
+    return ok;
+}
+
 }  // namespace sog

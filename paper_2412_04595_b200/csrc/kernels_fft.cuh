@@ -328,7 +328,7 @@ __device__ __forceinline__ void zr_stage(C (&x)[E], C* buf, int tau, int Tc, int
         if (Ns > 1) {
             const C* w = tw + jk * (R - 1);
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&w[r - 1]));
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r - 1]);   // shared or global (L1) table
         }
         dft_small<R>(v);
 #pragma unroll
@@ -436,6 +436,178 @@ static __global__ void k_mult_table(double* __restrict__ out, long long M, int n
 static __global__ void k_mult_table_f(float* __restrict__ out, const double* __restrict__ in, long long n) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n) out[e] = (float)in[e];
+}
+
+// ---------------------------------------------------------------------------------------
+// Plane FFTs of S4 / S6 (x and y), in place of a 2D r2c / c2r library transform of the z-pruned
+// planes; both are register-resident like k_zpass_r (zr_fft), one pass over HBM each.
+//
+// Rows (y): a real row of Iy = 2 n2 samples is the complex sequence z_n = x_2n + i x_2n+1 of length
+// n2; with Z = FFT_n2(z) and W = e^{-2 pi i / Iy} the half spectrum is, for k = 0 .. n2,
+//   X_k = (Z_k + conj Z_{n2-k}) / 2 - i W^k (Z_k - conj Z_{n2-k}) / 2          (Z_{n2} = Z_0)
+// and the unnormalised inverse (x_m = sum_k X_k e^{+2 pi i k m / Iy} over the Hermitian extension)
+// is z = IFFT_n2(Z'), Z'_k = (X_k + conj X_{n2-k}) + i W^{-k} (X_k - conj X_{n2-k}), x_2n = Re z_n,
+// x_2n+1 = Im z_n.  A CTA transforms BR rows (row = (plane, x)); thread (b, tau), b = t mod BR.
+// wpost[k] = W^k, k = 0 .. n2 (host table, long double).
+// the stage twiddles of plan f (ntw = sum of Ns (R - 1)) copied into shared memory
+template <typename C>
+__device__ __forceinline__ const C* stage_twiddles(C* sm, const C* __restrict__ tw, const FftStages& f) {
+    const int ntw = f.tw[f.nst - 1] + f.Ns[f.nst - 1] * (f.R[f.nst - 1] - 1);
+    for (int i = threadIdx.x; i < ntw; i += blockDim.x) sm[i] = tw[i];
+    return sm;
+}
+
+template <typename T, int E, int BR>
+__global__ void __launch_bounds__(E >= 16 ? 256 : 512, E >= 16 ? 2 : 1) k_rows_r2c(const T* __restrict__ in, typename Cplx<T>::C* __restrict__ out,
+                                                  long long nrows, int nyh, FftStages f,
+                                                  const typename Cplx<T>::C* __restrict__ tw,
+                                                  const typename Cplx<T>::C* __restrict__ wpost) {
+    using C = typename Cplx<T>::C;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* buf = reinterpret_cast<C*>(smraw);                 // [n2 + 1][BR], then the stage twiddles
+    const int n2 = f.n, Tc = n2 / E;
+    const int t = threadIdx.x, b = t & (BR - 1), tau = t / BR;
+    const long long r0 = (long long)blockIdx.x * BR;
+    const C* stw = stage_twiddles(buf + (n2 + 1) * BR, tw, f);
+    const C* src = reinterpret_cast<const C*>(in);        // row r = complex [r n2, r n2 + n2)
+    const int nt = blockDim.x;                            // BR Tc: BR n2 = nt E samples
+    {
+        C v[E];                                           // all loads in flight before the stores
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int idx = t + k * nt, bb = idx & (BR - 1), n = idx / BR;
+            v[k].x = T(0);
+            v[k].y = T(0);
+            if (r0 + bb < nrows) v[k] = src[(size_t)(r0 + bb) * n2 + n];
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int idx = t + k * nt;
+            buf[(idx / BR) * BR + (idx & (BR - 1))] = v[k];
+        }
+    }
+    __syncthreads();
+    C x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = buf[(tau + Tc * k) * BR + b];
+    zr_fft<E, BR>(x, buf, tau, Tc, b, f, stw);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; ++k) buf[(tau + Tc * k) * BR + b] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk <= E; ++kk) {                     // BR nyh = nt E + BR outputs
+        const int idx = t + kk * nt, bb = idx & (BR - 1), k = idx / BR;
+        if (idx >= BR * nyh || r0 + bb >= nrows) continue;
+        const C zk = buf[(k == n2 ? 0 : k) * BR + bb];
+        const C zc = buf[(k == 0 || k == n2 ? 0 : n2 - k) * BR + bb];
+        C fe, d;
+        fe.x = T(0.5) * (zk.x + zc.x);                    // (Z_k + conj Z_{n2-k}) / 2
+        fe.y = T(0.5) * (zk.y - zc.y);
+        d.x = T(0.5) * (zk.x - zc.x);                     // (Z_k - conj Z_{n2-k}) / 2
+        d.y = T(0.5) * (zk.y + zc.y);
+        const C w = wpost[k];
+        const C wd = cmul(w, d);
+        C X;
+        X.x = fe.x + wd.y;                                // fe - i W^k d
+        X.y = fe.y - wd.x;
+        out[(size_t)(r0 + bb) * nyh + k] = X;
+    }
+}
+
+template <typename T, int E, int BR>
+__global__ void __launch_bounds__(E >= 16 ? 256 : 512) k_rows_c2r(const typename Cplx<T>::C* __restrict__ in, T* __restrict__ out,
+                                                  long long nrows, int nyh, FftStages f,
+                                                  const typename Cplx<T>::C* __restrict__ tw,
+                                                  const typename Cplx<T>::C* __restrict__ wpost) {
+    using C = typename Cplx<T>::C;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* buf = reinterpret_cast<C*>(smraw);                 // [nyh][BR] (then the exchange buffer), twiddles
+    const int n2 = f.n, Tc = n2 / E;
+    const int t = threadIdx.x, b = t & (BR - 1), tau = t / BR;
+    const long long r0 = (long long)blockIdx.x * BR;
+    const C* stw = stage_twiddles(buf + (n2 + 1) * BR, tw, f);
+    const int nt = blockDim.x;                            // BR nyh = nt E + BR inputs
+    {
+        C v[E + 1];                                       // all loads in flight before the stores
+#pragma unroll
+        for (int kk = 0; kk <= E; ++kk) {
+            const int idx = t + kk * nt, bb = idx & (BR - 1), k = idx / BR;
+            v[kk].x = T(0);
+            v[kk].y = T(0);
+            if (idx < BR * nyh && r0 + bb < nrows) v[kk] = in[(size_t)(r0 + bb) * nyh + k];
+        }
+#pragma unroll
+        for (int kk = 0; kk <= E; ++kk) {
+            const int idx = t + kk * nt;
+            if (idx < BR * nyh) buf[idx] = v[kk];         // [k][BR]: idx = k BR + bb
+        }
+    }
+    __syncthreads();
+    C x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int n = tau + Tc * k;
+        const C a = buf[n * BR + b], c = buf[(n2 - n) * BR + b];
+        C s, d;
+        s.x = a.x + c.x;                                  // X_n + conj X_{n2-n}
+        s.y = a.y - c.y;
+        d.x = a.x - c.x;                                  // X_n - conj X_{n2-n}
+        d.y = a.y + c.y;
+        C w = wpost[n];
+        w.y = -w.y;                                       // W^{-n}
+        const C wd = cmul(w, d);
+        // Z' = s + i W^{-n} d; the inverse is conj(FFT(conj Z'))
+        x[k].x = s.x - wd.y;
+        x[k].y = -(s.y + wd.x);
+    }
+    zr_fft<E, BR>(x, buf, tau, Tc, b, f, stw);
+    if (r0 + b < nrows) {
+        C* dst = reinterpret_cast<C*>(out) + (size_t)(r0 + b) * n2;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            C v = x[k];
+            v.y = -v.y;                                   // (x_2n, x_2n+1) = conj
+            dst[tau + Tc * k] = v;
+        }
+    }
+}
+
+// x: FFT of length Ix along x of every (plane, ky) column of X [planes][Ix][nyh], in place; a CTA
+// owns B adjacent ky of one plane.  INV: the unnormalised inverse, conj(FFT(conj)).
+template <typename T, int E, int B, bool INV>
+__global__ void __launch_bounds__(E >= 16 ? 256 : 512, E >= 16 ? 2 : 1) k_xfft(typename Cplx<T>::C* __restrict__ X, int Ix, int nyh, int nbk, FftStages f,
+                                              const typename Cplx<T>::C* __restrict__ tw) {
+    using C = typename Cplx<T>::C;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* buf = reinterpret_cast<C*>(smraw);                 // [Ix][B], then the stage twiddles
+    const C* stw = stage_twiddles(buf + Ix * B, tw, f);
+    const int Tc = Ix / E;
+    const int t = threadIdx.x, b = t & (B - 1), tau = t / B;
+    const int pz = blockIdx.x / nbk, ky = (blockIdx.x - pz * nbk) * B + b;
+    const bool col = ky < nyh;
+    C* base = X + ((size_t)pz * Ix + tau) * nyh + ky;
+    const size_t stride = (size_t)Tc * nyh;
+    C x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        C v;
+        v.x = T(0);
+        v.y = T(0);
+        if (col) v = base[k * stride];
+        if (INV) v.y = -v.y;
+        x[k] = v;
+    }
+    __syncthreads();                                      // twiddles staged
+    zr_fft<E, B>(x, buf, tau, Tc, b, f, stw);
+    if (col) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            C v = x[k];
+            if (INV) v.y = -v.y;
+            base[k * stride] = v;
+        }
+    }
 }
 
 }  // namespace sog

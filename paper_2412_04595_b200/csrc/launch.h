@@ -42,6 +42,14 @@ int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, in
                  bool f32, cudaStream_t st);
 int launch_zpass_r(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
                    const void* mult, bool f32, int E, int B, cudaStream_t st);
+// plane FFTs of S4 / S6 (kernels_fft.cuh): rows r2c (inv: c2r) of nrows real rows of 2 f.n samples <->
+// nyh = f.n + 1 complex; x FFT of length Ix of every (plane, ky) column of X [planes][Ix][nyh], in
+// place.  wpost = e^{-2 pi i k / (2 f.n)}, k <= f.n.  1 = (E, B) not compiled / too large.
+int launch_rows_fft(bool inv, const void* in, void* out, long long nrows, int nyh, const FftStages& f, const void* tw,
+                    const void* wpost, bool f32, int E, int BR, cudaStream_t st);
+int launch_xfft(bool inv, void* X, long long planes, int Ix, int nyh, const FftStages& f, const void* tw, bool f32,
+                int E, int B, cudaStream_t st);
+bool plane_fft_supported(int n, int E, int B);
 // S5 multiplier table [Izs][M] (fp64, or fp32 through the fp64 scratch tmp)
 int build_mult_table(void* out, long long M, int nyh, int Izs, int L, const double* A, const double* Tx, int Ix,
                      const double* Ty, const double* Tz, bool f32, void* tmp, cudaStream_t st);

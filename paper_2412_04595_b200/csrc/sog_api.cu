@@ -147,6 +147,11 @@ struct sog_plan {
     bool zpass = false;
     int zr_E = 0, zr_B = 0;                         // register-resident variant (SOG_ZPASS=2)
     FftStages zst{};
+    // plane FFTs (x, y) of S4 / S6 by k_rows_r2c / k_xfft / k_rows_c2r (SOG_PLANEFFT=0: cuFFT 2D)
+    bool pfft = false;
+    int pr_E = 0, pr_B = 0, px_E = 0, px_B = 0;
+    FftStages prst{}, pxst{};
+    void *d_prtw = nullptr, *d_pxtw = nullptr, *d_wpost = nullptr;
     void* d_ztw = nullptr;                          // twiddles (double2, or float2 in fp32 mode)
     void* d_mult = nullptr;                         // S5 table [Izs][Ix nyh] (register-resident z pass)
     bool has_mid = false;
@@ -253,7 +258,7 @@ void free_plan(sog_plan* pl) {
     for (cufftHandle h : {pl->mfwd, pl->minv, pl->lfwd, pl->linv, pl->f2f, pl->f2i, pl->fxf, pl->fxi, pl->minv_full,
                           pl->mzfft})
         if (h) cufftDestroy(h);
-    for (void* p : {(void*)pl->mX, (void*)pl->mY, pl->d_ztw, pl->d_mult})
+    for (void* p : {(void*)pl->mX, (void*)pl->mY, pl->d_ztw, pl->d_mult, pl->d_prtw, pl->d_pxtw, pl->d_wpost})
         if (p) cudaFree(p);
     for (auto& e : pl->ev)
         if (e) cudaEventDestroy(e);
@@ -472,6 +477,49 @@ int setup(sog_plan* pl) {
                         return rc;
                     }
                     pl->zpass = true;
+                }
+            }
+            // plane FFTs: rows of Iy = 2 n2 reals through a complex FFT of n2, x columns of Ix; E elements
+            // per thread (radices dividing E), B rows / columns per CTA (SOG_PLANEFFT_B overrides both)
+            if (p.Iy % 2 == 0 && !(std::getenv("SOG_PLANEFFT") && std::atoi(std::getenv("SOG_PLANEFFT")) == 0)) {
+                // c5 (ncu, per launch): rows r2c / c2r 1.65 / 1.46 ms at 4 rows per CTA, x FFT 1.37 ms at
+                // 8 columns, E = 20; cuFFT's 2D pair 3.56 / 3.61 ms
+                const char* eb = std::getenv("SOG_PLANEFFT_B");
+                const int Brow = eb ? std::atoi(eb) : 4, Bx = eb ? std::atoi(eb) : 8;
+                std::vector<double2> twr, twx;
+                const char* ee = std::getenv("SOG_PLANEFFT_E");
+                const int Eonly = ee ? std::atoi(ee) : 0;
+                auto pick = [&](int n, int B, FftStages& f, std::vector<double2>& tw, int& Esel) {
+                    for (int E : {20, 16, 10, 8})
+                        if (!Eonly || E == Eonly)
+                            if (plane_fft_supported(n, E, B) && fft_plan_stages(n, f, tw, E)) {
+                                Esel = E;
+                                return true;
+                            }
+                    return false;
+                };
+                const int n2h = p.Iy / 2;
+                if (pick(n2h, Brow, pl->prst, twr, pl->pr_E) && pick(p.Ix, Bx, pl->pxst, twx, pl->px_E)) {
+                    pl->pr_B = Brow;
+                    pl->px_B = Bx;
+                    std::vector<double2> wp(n2h + 1);
+                    for (int k = 0; k <= n2h; ++k) {
+                        const long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)k /
+                                              (long double)p.Iy;
+                        wp[k] = make_double2((double)cosl(a), (double)sinl(a));
+                    }
+                    for (auto* pr : {&twr, &twx, &wp}) {
+                        void** dst = pr == &twr ? &pl->d_prtw : pr == &twx ? &pl->d_pxtw : &pl->d_wpost;
+                        if (pl->f32) {
+                            std::vector<float2> t2(pr->size());
+                            for (size_t i = 0; i < pr->size(); ++i)
+                                t2[i] = make_float2((float)(*pr)[i].x, (float)(*pr)[i].y);
+                            if ((rc = upload(pl, (float2**)dst, t2))) return rc;
+                        } else if ((rc = upload(pl, (double2**)dst, *pr))) {
+                            return rc;
+                        }
+                    }
+                    pl->pfft = true;
                 }
             }
             if (pl->zpass && pl->zr_E) {   // S5 table for the register-resident z pass
@@ -900,7 +948,15 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         const int nyh = p.Iy / 2 + 1;
         const long long M = (long long)p.Ix * nyh;
         const size_t gp = (size_t)p.Ix * p.Iy;
-        if (pl->f32) {
+        if (pl->pfft) {
+            const size_t esz = pl->f32 ? sizeof(float) : sizeof(double);
+            if ((rc = lchk(launch_rows_fft(false, (const char*)pl->mgrid + esz * gp * pl->zs0, pl->mX,
+                                           (long long)pl->nzf * p.Ix, nyh, pl->prst, pl->d_prtw, pl->d_wpost, pl->f32,
+                                           pl->pr_E, pl->pr_B, st))) ||
+                (rc = lchk(launch_xfft(false, pl->mX, pl->nzf, p.Ix, nyh, pl->pxst, pl->d_pxtw, pl->f32, pl->px_E,
+                                       pl->px_B, st))))
+                return rc;
+        } else if (pl->f32) {
             CKF(cufftExecR2C(pl->mfwd, (float*)pl->mgrid + gp * pl->zs0, (cufftComplex*)pl->mX));
         } else {
             CKF(cufftExecD2Z(pl->mfwd, pl->mgrid + gp * pl->zs0, pl->mX));
@@ -935,8 +991,18 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
         if ((rc = lchk(launch_zfft_transpose(pl->mspec, pl->mX, nz, M, p.Izs, z0, false, pl->f32, st)))) return rc;
         }
         const cufftHandle inv = full ? pl->minv_full : pl->minv;
-        if (pl->f32) CKF(cufftExecC2R(inv, (cufftComplex*)pl->mX, (float*)pl->mpsi + gp * z0));
-        else CKF(cufftExecZ2D(inv, pl->mX, pl->mpsi + gp * z0));
+        if (pl->pfft) {
+            const size_t esz = pl->f32 ? sizeof(float) : sizeof(double);
+            if ((rc = lchk(launch_xfft(true, pl->mX, nz, p.Ix, nyh, pl->pxst, pl->d_pxtw, pl->f32, pl->px_E, pl->px_B,
+                                       st))) ||
+                (rc = lchk(launch_rows_fft(true, pl->mX, (char*)pl->mpsi + esz * gp * z0, (long long)nz * p.Ix, nyh,
+                                           pl->prst, pl->d_prtw, pl->d_wpost, pl->f32, pl->pr_E, pl->pr_B, st))))
+                return rc;
+        } else if (pl->f32) {
+            CKF(cufftExecC2R(inv, (cufftComplex*)pl->mX, (float*)pl->mpsi + gp * z0));
+        } else {
+            CKF(cufftExecZ2D(inv, pl->mX, pl->mpsi + gp * z0));
+        }
         mark(pl, 6);
         if (stop_stage == 2) return SOG_OK;
         if ((rc = st_mid_gather(pl))) return rc;
