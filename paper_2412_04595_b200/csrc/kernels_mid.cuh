@@ -626,6 +626,8 @@ struct GRing {
     static constexpr int HOFF = ((6 * P + AL - 1) / AL) * AL;
     static constexpr int WSZ = HOFF + AL;                         // per-particle weight scratch
     static constexpr int WB = 2;                                  // particles per warp batch
+    static constexpr int NSEG = 4;                                // Gaussian weights: segments per axis
+    static constexpr int SEGL = (P + NSEG - 1) / NSEG;            //   and stencil points per segment
     static constexpr int NR = (P * P + 31) / 32;                  // column rounds per lane
     static constexpr size_t BYTES = sizeof(T) * (size_t(DR) * PL + 8 * WB * WSZ);
     static constexpr bool FITS = BYTES <= 227 * 1024;
@@ -710,21 +712,32 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
         coffS[r] = unsigned(ca[r] * WYP + cbb[r]) * unsigned(sizeof(T));
     }
     const unsigned ringS = smem_u32(ring);
-    // issue async copies of planes [p0, p1) of the window into their ring slots
+    // issue async copies of planes [p0, p1) of the window into their ring slots: one window row
+    // (plane, x) per warp iteration, lanes along y (row bases computed once per row, warp-uniform)
+    constexpr int YL = (WY + 31) / 32;                   // y elements per lane
+    int gyl[YL];
+#pragma unroll
+    for (int k = 0; k < YL; ++k) gyl[k] = wrapc(Y0 + lane + 32 * k, a.Iy);
     auto load_planes = [&](int p0, int p1) {
-        constexpr int NPL = WX * WY;
-        const int nload = (p1 - p0) * NPL;
-        for (int e = tid; e < nload; e += 256) {
-            const int pz = e / NPL, rem = e - pz * NPL;
-            const int xr = rem / WY, yr = rem - xr * WY;
+        const int nrow = (p1 - p0) * WX;
+        for (int rw = warp; rw < nrow; rw += 8) {
+            const int pz = rw / WX, xr = rw - pz * WX;
             const int plane = p0 + pz;
-            const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr, gy = wrapc(Y0 + yr, a.Iy);
-            T* dst = ring + (plane % DR) * PL + xr * WYP + yr;
+            const int gx = a.px ? wrapc(X0 + xr, a.Ix) : X0 + xr;
+            T* dst = ring + (plane % DR) * PL + xr * WYP;
             if (gx < a.Ixk) {
-                const T* srcp = psi + ((size_t)plane * a.Ixk + gx) * a.Iy + gy;
-                if (sizeof(T) == 8) cp_async8(dst, srcp); else cp_async4(dst, srcp);
+                const T* srow = psi + ((size_t)plane * a.Ixk + gx) * a.Iy;
+#pragma unroll
+                for (int k = 0; k < YL; ++k) {
+                    const int yr = lane + 32 * k;
+                    if (yr < WY) {
+                        if (sizeof(T) == 8) cp_async8(dst + yr, srow + gyl[k]); else cp_async4(dst + yr, srow + gyl[k]);
+                    }
+                }
             } else {
-                *dst = T(0);
+#pragma unroll
+                for (int k = 0; k < YL; ++k)
+                    if (lane + 32 * k < WY) dst[lane + 32 * k] = T(0);
             }
         }
     };
@@ -749,19 +762,32 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
             if (p1 > zh) { load_planes(zh, p1); zh = p1; }
             zl = max(zl, zh - DR);
         }
-        // particles of the chunk dealt round-robin over the 8 warps (k0 + warp + 8 i), WB at a time
+        // particles of the chunk dealt round-robin over the 8 warps (k0 + warp + 8 i), WB at a time.
+        // Weights of WB particles at once.  Gaussian window: lane = (particle, axis, segment of
+        // G::SEGL stencil points), each lane starts its segment with two exps and runs the recurrence
+        // over its points; KB window: lane = (particle, axis), all P points.  The lane's particle
+        // record (stencil start, one coordinate) of the next batch is loaded one batch ahead.
+        constexpr int NSG = KB ? 1 : G::NSEG;
+        const int pp = lane / (3 * NSG), rl = lane - pp * 3 * NSG, axl = rl / NSG, sg = rl - axl * NSG;
+        int4 in_n = make_int4(0, 0, 0, 0);
+        double x_n = 0.0;
+        auto fetch = [&](int kb) {
+            if (lane < 3 * NSG * G::WB && kb + 8 * pp < k1) {
+                in_n = a.minfo[kb + 8 * pp];
+                x_n = __ldg(reinterpret_cast<const double*>(&a.mpos[kb + 8 * pp]) + axl);
+            }
+        };
+        fetch(k0 + warp);
         for (int kb = k0 + warp; kb < k1; kb += G::WB * 8) {
             const int nb = min(G::WB, (k1 - kb + 7) / 8);
-            // weights of WB particles at once: lane = (particle lane/3, axis lane%3), recurrence
-            if (lane < 3 * nb) {
-                const int pp = lane / 3, axl = lane - 3 * pp;
-                const int4 in = a.minfo[kb + 8 * pp];
-                const d4 r = ld_d4(&a.mpos[kb + 8 * pp]);
+            const int4 in = in_n;
+            const double x = x_n;
+            fetch(kb + G::WB * 8);
+            if (lane < 3 * NSG * nb) {
                 const double hh = axl == 0 ? a.hx : (axl == 1 ? a.hy : a.hz);
                 const double hf = axl == 0 ? a.halfx : (axl == 1 ? a.halfy : a.halfz);
                 const double aa = axl == 0 ? a.invH2Sx : (axl == 1 ? a.invH2Sy : a.invH2Sz);
                 const double gg = axl == 0 ? a.gamma_x : (axl == 1 ? a.gamma_y : a.gamma_z);
-                const double x = axl == 0 ? r.x : (axl == 1 ? r.y : r.z);
                 const int sa = axl == 0 ? in.y : (axl == 1 ? in.z : in.w);
                 T* o = wsb + pp * G::WSZ + axl * P;
                 if constexpr (KB) {
@@ -777,18 +803,23 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                     // Gaussian recurrence; W' = 2 a (x_g - x) W (R11), stored with W so the gather
                     // loop reads it instead of every lane recomputing it
                     const double d0 = ((double)sa - hf) * hh - x;
-                    double w = exp(-aa * d0 * d0);
-                    double q = exp(-aa * hh * (2.0 * d0 + hh));
+                    const int i0 = sg * G::SEGL;
+                    const double di = d0 + i0 * hh;
+                    double w = exp(-aa * di * di);
+                    double q = exp(-aa * hh * (2.0 * di + hh));
                     const double a2 = 2.0 * aa;
 #pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        o[i] = T(w);
-                        o[3 * P + i] = T(a2 * (d0 + i * hh) * w);
+                    for (int k = 0; k < G::SEGL; ++k) {
+                        const int i = i0 + k;
+                        if (i < P) {
+                            o[i] = T(w);
+                            o[3 * P + i] = T(a2 * (d0 + i * hh) * w);
+                        }
                         w *= q;
                         q *= gg;
                     }
                 }
-                if (axl == 0) {
+                if (axl == 0 && sg == 0) {
                     int* hd = reinterpret_cast<int*>(wsb + pp * G::WSZ + G::HOFF);
                     hd[0] = a.px ? in.y - X0 + (in.y < 0 ? a.Ix : 0) : in.y - a.xorig - X0;   // relative to the tile
                     hd[1] = in.z - Y0 + (in.z < 0 ? a.Iy : 0);

@@ -30,6 +30,10 @@ struct Near4Args;
 struct Near3Args;
 struct NearPoly;
 int launch_near3p(const Near3Args& a, const NearPoly& p, int ncell, cudaStream_t st);
+struct Near5Args;
+// each pair once (kernels_near5.cuh), then out += the 13 forward-shell partials
+int launch_near5(const Near5Args& a, const NearPoly& p, int ncell, cudaStream_t st);
+int launch_near_fold(d4* out, const d4* part, int N, cudaStream_t st);
 // target-stationary near field (kernels_near4.cuh): 1 = unsupported degree / warps
 int launch_near4(const Near4Args& a, const NearPoly& p, int nw, cudaStream_t st);
 size_t near4_smem(int cap, int nw);

@@ -1,5 +1,6 @@
 // Launcher of the target-stationary near-field kernel (kernels_near4.cuh).
 #include "kernels_near4.cuh"
+#include "kernels_near5.cuh"
 #include "launch.h"
 #include "sog_internal.h"
 
@@ -45,6 +46,40 @@ int launch_near3p(const Near3Args& a, const NearPoly& p, int ncell, cudaStream_t
         case 56: return near3p_go<56>(a, p, ncell, st);
         default: return 1;
     }
+}
+
+template <int PD>
+int near5_go(const Near5Args& a, const NearPoly& p, int ncell, cudaStream_t st) {
+    NearPolyArg<PD> P;
+    for (int n = 0; n <= PD; ++n) P.c[n] = p.c[n];
+    P.inv_h = p.inv_h;
+    const size_t sh = near5_smem(a.cap);
+    if (sh > 227 * 1024) return 1;
+    if (cudaFuncSetAttribute(k_near5<PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess) return 2;
+    k_near5<PD><<<ncell, 32 * NEAR5_WARPS, sh, st>>>(a, P);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+int launch_near5(const Near5Args& a, const NearPoly& p, int ncell, cudaStream_t st) {
+    if (a.cap % 128) return 1;
+    switch (p.D) {
+        case 16: return near5_go<16>(a, p, ncell, st);
+        case 20: return near5_go<20>(a, p, ncell, st);
+        case 24: return near5_go<24>(a, p, ncell, st);
+        case 28: return near5_go<28>(a, p, ncell, st);
+        case 32: return near5_go<32>(a, p, ncell, st);
+        case 40: return near5_go<40>(a, p, ncell, st);
+        case 48: return near5_go<48>(a, p, ncell, st);
+        case 56: return near5_go<56>(a, p, ncell, st);
+        default: return 1;
+    }
+}
+
+int launch_near_fold(d4* out, const d4* part, int N, cudaStream_t st) {
+    if (N <= 0) return 0;
+    const long long nt = 4LL * N;
+    k_near_fold<><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(out, part, N);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
 int launch_near4(const Near4Args& a, const NearPoly& p, int nw, cudaStream_t st) {

@@ -27,7 +27,9 @@
 #include "kernels_mid.cuh"
 #include "launch.h"
 #include "kernels_near.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "kernels_near3.cuh"
+#include "kernels_near5.cuh"
 #include "kernels_near4.cuh"
 #include "kernels_sort.cuh"
 #include "sog_internal.h"
@@ -113,7 +115,11 @@ struct sog_plan {
     NearTable near;
     NearPoly npoly;                 // R16-G single polynomial (k_near4), when near4 is set
     bool near4 = false;
-    int near_mode = 5;              // SOG_NEAR: 3 (table, k_near3), 4 (k_near4), 5 (k_near3 + polynomial: default)
+    int near_mode = 5;              // SOG_NEAR: 3 (table, k_near3), 4 (k_near4), 5 (k_near3 + polynomial: default),
+                                    //   6 (k_near5: each pair once, + polynomial; one GPU, opt-in: slower)
+    int n5_cap = 0;                 // k_near5 staged sources per piece
+    bool nvtx_open = false;         // a stage NVTX range is open (mark())
+    d4* npart = nullptr;            // k_near5 forward-shell partials [N][13]
     int n4_kc = 1, n4_nw = 1, n4_cap = 0;
     double selfc = 0;
     cudaStream_t stream = nullptr;
@@ -249,7 +255,7 @@ void free_plan(sog_plan* pl) {
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
                     pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dstat, pl->lxyz, pl->lq, pl->sel_tmp,
-                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart};
+                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart, pl->npart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -321,7 +327,8 @@ int setup(sog_plan* pl) {
     {
         const char* env = std::getenv("SOG_NEAR");
         pl->near_mode = env ? std::atoi(env) : 5;
-        if (slab && pl->near_mode == 4) pl->near_mode = 5;       // k_near4 has no own-target filter
+        if (slab && (pl->near_mode == 4 || pl->near_mode == 6)) pl->near_mode = 5;   // own-target filter: k_near3
+        if (pl->near_mode == 6 && !(g.px && g.nzr == 1 && N < (1 << 27))) pl->near_mode = 5;
         if (pl->near_mode != 3 && !pl->f32 && g.ncx >= 3 && g.ncy >= 3 && build_near_poly(p, pl->npoly)) {
             const double m = std::max(1.0, double(pl->Ncap) / pl->ncell);       // mean particles per cell
             pl->n4_kc = std::max(1, std::min(g.ncz, int(140.0 / m)));
@@ -331,7 +338,12 @@ int setup(sog_plan* pl) {
             // expectation + 4 sigma (uniform input; rare overflows run in pieces)
             pl->n4_cap = std::max(256, std::min(capmax, int(expect + 4.0 * std::sqrt(expect) + 64)) & ~3);
             pl->near4 = true;
+            if (pl->near_mode == 6) {   // k_near5: 14 staged cells, expectation + 4 sigma, 128-blocks
+                const double e5 = 14.0 * m;
+                pl->n5_cap = std::min(4096, (int(e5 + 4.0 * std::sqrt(e5) + 16) + 127) & ~127);
+            }
         }
+        if (!pl->near4 && pl->near_mode == 6) pl->near_mode = 5;
     }
     int rc;
     if ((rc = dalloc(pl, &pl->pos, N)) || (rc = dalloc(pl, &pl->pos_s, N)) || (rc = dalloc(pl, &pl->o_near, N)) ||
@@ -342,6 +354,7 @@ int setup(sog_plan* pl) {
         (rc = dalloc(pl, &pl->qsums, 4)) || (rc = dalloc(pl, &pl->epart, ((size_t)N + 255) / 256 + 1)) || (rc = upload(pl, &pl->d_cF, pl->near.cF)) ||
         (rc = upload(pl, &pl->d_cdF, pl->near.cdF)))
         return rc;
+    if (pl->near4 && pl->near_mode == 6 && (rc = dalloc(pl, &pl->npart, (size_t)N * NEAR5_SLOTS))) return rc;
     CK(cudaMallocHost((void**)&pl->pinned, 8 * sizeof(double)));
     // mid range
     pl->has_mid = p.m >= 0;
@@ -723,8 +736,17 @@ int lchk(int r) {
     return SOG_OK;
 }
 
+// NVTX ranges (host-side, one per pipeline stage; a no-op unless a profiler injects NVTX): the
+// range opened at mark k covers the launches of stage k
+const char* const kStageName[] = {"sog S1 sort", "sog S2 near", "sog S3 mid spread", "sog S4 mid FFT",
+                                  "sog S5 mid scale", "sog S6 mid IFFT", "sog S7 mid gather",
+                                  "sog S8 long spread", "sog S9-S11 long FFT/scale/IFFT", "sog S12 long gather",
+                                  "sog S13 combine"};
 void mark(sog_plan* pl, int k) {
     if (pl->flags & SOG_TIMING) cudaEventRecord(pl->ev[k], pl->stream);
+    if (pl->nvtx_open) nvtxRangePop();
+    pl->nvtx_open = k < 11;
+    if (pl->nvtx_open) nvtxRangePushA(kStageName[k]);
 }
 
 // ---- pipeline stages (sorted order outputs o_near / o_mid / o_long) --------------------------
@@ -791,6 +813,15 @@ int st_near(sog_plan* pl) {
                     sizeof(float4) * a.cap;
         CK(cudaFuncSetAttribute(k_near3f<NEAR_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_near3f<NEAR_D><<<pl->ncell, 32 * NEAR3_WARPS, sh, st>>>(a);
+    } else if (pl->near4 && pl->near_mode == 6) {   // k_near5: each pair once (+ fold of the partials)
+        Near5Args a;
+        a.pos = pl->pos_s; a.start = pl->start; a.out = pl->o_near; a.part = pl->npart;
+        a.rc2 = p.rc * p.rc;
+        a.rc2f = (float)(a.rc2 * (1.0 + 1e-5)) + 1e-5f;
+        a.g = pl->geo;
+        a.cap = pl->n5_cap;
+        if ((rc = lchk(launch_near5(a, pl->npoly, pl->ncell, st)))) return rc;
+        if ((rc = lchk(launch_near_fold(pl->o_near, pl->npart, N, st)))) return rc;
     } else if (pl->near4 && pl->near_mode == 5) {   // k_near3 with the single polynomial (R16-G)
         Near3Args a;
         a.pos = pl->pos_s; a.start = pl->start; a.cF = pl->d_cF; a.out = pl->o_near;
@@ -1191,7 +1222,10 @@ int eval_graph(sog_plan* pl, const double* xyz, const double* q, double* phi, do
         if (ei != cudaSuccess) { pl->gexec = nullptr; return fail(SOG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
         std::memcpy(pl->gkey, key, sizeof key);
     }
-    CK(cudaGraphLaunch(pl->gexec, pl->stream));
+    nvtxRangePushA("sog_eval (CUDA graph replay)");
+    const cudaError_t el = cudaGraphLaunch(pl->gexec, pl->stream);
+    nvtxRangePop();
+    CK(el);
     return SOG_OK;
 }
 }  // namespace
@@ -1314,7 +1348,7 @@ int sog_launches_per_eval(const sog_plan* pl) {
     // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
     // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
     // [transpose,] gather, combine  (cuFFT launches are not counted)
-    return 2 + 2 + 2 + 1 + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 2;
+    return 2 + 2 + 2 + 1 + (pl->near4 && pl->near_mode == 6 ? 1 : 0) + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 2;
 }
 
 }  // extern "C"
