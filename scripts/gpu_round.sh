@@ -1,8 +1,9 @@
-# Round evidence (run on the GPU box via gpurun): smoke, main bench (the driver's command), reference
+# Round evidence (run on the GPU box via gpurun): GPU test suite, smoke, main bench (the driver's command), reference
 # arm, variant benches (each timed region >= ~0.5 s), ncu launch list of one c5 evaluation, ncu --set
 # full of the stage kernels of one c5 evaluation (summary, traffic table, details).  TAG = r02.
 TAG=${TAG:-r02}
 mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/${TAG}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -2 gpurun_out/smoke.log
 timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.log 2>&1; echo bench=$?; tail -1 gpurun_out/${TAG}_bench.log | cut -c1-400
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_ref.log 2>&1; echo ref=$?

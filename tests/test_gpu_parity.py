@@ -404,3 +404,31 @@ def test_general_b_table4_workload():
     assert rel(phi[t], phi_o) <= TOL_FP64 and rel(F[t], F_o) <= TOL_FP64, (rel(phi[t], phi_o), rel(F[t], F_o))
     ref, g = ewald2d.ewald2d_targets(xyz, q, L, t[:32], tol=1e-16)
     assert np.max(np.abs(phi[t[:32]] - ref)) / np.max(np.abs(ref)) <= 1e-12
+
+
+@pytest.mark.parametrize("name,N", [("c5", 5000), ("c4", 4000), ("c2", 3000)])
+def test_near_each_pair_once_small(name, N, monkeypatch):
+    """SOG_NEAR=6: the near sum over each pair once (k_near5, Newton's third law over the forward
+    half shell + the 13-slot fold) at the small shapes, against the oracle element by element."""
+    monkeypatch.setenv("SOG_NEAR", "6")
+    xyz, q, L = config_system(name, N=N)
+    op = make_plan(len(q), *L, 1e-6)
+    check_total(op, xyz, q)
+
+
+def test_near_each_pair_once_full_c5(monkeypatch):
+    """SOG_NEAR=6 at full c5 (N=1e7): the near component at 64 sampled targets vs the oracle, and
+    bitwise-equal repeated evaluations (every sum in k_near5 and the fold runs in a fixed order)."""
+    monkeypatch.setenv("SOG_NEAR", "6")
+    xyz, q, L = config_system("c5")
+    op = make_plan(len(q), *L, 1e-6)
+    pl = gpu_plan(op)
+    assert pl.describe()["near_kernel"] == 6
+    xd, qd = to_dev(xyz, q)
+    c1 = pl.components(xd, qd).cpu().numpy()
+    c2 = pl.components(xd, qd).cpu().numpy()
+    pl.close()
+    assert np.array_equal(c1, c2)
+    t = np.random.default_rng(5).choice(len(q), 64, replace=False)
+    po, go = O.near_field(op, O.canonicalize(xyz, op), q, targets=t)
+    assert rel(c1[0][t, 0], po) <= TOL_FP64 and rel(c1[0][t, 1:], go) <= TOL_FP64
