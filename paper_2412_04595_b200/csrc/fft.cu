@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <cmath>
 #include <vector>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "kernels_fft.cuh"
 #include "launch.h"
 
@@ -103,6 +105,65 @@ int zpass_r_go(void* X, long long M, int zin0, int nin, int zout0, int nout, con
     k_zpass_r<T, E, B><<<(unsigned)((M + B - 1) / B), B * Tc, sh, st>>>((C*)X, M, zin0, nin, zout0, nout, f,
                                                                      (const C*)tw, (const T*)mult);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+// ---- TMA z pass (fp64): tensor maps through the driver entry point (no libcuda link) ----
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+// 2D fp64 tensor [rows][cols] (row pitch cols doubles), box [box_rows][box_cols]
+bool tmap_2d(ZrTmap& m, const void* base, long long cols, long long rows, int box_cols, int box_rows) {
+    auto enc = tmap_encode();
+    if (!enc || rows <= 0) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    static_assert(sizeof(ZrTmap) == sizeof(CUtensorMap), "tensor map size");
+    return enc(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims,
+               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+template <int E, int B>
+int zpass_t_go(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+               const void* mult, cudaStream_t st) {
+    const int Tc = f.n / E;
+    if (f.n % E || B * Tc > 512) return 1;
+    for (int s = 0; s < f.nst; ++s)
+        if (E % f.R[s]) return 1;
+    ZrTmap tin, tout, tmul;
+    if (!tmap_2d(tin, X, 2 * M, nin, 2 * B, ZR_BOX) || !tmap_2d(tout, X, 2 * M, nout, 2 * B, ZR_BOX) ||
+        !tmap_2d(tmul, mult, M, f.n, B, ZR_BOX))
+        return 1;
+    const size_t sh = zr_smem(f.n, B);
+    if (sh > 227 * 1024) return 1;
+    if (cudaFuncSetAttribute(k_zpass_t<E, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
+        return 2;
+    k_zpass_t<E, B><<<(unsigned)((M + B - 1) / B), B * Tc, sh, st>>>(tin, tout, tmul, M, zin0, nin, zout0, nout, f,
+                                                                    (const double2*)tw);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+// 1 = not supported here (the caller keeps k_zpass_r): fp32, odd M, another (E, B)
+int launch_zpass_t(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+                   const void* mult, int E, int B, cudaStream_t st) {
+    if (M % 2 || M * 2 > (1LL << 31)) return 1;
+#define SOG_ZT(EE, BB) \
+    if (E == EE && B == BB) return zpass_t_go<EE, BB>(X, M, zin0, nin, zout0, nout, f, tw, mult, st);
+    SOG_ZT(10, 2) SOG_ZT(8, 2) SOG_ZT(12, 2) SOG_ZT(16, 2)
+#undef SOG_ZT
+    return 1;
 }
 
 int launch_zpass_r(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,

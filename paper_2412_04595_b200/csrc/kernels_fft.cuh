@@ -367,6 +367,114 @@ __device__ __forceinline__ void zr_fft(C (&x)[E], C* buf, int tau, int Tc, int b
 #undef SOG_ZR_LOOP
 }
 
+// ---- TMA helpers (raw PTX; tensor maps encoded on the host per launch) ----
+__device__ __forceinline__ unsigned zr_sa(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void zr_mbar_init(unsigned long long* b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(zr_sa(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void zr_mbar_expect(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(zr_sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void zr_mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "ZW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra ZW_%=;\n}" ::"r"(zr_sa(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void zr_tma_load(void* dst, const void* tmap, int c0, int c1, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            zr_sa(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(zr_sa(bar))
+        : "memory");
+}
+__device__ __forceinline__ void zr_tma_store(const void* tmap, int c0, int c1, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap), "r"(c0),
+                 "r"(c1), "r"(zr_sa(src))
+                 : "memory");
+}
+
+// Opaque 128-byte tensor map (CUtensorMap), passed by value as a __grid_constant__ parameter
+struct __align__(64) ZrTmap {
+    unsigned long long w[16];
+};
+constexpr int ZR_BOX = 256;          // rows per TMA box
+constexpr int ZR_PAD = ZR_BOX + 8;   // staging rows past n (the last box may run past the transform)
+// byte offset of the S5 rows (128-byte aligned, as every TMA destination) and the total staging
+__host__ __device__ constexpr size_t zr_mb_off(int n, int B) { return ((size_t)(n + ZR_PAD) * B * 16 + 127) & ~size_t(127); }
+__host__ __device__ constexpr size_t zr_smem(int n, int B) { return zr_mb_off(n, B) + (size_t)(n + ZR_PAD) * B * 8; }
+
+// k_zpass_r with the column block moved by TMA (fp64): the CTA's B adjacent (x, ky) columns of
+// the written planes arrive in shared memory as boxes of ZR_BOX rows x B complex (one elected
+// thread, mbarrier completion; rows outside the written planes are zero-filled by the tensor
+// map's bounds), the S5 table rows of the same columns likewise, and the result rows leave by
+// TMA stores clipped to the rows the gather reads.  No L1 traffic for the 32-byte row segments
+// that made the thread-load version L1-bound.  Staging starts on a 128-byte aligned row.
+template <int E, int B>
+__global__ void __launch_bounds__(512) k_zpass_t(const __grid_constant__ ZrTmap tin, const __grid_constant__ ZrTmap tout,
+                                                 const __grid_constant__ ZrTmap tmul, long long M, int zin0, int nin,
+                                                 int zout0, int nout, FftStages f, const double2* __restrict__ tw) {
+    static_assert(128 % (16 * B) == 0, "128-byte row groups");
+    constexpr int RA = 128 / (16 * B);                    // rows per 128 bytes of staging
+    extern __shared__ __align__(128) unsigned char smraw[];
+    const int n = f.n, Tc = n / E;
+    double2* buf = reinterpret_cast<double2*>(smraw);                       // [n + ZR_PAD][B]
+    double* mb = reinterpret_cast<double*>(smraw + zr_mb_off(n, B));        // [n + ZR_PAD][B]
+    __shared__ unsigned long long bar[2];
+    const int t = threadIdx.x, b = t & (B - 1), tau = t / B;
+    const int m0 = (int)((long long)blockIdx.x * B);
+    const int zi = zin0 - zin0 % RA;
+    if (t == 0) {
+        zr_mbar_init(&bar[0], 1);
+        zr_mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        const int nbx = (zin0 + nin - zi + ZR_BOX - 1) / ZR_BOX;
+        zr_mbar_expect(&bar[0], (unsigned)(nbx * ZR_BOX * B * 16));
+        for (int j = 0; j < nbx; ++j) zr_tma_load(buf + (size_t)(zi + ZR_BOX * j) * B, &tin, 2 * m0, zi - zin0 + ZR_BOX * j, &bar[0]);
+        const int nbm = (n + ZR_BOX - 1) / ZR_BOX;
+        zr_mbar_expect(&bar[1], (unsigned)(nbm * ZR_BOX * B * 8));
+        for (int j = 0; j < nbm; ++j) zr_tma_load(mb + (size_t)ZR_BOX * j * B, &tmul, m0, ZR_BOX * j, &bar[1]);
+    }
+    zr_mbar_wait(&bar[0], 0);
+    double2 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const int z = tau + Tc * k;
+        x[k] = (z >= zin0 && z < zin0 + nin) ? buf[(size_t)z * B + b] : make_double2(0.0, 0.0);
+    }
+    zr_fft<E, B>(x, buf, tau, Tc, b, f, tw);
+    zr_mbar_wait(&bar[1], 0);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const double m = mb[(size_t)(tau + Tc * k) * B + b];
+        x[k].x *= m;
+        x[k].y *= -m;
+    }
+    zr_fft<E, B>(x, buf, tau, Tc, b, f, tw);
+    __syncthreads();                                      // the last exchange's reads are done
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        double2 v = x[k];
+        v.y = -v.y;
+        buf[(size_t)(tau + Tc * k) * B + b] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+        const int zo = zout0 - zout0 % RA;
+        const int nbo = (zout0 + nout - zo + ZR_BOX - 1) / ZR_BOX;
+        for (int j = 0; j < nbo; ++j) zr_tma_store(&tout, 2 * m0, zo - zout0 + ZR_BOX * j, buf + (size_t)(zo + ZR_BOX * j) * B);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
 template <typename T, int E, int B>
 __global__ void __launch_bounds__(512) k_zpass_r(typename Cplx<T>::C* __restrict__ X, long long M, int zin0, int nin,
                                                  int zout0, int nout, FftStages f,

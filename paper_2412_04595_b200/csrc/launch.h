@@ -44,6 +44,9 @@ bool fft_plan_stages(int n, FftStages& f, std::vector<double2>& tw, int E = 0);
 int launch_zpass(void* X, long long M, int nyh, int zin0, int nin, int zout0, int nout, const FftStages& f,
                  const void* tw, int L, const double* A, const double* Tx, int Ix, const double* Ty, const double* Tz,
                  bool f32, cudaStream_t st);
+// the same with TMA row blocks (fp64, B = 2); 1 = not supported (use launch_zpass_r)
+int launch_zpass_t(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
+                   const void* mult, int E, int B, cudaStream_t st);
 int launch_zpass_r(void* X, long long M, int zin0, int nin, int zout0, int nout, const FftStages& f, const void* tw,
                    const void* mult, bool f32, int E, int B, cudaStream_t st);
 // plane FFTs of S4 / S6 (kernels_fft.cuh): rows r2c (inv: c2r) of nrows real rows of 2 f.n samples <->

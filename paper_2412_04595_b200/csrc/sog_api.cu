@@ -998,9 +998,14 @@ int run_pipeline(sog_plan* pl, const double* xyz, const double* q, int stop_stag
             // S4 (z), S5, S6 (z) in one kernel, in place on the plane spectra
             mark(pl, 4);
             if (pl->zr_E) {
-                if ((rc = lchk(launch_zpass_r(pl->mX, M, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, pl->d_mult,
-                                              pl->f32, pl->zr_E, pl->zr_B, st))))
-                    return rc;
+                // TMA row blocks (fp64) unless SOG_ZPASS_TMA=0; 1 = not supported: thread loads
+                static const bool tma = !(std::getenv("SOG_ZPASS_TMA") && std::atoi(std::getenv("SOG_ZPASS_TMA")) == 0);
+                int zr = pl->f32 || !tma ? 1 : launch_zpass_t(pl->mX, M, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw,
+                                                               pl->d_mult, pl->zr_E, pl->zr_B, st);
+                if (zr == 1)
+                    zr = launch_zpass_r(pl->mX, M, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, pl->d_mult, pl->f32,
+                                        pl->zr_E, pl->zr_B, st);
+                if ((rc = lchk(zr))) return rc;
             } else if ((rc = lchk(launch_zpass(pl->mX, M, nyh, pl->zs0, pl->nzf, z0, nz, pl->zst, pl->d_ztw, p.m + 1,
                                                pl->d_A, pl->d_Tx, p.Ix, pl->d_Ty, pl->d_Tz, pl->f32, st)))) {
                 return rc;
