@@ -120,18 +120,35 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
     }();
     return fn;
 }
+}  // namespace
+
+bool encode_tmap_f64(void* map128, const void* base, int rank, const unsigned long long* dims,
+                     const unsigned long long* strides_bytes, const unsigned* box) {
+    auto enc = tmap_encode();
+    if (!enc || rank < 1 || rank > 5) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        if (dims[i] == 0) return false;
+        d[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) st[i] = strides_bytes[i];
+    }
+    static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
+    return enc(reinterpret_cast<CUtensorMap*>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank,
+               const_cast<void*>(base), d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
 // 2D fp64 tensor [rows][cols] (row pitch cols doubles), box [box_rows][box_cols]
 bool tmap_2d(ZrTmap& m, const void* base, long long cols, long long rows, int box_cols, int box_rows) {
-    auto enc = tmap_encode();
-    if (!enc || rows <= 0) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-    const cuuint32_t es[2] = {1, 1};
-    static_assert(sizeof(ZrTmap) == sizeof(CUtensorMap), "tensor map size");
-    return enc(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims,
-               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (rows <= 0) return false;
+    const unsigned long long dims[2] = {(unsigned long long)cols, (unsigned long long)rows};
+    const unsigned long long strides[1] = {(unsigned long long)cols * sizeof(double)};
+    const unsigned box[2] = {(unsigned)box_cols, (unsigned)box_rows};
+    return encode_tmap_f64(&m, base, 2, dims, strides, box);
 }
 }  // namespace
 

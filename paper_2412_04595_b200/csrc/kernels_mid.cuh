@@ -618,7 +618,10 @@ template <int P, typename T = double, bool KB = false>
 struct GRing {
     static constexpr int WX = MZ_TX + P - 1, WY = MZ_TY + P - 1;
     static constexpr int WYP = WY + ((P - WY) % 16 + 16) % 16;   // row pitch = P (mod 16): conflict-free
-    static constexpr int PL = WX * WYP;                           // plane size (elements)
+    // ring slot stride (elements): holds a WX x WYP window (cp.async rows) or a dense WX x WY TMA box,
+    // rounded up to 128 bytes (TMA destinations)
+    static constexpr int E128 = 128 / int(sizeof(T));
+    static constexpr int PL = ((WX * WYP > WX * WY ? WX * WYP : WX * WY) + E128 - 1) / E128 * E128;
     static constexpr int D = MZ_ZC + P - 1;                       // planes a chunk reads
     static constexpr int DR = D + MZ_ZC;                          // ring: + the next chunk's planes (prefetch)
     static constexpr int AL = 16 / int(sizeof(T));
@@ -686,14 +689,39 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // separable weights of WB particles at once (lane = particle x axis, Gaussian recurrence) and
 // gathers them one at a time, lanes over the P x P columns (z contracted per lane, W' from the
 // stored W), 4-value butterfly reduction.
+// TMA plane boxes for the gather ring (fp64): a 3D tensor map of Psi [Izs][Ixk][Iy] with box
+// {WY, WX, 1}, and the stencil-column assignment for the dense box pitch WY: column col[r * 32 + l]
+// (a P + b, or -1) for lane l in round r, grouped so that the 16 lanes of a half-warp hit 16
+// distinct 8-byte bank pairs (a WY + b mod 16) wherever the residue classes allow.
+struct __align__(64) GatherTma {
+    unsigned long long map[16];          // CUtensorMap
+    short col[128];
+    int ok;                              // 0: cp.async rows only
+};
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, int c1, int c2, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int P, typename T = double, bool KB = false>
 __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(MidZArgs a, const T* __restrict__ psi,
-                                                                              d4* __restrict__ out) {
+                                                                              d4* __restrict__ out,
+                                                                              const __grid_constant__ GatherTma tm) {
     using G = GRing<P, T, KB>;
     constexpr int DR = G::DR, PL = G::PL, WX = G::WX, WY = G::WY, WYP = G::WYP, NR = G::NR;
-    extern __shared__ __align__(16) unsigned char smraw[];
+    // the mbarrier takes a whole 128-byte static block so that the dynamic ring after it starts on a
+    // 128-byte boundary (TMA destinations)
+    __shared__ __align__(128) unsigned long long tbarv[16];
+    unsigned long long& tbar = tbarv[0];
+    extern __shared__ __align__(128) unsigned char smraw[];
     T* sm = reinterpret_cast<T*>(smraw);
-    T* ring = sm;                                        // [DR][WX][WYP]
+    T* ring = sm;                                        // [DR][PL]: WX rows of pitch WYP (or WY)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     T* wsb = sm + DR * PL + warp * G::WB * G::WSZ;
     const int tx = a.tlo + blockIdx.x / a.nty, ty = blockIdx.x % a.nty;
@@ -701,17 +729,38 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
     const int X0 = tx * MZ_TX, Y0 = ty * MZ_TY;
     const int cb = a.c_lo + blockIdx.y * a.cps;
     const int ce = min(cb + a.cps, a.c_hi + 1);
-    // this lane's stencil columns (a, b), row-major over P x P
+    const unsigned ringS = smem_u32(ring);
+    // TMA plane boxes when the window does not wrap (x periodic: X0 + WX <= Ix; y: Y0 + WY <= Iy;
+    // an x-slab's rows past Ixk are the box's zero fill), else cp.async rows (pitch WYP)
+    const bool use_tma = sizeof(T) == 8 && tm.ok && (!a.px || X0 + WX <= a.Ix) && Y0 + WY <= a.Iy && (ringS & 127) == 0;
+    const int pitch = use_tma ? WY : WYP;
+    // this lane's stencil columns (a, b): row-major over P x P (pitch WYP), or the bank-grouped
+    // assignment of the TMA pitch; lanes without a column contribute nothing (cok)
     int ca[NR], cbb[NR];
+    bool cok[NR];
     unsigned coffS[NR];                                  // column byte offsets in a plane window
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-        const int idx = lane + 32 * r;
-        ca[r] = idx < P * P ? idx / P : 0;
-        cbb[r] = idx < P * P ? idx - ca[r] * P : 0;
-        coffS[r] = unsigned(ca[r] * WYP + cbb[r]) * unsigned(sizeof(T));
+        const int idx = use_tma ? tm.col[lane + 32 * r] : (lane + 32 * r < P * P ? lane + 32 * r : -1);
+        cok[r] = idx >= 0;
+        ca[r] = idx >= 0 ? idx / P : 0;
+        cbb[r] = idx >= 0 ? idx - ca[r] * P : 0;
+        coffS[r] = unsigned(ca[r] * pitch + cbb[r]) * unsigned(sizeof(T));
     }
-    const unsigned ringS = smem_u32(ring);
+    if (tid == 0) {
+        mbar_init(&tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    bool tpend = false;                                  // a TMA batch is in flight (uniform)
+    unsigned tph = 0;                                    // its mbarrier phase parity
+    auto tma_wait = [&]() {
+        if (tpend) {
+            mbar_wait(&tbar, tph);
+            tph ^= 1u;
+            tpend = false;
+        }
+    };
     // issue async copies of planes [p0, p1) of the window into their ring slots: one window row
     // (plane, x) per warp iteration, lanes along y (row bases computed once per row, warp-uniform)
     constexpr int YL = (WY + 31) / 32;                   // y elements per lane
@@ -719,6 +768,16 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
 #pragma unroll
     for (int k = 0; k < YL; ++k) gyl[k] = wrapc(Y0 + lane + 32 * k, a.Iy);
     auto load_planes = [&](int p0, int p1) {
+        if (use_tma) {                                   // one box per plane, issued by one thread
+            if (p1 <= p0) return;
+            tma_wait();                                  // one batch in flight at a time
+            if (tid == 0) {
+                mbar_expect_tx(&tbar, unsigned((p1 - p0) * WX * WY * sizeof(T)));
+                for (int pl = p0; pl < p1; ++pl) tma_load_3d(ring + (pl % DR) * PL, &tm.map, Y0, X0, pl, &tbar);
+            }
+            tpend = true;
+            return;
+        }
         const int nrow = (p1 - p0) * WX;
         for (int rw = warp; rw < nrow; rw += 8) {
             const int pz = rw / WX, xr = rw - pz * WX;
@@ -754,7 +813,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
             zl = nlo;
             zh = nhi;
         }
-        cp_async_wait_all();
+        if (use_tma) tma_wait(); else cp_async_wait_all();
         __syncthreads();
         // prefetch the next chunk's new planes into the slots of planes < nlo (no longer read)
         {
@@ -837,7 +896,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                     wz[i] = wsc[2 * P + i];
                     dwz[i] = wsc[5 * P + i];
                 }
-                const unsigned o0 = ringS + unsigned(hd.x * WYP + hd.y) * unsigned(sizeof(T));
+                const unsigned o0 = ringS + unsigned(hd.x * pitch + hd.y) * unsigned(sizeof(T));
                 T phi = 0, gx = 0, gy = 0, gz = 0;
                 // contraction of one stencil column (z first), then the separable x / y weights
                 auto column = [&](int rr, const T t0, const T t1) {
@@ -854,7 +913,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                     const unsigned zb = o0 + unsigned(hd.z * PL) * unsigned(sizeof(T));
 #pragma unroll
                     for (int rr = 0; rr < NR; ++rr) {
-                        if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                        if (!cok[rr]) continue;                  // no column for this lane in this round
                         T t0 = 0, t1 = 0;
                         zcontract<PL * int(sizeof(T))>(zb + coffS[rr], wz, dwz, t0, t1,
                                                        std::make_integer_sequence<int, P>{});
@@ -871,7 +930,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                     }
 #pragma unroll
                     for (int rr = 0; rr < NR; ++rr) {
-                        if (rr == NR - 1 && lane + 32 * rr >= P * P) break;
+                        if (!cok[rr]) continue;
                         const unsigned cS = coffS[rr];
                         T t0 = 0, t1 = 0;
 #pragma unroll
@@ -901,6 +960,7 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
         }
     }
     cp_async_wait_all();                                 // no copy may outlive the CTA
+    tma_wait();
 }
 
 // S7 gather for wide windows whose plane ring does not fit in shared memory: same work split

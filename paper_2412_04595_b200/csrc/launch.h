@@ -23,6 +23,10 @@ int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32
 int launch_mid_gather_z(const MidZArgs& a, int P, int nseg, int nmid, const void* psi, d4* out, bool f32,
                         cudaStream_t st);
 size_t mid_gather_smem(int P);
+// fp64 tensor map (CUtensorMap, 128 bytes) through the driver entry point; dims / box innermost first,
+// strides_bytes of dims 1..rank-1.  false: no driver entry point or an invalid shape
+bool encode_tmap_f64(void* map128, const void* base, int rank, const unsigned long long* dims,
+                     const unsigned long long* strides_bytes, const unsigned* box);
 int launch_zfft_transpose(const void* in, void* out, int nz, long long M, int Izs, int z0, bool fwd, bool f32,
                           cudaStream_t st);
 struct FftStages;

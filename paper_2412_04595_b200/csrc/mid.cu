@@ -1,6 +1,8 @@
 // Mid-range stencil kernels (Algorithm 1) and their launchers.
-#include "kernels_mid.cuh"
 #include <cstdlib>
+#include <cstring>
+#include <vector>
+#include "kernels_mid.cuh"
 #include "launch.h"
 
 namespace sog {
@@ -91,13 +93,46 @@ int launch_mid_spread_z(const MidZArgs& a, int P, int nseg, void* grid, bool f32
     }
 }
 
+// TMA boxes for the gather ring (fp64): the tensor map of Psi [Izs][Ixk][Iy] and the bank-grouped
+// column assignment for the dense box pitch WY (kernels_mid.cuh, GatherTma).  SOG_GATHER_TMA=0: off.
+template <int P, typename T, bool KB>
+void gather_tma(const MidZArgs& a, const T* psi, GatherTma& tm) {
+    using G = GRing<P, T, KB>;
+    constexpr int NR = G::NR, WX = G::WX, WY = G::WY;
+    std::memset(&tm, 0, sizeof tm);
+    static const bool on = !(std::getenv("SOG_GATHER_TMA") && std::atoi(std::getenv("SOG_GATHER_TMA")) == 0);
+    if (sizeof(T) != 8 || !on || 2 * NR > 8 || (WY * sizeof(T)) % 16 || ((size_t)a.Iy * sizeof(T)) % 16) return;
+    const unsigned long long dims[3] = {(unsigned long long)a.Iy, (unsigned long long)a.Ixk, (unsigned long long)a.Izs};
+    const unsigned long long strides[2] = {(unsigned long long)a.Iy * sizeof(T),
+                                           (unsigned long long)a.Ixk * a.Iy * sizeof(T)};
+    const unsigned box[3] = {(unsigned)WY, (unsigned)WX, 1u};
+    if (!encode_tmap_f64(tm.map, psi, 3, dims, strides, box)) return;
+    // member i of residue class r = (a WY + b) mod 16 -> half-warp group i, lane position r; the
+    // members past the last group fill the free lanes (a 2-way conflict there)
+    for (int i = 0; i < 128; ++i) tm.col[i] = -1;
+    std::vector<int> cls[16], spill;
+    for (int aa = 0; aa < P; ++aa)
+        for (int bb = 0; bb < P; ++bb) cls[(aa * WY + bb) % 16].push_back(aa * P + bb);
+    for (int r = 0; r < 16; ++r)
+        for (size_t i = 0; i < cls[r].size(); ++i) {
+            if ((int)i < 2 * NR) tm.col[(i / 2) * 32 + (i % 2) * 16 + r] = (short)cls[r][i];
+            else spill.push_back(cls[r][i]);
+        }
+    for (int c : spill)
+        for (int i = 128 - 1; i >= 0; --i)
+            if (i < 32 * NR && tm.col[i] < 0) { tm.col[i] = (short)c; break; }
+    tm.ok = 1;
+}
+
 template <int P, typename T, bool KB>
 int gather_ring(const MidZArgs& a, int nseg, const T* psi, d4* out, cudaStream_t st) {
     const size_t sh = GRing<P, T, KB>::BYTES;
     if (cudaFuncSetAttribute(k_mid_gather_z<P, T, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) !=
         cudaSuccess)
         return 2;
-    k_mid_gather_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out);
+    GatherTma tm;
+    gather_tma<P, T, KB>(a, psi, tm);
+    k_mid_gather_z<P, T, KB><<<dim3(a.ntout * a.nty, nseg), 256, sh, st>>>(a, psi, out, tm);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
