@@ -1350,10 +1350,16 @@ int sog_set_stream(sog_plan* pl, void* s) {
 
 int sog_launches_per_eval(const sog_plan* pl) {
     if (!pl) return fail(SOG_EINVAL, "null plan");
-    // prepare, scan (1 CUB kernel pair), scatter, cellsort, origins, near,
-    // [mid: key, scan, scatter, bucket, spread, scale, gather], long: spread, reduce, scale,
-    // [transpose,] gather, combine  (cuFFT launches are not counted)
-    return 2 + 2 + 2 + 1 + (pl->near4 && pl->near_mode == 6 ? 1 : 0) + (pl->has_mid ? 8 : 0) + (pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5)) + 2;
+    // launches of this library's own kernels per whole-box evaluation (CUB's scan kernels counted,
+    // cuFFT's not): sort = prepare, scan (init + scan), scatter, cellsort, stencil origins; near
+    // (+ fold for k_near5); mid = key, scan (2), place (scatter + bucket), spread, plane FFTs (rows +
+    // x, forward and inverse: 4) or the cuFFT chain's transposes (2), z pass (1) or pencil scale (1),
+    // gather; long = spread (+ sum), scale, [transpose,] gather; combine + energy sum
+    int n = 1 + 2 + 1 + 1 + 1;
+    n += 1 + (pl->near4 && pl->near_mode == 6 ? 1 : 0);
+    if (pl->has_mid) n += 1 + 2 + 2 + 1 + (pl->pfft ? 4 : 0) + (pl->zpass ? 1 : 3) + 1;
+    n += pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5);
+    return n + 2;
 }
 
 }  // extern "C"

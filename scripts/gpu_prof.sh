@@ -9,3 +9,4 @@ python scripts/ncu_summary.py gpurun_out/$TAG.ncu-rep > gpurun_out/${TAG}_summar
 ncu -i gpurun_out/$TAG.ncu-rep --page details > gpurun_out/${TAG}_details.txt 2>&1
 ncu -i gpurun_out/$TAG.ncu-rep --page source --csv > gpurun_out/${TAG}_source.csv 2>&1
 cat gpurun_out/${TAG}_summary.txt
+rm -f gpurun_out/$TAG.ncu-rep
