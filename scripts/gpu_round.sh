@@ -17,7 +17,7 @@ done
 python scripts/profile_eval.py c5 2 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python scripts/profile_eval.py c5 2 > gpurun_out/ncu_launch.log 2>&1; echo ncu_launch=$?
 python scripts/profile_eval.py c5 1 > gpurun_out/plain1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_near3|k_mid_gather_z|k_mid_spread_z|k_long_gather_bc|k_long_spread_gemm|k_zpass_r|k_combine" -s 0 -c 7 -o gpurun_out/${TAG}_full python scripts/profile_eval.py c5 1 > gpurun_out/ncu_full.log 2>&1; echo ncu_full=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_near3|k_mid_gather_z|k_mid_spread_zm|k_long_gather_bc|k_long_spread_gemm|k_zpass_t|k_combine|k_rows|k_xfft" -s 0 -c 11 -o gpurun_out/${TAG}_full python scripts/profile_eval.py c5 1 > gpurun_out/ncu_full.log 2>&1; echo ncu_full=$?
 python scripts/ncu_summary.py gpurun_out/${TAG}_full.ncu-rep > gpurun_out/${TAG}_ncu_full_summary.txt 2>&1
 ncu -i gpurun_out/${TAG}_full.ncu-rep --page details > gpurun_out/${TAG}_ncu_full_details.txt 2>&1
 python scripts/ncu_traffic.py gpurun_out/${TAG}_full.ncu-rep gpurun_out/${TAG}_ncu_traffic.json ${TAG}_ncu_full_details.txt > /dev/null 2>&1; echo traffic=$?
