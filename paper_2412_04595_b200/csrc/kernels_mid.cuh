@@ -678,6 +678,16 @@ __device__ __forceinline__ void zcontract(unsigned a, const T* wz, const T* dwz,
       t1 = fma(dwz[KZ], lds_off<KZ * PLB>(a, T(0)), t1)), ...);
 }
 
+// the same for a particle whose planes wrap around the ring: planes kz < N1 sit at the slots after
+// its first one (base a1), planes kz >= N1 at slot kz - N1 from the ring origin (base a2); N1 is a
+// compile-time constant, so every load still has an immediate offset
+template <int PLB, int N1, typename T, int... KZ>
+__device__ __forceinline__ void zcontract_w(unsigned a1, unsigned a2, const T* wz, const T* dwz, T& t0, T& t1,
+                                            std::integer_sequence<int, KZ...>) {
+    ((t0 = fma(wz[KZ], lds_off<(KZ < N1 ? KZ : KZ - N1) * PLB>(KZ < N1 ? a1 : a2, T(0)), t0),
+      t1 = fma(dwz[KZ], lds_off<(KZ < N1 ? KZ : KZ - N1) * PLB>(KZ < N1 ? a1 : a2, T(0)), t1)), ...);
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -920,26 +930,32 @@ __global__ void __launch_bounds__(256, GRing<P, T, KB>::MINB) k_mid_gather_z(Mid
                         column(rr, t0, t1);
                     }
                 } else {
-                    // shared byte addresses of the particle's window origin in its P (wrapped) planes
-                    unsigned pbS[P];
-                    int zs = hd.z;
+                    // the particle's planes wrap around the ring after n1 = DR - hd.z of them: one
+                    // instantiation per n1, immediate offsets from two bases
+                    const unsigned zb1 = o0 + unsigned(hd.z * PL) * unsigned(sizeof(T));
+                    auto rounds = [&](auto n1c) {
+                        constexpr int N1 = decltype(n1c)::value;
+                        if constexpr (N1 < P) {
 #pragma unroll
-                    for (int i = 0; i < P; ++i) {
-                        pbS[i] = o0 + unsigned(zs * PL) * unsigned(sizeof(T));
-                        zs = zs + 1 == DR ? 0 : zs + 1;
-                    }
-#pragma unroll
-                    for (int rr = 0; rr < NR; ++rr) {
-                        if (!cok[rr]) continue;
-                        const unsigned cS = coffS[rr];
-                        T t0 = 0, t1 = 0;
-#pragma unroll
-                        for (int kz = 0; kz < P; ++kz) {
-                            const T v = lds_t(pbS[kz] + cS, T(0));
-                            t0 = fma(wz[kz], v, t0);
-                            t1 = fma(dwz[kz], v, t1);
+                            for (int rr = 0; rr < NR; ++rr) {
+                                if (!cok[rr]) continue;
+                                T t0 = 0, t1 = 0;
+                                zcontract_w<PL * int(sizeof(T)), N1>(zb1 + coffS[rr], o0 + coffS[rr], wz, dwz, t0, t1,
+                                                                    std::make_integer_sequence<int, P>{});
+                                column(rr, t0, t1);
+                            }
                         }
-                        column(rr, t0, t1);
+                    };
+                    switch (DR - hd.z) {
+#define SOG_WRAP_CASE(n) \
+    case n: rounds(std::integral_constant<int, n>{}); break;
+                        SOG_WRAP_CASE(1) SOG_WRAP_CASE(2) SOG_WRAP_CASE(3) SOG_WRAP_CASE(4) SOG_WRAP_CASE(5)
+                        SOG_WRAP_CASE(6) SOG_WRAP_CASE(7) SOG_WRAP_CASE(8) SOG_WRAP_CASE(9) SOG_WRAP_CASE(10)
+                        SOG_WRAP_CASE(11) SOG_WRAP_CASE(12) SOG_WRAP_CASE(13) SOG_WRAP_CASE(14) SOG_WRAP_CASE(15)
+                        SOG_WRAP_CASE(16) SOG_WRAP_CASE(17) SOG_WRAP_CASE(18) SOG_WRAP_CASE(19) SOG_WRAP_CASE(20)
+                        SOG_WRAP_CASE(21) SOG_WRAP_CASE(22) SOG_WRAP_CASE(23) SOG_WRAP_CASE(24)
+#undef SOG_WRAP_CASE
+                        default: break;
                     }
                 }
                 // 4-value butterfly (fp64): after two levels each lane carries one value

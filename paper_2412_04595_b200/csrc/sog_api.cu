@@ -75,6 +75,44 @@ __global__ void k_combine_g(const d4* __restrict__ nearo, const d4* __restrict__
     }
 }
 
+// S13 in two passes (single GPU): sorted order with coalesced component reads -> tot[j] = (phi,
+// F = -q grad phi) and the per-block energy partials, then caller order with one 32-byte random read
+// per particle (the one-pass gather form reads four random 32-byte records per particle)
+__global__ void k_combine_s(const d4* __restrict__ nearo, const d4* __restrict__ mido, const d4* __restrict__ longo,
+                            const d4* __restrict__ pos, int n, double selfc, d4* __restrict__ tot,
+                            double* __restrict__ epart) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (j < n) {
+        const d4 a = ld_d4(&nearo[j]), b = ld_d4(&mido[j]), c = ld_d4(&longo[j]);
+        const double q = ld_d4(&pos[j]).w;
+        const double ph = a.x + b.x + c.x - q * selfc;
+        st_d4(&tot[j], d4{ph, -q * (a.y + b.y + c.y), -q * (a.z + b.z + c.z), -q * (a.w + b.w + c.w)});
+        e = 0.5 * q * ph;                                  // U = 1/2 sum q phi
+    }
+    __shared__ double se[32];
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0) se[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += se[w];
+        epart[blockIdx.x] = t;
+    }
+}
+__global__ void k_combine_u(const d4* __restrict__ tot, const int* __restrict__ iperm, int n, double* __restrict__ phi,
+                            double* __restrict__ force) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const d4 v = ld_d4(&tot[iperm[i]]);
+    if (phi) phi[i] = v.x;
+    if (force) {
+        force[3 * (size_t)i] = v.y;
+        force[3 * (size_t)i + 1] = v.z;
+        force[3 * (size_t)i + 2] = v.w;
+    }
+}
+
 // out = sum of part[0..n) in a fixed order (one block)
 __global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
     __shared__ double s[1024];
@@ -120,6 +158,7 @@ struct sog_plan {
     int n5_cap = 0;                 // k_near5 staged sources per piece
     bool nvtx_open = false;         // a stage NVTX range is open (mark())
     d4* npart = nullptr;            // k_near5 forward-shell partials [N][13]
+    d4* o_tot = nullptr;            // two-pass combine (single GPU): (phi, F) in sorted order
     int n4_kc = 1, n4_nw = 1, n4_cap = 0;
     double selfc = 0;
     cudaStream_t stream = nullptr;
@@ -255,7 +294,7 @@ void free_plan(sog_plan* pl) {
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
                     pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dstat, pl->lxyz, pl->lq, pl->sel_tmp,
-                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart, pl->npart};
+                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart, pl->npart, pl->o_tot};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (pl->pinned) cudaFreeHost(pl->pinned);
@@ -355,6 +394,9 @@ int setup(sog_plan* pl) {
         (rc = upload(pl, &pl->d_cdF, pl->near.cdF)))
         return rc;
     if (pl->near4 && pl->near_mode == 6 && (rc = dalloc(pl, &pl->npart, (size_t)N * NEAR5_SLOTS))) return rc;
+    if (!slab && !(std::getenv("SOG_COMBINE2") && std::atoi(std::getenv("SOG_COMBINE2")) == 0) &&
+        (rc = dalloc(pl, &pl->o_tot, N)))
+        return rc;
     CK(cudaMallocHost((void**)&pl->pinned, 8 * sizeof(double)));
     // mid range
     pl->has_mid = p.m >= 0;
@@ -1190,8 +1232,14 @@ int eval_body(sog_plan* pl, const double* xyz, const double* q, double* phi, dou
     int rc = run_pipeline(pl, xyz, q);
     if (rc) return rc;
     const int N = int(pl->p.N);
-    k_combine_g<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->iperm, N,
-                                                         pl->selfc, phi, force, pl->epart);
+    if (pl->o_tot) {
+        k_combine_s<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, N, pl->selfc,
+                                                             pl->o_tot, pl->epart);
+        k_combine_u<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_tot, pl->iperm, N, phi, force);
+    } else {
+        k_combine_g<<<(N + 255) / 256, 256, 0, pl->stream>>>(pl->o_near, pl->o_mid, pl->o_long, pl->pos_s, pl->iperm, N,
+                                                             pl->selfc, phi, force, pl->epart);
+    }
     k_sum_partials<<<1, 1024, 0, pl->stream>>>(pl->epart, (N + 255) / 256, pl->qsums + 2);
     CK(cudaGetLastError());
     mark(pl, 11);
@@ -1359,7 +1407,7 @@ int sog_launches_per_eval(const sog_plan* pl) {
     n += 1 + (pl->near4 && pl->near_mode == 6 ? 1 : 0);
     if (pl->has_mid) n += 1 + 2 + 2 + 1 + (pl->pfft ? 4 : 0) + (pl->zpass ? 1 : 3) + 1;
     n += pl->p.long_method == 1 ? 4 : (pl->long_small ? 4 : 5);
-    return n + 2;
+    return n + (pl->o_tot ? 3 : 2);
 }
 
 }  // extern "C"
