@@ -91,8 +91,8 @@ __device__ __forceinline__ void near_pair(const KF& kf, const Near3Args& a, cons
     gz = fma(cc, dz, gz);
 }
 
-template <int D, int PD = 0, int MINB = 1>
-__global__ void __launch_bounds__(32 * NEAR3_WARPS, MINB) k_near3(Near3Args a, NearPolyArg<PD == 0 ? 1 : PD> poly = {}) {
+template <int D, int PD = 0>
+__global__ void __launch_bounds__(32 * NEAR3_WARPS) k_near3(Near3Args a, NearPolyArg<PD == 0 ? 1 : PD> poly = {}) {
     extern __shared__ double sm[];
     double* tab = sm;                                                   // [K*(D+1)] (PD == 0)
     double2* shift = reinterpret_cast<double2*>(sm + (PD == 0 ? ((a.K * (D + 1) + 1) & ~1) : 0));   // [9]

@@ -30,14 +30,6 @@ int near3p_go(const Near3Args& a, const NearPoly& p, int ncell, cudaStream_t st)
     for (int n = 0; n <= PD; ++n) P.c[n] = p.c[n];
     P.inv_h = p.inv_h;
     const size_t sh = 10 * sizeof(double2) + NEAR3_WARPS * 160 * sizeof(int) + 16 * (size_t)a.cap;
-    // SOG_NEAR_MINB=8: register budget for 8 CTAs per SM (64 registers) instead of the compiler's 70 (7)
-    static const int minb = std::getenv("SOG_NEAR_MINB") ? std::atoi(std::getenv("SOG_NEAR_MINB")) : 1;
-    if (minb == 8) {
-        if (cudaFuncSetAttribute(k_near3<NEAR_D, PD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
-            return 2;
-        k_near3<NEAR_D, PD, 8><<<ncell, 32 * NEAR3_WARPS, sh, st>>>(a, P);
-        return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
-    }
     if (cudaFuncSetAttribute(k_near3<NEAR_D, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh) != cudaSuccess)
         return 2;
     k_near3<NEAR_D, PD><<<ncell, 32 * NEAR3_WARPS, sh, st>>>(a, P);
