@@ -126,6 +126,20 @@ int sog_eval(sog_plan* p, const double* xyz, const double* q, double* phi, doubl
  * results back, and returns after the results are in host memory. */
 int sog_eval_host(sog_plan* p, const double* xyz, const double* q, double* phi, double* force);
 
+/* Pipelined host-buffer evaluation of independent systems back to back (same plan, same N): the
+ * copy of the inputs is enqueued on a copy-in stream, the evaluation on the plan's stream once they
+ * have arrived, and the copy of phi / force (either may be NULL) on a copy-out stream once it has
+ * finished; the call returns without waiting.  Two device staging sets alternate, so the copies of
+ * one call overlap the evaluation of the previous one (PCIe copies under the compute).  Host
+ * buffers must stay valid, and inputs unmodified, until sog_host_wait(); pinned host memory makes
+ * the copies asynchronous.  No CUDA graph (the staging pointers alternate) and no per-call host
+ * synchronisation: input validation (unless SOG_NO_VALIDATE) is accumulated on the device and
+ * reported by sog_host_wait.  Single-GPU plans only (SOG_EINVAL for an x-slab rank's plan). */
+int sog_eval_host_async(sog_plan* p, const double* xyz, const double* q, double* phi, double* force);
+/* Wait for every pending sog_eval_host_async call (results in host memory); returns
+ * SOG_ENONFINITE / SOG_EZRANGE / SOG_ENONNEUTRAL if any of them had invalid input. */
+int sog_host_wait(sog_plan* p);
+
 /* Per-component outputs for parity testing: out is a DEVICE buffer of 3*N*4 doubles laid
  * out [component][i][4] with component 0 = near (Phi^N, grad Phi^N), 1 = mid, 2 = long,
  * and the 4 values (phi, dphi/dx, dphi/dy, dphi/dz), caller order, self term NOT removed. */

@@ -113,6 +113,14 @@ __global__ void k_combine_u(const d4* __restrict__ tot, const int* __restrict__ 
     }
 }
 
+// pipelined host path: fold one evaluation's input status into the accumulated status word
+__global__ void k_status_accum(const unsigned* __restrict__ dflags, const double* __restrict__ qsums,
+                               unsigned* __restrict__ acc) {
+    unsigned f = *dflags;
+    if (fabs(qsums[0]) > 1e-12 * qsums[1]) f |= 4u;      // not charge neutral (check_flags' rule)
+    *acc |= f;
+}
+
 // out = sum of part[0..n) in a fixed order (one block)
 __global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
     __shared__ double s[1024];
@@ -159,6 +167,13 @@ struct sog_plan {
     bool nvtx_open = false;         // a stage NVTX range is open (mark())
     d4* npart = nullptr;            // k_near5 forward-shell partials [N][13]
     d4* o_tot = nullptr;            // two-pass combine (single GPU): (phi, F) in sorted order
+    // pipelined host path (sog_eval_host_async): two device staging sets, copy-in / copy-out streams
+    double *ax[2] = {}, *aq[2] = {}, *aphi[2] = {}, *aforce[2] = {};
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+    bool a_used[2] = {false, false};
+    int aslot = 0;
+    unsigned* astat = nullptr;      // input status accumulated over the calls since sog_host_wait
     int n4_kc = 1, n4_nw = 1, n4_cap = 0;
     double selfc = 0;
     cudaStream_t stream = nullptr;
@@ -294,9 +309,16 @@ void free_plan(sog_plan* pl) {
                     pl->mpsi, pl->d_Tn, pl->lpart2, pl->ldbg, pl->mkey, pl->mcount, pl->mstart, pl->mcursor, pl->mtmp, pl->mpos, pl->minfo,
                     pl->scan_tmp, pl->spec2, pl->specx, pl->sbuf, pl->rbuf, pl->hsb, pl->hrb, pl->own, pl->hsend,
                     pl->hrecv, pl->pos_long, pl->fl, pl->fr, pl->nsel, pl->dstat, pl->lxyz, pl->lq, pl->sel_tmp,
-                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart, pl->npart, pl->o_tot};
+                    pl->ldS, pl->ldP, pl->ldpart, pl->d_Kd, pl->epart, pl->npart, pl->o_tot,
+                    pl->ax[0], pl->ax[1], pl->aq[0], pl->aq[1], pl->aphi[0], pl->aphi[1], pl->aforce[0],
+                    pl->aforce[1], pl->astat};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i)
+        for (cudaEvent_t e : {pl->ev_in[i], pl->ev_comp[i], pl->ev_out[i]})
+            if (e) cudaEventDestroy(e);
+    if (pl->cin) cudaStreamDestroy(pl->cin);
+    if (pl->cout) cudaStreamDestroy(pl->cout);
     if (pl->pinned) cudaFreeHost(pl->pinned);
     if (pl->pin_i) cudaFreeHost(pl->pin_i);
     if (pl->pin_d) cudaFreeHost(pl->pin_d);
@@ -1309,6 +1331,68 @@ int sog_eval_host(sog_plan* pl, const double* xyz, const double* q, double* phi,
     if (phi) CK(cudaMemcpyAsync(phi, pl->h_phi, N * sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
     if (force) CK(cudaMemcpyAsync(force, pl->h_force, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
     CK(cudaStreamSynchronize(pl->stream));
+    return SOG_OK;
+}
+
+int sog_eval_host_async(sog_plan* pl, const double* xyz, const double* q, double* phi, double* force) {
+    if (!pl || !xyz || !q) return fail(SOG_EINVAL, "null argument");
+    if (pl->R > 1) return fail(SOG_EINVAL, "the pipelined host path is single-GPU (use sog_dist_eval)");
+    const size_t N = pl->p.N;
+    int rc;
+    if (!pl->cin) {
+        for (int i = 0; i < 2; ++i) {
+            if ((rc = dalloc(pl, &pl->ax[i], 3 * N)) || (rc = dalloc(pl, &pl->aq[i], N)) ||
+                (rc = dalloc(pl, &pl->aphi[i], N)) || (rc = dalloc(pl, &pl->aforce[i], 3 * N)))
+                return rc;
+            CK(cudaEventCreateWithFlags(&pl->ev_in[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&pl->ev_comp[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&pl->ev_out[i], cudaEventDisableTiming));
+        }
+        if ((rc = dalloc(pl, &pl->astat, 1))) return rc;
+        CK(cudaMemset(pl->astat, 0, sizeof(unsigned)));
+        CK(cudaStreamCreateWithFlags(&pl->cin, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&pl->cout, cudaStreamNonBlocking));
+    }
+    const int sl = pl->aslot;
+    pl->aslot ^= 1;
+    // inputs: staging set sl, once the evaluation two calls back has consumed it
+    if (pl->a_used[sl]) CK(cudaStreamWaitEvent(pl->cin, pl->ev_comp[sl], 0));
+    CK(cudaMemcpyAsync(pl->ax[sl], xyz, 3 * N * sizeof(double), cudaMemcpyHostToDevice, pl->cin));
+    CK(cudaMemcpyAsync(pl->aq[sl], q, N * sizeof(double), cudaMemcpyHostToDevice, pl->cin));
+    CK(cudaEventRecord(pl->ev_in[sl], pl->cin));
+    // evaluation on the plan's stream once the inputs are in and set sl's previous outputs are out
+    CK(cudaStreamWaitEvent(pl->stream, pl->ev_in[sl], 0));
+    if (pl->a_used[sl]) CK(cudaStreamWaitEvent(pl->stream, pl->ev_out[sl], 0));
+    const unsigned saved = pl->flags;
+    pl->flags &= ~(unsigned)(SOG_GRAPH | SOG_TIMING);    // alternating pointers: no graph; no host syncs
+    rc = eval_body(pl, pl->ax[sl], pl->aq[sl], phi ? pl->aphi[sl] : nullptr, force ? pl->aforce[sl] : nullptr);
+    pl->flags = saved;
+    if (rc) return rc;
+    if (!(pl->flags & SOG_NO_VALIDATE)) k_status_accum<<<1, 1, 0, pl->stream>>>(pl->dflags, pl->qsums, pl->astat);
+    CK(cudaEventRecord(pl->ev_comp[sl], pl->stream));
+    // outputs back on the copy-out stream
+    CK(cudaStreamWaitEvent(pl->cout, pl->ev_comp[sl], 0));
+    if (phi) CK(cudaMemcpyAsync(phi, pl->aphi[sl], N * sizeof(double), cudaMemcpyDeviceToHost, pl->cout));
+    if (force) CK(cudaMemcpyAsync(force, pl->aforce[sl], 3 * N * sizeof(double), cudaMemcpyDeviceToHost, pl->cout));
+    CK(cudaEventRecord(pl->ev_out[sl], pl->cout));
+    pl->a_used[sl] = true;
+    return SOG_OK;
+}
+
+int sog_host_wait(sog_plan* pl) {
+    if (!pl) return fail(SOG_EINVAL, "null plan");
+    if (!pl->cin) return SOG_OK;
+    CK(cudaStreamSynchronize(pl->cout));
+    CK(cudaStreamSynchronize(pl->stream));
+    unsigned f = 0;
+    CK(cudaMemcpy(&f, pl->astat, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(pl->astat, 0, sizeof(unsigned)));
+    double e = 0.0;
+    CK(cudaMemcpy(&e, pl->qsums + 2, sizeof(double), cudaMemcpyDeviceToHost));
+    pl->last_energy = e;
+    if (f & FLAG_NONFINITE) return fail(SOG_ENONFINITE, "non-finite position or charge (pipelined call)");
+    if (f & FLAG_ZRANGE) return fail(SOG_EZRANGE, "z outside [-Lz/2, Lz/2] (pipelined call)");
+    if (f & 4u) return fail(SOG_ENONNEUTRAL, "system not charge neutral (pipelined call)");
     return SOG_OK;
 }
 

@@ -14,7 +14,8 @@ STATUS = {0: "SOG_OK", -1: "SOG_EINVAL", -2: "SOG_ENONNEUTRAL", -3: "SOG_EZRANGE
           -4: "SOG_ENONFINITE", -5: "SOG_EINFEASIBLE", -6: "SOG_ECUDA", -7: "SOG_ENCCL", -8: "SOG_ENOMEM"}
 TIMING_NAMES = ["sort", "near", "mid_spread", "mid_fft_fwd", "mid_scale", "mid_fft_inv", "mid_gather",
                 "long_spread", "long_fft_scale_ifft", "long_gather", "combine"]
-EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval", "sog_eval_host", "sog_eval_components",
+EXPORTS = ["sog_plan_create", "sog_plan_choose", "sog_plan_create_ex", "sog_eval", "sog_eval_host", "sog_eval_host_async",
+           "sog_host_wait", "sog_eval_components",
            "sog_debug_stage", "sog_last_energy", "sog_plan_destroy", "sog_last_error", "sog_plan_describe",
            "sog_get_timings", "sog_set_flags", "sog_set_stream", "sog_launches_per_eval",
            "sog_nccl_selftest", "sog_nccl_unique_id", "sog_dist_create", "sog_dist_create_loopback", "sog_dist_eval",
@@ -79,9 +80,11 @@ def load_library():
     lib.sog_plan_choose.argtypes = [ctypes.c_int64, D, D, D, D, ctypes.POINTER(Opts), ctypes.c_char_p, S]
     lib.sog_plan_create_ex.restype = P
     lib.sog_plan_create_ex.argtypes = [ctypes.c_int64, D, D, D, D, ctypes.POINTER(Opts)]
-    for name in ("sog_eval", "sog_eval_host"):
+    for name in ("sog_eval", "sog_eval_host", "sog_eval_host_async"):
         getattr(lib, name).restype = I
         getattr(lib, name).argtypes = [P, P, P, P, P]
+    lib.sog_host_wait.restype = I
+    lib.sog_host_wait.argtypes = [P]
     lib.sog_eval_components.restype = I
     lib.sog_eval_components.argtypes = [P, P, P, P]
     lib.sog_debug_stage.restype = I
@@ -262,6 +265,25 @@ class Plan:
                 raise ValueError(f"{name} must have shape {shape}")
         self._check(self.lib.sog_eval_host(self.h, xyz_p, q_p, _host_ptr(phi), _host_ptr(force)))
         return phi, force
+
+    def eval_host_async(self, xyz, q, phi, force):
+        """Pipelined host-buffer path (sog_eval_host_async): enqueue and return; results are in phi /
+        force (host arrays, pinned CPU tensors for asynchronous copies) after host_wait().  The
+        arrays must stay alive and the inputs unmodified until then."""
+        for a, shape, name in ((xyz, (self.N, 3), "xyz"), (q, (self.N,), "q"), (phi, (self.N,), "phi"),
+                               (force, (self.N, 3), "force")):
+            if tuple(a.shape) != shape:
+                raise ValueError(f"{name} must have shape {shape}")
+        self._pending = getattr(self, "_pending", []) + [(xyz, q, phi, force)]
+        self._check(self.lib.sog_eval_host_async(self.h, _host_ptr(xyz), _host_ptr(q), _host_ptr(phi),
+                                                 _host_ptr(force)))
+
+    def host_wait(self):
+        """Wait for every pending eval_host_async call."""
+        try:
+            self._check(self.lib.sog_host_wait(self.h))
+        finally:
+            self._pending = []
 
     def components(self, xyz, q):
         """[3, N, 4] tensor: near / mid / long (phi, dphi/dx, dphi/dy, dphi/dz), self term not removed."""

@@ -184,6 +184,44 @@ def test_determinism_and_host_path():
     assert np.array_equal(ph, a[0].cpu().numpy()) and np.array_equal(F, a[1].cpu().numpy())
 
 
+def test_pipelined_host_path():
+    """sog_eval_host_async / sog_host_wait: three independent systems (same plan) enqueued back to
+    back with alternating staging sets give the same bits as one-at-a-time device evaluations, the
+    energy of the last one, and invalid input in any pipelined call is reported by host_wait."""
+    xyz, q, L = config_system("c2", N=20000)
+    op = make_plan(len(q), *L, 1e-6)
+    pl = gpu_plan(op, validate=True)
+    rng = np.random.default_rng(11)
+    systems = []
+    for k in range(3):
+        x = np.ascontiguousarray(xyz + rng.uniform(-0.3, 0.3, xyz.shape) * np.array([1, 1, 0]))
+        qq = q * (1 if k % 2 == 0 else -1)
+        systems.append((torch.from_numpy(x).pin_memory(), torch.from_numpy(np.ascontiguousarray(qq)).pin_memory()))
+    outs = [(torch.empty(len(q), dtype=torch.float64).pin_memory(), torch.empty(len(q), 3, dtype=torch.float64).pin_memory())
+            for _ in systems]
+    for (x, qq), (ph, F) in zip(systems, outs):
+        pl.eval_host_async(x, qq, ph, F)
+    pl.host_wait()
+    for (x, qq), (ph, F) in zip(systems, outs):
+        a = pl.eval(x.cuda(), qq.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(ph, a[0].cpu()) and torch.equal(F, a[1].cpu())
+    U_last = pl.energy()
+    pl.eval_host_async(*systems[2], *outs[2])
+    pl.host_wait()
+    assert pl.energy() == U_last
+    bad = systems[1][0].clone()
+    bad[7, 2] = 10.0 * L[2]                      # z outside [-Lz/2, Lz/2]
+    pl.eval_host_async(systems[0][0], systems[0][1], *outs[0])
+    pl.eval_host_async(bad, systems[1][1], *outs[1])
+    from paper_2412_04595_b200.sog import SogError
+    with pytest.raises(SogError):
+        pl.host_wait()
+    pl.eval_host_async(systems[0][0], systems[0][1], *outs[0])
+    pl.host_wait()                               # the error state does not stick
+    pl.close()
+
+
 def test_cuda_graph_replay_is_bitwise_identical():
     """SOG_GRAPH: the captured evaluation gives the same bits as the stream launches, re-captures
     when the caller's buffers change, and follows new input values in the same buffers."""
