@@ -370,8 +370,9 @@ def _host_ptr(a):
             raise ValueError("host arrays must be C-contiguous float64")
         return a.ctypes.data
     # torch CPU tensor
-    if a.is_cuda or not a.is_contiguous():
-        raise ValueError("host tensors must be contiguous CPU tensors")
+    import torch
+    if a.is_cuda or not a.is_contiguous() or a.dtype != torch.float64:
+        raise ValueError("host tensors must be contiguous float64 CPU tensors")
     return a.data_ptr()
 
 
