@@ -259,7 +259,7 @@ int xfft_go(bool inv, void* X, long long planes, int Ix, int nyh, const FftStage
 }
 
 #define SOG_PF_CASES(M_) M_(20, 2) M_(8, 4) M_(8, 8) M_(8, 16) M_(10, 4) M_(10, 8) M_(10, 16) M_(16, 4) M_(16, 8) M_(16, 16) \
-    M_(20, 4) M_(20, 8) M_(20, 16)
+    M_(20, 4) M_(20, 8) M_(20, 16) M_(12, 4) M_(12, 8) M_(12, 16)
 
 int launch_rows_fft(bool inv, const void* in, void* out, long long nrows, int nyh, const FftStages& f, const void* tw,
                     const void* wpost, bool f32, int E, int BR, cudaStream_t st) {

@@ -567,7 +567,7 @@ int setup(sog_plan* pl) {
                 const char* ee = std::getenv("SOG_PLANEFFT_E");
                 const int Eonly = ee ? std::atoi(ee) : 0;
                 auto pick = [&](int n, int B, FftStages& f, std::vector<double2>& tw, int& Esel) {
-                    for (int E : {20, 16, 10, 8})
+                    for (int E : {20, 16, 12, 10, 8})     // 12: lengths with radix 3 (576 = 2^6 3^2, 288, 96)
                         if (!Eonly || E == Eonly)
                             if (plane_fft_supported(n, E, B) && fft_plan_stages(n, f, tw, E)) {
                                 Esel = E;
