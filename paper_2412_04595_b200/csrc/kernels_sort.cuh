@@ -106,6 +106,32 @@ __global__ void k_cellsort(const int* __restrict__ start, int ncell, const int* 
     int lane = threadIdx.x & 31;
     if (warp >= ncell) return;
     int s = start[warp], n = start[warp + 1] - s;
+    if (n <= 64) {
+        // the cell's (z, index) pairs in registers (two per lane), ranks by broadcasting each pair:
+        // the same order as the loop below without its dependent global loads per comparison
+        const int e0 = lane, e1 = lane + 32;
+        const int m0 = e0 < n ? tmp[s + e0] : 0, m1 = e1 < n ? tmp[s + e1] : 0;
+        const double z0 = e0 < n ? pos[m0].z : 0.0, z1 = e1 < n ? pos[m1].z : 0.0;
+        int r0 = 0, r1 = 0;
+        for (int f = 0; f < n; ++f) {
+            const int src = f & 31;
+            const double zo = __shfl_sync(0xffffffffu, f < 32 ? z0 : z1, src);
+            const int o = __shfl_sync(0xffffffffu, f < 32 ? m0 : m1, src);
+            r0 += (zo < z0 || (zo == z0 && o < m0));
+            r1 += (zo < z1 || (zo == z1 && o < m1));
+        }
+        if (e0 < n) {
+            perm[s + r0] = m0;
+            iperm[m0] = s + r0;
+            st_d4(&pos_s[s + r0], ld_d4(&pos[m0]));
+        }
+        if (e1 < n) {
+            perm[s + r1] = m1;
+            iperm[m1] = s + r1;
+            st_d4(&pos_s[s + r1], ld_d4(&pos[m1]));
+        }
+        return;
+    }
     for (int e = lane; e < n; e += 32) {
         int my = tmp[s + e];
         const double zm = pos[my].z;
