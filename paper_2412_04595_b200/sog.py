@@ -61,7 +61,16 @@ def _set_window(o, window, params, long_method="fft"):
 
 
 def lib_path() -> str:
-    return os.path.join(HERE, "lib", "libsog.so")
+    # SOG_LIB: another in-tree build of the same library under lib/ (A/B measurements of kernel
+    # variants, scripts/gpu_ab_libs.sh); nothing outside the package's lib/ directory is loaded
+    lib_dir = os.path.join(HERE, "lib")
+    alt = os.environ.get("SOG_LIB")
+    if alt:
+        alt = os.path.realpath(alt if os.path.isabs(alt) else os.path.join(lib_dir, alt))
+        if os.path.dirname(alt) != os.path.realpath(lib_dir):
+            raise ImportError(f"SOG_LIB={alt}: only builds in {lib_dir} can be loaded")
+        return alt
+    return os.path.join(lib_dir, "libsog.so")
 
 
 def load_library():

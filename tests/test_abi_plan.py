@@ -115,3 +115,15 @@ def test_general_b_c1_solve_matches_oracle(b, tol):
     assert abs(d["r0"] - op.r0) <= 1e-14 * op.r0 and abs(d["omega"] - op.omega) <= 1e-14
     for k in ("M", "m", "Ix", "Iy", "Izs", "P", "Pc", "Ilx"):
         assert d[k] == getattr(op, k), k
+
+
+def test_sog_lib_override_stays_in_tree(monkeypatch, tmp_path):
+    """SOG_LIB (A/B of in-tree builds) may name a build under the package's lib/ only."""
+    lib_dir = os.path.dirname(B.lib_path())
+    monkeypatch.setenv("SOG_LIB", "libsog_variant.so")
+    assert B.lib_path() == os.path.join(os.path.realpath(lib_dir), "libsog_variant.so")
+    monkeypatch.setenv("SOG_LIB", str(tmp_path / "libsog.so"))
+    with pytest.raises(ImportError):
+        B.lib_path()
+    monkeypatch.delenv("SOG_LIB")
+    assert B.lib_path() == os.path.join(lib_dir, "libsog.so")
