@@ -476,6 +476,70 @@ def long_gather(plan: Plan, xyz, Psi: np.ndarray):
     return A * phi, A * grad
 
 
+# ------------------------------------------- App. C: one-sided Taylor form of Alg. 2 steps 1-3
+# Not on the GPU path (NEXT #3): kept as a checked reference for the measured
+# comparison with the two-sided K_ab form (tests/test_oracle_pins.py::test_taylor_variant_*).
+def taylor_bound(plan: Plan, Q: int) -> float:
+    """Lemma lemma::Taylor (Eq. eq::Taylor2, P:1272-1275) for the variable App. C expands in
+    (R23): the Lagrange remainder x^Q / Q! at x = (z_a - z_j)^2 / s^2 <= L_z^2 / s_{m+1}^2 = 1/eta^2
+    (z_a - z_j spans [-L_z, L_z], twice the lemma's interval, so (2 eta)^{2Q} becomes eta^{2Q}),
+    eta = s_{m+1} / L_z here."""
+    _, s = plan.weights()
+    eta = s[plan.m + 1] / plan.Lz
+    return 1.0 / (math.factorial(Q) * eta ** (2 * Q))
+
+
+def long_spread_taylor(plan: Plan, xyz, q, Q: int) -> np.ndarray:
+    """App. C: S^p_grid([r, z_a]) = sum_j q_j W(r - r_j) ((z_a - z_j)/L_z)^{2p},
+    p = 0..Q-1, on the long grid x the Pc Chebyshev proxies z_a; shape (Q, Pc, Ilx, Ily)."""
+    (gx, Wx, _), (gy, Wy, _) = long_stencils(plan, xyz)
+    za = 0.5 * plan.Lz * cheb_nodes(plan.Pc)
+    d = (za[None, :] - xyz[:, 2][:, None]) / plan.Lz                       # (n, Pc)
+    mom = np.stack([d ** (2 * p) for p in range(Q)], axis=1).reshape(len(q), -1)   # (n, Q Pc)
+    G = np.zeros(Q * plan.Pc * plan.Ilx * plan.Ily)
+    layer = np.arange(Q * plan.Pc) * (plan.Ilx * plan.Ily)
+    for a in range(plan.Pl):
+        for b in range(plan.Pl):
+            idx = (gx[:, a] * plan.Ily + gy[:, b])[:, None] + layer[None, :]
+            val = (q * Wx[:, a] * Wy[:, b])[:, None] * mom
+            np.add.at(G, idx.ravel(), val.ravel())
+    return G.reshape(Q, plan.Pc, plan.Ilx, plan.Ily)
+
+
+def long_coeff_taylor(plan: Plan, Q: int) -> np.ndarray:
+    """A_p(kdot) (P:1284-1287) = (-1)^p / p! |W_hat(kdot)|^{-2} sum_{l>m} w_l L_z^{2p} / s_l^{2p-2}
+    e^{-s_l^2 |kdot|^2 / 4}, with the factor pi of Eq. eq::trun2 as in long_kernel and, at kdot = 0,
+    the p = 0 term dropped (R10: the constant of e^{-d^2/s^2} is the expm1 that long_kernel removes);
+    shape (Q, Ilx, Ily//2+1)."""
+    w, s = plan.weights()
+    kx = 2.0 * np.pi * np.fft.fftfreq(plan.Ilx, d=plan.hlx)
+    ky = 2.0 * np.pi * np.fft.rfftfreq(plan.Ily, d=plan.hly)
+    k2 = kx[:, None] ** 2 + ky[None, :] ** 2
+    A = np.zeros((Q,) + k2.shape)
+    for p in range(Q):
+        for ell in range(plan.m + 1, plan.M + 1):
+            A[p] += w[ell] * s[ell] ** 2 * (plan.Lz / s[ell]) ** (2 * p) * np.exp(-s[ell] ** 2 * k2 / 4.0)
+        A[p] *= (-1) ** p / math.factorial(p)
+    A[0, 0, 0] = 0.0
+    Hx = window_half_width(plan.window, plan.Pl, plan.hlx)
+    Hy = window_half_width(plan.window, plan.Pl, plan.hly)
+    What = window_hat(plan, kx, Hx, long=True)[:, None] * window_hat(plan, ky, Hy, long=True)[None, :]
+    return math.pi * A / What[None] ** 2
+
+
+def long_range_taylor(plan: Plan, xyz, q, Q: int, targets=None):
+    """Phi^long by App. C: 2D FFT of every (p, z_a) layer, S_hat_scal(kdot, z_a) = sum_p A_p(kdot)
+    S_hat^p(kdot, z_a), inverse 2D FFT per proxy layer, and the gather of Alg. 2 step 5
+    (window in x, y, Chebyshev interpolation in z at the target: the moments are polynomials of
+    degree 2(Q-1) in z_a, exact in the Pc-point interpolant when Pc >= 2Q - 1)."""
+    tgt = slice(None) if targets is None else np.asarray(targets)
+    G = long_spread_taylor(plan, xyz, q, Q)
+    Ghat = scipy.fft.rfft2(G, axes=(2, 3), workers=_WORKERS)
+    Psi_hat = np.einsum("pxy,paxy->axy", long_coeff_taylor(plan, Q), Ghat)
+    Psi = scipy.fft.irfft2(Psi_hat, s=G.shape[2:], axes=(1, 2), workers=_WORKERS)
+    return long_gather(plan, xyz[tgt], Psi)
+
+
 # --------------------------------------------------- long range without FFT (Alg. 3, App. B)
 def long_modes(plan: Plan):
     """R8-D mode set: kx = 2 pi n / Lx, n = -Kx..Kx; ky = 2 pi n / Ly, n = 0..Ky (half plane:

@@ -446,3 +446,41 @@ def test_validation_errors():
         P.make_plan(10, 5.0, 5.0, 5.0, 1e-15)
     x = sog.canonicalize(np.array([[3.0, -2.6, 0.1], [-2.5, 2.5, 2.5]]), p)
     assert np.allclose(x, [[-2.0, 2.4, 0.1], [-2.5, -2.5, 2.5]])
+
+
+# ------------------------------------------------------------------ App. C Taylor form (NEXT #3)
+def test_taylor_variant_kernel_within_lagrange_bound():
+    """App. C: sum_p A_p(kdot) ((z_a - z_b)/L_z)^{2p} -> K_ab(kdot) (the two-sided
+    kernel, R9/R10) with the Lagrange remainder of Lemma lemma::Taylor (Eq. eq::Taylor2) over
+    z_a - z_b in [-L_z, L_z] (R23)."""
+    p = P.make_plan(300, 20.0, 20.0, 4.0, 1e-10)
+    assert p.m >= 0
+    K = sog.long_kernel(p)
+    za = 0.5 * p.Lz * P.cheb_nodes(p.Pc)
+    d = (za[:, None] - za[None, :]) / p.Lz
+    errs = []
+    for Q in (16, 24, 32, 40):
+        A = sog.long_coeff_taylor(p, Q)
+        KT = sum(A[k][None, None] * (d ** (2 * k))[:, :, None, None] for k in range(Q))
+        err = np.max(np.abs(KT - K)) / np.max(np.abs(K))
+        assert err <= sog.taylor_bound(p, Q)
+        errs.append(err)
+    assert errs[-1] < 1e-9 and errs[0] > 1e3 * errs[-1]         # converging, not constant
+
+
+def test_taylor_variant_converges_to_exact(small_system):
+    """App. C's one-sided Taylor form of Alg. 2 -> the SOG-exact long sum (Eq. eq::trun2, P:907);
+    with a Q whose Lagrange bound is below tol the error is that of the plan."""
+    xyz, q, L = small_system
+    t = np.arange(12)
+    for tol in (1e-6, 1e-10):
+        p = P.make_plan(len(q), *L, tol)
+        x = sog.canonicalize(xyz, p)
+        ex = sog_exact.long_exact(p, x, q, t)
+        Q = next(k for k in range(1, 200) if sog.taylor_bound(p, k) < 0.01 * tol)
+        phi, grad = sog.long_range_taylor(p, x, q, Q, t)
+        assert np.max(np.abs(phi - ex[0])) < 10 * tol
+        assert np.max(np.abs(grad - ex[1])) < 100 * tol
+        # too few terms: the truncation shows (the bound is not vacuous here)
+        phi2, _ = sog.long_range_taylor(p, x, q, max(1, Q // 4), t)
+        assert np.max(np.abs(phi2 - ex[0])) > 100 * tol
