@@ -155,6 +155,29 @@ def friendly_even(n: int) -> int:
     return n
 
 
+def z_friendly_even(n: int) -> int:
+    """Padded z size Izs (R7-Z): the smallest even 2^a 3^b or 2^a 5^b >= n (sizes the library's fused
+    z pass has a radix set for), unless that exceeds 4096 (beyond the fused pass): then
+    friendly_even(n).  Any Izs >= the R7 minimum is a valid padding (P:460-462 only needs the
+    free direction padded by at least the Gaussian's reach)."""
+    base = friendly_even(n)
+    if base > 4096:
+        return base
+    m = base
+    while True:
+        r = m
+        while r % 2 == 0:
+            r //= 2
+        r3, r5 = r, r
+        while r3 % 3 == 0:
+            r3 //= 3
+        while r5 % 5 == 0:
+            r5 //= 5
+        if r3 == 1 or r5 == 1:
+            return m
+        m += 2
+
+
 def window_h_alias(P: int, S: float, eps_w: float, s: float) -> float:
     """Largest mesh size h for which the aliasing term of Thm 4.2,
     exp(-pi^2 mu (P-1)^2 / (4 s^2 S)) with mu = s^2 - H^2/S, H=(P-1)h/2,
@@ -417,7 +440,7 @@ def make_plan(N: int, Lx: float, Ly: float, Lz: float, tol: float, **over) -> Pl
         p.Iz = max(1, math.ceil(Lz / h))
         Hz = (P - 1) * p.hz / 2.0
         pad = max(2.0 * (Hz + p.hz), sm * math.sqrt(math.log(PAD_C / tol)))   # R7
-        p.Izs = friendly_even(math.ceil((Lz + pad) / p.hz))
+        p.Izs = z_friendly_even(math.ceil((Lz + pad) / p.hz))   # R7, R7-Z
     sl = s0 * b ** (m + 1)
 
     def cost_long(P, h):

@@ -40,6 +40,21 @@ long friendly_even(long n) {
     return n;
 }
 
+// R7-Z: padded z size, the smallest even 2^a 3^b or 2^a 5^b >= n (a radix set of the fused z pass)
+// unless that exceeds 4096, else friendly_even (oracle/plan.py z_friendly_even)
+long z_friendly_even(long n) {
+    const long base = friendly_even(n);
+    if (base > 4096) return base;
+    for (long m = base;; m += 2) {
+        long r = m;
+        while (r % 2 == 0) r /= 2;
+        long r3 = r, r5 = r;
+        while (r3 % 3 == 0) r3 /= 3;
+        while (r5 % 5 == 0) r5 /= 5;
+        if (r3 == 1 || r5 == 1) return m;
+    }
+}
+
 // Largest h keeping the Thm 4.2 aliasing term exp(-pi^2 mu (P-1)^2/(4 s^2 S)) <= eps,
 // mu = s^2 - H^2/S, H = (P-1) h / 2.  0 if infeasible.
 double h_alias(int P, double S, double eps, double s) {
@@ -286,7 +301,7 @@ bool choose_params(Params& p, const RuleKnobs& k, std::string& err) {
         const double hz = p.hz();
         const double Hz = (p.P - 1) * hz / 2.0;
         const double pad = std::max(2.0 * (Hz + hz), padimg);          // R7
-        p.Izs = friendly_even(long(std::ceil((p.Lz + pad) / hz)));
+        p.Izs = z_friendly_even(long(std::ceil((p.Lz + pad) / hz)));   // R7, R7-Z
     }
     const double sl = s0 * std::pow(p.b, p.m + 1);
     auto cost_long = [&](int P, double h) {
