@@ -304,7 +304,7 @@ def stage_roofline(plan, stages, N, L, long_method="fft", precision="fp64"):
     ms = stages[name]
     # DRAM traffic of that kernel from the committed ncu --set full capture (per launch), if any
     traffic = None
-    for tp in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):
+    for tp in ("r02h_ncu_traffic.json", "r02_ncu_traffic.json", "r01_ncu_traffic.json"):
         tpath = os.path.join(ROOT, "profiles", tp)
         if os.path.exists(tpath):
             t = json.load(open(tpath)).get(name)
